@@ -1,0 +1,391 @@
+"""Benchmark of the top-level exhaustive (x, y, theta) pose search on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg2] [--impl ours|reference]
+
+Metric (BASELINE.json): pose-evals/s = top-level poses x top-level model points
+per second of top-level search, plus detect latency per image.  One JSON line
+on rank 0.  See DESIGN.md "Measurement" for every field.
+
+  value   top-level search with the working pyramid resident in HBM (search
+          call of the product C-ABI: screen + band select + exact fp64 verify
+          + top-k [+ NCCL all-gather of per-GPU top-k for N > 1]), L2 flushed
+          between steps, CUDA events on the library's stream, max over ranks.
+  e2e     the same metric through the public detect call with a HOST image:
+          H2D of the level-0 image from pinned memory, device pyramid + Sobel,
+          top-level search, refinement down every level, D2H of the outcome.
+  --impl reference   the reference's own CPU search (oracle/_ref, built from
+          /root/reference sources) on this box's host cores, all threads.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import paper_2112_05576_b200 as ea  # noqa: E402
+from paper_2112_05576_b200 import abi  # noqa: E402
+
+D = abi.deg_to_rad
+
+# SURVEY.md §8(d) d2/d3 conventions: l_bracket template, level-0 grid
+# x in [0, W-1], y in [0, H-1] with step 2^(L-1) (unit steps at the top),
+# theta in [0, 360 - dtheta]; nb 3, signed, topk 5, radius 2, min_score 0.5.
+CONFIGS = {
+    "cfg1": dict(desc="640x480 search image, 128x128 model, 1 deg over 360, 3 levels, nb 3",
+                 W=640, H=480, size=128, pose=(320, 240, 30.0), clutter=40, seed=7,
+                 occluder=None, illum=(1.0, 0.0, 1.0), sigma=0.0, nseed=0, L=3, dt=1.0),
+    "cfg2": dict(desc="1280x1024 search image, 200x200 model, 0.5 deg over 360, 4 levels, "
+                      "occlusion + illumination change + noise, nb 3",
+                 W=1280, H=1024, size=200, pose=(640, 512, 30.0), clutter=80, seed=11,
+                 occluder=(540, 412, 100, 200, 200.0), illum=(1.7, -30.0, 1.2), sigma=2.0,
+                 nseed=13, L=4, dt=0.5),
+    "cfg3": dict(desc="2592x1944 (5 MP) search image, 256x256 model, 0.25 deg full rotation, "
+                      "5 levels, nb 3",
+                 W=2592, H=1944, size=256, pose=(1296, 972, 30.0), clutter=200, seed=7,
+                 occluder=None, illum=(1.0, 0.0, 1.0), sigma=0.0, nseed=0, L=5, dt=0.25),
+}
+
+SMEM_BYTES_PER_CLK_PER_SM = 128
+ALG_BYTES_PER_EVAL = 72  # (2r+1)^2 = 9 window pixels x 8 B float2
+
+
+def make_inputs(name):
+    c = CONFIGS[name]
+    spec = ea.SceneSpec(c["W"], c["H"], "l_bracket", c["size"],
+                        (c["pose"][0], c["pose"][1], D(c["pose"][2])), c["clutter"], c["seed"],
+                        c["occluder"], c["illum"], c["sigma"], c["nseed"])
+    img, tmpl, truth, occ = ea.compose_scene(spec)
+    L = c["L"]
+    step = float(1 << (L - 1))
+    grid = ea.PoseGrid(0.0, c["W"] - 1.0, step, 0.0, c["H"] - 1.0, step, 0.0,
+                       D(360.0 - c["dt"]), D(c["dt"]))
+    cfg = ea.SearchConfig(grid=grid, num_levels=L, score_params=ea.ScoreParams(3), topk=5,
+                          refine_radius=2, min_score=0.5)
+    return img, tmpl, cfg, truth
+
+
+def top_grid(cfg):
+    s = float(1 << (cfg.num_levels - 1))
+    g = cfg.grid
+    return ea.PoseGrid(g.x0 / s, g.x1 / s, g.dx / s, g.y0 / s, g.y1 / s, g.dy / s, g.t0, g.t1,
+                       g.dt)
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index, self.rows, self.proc = index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "20"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+            t0 = time.time()
+            while not self.rows and time.time() - t0 < 5.0:  # sampler live before timing
+                time.sleep(0.02)
+            self.rows.clear()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if r[2 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "MEASURED_PEAKS.json"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "B200_PROFILING.md fallback"
+
+
+# ---- reference CPU arm -----------------------------------------------------------------
+def reference_sample(name, target_s=12.0, threads=0):
+    """The reference's own search_topk (Backend Parallel, all host threads)
+    on a theta slice of the top level: returns (pose_evals, seconds, sample)."""
+    from oracle.pyoracle import ReferenceLib
+    ref = ReferenceLib()
+    img, tmpl, cfg, _ = make_inputs(name)
+    L = cfg.num_levels
+    tp, wp = ref.build_pyramid(tmpl, L), ref.build_pyramid(img, L)
+    models, fields = ref.prepare_levels(tp, wp, cfg)
+    m, f = models[L - 1], fields[L - 1]
+    tg = top_grid(cfg)
+    nx, ny, nt = ref.grid_counts(tg)
+    n = len(m.points)
+    threads = threads or len(os.sched_getaffinity(0))
+
+    def run(nth):
+        g = ea.PoseGrid(tg.x0, tg.x1, tg.dx, tg.y0, tg.y1, tg.dy, tg.t0,
+                        tg.t0 + (nth - 1) * tg.dt, tg.dt)
+        assert ref.grid_counts(g)[2] == nth
+        t0 = time.perf_counter()
+        ref.search_topk(m.points, f, g, cfg.score_params, cfg.topk, threads=threads)
+        return time.perf_counter() - t0
+
+    probe = max(1, min(nt, threads // 8 or 1))
+    dt = run(probe)
+    nth = int(min(nt, max(probe, probe * target_s / max(dt, 1e-3))))
+    secs = run(nth)
+    evals = nx * ny * nth * n
+    sample = (f"{name} top level, theta slice {nth}/{nt} ({nx}x{ny} translations, {n} model "
+              f"points), reference search_topk Backend::Parallel")
+    return evals, secs, sample, threads
+
+
+def bench_reference(args, rank, world):
+    if rank != 0:
+        return
+    rates = []
+    for i in range(args.warmup + args.steps):
+        evals, secs, sample, threads = reference_sample(args.config, args.ref_seconds)
+        if i >= args.warmup:
+            rates.append(evals / secs)
+    v = statistics.median(rates)
+    line = {"impl": "reference", "metric": "pose-evals/sec", "value": v,
+            "unit": "pose-evals/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "higher_is_better": True, "scaling": "none",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{args.config}: {CONFIGS[args.config]['desc']}"},
+            "cpu_baseline": {"value": v, "unit": "pose-evals/s", "cores": threads,
+                             "kind": "reference", "sample": sample},
+            "e2e": {"value": v, "unit": "pose-evals/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---- our arm -------------------------------------------------------------------------------
+def bench_ours(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    stream = torch.cuda.current_stream(dev)
+    ctx = ea.Context(local_rank)
+    ctx.set_stream(stream.cuda_stream)
+    ctx.set_timing(True)
+
+    img, tmpl, cfg, truth = make_inputs(args.config)
+    det = ea.Detector(tmpl, cfg, ctx)           # template side, once (untimed prep)
+    det.levels.set_image(img)                    # working pyramid resident in HBM
+    tg = top_grid(cfg)
+    nx, ny, nt = ea.grid_counts(tg)
+    L = cfg.num_levels
+    n_top = len(det.levels.model(L - 1).points)
+    it0, it1 = nt * rank // world, nt * (rank + 1) // world
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
+
+    def gather(seeds):
+        if world == 1:
+            return seeds
+        t = torch.zeros((cfg.topk, 5), dtype=torch.float64, device=dev)
+        for i, s in enumerate(seeds):
+            t[i] = torch.tensor([s.score, float(s.grid_index), s.pose.ux, s.pose.uy,
+                                 s.pose.theta], dtype=torch.float64)
+        t[len(seeds):, 0] = float("nan")
+        out = torch.empty((world * cfg.topk, 5), dtype=torch.float64, device=dev)
+        dist.all_gather_into_tensor(out, t)
+        rows = out.cpu().numpy()
+        cands = [ea.ScoredPose(r[0], int(r[1]), ea.Pose(r[2], r[3], r[4]))
+                 for r in rows if not np.isnan(r[0])]
+        return ea.merge_topk(cands, cfg.topk)
+
+    def top_step():
+        seeds = ea.search_top_slab(det.levels, cfg, it0, it1)
+        return gather(seeds)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    # ---- value: device-resident top-level search --------------------------------------
+    for _ in range(args.warmup):
+        top_step()
+    barrier()
+    launches0 = ctx.kernel_launches()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    screen_ms, seeds = [], None
+    with ClockSampler(local_rank) as clk:
+        for i in range(args.steps):
+            flush.zero_()
+            ev[i][0].record(stream)
+            seeds = top_step()
+            ev[i][1].record(stream)
+            screen_ms.append(ctx.stats()["screen_ms"])
+        barrier()
+    launches = ctx.kernel_launches() - launches0
+    st = ctx.stats()
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    tot_ms = sum(step_ms)
+    if world > 1:
+        t = torch.tensor([tot_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot_ms = float(t.item())
+    pose_pts = nx * ny * nt * n_top  # whole job, all ranks
+    value = pose_pts * args.steps / (tot_ms / 1e3)
+
+    # ---- e2e: public detect call with a host image ------------------------------------------
+    pinned = torch.from_numpy(img).pin_memory()
+    host_img = pinned.numpy()
+    k = cfg.topk
+    h2d = img.size * 8
+    d2h = (48 + 16 * k) + (L - 1) * (32 * k + 4 * (k + 1))
+
+    def detect_step():
+        if world == 1:
+            return det.detect(host_img)
+        det.levels.set_image(host_img)
+        s = gather(ea.search_top_slab(det.levels, cfg, it0, it1))
+        out = ea.refine(det.levels, cfg, s) if rank == 0 else None
+        return out
+
+    for _ in range(args.warmup):
+        detect_step()
+    barrier()
+    eev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    outcome = None
+    for i in range(args.steps):
+        flush.zero_()
+        eev[i][0].record(stream)
+        outcome = detect_step()
+        eev[i][1].record(stream)
+    barrier()
+    e2e_ms = sum(a.elapsed_time(b) for a, b in eev)
+    if world > 1:
+        t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    e2e = pose_pts * args.steps / (e2e_ms / 1e3)
+
+    if rank != 0:
+        return
+    peaks, peak_src = measured_peaks()
+    sm_mhz = float(peaks.get("sm_max_mhz", 1965.0))
+    n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
+    smem_peak_gbs = n_sm * SMEM_BYTES_PER_CLK_PER_SM * sm_mhz * 1e6 / 1e9
+    kernel_ms = statistics.median(screen_ms)
+    local_evals = nx * ny * (it1 - it0) * n_top
+    achieved = local_evals * ALG_BYTES_PER_EVAL / (kernel_ms / 1e3) / 1e9
+    S = 16 if ((ny + 127) // 128) * 128 * 18 <= ((ny + 63) // 64) * 64 * 20 else 8
+    actual_b = (S + 2) / S * (10 / 8) * 8  # smem bytes the lattice kernel really loads / eval
+    line = {
+        "metric": "pose-evals/sec", "value": value, "unit": "pose-evals/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot_ms / args.steps,
+        "higher_is_better": True, "scaling": "strong" if world > 1 else "none",
+        "vs_baseline": None, "dtype": "f32 screen + f64 exact verify", "data": "synthetic",
+        "config": {"workload": f"{args.config}: {CONFIGS[args.config]['desc']}",
+                   "top_level_grid": f"{nx}x{ny}x{nt}", "top_model_points": n_top,
+                   "pose_evals_per_step": pose_pts, "l2": "flushed (256 MiB write) between steps",
+                   "parallelism": f"theta-slab x{world}" if world > 1 else "single GPU"},
+        "e2e": {"value": e2e, "unit": "pose-evals/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "detect_latency_ms": e2e_ms / args.steps},
+        "roofline": {"bound": "smem", "kernel": "screen_fast_kernel" if st["screen_path"] == 1
+                     else "screen_general_kernel", "achieved": achieved,
+                     "peak": smem_peak_gbs, "unit": "GB/s", "frac": achieved / smem_peak_gbs,
+                     "traffic": None,
+                     "algorithmic_bytes_per_eval": ALG_BYTES_PER_EVAL,
+                     "smem_bytes_loaded_per_eval": actual_b,
+                     "frac_smem_loaded": local_evals * actual_b / (kernel_ms / 1e3) / 1e9
+                     / smem_peak_gbs,
+                     "kernel_ms": kernel_ms, "kernel_share_of_step": kernel_ms /
+                     statistics.median(step_ms),
+                     "peak_source": f"{n_sm} SMs x 128 B/clk x sm_max_mhz from {peak_src}"},
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+        "search": {"candidates": st["candidates"], "screen_delta": st["screen_delta"],
+                   "flagged_points": st["flagged_points"],
+                   "detected": bool(outcome.found) if outcome is not None else None,
+                   "pose": outcome.pose.astuple() if outcome is not None else None,
+                   "score": outcome.score if outcome is not None else None,
+                   "truth": truth},
+    }
+    if not args.no_cpu_baseline:
+        try:
+            evals, secs, sample, threads = reference_sample(args.config, args.ref_seconds)
+            line["cpu_baseline"] = {"value": evals / secs, "unit": "pose-evals/s",
+                                    "cores": threads, "kind": "reference", "sample": sample}
+        except Exception as e:  # oracle/_ref missing on this box
+            line["cpu_baseline"] = {"value": None, "unit": "pose-evals/s", "cores": 0,
+                                    "kind": "reference", "sample": f"unavailable: {e}"}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--ref-seconds", type=float, default=10.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        if args.steps > 3:
+            args.steps = 3  # each step is a ~10 s CPU sample; keep the run to minutes
+        args.warmup = min(args.warmup, 1)
+        bench_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        bench_ours(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,1450 @@
+// api.cu -- the C-ABI of include/edgealign_b200.h: host orchestration of the
+// sm_100a kernels, mirroring the reference API one entry point at a time.
+//
+// Host fp64 arithmetic that must match the reference bit for bit (grid
+// lattice, refinement lattice, glibc cos/sin of every searched theta) is
+// compiled with -ffp-contract=off, like the reference (CMakeLists.txt:12-14).
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "host_model.h"
+#include "kernels.cuh"
+
+using namespace eab;
+
+namespace {
+
+thread_local std::string g_err;
+thread_local double g_err_value = 0.0;
+
+template <class F>
+ea_status guard(F&& f) {
+    try {
+        f();
+        g_err.clear();
+        g_err_value = 0.0;
+        return EA_OK;
+    } catch (const Failure& e) {
+        g_err = e.what();
+        g_err_value = e.value;
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        g_err = "out of host memory";
+        return EA_ERR_INTERNAL;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return EA_ERR_INTERNAL;
+    }
+}
+
+void need(const void* p, const char* what) {
+    if (!p) fail(EA_ERR_INVALID_ARGUMENT, std::string(what) + " must not be null");
+}
+
+// ---- pose geometry: pose.h:45-92 ----------------------------------------------
+uint64_t axis_count(double lo, double hi, double step) {  // pose.h:45-49
+    return (uint64_t)std::floor((hi - lo) / step + 1e-9) + 1;
+}
+
+ea_grid_counts counts_of(const ea_pose_grid& g) {  // pose.h:52-67
+    if (!(std::isfinite(g.x0) && std::isfinite(g.x1) && std::isfinite(g.dx) &&
+          std::isfinite(g.y0) && std::isfinite(g.y1) && std::isfinite(g.dy) &&
+          std::isfinite(g.t0) && std::isfinite(g.t1) && std::isfinite(g.dt))) {
+        fail(EA_ERR_INVALID_ARGUMENT, "pose grid has non-finite bounds");
+    }
+    if (g.dx <= 0.0 || g.dy <= 0.0 || g.dt <= 0.0)
+        fail(EA_ERR_INVALID_ARGUMENT, "pose grid steps must be positive");
+    if (g.x0 > g.x1 || g.y0 > g.y1 || g.t0 > g.t1)
+        fail(EA_ERR_INVALID_ARGUMENT, "pose grid range start exceeds end");
+    return ea_grid_counts{axis_count(g.x0, g.x1, g.dx), axis_count(g.y0, g.y1, g.dy),
+                          axis_count(g.t0, g.t1, g.dt)};
+}
+
+ea_pose pose_of(const ea_pose_grid& g, const ea_grid_counts& c, uint64_t index) {
+    const uint64_t total = c.nx * c.ny * c.nt;
+    if (index >= total) {
+        fail(EA_ERR_BOUNDS, "pose index " + std::to_string(index) + " out of range (grid size " +
+                                std::to_string(total) + ")");
+    }
+    const uint64_t plane = c.nx * c.ny;
+    const uint64_t it = index / plane, rem = index % plane;
+    const uint64_t iy = rem / c.nx, ix = rem % c.nx;
+    return ea_pose{g.x0 + (double)ix * g.dx, g.y0 + (double)iy * g.dy, g.t0 + (double)it * g.dt};
+}
+
+void validate_params(const ea_score_params& p) {  // similarity.cpp:15-23
+    if (p.neighborhood < 1 || p.neighborhood % 2 == 0) {
+        fail(EA_ERR_INVALID_ARGUMENT,
+             "neighborhood must be odd and >= 1, got " + std::to_string(p.neighborhood));
+    }
+    if (!(p.eps_mag > 0.0)) fail(EA_ERR_INVALID_ARGUMENT, "eps_mag must be positive");
+}
+
+// ---- device plumbing ---------------------------------------------------------
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) EAB_CUDA(cudaSetDevice(dev));
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+void h2d(ea_ctx* ctx, void* dst, const void* src, size_t bytes) {
+    if (bytes) EAB_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, ctx->stream));
+}
+void d2h(ea_ctx* ctx, void* dst, const void* src, size_t bytes) {
+    if (bytes) EAB_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+}
+void sync(ea_ctx* ctx) { EAB_CUDA(cudaStreamSynchronize(ctx->stream)); }
+
+// H2D of pageable host data through the context's pinned staging buffer.
+void h2d_staged(ea_ctx* ctx, void* dst, const void* src, size_t bytes) {
+    if (!bytes) return;
+    cudaPointerAttributes attr{};
+    if (cudaPointerGetAttributes(&attr, src) == cudaSuccess &&
+        attr.type == cudaMemoryTypeHost) {  // already pinned
+        h2d(ctx, dst, src, bytes);
+        return;
+    }
+    cudaGetLastError();
+    sync(ctx);  // staging buffer may still feed an earlier copy
+    void* st = ctx->h_stage.ensure(bytes);
+    std::memcpy(st, src, bytes);
+    h2d(ctx, dst, st, bytes);
+}
+
+// glibc cos/sin of theta_it = t0 + (double)it * dt (scan_range search.cpp:81-84,
+// rotate_model similarity.cpp:68-70), cached per grid.
+const std::vector<double>& theta_cs(ea_ctx* ctx, double t0, double dt, uint64_t nt) {
+    std::vector<double> key{t0, dt, (double)nt};
+    auto it = ctx->cs_cache.find(key);
+    if (it != ctx->cs_cache.end()) return it->second;
+    if (ctx->cs_cache.size() > 64) ctx->cs_cache.clear();
+    std::vector<double> cs(2 * nt);
+    for (uint64_t i = 0; i < nt; ++i) {
+        const double theta = t0 + (double)i * dt;
+        cs[2 * i] = std::cos(theta);
+        cs[2 * i + 1] = std::sin(theta);
+    }
+    return ctx->cs_cache.emplace(std::move(key), std::move(cs)).first->second;
+}
+
+ea_field* new_field(int w, int h) {
+    auto* f = new ea_field;
+    f->width = w;
+    f->height = h;
+    try {
+        f->g.ensure(sizeof(double) * 3 * (size_t)w * h);
+    } catch (...) {
+        delete f;
+        throw;
+    }
+    return f;
+}
+
+void sobel_into(ea_ctx* ctx, const double* d_img, int w, int h, ea_field* f) {
+    if (w < 3 || h < 3) {
+        fail(EA_ERR_SIZE, "compute_gradients needs at least 3x3, got " + std::to_string(w) + "x" +
+                              std::to_string(h));
+    }
+    launch_sobel(ctx, d_img, w, h, f->gx(), f->gy(), f->mag());
+    f->ring_max = 0.0;  // Sobel leaves the border ring at exactly 0
+}
+
+ea_model* new_model(ea_ctx* ctx, const ea_edge_point* pts, int n, double cx, double cy,
+                    int level) {
+    auto* m = new ea_model;
+    try {
+        m->n = n;
+        m->centroid_x = cx;
+        m->centroid_y = cy;
+        m->source_level = level;
+        m->host.assign(pts, pts + n);
+        if (n > 0) {
+            std::vector<double> soa(4 * (size_t)n);
+            for (int i = 0; i < n; ++i) {
+                soa[i] = pts[i].x_rel;
+                soa[n + i] = pts[i].y_rel;
+                soa[2 * n + i] = pts[i].dx;
+                soa[3 * n + i] = pts[i].dy;
+            }
+            m->pts.ensure(soa.size() * sizeof(double));
+            h2d_staged(ctx, m->pts.p, soa.data(), soa.size() * sizeof(double));
+            sync(ctx);
+        }
+    } catch (...) {
+        delete m;
+        throw;
+    }
+    return m;
+}
+
+int pyramid_levels_feasible(int w, int h) {  // image.cpp:263-272
+    int levels = 1;
+    while (w / 2 >= 8 && h / 2 >= 8) {
+        w /= 2;
+        h /= 2;
+        ++levels;
+    }
+    return levels;
+}
+
+// build_pyramid (image.cpp:274-291) on the device: level 0 at d_buf, each next
+// level appended.  Returns level offsets/dims.
+void device_pyramid(ea_ctx* ctx, double* d_buf, int w, int h, int levels,
+                    std::vector<size_t>* offs, std::vector<int>* dims) {
+    if (levels < 1) fail(EA_ERR_INVALID_ARGUMENT, "num_levels must be >= 1");
+    const int feasible = pyramid_levels_feasible(w, h);
+    if (levels > feasible) {
+        fail(EA_ERR_SIZE, "pyramid of " + std::to_string(levels) +
+                              " levels would drop below 8x8; maximum feasible level count is " +
+                              std::to_string(feasible));
+    }
+    size_t off = 0;
+    for (int l = 0; l < levels; ++l) {
+        offs->push_back(off);
+        dims->push_back(w);
+        dims->push_back(h);
+        if (l + 1 < levels) launch_downsample(ctx, d_buf + off, w, h, d_buf + off + (size_t)w * h);
+        off += (size_t)w * h;
+        w /= 2;
+        h /= 2;
+    }
+}
+
+size_t pyramid_elems(int w, int h, int levels) {
+    size_t t = 0;
+    for (int l = 0; l < levels; ++l) {
+        t += (size_t)w * h;
+        w /= 2;
+        h /= 2;
+    }
+    return t;
+}
+
+// ---- the top-level search --------------------------------------------------------
+struct TopOut {
+    std::vector<ea_scored_pose> poses;
+};
+
+bool is_int(double v) { return std::floor(v) == v && std::fabs(v) <= 1048576.0; }
+
+// Shared by search_topk, search_top_slab and screen_map: tables, plane and the
+// screening pass.  Returns the fixed-point exponent chosen.
+struct ScreenPlan {
+    ea_grid_counts c{};
+    uint64_t it_begin = 0, it_count = 0, slab_poses = 0;
+    int fold_e = 0;
+    double delta = 0.0;
+    bool fast = false;
+};
+
+ScreenPlan screen(ea_ctx* ctx, const ea_model* m, const ea_field* f, const ea_pose_grid& g,
+                  const ea_score_params& p, uint64_t it_begin, uint64_t it_end) {
+    ScreenPlan plan;
+    plan.c = counts_of(g);
+    if (it_end == 0 || it_end > plan.c.nt) it_end = plan.c.nt;
+    if (it_begin > it_end) it_begin = it_end;
+    plan.it_begin = it_begin;
+    plan.it_count = it_end - it_begin;
+    const uint64_t plane_poses = plan.c.nx * plan.c.ny;
+    plan.slab_poses = plane_poses * plan.it_count;
+    if (plan.slab_poses >= (1ull << 32))
+        fail(EA_ERR_INVALID_ARGUMENT, "pose grid slab exceeds 2^32 poses; shard it by theta");
+    const int n = m->n;
+    const int R = (p.neighborhood - 1) / 2;
+
+    // Tables for the slab's thetas.
+    const std::vector<double>& cs_all = theta_cs(ctx, g.t0, g.dt, plan.c.nt);
+    const size_t nth = plan.it_count;
+    double* d_cs = (double*)ctx->cs.ensure(sizeof(double) * 2 * (nth ? nth : 1));
+    h2d_staged(ctx, d_cs, cs_all.data() + 2 * it_begin, sizeof(double) * 2 * nth);
+    // Slab-relative rotation tables: row (it - it_begin) of px|py|dx|dy and of
+    // the lattice table.
+    const size_t slab_pairs = nth * (size_t)n;
+    double* rot = (double*)ctx->rot_exact.ensure(sizeof(double) * 4 * (slab_pairs ? slab_pairs : 1));
+    int4* scr = (int4*)ctx->rot_screen.ensure(sizeof(int4) * (slab_pairs ? slab_pairs : 1));
+    SearchCtrl* ctrl = (SearchCtrl*)ctx->ctrl.ensure(sizeof(SearchCtrl));
+    unsigned* hist = (unsigned*)ctx->hist.ensure(sizeof(unsigned) * kHistBins);
+    EAB_CUDA(cudaMemsetAsync(ctrl, 0, sizeof(SearchCtrl), ctx->stream));
+    EAB_CUDA(cudaMemsetAsync(hist, 0, sizeof(unsigned) * kHistBins, ctx->stream));
+    launch_rotate(ctx, m->pts.as<double>(), n, d_cs, (int)nth, rot, scr, &ctrl->flags);
+
+    // Fixed-point fold exponent: sums of n votes stay below 2^31.
+    int e = 0;
+    while (((uint64_t)n << (22 - e)) >= (1ull << 31)) ++e;
+    plan.fold_e = e;
+    const float K = std::ldexp(3.0f, e);
+    unsigned B3;
+    std::memcpy(&B3, &K, sizeof B3);
+    // |S_f - S| <= 2^(e-20) (candidate + fold rounding) + 2^-23 (final fp32 store)
+    plan.delta = std::ldexp(1.0, e - 20) + std::ldexp(1.0, -23);
+
+    // Path choice.
+    // Integer origin + unit steps: every translation is an exact integer,
+    // so centre = floor(px + 0.5) + u (lattice_offset); x1/y1 only bound the
+    // counts and must keep |u| < 2^20.
+    const bool lattice = is_int(g.x0) && is_int(g.y0) && std::fabs(g.x1) <= 1048576.0 &&
+                         std::fabs(g.y1) <= 1048576.0 && g.dx == 1.0 && g.dy == 1.0 && R <= 2 &&
+                         f->ring_max < p.eps_mag;
+    int shift = 4;
+    {
+        const uint64_t ny = plan.c.ny;
+        const uint64_t cost16 = ((ny + 127) / 128) * 128 * 18;
+        const uint64_t cost8 = ((ny + 63) / 64) * 64 * 20;
+        shift = cost16 <= cost8 ? 4 : 3;
+    }
+    const PlaneGeom geom = plane_geom(f->width, f->height, shift);
+    float2* plane = (float2*)ctx->plane.ensure(sizeof(float2) * geom.elems);
+    EAB_CUDA(cudaMemsetAsync(plane, 0, sizeof(float2) * geom.elems, ctx->stream));
+    launch_plane(ctx, f, p.eps_mag, geom, plane, &ctrl->ring_bad);
+    float* map = (float*)ctx->map.ensure(sizeof(float) * (plan.slab_poses ? plan.slab_poses : 1));
+
+    ScreenArgs a{};
+    a.plane = plane;
+    a.geom = geom;
+    a.rot_screen = scr;
+    a.rot_exact = rot;
+    a.rot_stride = slab_pairs;
+    a.n = n;
+    a.it_begin = it_begin;
+    a.it_count = plan.it_count;
+    a.nx = plan.c.nx;
+    a.ny = plan.c.ny;
+    a.ix0 = lattice ? (int)g.x0 : 0;
+    a.iy0 = lattice ? (int)g.y0 : 0;
+    a.x0 = g.x0;
+    a.dx = g.dx;
+    a.y0 = g.y0;
+    a.dy = g.dy;
+    a.R = R;
+    a.ignore = p.polarity == EA_POLARITY_IGNORE;
+    a.K = K;
+    a.B3 = B3;
+    a.scale = (float)(std::ldexp(1.0, e - 22) / (double)n);
+    a.map = map;
+    a.hist = hist;
+    a.ctrl = ctrl;
+    plan.fast = false;
+    if (ctx->timing) EAB_CUDA(cudaEventRecord(ctx->ev[1], ctx->stream));
+    if (plan.slab_poses) {
+        if (lattice) plan.fast = launch_screen_fast(ctx, a);
+        if (!plan.fast) launch_screen_general(ctx, a);
+    }
+    if (ctx->timing) EAB_CUDA(cudaEventRecord(ctx->ev[2], ctx->stream));
+    ctx->stats.screen_path = plan.fast ? 1 : 2;
+    return plan;
+}
+
+ExactArgs exact_args(const ea_field* f, const ea_score_params& p, const double* rot,
+                     size_t rot_stride, int n) {
+    ExactArgs x{};
+    x.gx = f->gx();
+    x.gy = f->gy();
+    x.mag = f->mag();
+    x.W = f->width;
+    x.H = f->height;
+    x.R = (p.neighborhood - 1) / 2;
+    x.ignore = p.polarity == EA_POLARITY_IGNORE;
+    x.eps = p.eps_mag;
+    x.rot_exact = rot;
+    x.rot_stride = rot_stride;
+    x.n = n;
+    return x;
+}
+
+// run_search (search.cpp:95-140) on theta indices [it_begin, it_end).
+std::vector<ea_scored_pose> top_search(ea_ctx* ctx, const ea_model* m, const ea_field* f,
+                                       const ea_pose_grid& g, const ea_score_params& p, int k,
+                                       uint64_t it_begin, uint64_t it_end) {
+    validate_params(p);
+    if (m->n == 0) fail(EA_ERR_INVALID_ARGUMENT, "search needs a nonempty model");
+    if (k < 1) fail(EA_ERR_INVALID_ARGUMENT, "topk must be >= 1");
+    ctx->stats = ea_search_stats{};
+    if (ctx->timing) EAB_CUDA(cudaEventRecord(ctx->ev[0], ctx->stream));
+    const ScreenPlan plan = screen(ctx, m, f, g, p, it_begin, it_end);
+    std::vector<ea_scored_pose> out;
+    ctx->stats.poses = plan.slab_poses;
+    ctx->stats.pose_points = plan.slab_poses * (uint64_t)m->n;
+    if (plan.slab_poses == 0) return out;
+    const int n = m->n;
+    SearchCtrl* ctrl = ctx->ctrl.as<SearchCtrl>();
+    // delta widened on device by the rounding-ambiguous pairs (lattice path only)
+    launch_threshold(ctx, ctx->hist.as<unsigned>(), k, plan.delta, plan.fast ? n : 0, ctrl);
+
+    unsigned long long cap = std::max<size_t>(ctx->cand.cap / sizeof(unsigned), 1u << 16);
+    const size_t slab_pairs = plan.it_count * (size_t)n;
+    ExactArgs x = exact_args(f, p, ctx->rot_exact.as<double>(), slab_pairs, n);
+    x.nx = plan.c.nx;
+    x.ny = plan.c.ny;
+    x.it_begin = plan.it_begin;
+    x.x0 = g.x0;
+    x.dx = g.dx;
+    x.y0 = g.y0;
+    x.dy = g.dy;
+    for (int attempt = 0; attempt < 2; ++attempt) {
+        unsigned* cand = (unsigned*)ctx->cand.ensure(sizeof(unsigned) * cap);
+        double* cs = (double*)ctx->cand_score.ensure(sizeof(double) * cap);
+        double* tk = (double*)ctx->topk.ensure((sizeof(double) + sizeof(unsigned long long)) *
+                                               (size_t)k);
+        unsigned long long* tki = reinterpret_cast<unsigned long long*>(tk + k);
+        if (attempt > 0) {
+            EAB_CUDA(cudaMemsetAsync(&ctrl->cand_count, 0, sizeof(unsigned long long),
+                                     ctx->stream));
+        }
+        launch_compact(ctx, ctx->map.as<float>(), plan.slab_poses, ctrl, cand, cap);
+        launch_rescore(ctx, x, cand, ctrl, cap, cs);
+        launch_select(ctx, cand, cs, ctrl, cap, k, plan.it_begin * plan.c.nx * plan.c.ny, tk, tki);
+        const size_t res_bytes = (sizeof(double) + sizeof(unsigned long long)) * (size_t)k;
+        char* h = (char*)ctx->h_out.ensure(sizeof(SearchCtrl) + res_bytes);
+        d2h(ctx, h, ctrl, sizeof(SearchCtrl));
+        d2h(ctx, h + sizeof(SearchCtrl), tk, res_bytes);
+        if (ctx->timing) EAB_CUDA(cudaEventRecord(ctx->ev[3], ctx->stream));
+        sync(ctx);
+        if (ctx->timing) {
+            float ms = 0.f;
+            EAB_CUDA(cudaEventElapsedTime(&ms, ctx->ev[1], ctx->ev[2]));
+            ctx->stats.screen_ms = ms;
+            EAB_CUDA(cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[3]));
+            ctx->stats.top_ms = ms;
+        }
+        SearchCtrl hc;
+        std::memcpy(&hc, h, sizeof hc);
+        ctx->stats.candidates = hc.cand_count;
+        ctx->stats.candidates_needed = hc.needed;
+        ctx->stats.threshold = hc.thr;
+        ctx->stats.flagged_points = hc.flags;
+        ctx->stats.screen_delta = plan.delta + (plan.fast ? 2.0 * hc.flags / n : 0.0);
+        if (hc.cand_count > cap) {  // band admitted more than the buffer: grow, redo
+            cap = hc.cand_count;
+            continue;
+        }
+        const double* hs = reinterpret_cast<const double*>(h + sizeof(SearchCtrl));
+        const unsigned long long* hi = reinterpret_cast<const unsigned long long*>(hs + k);
+        for (int r = 0; r < hc.n_out; ++r) {
+            out.push_back(ea_scored_pose{hs[r], hi[r], pose_of(g, plan.c, hi[r])});
+        }
+        return out;
+    }
+    fail(EA_ERR_INTERNAL, "candidate buffer did not converge");
+}
+
+// ---- refinement (search_levels search.cpp:254-357) -----------------------------
+struct Beam {
+    ea_pose pose;
+    double score;
+    uint64_t top_index;
+};
+
+void refine_levels(ea_ctx* ctx, const ea_levels* lv, const ea_search_config& cfg,
+                   const ea_pose_grid& top_grid, std::vector<Beam> beam, ea_outcome* out) {
+    const int top = cfg.num_levels - 1;
+    std::memset(out, 0, sizeof(*out));
+    int nt = 0;
+    auto trace = [&](int level, const Beam& b) {
+        if (nt < EA_MAX_LEVELS) {
+            out->trace[nt].level = level;
+            out->trace[nt].pose = b.pose;
+            out->trace[nt].score = b.score;
+            ++nt;
+        }
+    };
+    trace(top, beam[0]);
+    const double theta_floor = 0.25 * (3.14159265358979323846 / 180.0);  // deg_to_rad(0.25)
+    double step_x = top_grid.dx, step_y = top_grid.dy, step_t = top_grid.dt;
+    const int R = cfg.refine_radius;
+    const int side = 2 * R + 1;
+    const ea_score_params& p = cfg.score_params;
+    for (int level = top - 1; level >= 0; --level) {
+        step_x /= 2.0;
+        step_y /= 2.0;
+        step_t = std::max(step_t / 2.0, theta_floor);
+        const ea_model* m = lv->models[level];
+        const ea_field* f = lv->fields[level];
+        const int n = m->n;
+        const int P = (int)beam.size();
+        const int nslot = P * side;
+        const int count = nslot * side * side;
+        // host: thetas (glibc cos/sin) and the lattice in generation order
+        const size_t cs_bytes = sizeof(double) * 2 * nslot;
+        const size_t p2_bytes = sizeof(double) * 2 * count;
+        const size_t p3_bytes = sizeof(double) * 3 * count;
+        const size_t i_bytes = sizeof(int) * count;
+        const size_t total = cs_bytes + p2_bytes + p3_bytes + 2 * i_bytes;
+        sync(ctx);
+        char* hb = (char*)ctx->h_stage.ensure(total);
+        double* hcs = (double*)hb;
+        double* hp2 = (double*)(hb + cs_bytes);
+        double* hp3 = (double*)(hb + cs_bytes + p2_bytes);
+        int* hslot = (int*)(hb + cs_bytes + p2_bytes + p3_bytes);
+        int* hpar = hslot + count;
+        int e = 0;
+        for (int pi = 0; pi < P; ++pi) {
+            const double cx = beam[pi].pose.ux * 2.0;
+            const double cy = beam[pi].pose.uy * 2.0;
+            const double ct = beam[pi].pose.theta;
+            for (int kt = -R; kt <= R; ++kt) {
+                const double theta = ct + (double)kt * step_t;
+                const int slot = pi * side + (kt + R);
+                hcs[2 * slot] = std::cos(theta);
+                hcs[2 * slot + 1] = std::sin(theta);
+                for (int ky = -R; ky <= R; ++ky) {
+                    for (int kx = -R; kx <= R; ++kx) {
+                        const double ux = cx + (double)kx * step_x;
+                        const double uy = cy + (double)ky * step_y;
+                        hp2[2 * e] = ux;
+                        hp2[2 * e + 1] = uy;
+                        hp3[3 * e] = ux;
+                        hp3[3 * e + 1] = uy;
+                        hp3[3 * e + 2] = theta;
+                        hslot[e] = slot;
+                        hpar[e] = pi;
+                        ++e;
+                    }
+                }
+            }
+        }
+        char* db = (char*)ctx->refine_poses.ensure(total);
+        h2d(ctx, db, hb, total);
+        const double* dcs = (const double*)db;
+        const double* dp2 = (const double*)(db + cs_bytes);
+        const double* dp3 = (const double*)(db + cs_bytes + p2_bytes);
+        const int* dslot = (const int*)(db + cs_bytes + p2_bytes + p3_bytes);
+        const int* dpar = dslot + count;
+        const size_t pairs = (size_t)nslot * n;
+        double* rot = (double*)ctx->rot_exact.ensure(sizeof(double) * 4 * (pairs ? pairs : 1));
+        launch_rotate(ctx, m->pts.as<double>(), n, dcs, nslot, rot, nullptr, nullptr);
+        double* sc = (double*)ctx->refine_scores.ensure(sizeof(double) * count);
+        launch_refine_score(ctx, exact_args(f, p, rot, pairs, n), dp2, dslot, count, sc, nullptr);
+        const int k = cfg.topk;
+        char* bb = (char*)ctx->beam.ensure(sizeof(double) * 4 * k + sizeof(int) * (k + 1));
+        double* bout = (double*)bb;
+        int* bpar = (int*)(bb + sizeof(double) * 4 * k);
+        int* bcnt = bpar + k;
+        launch_beam_select(ctx, dp3, sc, dpar, count, k, bout, bpar, bcnt);
+        const size_t bbytes = sizeof(double) * 4 * k + sizeof(int) * (k + 1);
+        char* hbo = (char*)ctx->h_out.ensure(bbytes);
+        d2h(ctx, hbo, bb, bbytes);
+        sync(ctx);
+        const double* hbout = (const double*)hbo;
+        const int* hbpar = (const int*)(hbo + sizeof(double) * 4 * k);
+        const int kept = hbpar[k];
+        std::vector<Beam> next;
+        for (int q = 0; q < kept; ++q) {
+            next.push_back(Beam{ea_pose{hbout[4 * q], hbout[4 * q + 1], hbout[4 * q + 2]},
+                                hbout[4 * q + 3], beam[hbpar[q]].top_index});
+        }
+        beam.swap(next);
+        trace(level, beam[0]);
+    }
+    out->n_trace = nt;
+    out->pose = beam[0].pose;
+    out->score = beam[0].score;
+    out->grid_index = beam[0].top_index;
+    out->found = beam[0].score >= cfg.min_score ? 1 : 0;
+}
+
+ea_pose_grid top_grid_of(const ea_search_config& cfg) {  // search.cpp:264-273
+    const int top = cfg.num_levels - 1;
+    const double scale = (double)(1 << top);
+    ea_pose_grid g = cfg.grid;
+    g.x0 /= scale;
+    g.x1 /= scale;
+    g.dx /= scale;
+    g.y0 /= scale;
+    g.y1 /= scale;
+    g.dy /= scale;
+    return g;
+}
+
+void check_search_config(const ea_levels* lv, const ea_search_config& cfg) {
+    validate_params(cfg.score_params);
+    if (cfg.topk < 1 || cfg.refine_radius < 1)
+        fail(EA_ERR_INVALID_ARGUMENT, "topk and refine_radius must be >= 1");
+    if (cfg.num_levels < 1 || (int)lv->models.size() < cfg.num_levels)
+        fail(EA_ERR_INVALID_ARGUMENT, "prepared levels do not cover num_levels");
+    if ((int)lv->fields.size() < cfg.num_levels)
+        fail(EA_ERR_INVALID_ARGUMENT, "prepared levels have no working image");
+    if (cfg.num_levels > EA_MAX_LEVELS)
+        fail(EA_ERR_INVALID_ARGUMENT, "num_levels exceeds EA_MAX_LEVELS");
+}
+
+std::vector<Beam> seeds_to_beam(const std::vector<ea_scored_pose>& seeds) {
+    std::vector<Beam> beam;
+    for (const auto& s : seeds) beam.push_back(Beam{s.pose, s.score, s.grid_index});
+    return beam;
+}
+
+// Template side of prepare_levels (search.cpp:222-234) for one level.
+ea_model* template_model(ea_ctx* ctx, const double* d_img, int w, int h,
+                         const ea_search_config& cfg, int level) {
+    ea_field* tf = new_field(w, h);
+    std::vector<double> g(3 * (size_t)w * h);
+    try {
+        sobel_into(ctx, d_img, w, h, tf);
+        d2h(ctx, g.data(), tf->g.p, g.size() * sizeof(double));
+        sync(ctx);
+    } catch (...) {
+        delete tf;
+        throw;
+    }
+    delete tf;
+    const size_t np = (size_t)w * h;
+    const ea_edge_thresholds th =
+        cfg.has_thresholds ? cfg.thresholds : host_default_thresholds(g.data() + 2 * np, np);
+    double cx = 0, cy = 0;
+    std::vector<ea_edge_point> pts;
+    try {
+        pts = host_extract_edge_model(g.data(), g.data() + np, g.data() + 2 * np, w, h, th, &cx,
+                                      &cy);
+    } catch (const Failure& e) {
+        if (e.code == EA_ERR_EMPTY_MODEL) {
+            fail(EA_ERR_EMPTY_MODEL,
+                 "edge model extraction failed at pyramid level " + std::to_string(level) + ": " +
+                     e.what(),
+                 e.value);
+        }
+        throw;
+    }
+    return new_model(ctx, pts.data(), (int)pts.size(), cx, cy, level);
+}
+
+void free_levels(ea_levels* lv) {
+    if (!lv) return;
+    for (auto* m : lv->models) delete m;
+    for (auto* f : lv->fields) delete f;
+    delete lv;
+}
+
+void set_working_image(ea_ctx* ctx, ea_levels* lv, const double* image, int w, int h,
+                       int levels) {
+    if (w < 1 || h < 1) {
+        fail(EA_ERR_SIZE, "image dimensions must be at least 1x1, got " + std::to_string(w) + "x" +
+                              std::to_string(h));
+    }
+    const size_t elems = pyramid_elems(w, h, std::max(levels, 1));
+    double* d = (double*)lv->image.ensure(sizeof(double) * elems);
+    h2d_staged(ctx, d, image, sizeof(double) * (size_t)w * h);
+    std::vector<size_t> offs;
+    std::vector<int> dims;
+    device_pyramid(ctx, d, w, h, levels, &offs, &dims);
+    // reuse field objects when dims match
+    for (int l = 0; l < levels; ++l) {
+        const int lw = dims[2 * l], lh = dims[2 * l + 1];
+        if (l < (int)lv->fields.size() &&
+            (lv->fields[l]->width != lw || lv->fields[l]->height != lh)) {
+            delete lv->fields[l];
+            lv->fields[l] = nullptr;
+        }
+        if (l >= (int)lv->fields.size()) lv->fields.push_back(nullptr);
+        if (!lv->fields[l]) lv->fields[l] = new_field(lw, lh);
+        sobel_into(ctx, d + offs[l], lw, lh, lv->fields[l]);
+    }
+    while ((int)lv->fields.size() > levels) {
+        delete lv->fields.back();
+        lv->fields.pop_back();
+    }
+}
+
+}  // namespace
+
+// =============================================================================
+// C-ABI
+// =============================================================================
+extern "C" {
+
+const char* ea_last_error(void) { return g_err.c_str(); }
+double ea_last_error_value(void) { return g_err_value; }
+
+ea_status ea_ctx_create(int device, ea_ctx** out) {
+    return guard([&] {
+        need(out, "out");
+        int n = 0;
+        cudaError_t e = cudaGetDeviceCount(&n);
+        if (e != cudaSuccess || n == 0) {
+            cudaGetLastError();
+            fail(EA_ERR_CUDA, std::string("no CUDA device available (") +
+                                  (e != cudaSuccess ? cudaGetErrorString(e) : "0 devices") +
+                                  "); libedgealign_b200 has no CPU fallback");
+        }
+        if (device < 0 || device >= n) fail(EA_ERR_INVALID_ARGUMENT, "device index out of range");
+        DeviceGuard dg(device);
+        cudaDeviceProp prop{};
+        EAB_CUDA(cudaGetDeviceProperties(&prop, device));
+        if (prop.major < 10) {
+            fail(EA_ERR_CUDA, std::string("device ") + prop.name +
+                                  " is not sm_100 class; this build targets sm_100a only");
+        }
+        auto* c = new ea_ctx;
+        c->device = device;
+        c->sm_count = prop.multiProcessorCount;
+        c->smem_optin = prop.sharedMemPerBlockOptin;
+        cudaError_t se = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+        if (se != cudaSuccess) {
+            delete c;
+            cuda_check(se, "cudaStreamCreate");
+        }
+        c->own_stream = true;
+        *out = c;
+    });
+}
+
+void ea_ctx_destroy(ea_ctx* ctx) {
+    if (!ctx) return;
+    int prev = -1;
+    cudaGetDevice(&prev);
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    for (DevBuf* b : {&ctx->cs, &ctx->rot_exact, &ctx->rot_screen, &ctx->plane, &ctx->map,
+                      &ctx->hist, &ctx->ctrl, &ctx->cand, &ctx->cand_score, &ctx->topk,
+                      &ctx->refine_poses, &ctx->refine_scores, &ctx->beam, &ctx->accum64,
+                      &ctx->work})
+        b->release();
+    ctx->h_stage.release();
+    ctx->h_out.release();
+    for (auto& e : ctx->ev)
+        if (e) cudaEventDestroy(e);
+    if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+    if (prev >= 0) cudaSetDevice(prev);
+}
+
+ea_status ea_ctx_set_stream(ea_ctx* ctx, void* stream) {
+    return guard([&] {
+        need(ctx, "ctx");
+        DeviceGuard dg(ctx->device);
+        EAB_CUDA(cudaStreamSynchronize(ctx->stream));
+        if (ctx->own_stream && stream) {
+            cudaStreamDestroy(ctx->stream);
+            ctx->own_stream = false;
+        }
+        if (stream) {
+            ctx->stream = (cudaStream_t)stream;
+        } else if (!ctx->own_stream) {
+            EAB_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+            ctx->own_stream = true;
+        }
+    });
+}
+
+void* ea_ctx_stream(ea_ctx* ctx) { return ctx ? (void*)ctx->stream : nullptr; }
+
+ea_status ea_ctx_synchronize(ea_ctx* ctx) {
+    return guard([&] {
+        need(ctx, "ctx");
+        DeviceGuard dg(ctx->device);
+        sync(ctx);
+    });
+}
+
+ea_status ea_ctx_last_stats(const ea_ctx* ctx, ea_search_stats* out) {
+    return guard([&] {
+        need(ctx, "ctx");
+        need(out, "out");
+        *out = ctx->stats;
+    });
+}
+
+ea_status ea_ctx_set_timing(ea_ctx* ctx, int on) {
+    return guard([&] {
+        need(ctx, "ctx");
+        DeviceGuard dg(ctx->device);
+        if (on && !ctx->ev[0]) {
+            for (auto& e : ctx->ev) EAB_CUDA(cudaEventCreate(&e));
+        }
+        ctx->timing = on != 0;
+    });
+}
+
+uint64_t ea_ctx_kernel_launches(const ea_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+ea_status ea_host_alloc(size_t bytes, void** out) {
+    return guard([&] {
+        need(out, "out");
+        EAB_CUDA(cudaHostAlloc(out, bytes ? bytes : 1, cudaHostAllocDefault));
+    });
+}
+void ea_host_free(void* p) {
+    if (p) cudaFreeHost(p);
+}
+
+// ---- geometry ----------------------------------------------------------------
+ea_status ea_compute_grid_counts(const ea_pose_grid* g, ea_grid_counts* out) {
+    return guard([&] {
+        need(g, "grid");
+        need(out, "out");
+        *out = counts_of(*g);
+    });
+}
+
+ea_status ea_pose_at(const ea_pose_grid* g, uint64_t index, ea_pose* out) {
+    return guard([&] {
+        need(g, "grid");
+        need(out, "out");
+        *out = pose_of(*g, counts_of(*g), index);
+    });
+}
+
+// ---- image -------------------------------------------------------------------
+int ea_max_pyramid_levels(int w, int h) { return pyramid_levels_feasible(w, h); }
+
+ea_status ea_pyramid_dims(int w, int h, int levels, int* dims) {
+    return guard([&] {
+        need(dims, "dims");
+        for (int l = 0; l < levels; ++l) {
+            dims[2 * l] = w;
+            dims[2 * l + 1] = h;
+            w /= 2;
+            h /= 2;
+        }
+    });
+}
+
+ea_status ea_downsample(ea_ctx* ctx, const double* image, int w, int h, double* out) {
+    return guard([&] {
+        need(ctx, "ctx");
+        need(image, "image");
+        need(out, "out");
+        if (w < 2 || h < 2) {
+            fail(EA_ERR_SIZE, "downsample needs at least 2x2, got " + std::to_string(w) + "x" +
+                                  std::to_string(h));
+        }
+        DeviceGuard dg(ctx->device);
+        const size_t in = (size_t)w * h, on = (size_t)(w / 2) * (h / 2);
+        double* d = (double*)ctx->work.ensure(sizeof(double) * (in + on));
+        h2d_staged(ctx, d, image, sizeof(double) * in);
+        launch_downsample(ctx, d, w, h, d + in);
+        d2h(ctx, out, d + in, sizeof(double) * on);
+        sync(ctx);
+    });
+}
+
+ea_status ea_build_pyramid(ea_ctx* ctx, const double* image, int w, int h, int levels,
+                           double* out) {
+    return guard([&] {
+        need(ctx, "ctx");
+        need(image, "image");
+        need(out, "out");
+        if (w < 1 || h < 1) {
+            fail(EA_ERR_SIZE, "image dimensions must be at least 1x1, got " + std::to_string(w) +
+                                  "x" + std::to_string(h));
+        }
+        DeviceGuard dg(ctx->device);
+        if (levels < 1) fail(EA_ERR_INVALID_ARGUMENT, "num_levels must be >= 1");
+        const size_t elems = pyramid_elems(w, h, levels);
+        double* d = (double*)ctx->work.ensure(sizeof(double) * elems);
+        h2d_staged(ctx, d, image, sizeof(double) * (size_t)w * h);
+        std::vector<size_t> offs;
+        std::vector<int> dims;
+        device_pyramid(ctx, d, w, h, levels, &offs, &dims);
+        d2h(ctx, out, d, sizeof(double) * elems);
+        sync(ctx);
+    });
+}
+
+ea_status ea_compute_gradients(ea_ctx* ctx, const double* image, int w, int h, double* gx,
+                               double* gy, double* mag) {
+    return guard([&] {
+        need(ctx, "ctx");
+        need(image, "image");
+        need(gx, "gx");
+        need(gy, "gy");
+        need(mag, "mag");
+        DeviceGuard dg(ctx->device);
+        if (w < 3 || h < 3) {
+            fail(EA_ERR_SIZE, "compute_gradients needs at least 3x3, got " + std::to_string(w) +
+                                  "x" + std::to_string(h));
+        }
+        const size_t n = (size_t)w * h;
+        double* d = (double*)ctx->work.ensure(sizeof(double) * 4 * n);
+        h2d_staged(ctx, d, image, sizeof(double) * n);
+        launch_sobel(ctx, d, w, h, d + n, d + 2 * n, d + 3 * n);
+        d2h(ctx, gx, d + n, sizeof(double) * n);
+        d2h(ctx, gy, d + 2 * n, sizeof(double) * n);
+        d2h(ctx, mag, d + 3 * n, sizeof(double) * n);
+        sync(ctx);
+    });
+}
+
+ea_status ea_field_upload(ea_ctx* ctx, const double* gx, const double* gy, const double* mag,
+                          int w, int h, ea_field** out) {
+    return guard([&] {
+        need(ctx, "ctx");
+        need(out, "out");
+        need(gx, "gx");
+        need(gy, "gy");
+        need(mag, "mag");
+        if (w < 1 || h < 1) fail(EA_ERR_SIZE, "gradient field must be at least 1x1");
+        DeviceGuard dg(ctx->device);
+        ea_field* f = new_field(w, h);
+        try {
+            const size_t n = (size_t)w * h;
+            h2d_staged(ctx, f->gx(), gx, sizeof(double) * n);
+            h2d_staged(ctx, f->gy(), gy, sizeof(double) * n);
+            h2d_staged(ctx, f->mag(), mag, sizeof(double) * n);
+            double rm = 0.0;  // largest magnitude on the outer ring
+            for (int x = 0; x < w; ++x) {
+                rm = std::max(rm, std::max(mag[x], mag[(size_t)(h - 1) * w + x]));
+            }
+            for (int y = 0; y < h; ++y) {
+                rm = std::max(rm, std::max(mag[(size_t)y * w], mag[(size_t)y * w + w - 1]));
+            }
+            f->ring_max = rm;
+            for (size_t i = 0; i < n && std::isfinite(f->ring_max); ++i) {
+                if (!std::isfinite(mag[i])) f->ring_max = INFINITY;
+            }
+            sync(ctx);
+        } catch (...) {
+            delete f;
+            throw;
+        }
+        *out = f;
+    });
+}
+
+ea_status ea_field_from_image(ea_ctx* ctx, const double* image, int w, int h, ea_field** out) {
+    return guard([&] {
+        need(ctx, "ctx");
+        need(image, "image");
+        need(out, "out");
+        DeviceGuard dg(ctx->device);
+        if (w < 3 || h < 3) {
+            fail(EA_ERR_SIZE, "compute_gradients needs at least 3x3, got " + std::to_string(w) +
+                                  "x" + std::to_string(h));
+        }
+        ea_field* f = new_field(w, h);
+        try {
+            double* d = (double*)ctx->work.ensure(sizeof(double) * (size_t)w * h);
+            h2d_staged(ctx, d, image, sizeof(double) * (size_t)w * h);
+            sobel_into(ctx, d, w, h, f);
+            sync(ctx);
+        } catch (...) {
+            delete f;
+            throw;
+        }
+        *out = f;
+    });
+}
+
+ea_status ea_field_download(ea_ctx* ctx, const ea_field* f, double* gx, double* gy,
+                            double* mag) {
+    return guard([&] {
+        need(ctx, "ctx");
+        need(f, "field");
+        DeviceGuard dg(ctx->device);
+        const size_t n = (size_t)f->width * f->height;
+        if (gx) d2h(ctx, gx, f->gx(), sizeof(double) * n);
+        if (gy) d2h(ctx, gy, f->gy(), sizeof(double) * n);
+        if (mag) d2h(ctx, mag, f->mag(), sizeof(double) * n);
+        sync(ctx);
+    });
+}
+
+ea_status ea_field_dims(const ea_field* f, int* w, int* h) {
+    return guard([&] {
+        need(f, "field");
+        if (w) *w = f->width;
+        if (h) *h = f->height;
+    });
+}
+
+void ea_field_free(ea_field* f) { delete f; }
+
+// ---- template side -------------------------------------------------------------
+ea_status ea_default_thresholds(const double* mag, int w, int h, ea_edge_thresholds* out) {
+    return guard([&] {
+        need(mag, "mag");
+        need(out, "out");
+        *out = host_default_thresholds(mag, (size_t)w * h);
+    });
+}
+
+ea_status ea_extract_edge_model(const double* gx, const double* gy, const double* mag, int w,
+                                int h, const ea_edge_thresholds* th, int level,
+                                ea_edge_point* points, int cap, int* n_out, double* cx,
+                                double* cy) {
+    (void)level;
+    return guard([&] {
+        need(gx, "gx");
+        need(gy, "gy");
+        need(mag, "mag");
+        need(th, "thresholds");
+        need(n_out, "n_out");
+        double ccx = 0, ccy = 0;
+        const auto pts = host_extract_edge_model(gx, gy, mag, w, h, *th, &ccx, &ccy);
+        *n_out = (int)pts.size();
+        if (cx) *cx = ccx;
+        if (cy) *cy = ccy;
+        if (points) {
+            for (int i = 0; i < (int)pts.size() && i < cap; ++i) points[i] = pts[i];
+        }
+    });
+}
+
+ea_status ea_model_create(ea_ctx* ctx, const ea_edge_point* points, int n, double cx, double cy,
+                          int level, ea_model** out) {
+    return guard([&] {
+        need(ctx, "ctx");
+        need(out, "out");
+        if (n < 0) fail(EA_ERR_INVALID_ARGUMENT, "model point count must be >= 0");
+        if (n > 0) need(points, "points");
+        DeviceGuard dg(ctx->device);
+        *out = new_model(ctx, points, n, cx, cy, level);
+    });
+}
+
+int ea_model_size(const ea_model* m) { return m ? m->n : 0; }
+void ea_model_free(ea_model* m) { delete m; }
+
+// ---- similarity ------------------------------------------------------------------
+ea_status ea_validate_params(const ea_score_params* p) {
+    return guard([&] {
+        need(p, "params");
+        validate_params(*p);
+    });
+}
+
+ea_status ea_point_vote(ea_ctx* ctx, double dir_x, double dir_y, const ea_field* f, int cx,
+                        int cy, const ea_score_params* p, double* out) {
+    return guard([&] {
+        need(ctx, "ctx");
+        need(f, "field");
+        need(p, "params");
+        need(out, "out");
+        validate_params(*p);
+        DeviceGuard dg(ctx->device);
+        double* sc = (double*)ctx->refine_scores.ensure(sizeof(double) * 2);
+        launch_point_vote(ctx, f, cx, cy, (p->neighborhood - 1) / 2, dir_x, dir_y, p->eps_mag,
+                          p->polarity == EA_POLARITY_IGNORE, sc);
+        d2h(ctx, out, sc, sizeof(double));
+        sync(ctx);
+    });
+}
+
+ea_status ea_rotate_model(ea_ctx* ctx, const ea_model* m, double theta, double* px, double* py,
+                          double* dx, double* dy) {
+    return guard([&] {
+        need(ctx, "ctx");
+        need(m, "model");
+        DeviceGuard dg(ctx->device);
+        const int n = m->n;
+        if (n == 0) return;
+        const double hcs[2] = {std::cos(theta), std::sin(theta)};
+        double* dcs = (double*)ctx->cs.ensure(sizeof(double) * 2);
+        h2d_staged(ctx, dcs, hcs, sizeof hcs);
+        double* rot = (double*)ctx->rot_exact.ensure(sizeof(double) * 4 * n);
+        launch_rotate(ctx, m->pts.as<double>(), n, dcs, 1, rot, nullptr, nullptr);
+        if (px) d2h(ctx, px, rot, sizeof(double) * n);
+        if (py) d2h(ctx, py, rot + n, sizeof(double) * n);
+        if (dx) d2h(ctx, dx, rot + 2 * n, sizeof(double) * n);
+        if (dy) d2h(ctx, dy, rot + 3 * n, sizeof(double) * n);
+        sync(ctx);
+    });
+}
+
+ea_status ea_pose_score(ea_ctx* ctx, const ea_model* m, const ea_pose* pose, const ea_field* f,
+                        const ea_score_params* p, double* value, int* n_inbounds) {
+    return guard([&] {
+        need(ctx, "ctx");
+        need(m, "model");
+        need(pose, "pose");
+        need(f, "field");
+        need(p, "params");
+        validate_params(*p);
+        if (m->n == 0) fail(EA_ERR_INVALID_ARGUMENT, "pose_score needs a nonempty model");
+        DeviceGuard dg(ctx->device);
+        const int n = m->n;
+        struct {
+            double cs[2];
+            double uxuy[2];
+            int slot;
+        } h{{std::cos(pose->theta), std::sin(pose->theta)}, {pose->ux, pose->uy}, 0};
+        char* d = (char*)ctx->work.ensure(sizeof h);
+        h2d_staged(ctx, d, &h, sizeof h);
+        double* rot = (double*)ctx->rot_exact.ensure(sizeof(double) * 4 * n);
+        launch_rotate(ctx, m->pts.as<double>(), n, (const double*)d, 1, rot, nullptr, nullptr);
+        double* sc = (double*)ctx->refine_scores.ensure(sizeof(double) + sizeof(int));
+        int* inb = (int*)(sc + 1);
+        launch_refine_score(ctx, exact_args(f, *p, rot, (size_t)n, n),
+                            (const double*)(d + offsetof(decltype(h), uxuy)),
+                            (const int*)(d + offsetof(decltype(h), slot)), 1, sc, inb);
+        double hv[2];
+        d2h(ctx, hv, sc, sizeof(double) + sizeof(int));
+        sync(ctx);
+        if (value) *value = hv[0];
+        if (n_inbounds) std::memcpy(n_inbounds, &hv[1], sizeof(int));
+    });
+}
+
+// ---- search ---------------------------------------------------------------------------
+ea_status ea_search_topk(ea_ctx* ctx, const ea_model* m, const ea_field* f,
+                         const ea_pose_grid* g, const ea_score_params* p, int backend_kind,
+                         int k, ea_scored_pose* out, int* n_out) {
+    (void)backend_kind;
+    return guard([&] {
+        need(ctx, "ctx");
+        need(m, "model");
+        need(f, "field");
+        need(g, "grid");
+        need(p, "params");
+        need(n_out, "n_out");
+        DeviceGuard dg(ctx->device);
+        const auto r = top_search(ctx, m, f, *g, *p, k, 0, 0);
+        if (!r.empty()) need(out, "out");
+        for (size_t i = 0; i < r.size(); ++i) out[i] = r[i];
+        *n_out = (int)r.size();
+    });
+}
+
+ea_status ea_exhaustive_search(ea_ctx* ctx, const ea_model* m, const ea_field* f,
+                               const ea_pose_grid* g, const ea_score_params* p,
+                               int backend_kind, ea_scored_pose* out) {
+    int n = 0;
+    return ea_search_topk(ctx, m, f, g, p, backend_kind, 1, out, &n);
+}
+
+ea_status ea_search_topk_slab(ea_ctx* ctx, const ea_model* m, const ea_field* f,
+                              const ea_pose_grid* g, const ea_score_params* p, int k,
+                              uint64_t it_begin, uint64_t it_end, ea_scored_pose* out,
+                              int* n_out) {
+    return guard([&] {
+        need(ctx, "ctx");
+        need(m, "model");
+        need(f, "field");
+        need(g, "grid");
+        need(p, "params");
+        need(n_out, "n_out");
+        DeviceGuard dg(ctx->device);
+        if (it_end == 0) it_end = 1;  // an empty slab must be explicit: [b, e) with e > b
+        const auto r = top_search(ctx, m, f, *g, *p, k, it_begin, it_end);
+        for (size_t i = 0; i < r.size(); ++i) out[i] = r[i];
+        *n_out = (int)r.size();
+    });
+}
+
+ea_status ea_merge_topk(const ea_scored_pose* in, int n, int k, ea_scored_pose* out,
+                        int* n_out) {
+    return guard([&] {
+        need(n_out, "n_out");
+        if (k < 1) fail(EA_ERR_INVALID_ARGUMENT, "topk must be >= 1");
+        std::vector<ea_scored_pose> v(in, in + (n > 0 ? n : 0));
+        std::sort(v.begin(), v.end(), [](const ea_scored_pose& a, const ea_scored_pose& b) {
+            if (a.score != b.score) return a.score > b.score;  // better(), search.cpp:36-41
+            return a.grid_index < b.grid_index;
+        });
+        if ((int)v.size() > k) v.resize(k);
+        for (size_t i = 0; i < v.size(); ++i) out[i] = v[i];
+        *n_out = (int)v.size();
+    });
+}
+
+ea_status ea_score_map(ea_ctx* ctx, const ea_model* m, const ea_field* f, const ea_pose_grid* g,
+                       const ea_score_params* p, uint64_t max_cells, double* out) {
+    return guard([&] {
+        need(ctx, "ctx");
+        need(m, "model");
+        need(f, "field");
+        need(g, "grid");
+        need(p, "params");
+        validate_params(*p);
+        if (m->n == 0) fail(EA_ERR_INVALID_ARGUMENT, "score_map needs a nonempty model");
+        const ea_grid_counts c = counts_of(*g);
+        const uint64_t total = c.nx * c.ny * c.nt;
+        if (total > max_cells) {
+            fail(EA_ERR_BUDGET, "score_map needs " + std::to_string(total) +
+                                    " cells but the budget allows " + std::to_string(max_cells));
+        }
+        need(out, "out");
+        DeviceGuard dg(ctx->device);
+        const int n = m->n;
+        const std::vector<double>& cs = theta_cs(ctx, g->t0, g->dt, c.nt);
+        double* dcs = (double*)ctx->cs.ensure(sizeof(double) * 2 * c.nt);
+        h2d_staged(ctx, dcs, cs.data(), sizeof(double) * 2 * c.nt);
+        const size_t pairs = (size_t)c.nt * n;
+        double* rot = (double*)ctx->rot_exact.ensure(sizeof(double) * 4 * pairs);
+        launch_rotate(ctx, m->pts.as<double>(), n, dcs, (int)c.nt, rot, nullptr, nullptr);
+        ExactArgs x = exact_args(f, *p, rot, pairs, n);
+        x.nx = c.nx;
+        x.ny = c.ny;
+        x.it_begin = 0;
+        x.x0 = g->x0;
+        x.dx = g->dx;
+        x.y0 = g->y0;
+        x.dy = g->dy;
+        double* d = (double*)ctx->work.ensure(sizeof(double) * total);
+        launch_exact_map(ctx, x, total, d);
+        d2h(ctx, out, d, sizeof(double) * total);
+        sync(ctx);
+    });
+}
+
+ea_status ea_screen_map(ea_ctx* ctx, const ea_model* m, const ea_field* f, const ea_pose_grid* g,
+                        const ea_score_params* p, uint64_t max_cells, float* out, double* delta) {
+    return guard([&] {
+        need(ctx, "ctx");
+        need(m, "model");
+        need(f, "field");
+        need(g, "grid");
+        need(p, "params");
+        validate_params(*p);
+        if (m->n == 0) fail(EA_ERR_INVALID_ARGUMENT, "score_map needs a nonempty model");
+        const ea_grid_counts c = counts_of(*g);
+        const uint64_t total = c.nx * c.ny * c.nt;
+        if (total > max_cells) {
+            fail(EA_ERR_BUDGET, "score_map needs " + std::to_string(total) +
+                                    " cells but the budget allows " + std::to_string(max_cells));
+        }
+        need(out, "out");
+        DeviceGuard dg(ctx->device);
+        ctx->stats = ea_search_stats{};
+        const ScreenPlan plan = screen(ctx, m, f, *g, *p, 0, 0);
+        SearchCtrl hc;
+        d2h(ctx, &hc, ctx->ctrl.p, sizeof hc);
+        d2h(ctx, out, ctx->map.p, sizeof(float) * total);
+        sync(ctx);
+        ctx->stats.flagged_points = hc.flags;
+        ctx->stats.screen_delta = plan.delta + (plan.fast ? 2.0 * hc.flags / m->n : 0.0);
+        if (delta) *delta = ctx->stats.screen_delta;
+    });
+}
+
+// ---- coarse to fine ---------------------------------------------------------------------
+ea_status ea_prepare_levels(ea_ctx* ctx, const double* const* tl, const int* tdims, int nt,
+                            const double* const* wl, const int* wdims, int nw,
+                            const ea_search_config* cfg, ea_levels** out) {
+    return guard([&] {
+        need(ctx, "ctx");
+        need(cfg, "config");
+        need(out, "out");
+        if (cfg->num_levels < 1) fail(EA_ERR_INVALID_ARGUMENT, "num_levels must be >= 1");
+        const int L = cfg->num_levels;
+        if (nt < L || nw < L)
+            fail(EA_ERR_INVALID_ARGUMENT, "pyramids must provide " + std::to_string(L) + " levels");
+        DeviceGuard dg(ctx->device);
+        auto* lv = new ea_levels;
+        try {
+            for (int l = 0; l < L; ++l) {
+                const int tw = tdims[2 * l], th = tdims[2 * l + 1];
+                if (tw < 1 || th < 1) fail(EA_ERR_SIZE, "template level is empty");
+                double* d = (double*)ctx->work.ensure(sizeof(double) * (size_t)tw * th);
+                h2d_staged(ctx, d, tl[l], sizeof(double) * (size_t)tw * th);
+                if (tw < 3 || th < 3) {
+                    fail(EA_ERR_SIZE, "compute_gradients needs at least 3x3, got " +
+                                          std::to_string(tw) + "x" + std::to_string(th));
+                }
+                lv->models.push_back(template_model(ctx, d, tw, th, *cfg, l));
+                const int ww = wdims[2 * l], wh = wdims[2 * l + 1];
+                if (ww < 3 || wh < 3) {
+                    fail(EA_ERR_SIZE, "compute_gradients needs at least 3x3, got " +
+                                          std::to_string(ww) + "x" + std::to_string(wh));
+                }
+                ea_field* f = new_field(ww, wh);
+                lv->fields.push_back(f);
+                double* dw = (double*)ctx->work.ensure(sizeof(double) * (size_t)ww * wh);
+                h2d_staged(ctx, dw, wl[l], sizeof(double) * (size_t)ww * wh);
+                sobel_into(ctx, dw, ww, wh, f);
+                sync(ctx);
+            }
+        } catch (...) {
+            free_levels(lv);
+            throw;
+        }
+        *out = lv;
+    });
+}
+
+ea_status ea_prepare_models(ea_ctx* ctx, const double* tmpl, int tw, int th,
+                            const ea_search_config* cfg, ea_levels** out) {
+    return guard([&] {
+        need(ctx, "ctx");
+        need(tmpl, "template");
+        need(cfg, "config");
+        need(out, "out");
+        DeviceGuard dg(ctx->device);
+        const int L = cfg->num_levels;
+        if (tw < 1 || th < 1) fail(EA_ERR_SIZE, "template image is empty");
+        auto* lv = new ea_levels;
+        try {
+            const size_t elems = pyramid_elems(tw, th, std::max(L, 1));
+            double* d = (double*)ctx->work.ensure(sizeof(double) * elems);
+            h2d_staged(ctx, d, tmpl, sizeof(double) * (size_t)tw * th);
+            std::vector<size_t> offs;
+            std::vector<int> dims;
+            device_pyramid(ctx, d, tw, th, L, &offs, &dims);
+            for (int l = 0; l < L; ++l) {
+                lv->models.push_back(
+                    template_model(ctx, d + offs[l], dims[2 * l], dims[2 * l + 1], *cfg, l));
+            }
+        } catch (...) {
+            free_levels(lv);
+            throw;
+        }
+        *out = lv;
+    });
+}
+
+ea_status ea_levels_set_image(ea_ctx* ctx, ea_levels* lv, const double* image, int w, int h) {
+    return guard([&] {
+        need(ctx, "ctx");
+        need(lv, "levels");
+        need(image, "image");
+        DeviceGuard dg(ctx->device);
+        set_working_image(ctx, lv, image, w, h, (int)lv->models.size());
+        sync(ctx);
+    });
+}
+
+int ea_levels_count(const ea_levels* lv) { return lv ? (int)lv->models.size() : 0; }
+
+ea_status ea_levels_model(const ea_levels* lv, int level, ea_edge_point* points, int cap,
+                          int* n_out, double* cx, double* cy) {
+    return guard([&] {
+        need(lv, "levels");
+        need(n_out, "n_out");
+        if (level < 0 || level >= (int)lv->models.size())
+            fail(EA_ERR_BOUNDS, "level " + std::to_string(level) + " out of range");
+        const ea_model* m = lv->models[level];
+        *n_out = m->n;
+        if (cx) *cx = m->centroid_x;
+        if (cy) *cy = m->centroid_y;
+        if (points)
+            for (int i = 0; i < m->n && i < cap; ++i) points[i] = m->host[i];
+    });
+}
+
+const ea_field* ea_levels_field(const ea_levels* lv, int level) {
+    if (!lv || level < 0 || level >= (int)lv->fields.size()) return nullptr;
+    return lv->fields[level];
+}
+
+const ea_model* ea_levels_get_model(const ea_levels* lv, int level) {
+    if (!lv || level < 0 || level >= (int)lv->models.size()) return nullptr;
+    return lv->models[level];
+}
+
+void ea_levels_free(ea_levels* lv) { free_levels(lv); }
+
+ea_status ea_search_levels(ea_ctx* ctx, const ea_levels* lv, const ea_search_config* cfg,
+                           ea_outcome* out) {
+    return guard([&] {
+        need(ctx, "ctx");
+        need(lv, "levels");
+        need(cfg, "config");
+        need(out, "out");
+        check_search_config(lv, *cfg);
+        DeviceGuard dg(ctx->device);
+        const int top = cfg->num_levels - 1;
+        const ea_pose_grid tg = top_grid_of(*cfg);
+        const auto seeds = top_search(ctx, lv->models[top], lv->fields[top], tg,
+                                      cfg->score_params, cfg->topk, 0, 0);
+        const ea_search_stats keep = ctx->stats;
+        refine_levels(ctx, lv, *cfg, tg, seeds_to_beam(seeds), out);
+        const int launched = ctx->stats.kernels_launched;
+        ctx->stats = keep;
+        ctx->stats.kernels_launched = launched;
+    });
+}
+
+ea_status ea_search_top_slab(ea_ctx* ctx, const ea_levels* lv, const ea_search_config* cfg,
+                             uint64_t it_begin, uint64_t it_end, ea_scored_pose* seeds,
+                             int* n_seeds) {
+    return guard([&] {
+        need(ctx, "ctx");
+        need(lv, "levels");
+        need(cfg, "config");
+        need(n_seeds, "n_seeds");
+        check_search_config(lv, *cfg);
+        DeviceGuard dg(ctx->device);
+        const int top = cfg->num_levels - 1;
+        if (it_end == 0) it_end = 1;
+        const auto r = top_search(ctx, lv->models[top], lv->fields[top], top_grid_of(*cfg),
+                                  cfg->score_params, cfg->topk, it_begin, it_end);
+        for (size_t i = 0; i < r.size(); ++i) seeds[i] = r[i];
+        *n_seeds = (int)r.size();
+    });
+}
+
+ea_status ea_refine(ea_ctx* ctx, const ea_levels* lv, const ea_search_config* cfg,
+                    const ea_scored_pose* seeds, int n_seeds, ea_outcome* out) {
+    return guard([&] {
+        need(ctx, "ctx");
+        need(lv, "levels");
+        need(cfg, "config");
+        need(out, "out");
+        check_search_config(lv, *cfg);
+        if (n_seeds < 1) fail(EA_ERR_INVALID_ARGUMENT, "refinement needs at least one seed");
+        need(seeds, "seeds");
+        DeviceGuard dg(ctx->device);
+        std::vector<ea_scored_pose> v(seeds, seeds + std::min(n_seeds, cfg->topk));
+        refine_levels(ctx, lv, *cfg, top_grid_of(*cfg), seeds_to_beam(v), out);
+    });
+}
+
+ea_status ea_coarse_to_fine(ea_ctx* ctx, const double* const* tl, const int* tdims, int nt,
+                            const double* const* wl, const int* wdims, int nw,
+                            const ea_search_config* cfg, ea_outcome* out) {
+    ea_levels* lv = nullptr;
+    ea_status st = ea_prepare_levels(ctx, tl, tdims, nt, wl, wdims, nw, cfg, &lv);
+    if (st != EA_OK) return st;
+    st = ea_search_levels(ctx, lv, cfg, out);
+    free_levels(lv);
+    return st;
+}
+
+ea_status ea_detect(ea_ctx* ctx, ea_levels* lv, const double* image, int w, int h,
+                    const ea_search_config* cfg, ea_outcome* out) {
+    return guard([&] {
+        need(ctx, "ctx");
+        need(lv, "levels");
+        need(image, "image");
+        need(cfg, "config");
+        need(out, "out");
+        DeviceGuard dg(ctx->device);
+        if ((int)lv->models.size() < cfg->num_levels)
+            fail(EA_ERR_INVALID_ARGUMENT, "prepared levels do not cover num_levels");
+        set_working_image(ctx, lv, image, w, h, cfg->num_levels);
+        check_search_config(lv, *cfg);
+        const int top = cfg->num_levels - 1;
+        const ea_pose_grid tg = top_grid_of(*cfg);
+        const auto seeds = top_search(ctx, lv->models[top], lv->fields[top], tg,
+                                      cfg->score_params, cfg->topk, 0, 0);
+        const ea_search_stats keep = ctx->stats;
+        refine_levels(ctx, lv, *cfg, tg, seeds_to_beam(seeds), out);
+        const int launched = ctx->stats.kernels_launched;
+        ctx->stats = keep;
+        ctx->stats.kernels_launched = launched;
+    });
+}
+
+// ---- synthetic scenes ----------------------------------------------------------------------
+ea_status ea_render_template(int template_id, int size, double* out) {
+    return guard([&] {
+        need(out, "out");
+        host_render_template(template_id, size, out);
+    });
+}
+
+ea_status ea_compose_scene(const ea_scene_spec* spec, double* canvas, double* tmpl,
+                           ea_pose* truth_pose, double* occluded_fraction) {
+    return guard([&] {
+        need(spec, "spec");
+        need(canvas, "canvas");
+        need(tmpl, "template");
+        ea_pose tp{};
+        double occ = 0.0;
+        host_compose_scene(*spec, canvas, tmpl, &tp, &occ);
+        if (truth_pose) *truth_pose = tp;
+        if (occluded_fraction) *occluded_fraction = occ;
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,132 @@
+// common.cuh -- shared host/device infrastructure of libedgealign_b200.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <map>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "failure.h"
+
+namespace eab {
+
+inline void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) {
+        fail(EA_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+    }
+}
+#define EAB_CUDA(x) ::eab::cuda_check((x), #x)
+
+// ---- growable device buffer ------------------------------------------------
+struct DevBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    void* ensure(size_t bytes) {
+        if (bytes > cap) {
+            if (p) cudaFree(p);
+            p = nullptr;
+            cap = 0;
+            size_t want = bytes < 256 ? 256 : bytes;
+            EAB_CUDA(cudaMalloc(&p, want));
+            cap = want;
+        }
+        return p;
+    }
+    template <class T>
+    T* as() const { return static_cast<T*>(p); }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+    }
+};
+
+// ---- pinned host staging ---------------------------------------------------
+struct HostBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    void* ensure(size_t bytes) {
+        if (bytes > cap) {
+            if (p) cudaFreeHost(p);
+            p = nullptr;
+            cap = 0;
+            size_t want = bytes < 4096 ? 4096 : bytes;
+            EAB_CUDA(cudaHostAlloc(&p, want, cudaHostAllocDefault));
+            cap = want;
+        }
+        return p;
+    }
+    template <class T>
+    T* as() const { return static_cast<T*>(p); }
+    void release() {
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        cap = 0;
+    }
+};
+
+}  // namespace eab
+
+// ---- opaque handles of the C-ABI ------------------------------------------
+struct ea_field {
+    int width = 0, height = 0;
+    double ring_max = INFINITY;  // largest |g| on the outer pixel ring
+    eab::DevBuf g;  // gx | gy | mag, each width*height doubles
+    double* gx() const { return g.as<double>(); }
+    double* gy() const { return g.as<double>() + (size_t)width * height; }
+    double* mag() const { return g.as<double>() + 2 * (size_t)width * height; }
+};
+
+struct ea_model {
+    int n = 0;
+    double centroid_x = 0, centroid_y = 0;
+    int source_level = 0;
+    std::vector<ea_edge_point> host;  // AoS copy (template side stays on host too)
+    eab::DevBuf pts;                  // device SoA: x_rel | y_rel | dx | dy
+};
+
+struct ea_levels {
+    std::vector<ea_model*> models;  // owned
+    std::vector<ea_field*> fields;  // owned; may be empty until set_image
+    eab::DevBuf image;              // working level-0 image + pyramid scratch
+};
+
+struct ea_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    int sm_count = 0;
+    size_t smem_optin = 0;
+    uint64_t launches = 0;
+    ea_search_stats stats{};
+    bool timing = false;
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    // scratch
+    eab::DevBuf cs, rot_exact, rot_screen, plane, map, hist, ctrl, cand, cand_score, topk,
+        refine_poses, refine_scores, beam, accum64, work;
+    eab::HostBuf h_stage, h_out;
+    // glibc cos/sin tables of theta grids, cached per (t0, dt, nt)
+    std::map<std::vector<double>, std::vector<double>> cs_cache;
+};
+
+namespace eab {
+
+// Launch bookkeeping (the bench's gpu_launches claim comes from here).
+inline void count_launch(ea_ctx* ctx, int n = 1) {
+    ctx->launches += (uint64_t)n;
+    ctx->stats.kernels_launched += n;
+}
+
+inline void check_launch(const char* what) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        fail(EA_ERR_CUDA, std::string("kernel launch ") + what + ": " + cudaGetErrorString(e));
+    }
+}
+
+}  // namespace eab

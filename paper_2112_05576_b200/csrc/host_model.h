@@ -1,0 +1,23 @@
+// host_model.h -- host-side helpers of libedgealign_b200 (template side and
+// the synthetic scene generator).
+#pragma once
+
+#include <vector>
+
+#include "failure.h"
+
+namespace eab {
+
+
+ea_edge_thresholds host_default_thresholds(const double* mag, size_t count);
+std::vector<ea_edge_point> host_extract_edge_model(const double* gx, const double* gy,
+                                                   const double* mag, int w, int h,
+                                                   const ea_edge_thresholds& th,
+                                                   double* centroid_x, double* centroid_y);
+
+// Synthetic scenes (synth.cpp:24-300), host only: libm-dependent generator.
+void host_render_template(int id, int size, double* out);
+void host_compose_scene(const ea_scene_spec& s, double* canvas, double* tmpl,
+                        ea_pose* truth_pose, double* occluded_fraction);
+
+}  // namespace eab

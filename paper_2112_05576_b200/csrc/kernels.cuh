@@ -1,0 +1,182 @@
+// kernels.cuh -- launcher declarations and the exact fp64 scoring primitives
+// shared by the device kernels.
+#pragma once
+
+#include <math.h>
+
+#include "common.cuh"
+
+namespace eab {
+
+constexpr int kHistBins = 4096;           // screening-score histogram, [-1,1] in 2^-11 bins
+constexpr double kCoordGuard = 1e9;       // similarity.cpp:28
+
+// Geometry of the padded, row-skewed screening plane.
+struct PlaneGeom {
+    int W = 0, H = 0;   // unpadded field dims
+    int PW = 0;         // row pitch in float2 (>= W + 2)
+    int shift = 4;      // row skew: element (xp, yp) at yp*PW + (yp >> shift) + xp
+    size_t elems = 0;   // float2 count of the whole plane (rounded to 2 for 16 B copies)
+};
+
+inline PlaneGeom plane_geom(int W, int H, int shift) {
+    PlaneGeom g;
+    g.W = W;
+    g.H = H;
+    g.PW = W + 2;
+    g.shift = shift;
+    size_t e = (size_t)(H + 2) * g.PW + (size_t)((H + 1) >> shift) + 1;
+    g.elems = (e + 1) & ~(size_t)1;
+    return g;
+}
+
+// Control block shared by the top-level search kernels (one per context).
+struct SearchCtrl {
+    unsigned long long work_counter;  // dynamic work distribution of the screen kernel
+    unsigned long long cand_count;    // poses admitted by the band threshold
+    unsigned long long needed;        // histogram upper bound of cand_count
+    int ring_bad;                     // field border ring has mag >= eps somewhere
+    int flags;                        // rounding-ambiguous (theta, point) pairs
+    float thr;                        // band threshold on the fp32 screen score
+    int n_out;                        // entries written to the top-k output
+};
+
+// ---- exact fp64 primitives (reference op order) ------------------------------
+
+// vote_at + vote_span  similarity.cpp:30-52, kernels_scalar.cpp:39-56
+__device__ __forceinline__ double vote_exact(const double* __restrict__ gx,
+                                             const double* __restrict__ gy,
+                                             const double* __restrict__ mag, int W, int H,
+                                             int cx, int cy, int R, double dx, double dy,
+                                             double eps, bool absolute) {
+    const int x0 = cx - R < 0 ? 0 : cx - R;
+    const int x1 = cx + R >= W ? W - 1 : cx + R;
+    const int y0 = cy - R < 0 ? 0 : cy - R;
+    const int y1 = cy + R >= H ? H - 1 : cy + R;
+    if (x0 > x1 || y0 > y1) return 0.0;
+    double best = -INFINITY;
+    for (int y = y0; y <= y1; ++y) {
+        const size_t row = (size_t)y * W;
+        for (int x = x0; x <= x1; ++x) {
+            const double m = __ldg(mag + row + x);
+            double cand = 0.0;
+            if (m >= eps) {
+                cand = __ddiv_rn(__dadd_rn(__dmul_rn(dx, __ldg(gx + row + x)),
+                                           __dmul_rn(dy, __ldg(gy + row + x))),
+                                 m);
+            }
+            if (absolute) cand = fabs(cand);
+            if (cand > best) best = cand;
+        }
+    }
+    return best;
+}
+
+// One model point of score_rotated (similarity.cpp:102-116): projection,
+// guard, half-up rounding, bounds test, window vote.  Returns the vote and
+// sets *inb when the rounded centre is inside the field.
+__device__ __forceinline__ double point_term_exact(double rpx, double rpy, double rdx,
+                                                   double rdy, double ux, double uy,
+                                                   const double* gx, const double* gy,
+                                                   const double* mag, int W, int H, int R,
+                                                   double eps, bool absolute, int* inb) {
+    const double px = __dadd_rn(rpx, ux);
+    const double py = __dadd_rn(rpy, uy);
+    *inb = 0;
+    if (px > -kCoordGuard && px < kCoordGuard && py > -kCoordGuard && py < kCoordGuard) {
+        const int cx = (int)floor(__dadd_rn(px, 0.5));
+        const int cy = (int)floor(__dadd_rn(py, 0.5));
+        if (cx >= 0 && cx < W && cy >= 0 && cy < H) {
+            *inb = 1;
+            return vote_exact(gx, gy, mag, W, H, cx, cy, R, rdx, rdy, eps, absolute);
+        }
+    }
+    return 0.0;
+}
+
+// pose_at arithmetic (pose.h:84-91): base + (double)i * step, no contraction.
+__device__ __forceinline__ double lattice(double base, unsigned long long i, double step) {
+    return __dadd_rn(base, __dmul_rn((double)i, step));
+}
+
+// ---- launchers ---------------------------------------------------------------
+void launch_downsample(ea_ctx* ctx, const double* in, int w, int h, double* out);
+void launch_sobel(ea_ctx* ctx, const double* img, int w, int h, double* gx, double* gy,
+                  double* mag);
+void launch_plane(ea_ctx* ctx, const ea_field* f, double eps, const PlaneGeom& g,
+                  float2* plane, int* ring_bad);
+
+// rotate_model for many thetas: rot_exact = px|py|dx|dy (each nth*n doubles),
+// rot_screen = {ox, oy, dxf, dyf} per (theta, point) for the lattice kernel.
+void launch_rotate(ea_ctx* ctx, const double* pts_soa, int n, const double* cs, int nth,
+                   double* rot_exact, int4* rot_screen, int* flags);
+
+struct ScreenArgs {
+    const float2* plane;
+    PlaneGeom geom;
+    const int4* rot_screen;     // [theta - it_begin][point]
+    const double* rot_exact;    // px | py | dx | dy, rows theta - it_begin
+    size_t rot_stride;          // it_count * n (offset of py inside rot_exact)
+    int n;                      // model points
+    unsigned long long it_begin, it_count;
+    unsigned long long nx, ny;
+    // integer lattice (fast path)
+    int ix0, iy0;
+    // general grid
+    double x0, dx, y0, dy;
+    int R;
+    int ignore;
+    float K;          // fixed-point fold constant 3*2^e
+    unsigned B3;      // bits of K
+    float scale;      // 2^(e-22) / n
+    float* map;       // (it - it_begin) * nx * ny + iy * nx + ix
+    unsigned* hist;   // kHistBins
+    SearchCtrl* ctrl;
+};
+
+// Returns true if the smem lattice kernel handled the launch.
+bool launch_screen_fast(ea_ctx* ctx, const ScreenArgs& a);
+void launch_screen_general(ea_ctx* ctx, const ScreenArgs& a);
+
+// delta is widened on the device by 2*ctrl->flags/flag_n when flag_n > 0.
+void launch_threshold(ea_ctx* ctx, const unsigned* hist, int k, double delta, int flag_n,
+                      SearchCtrl* ctrl);
+void launch_point_vote(ea_ctx* ctx, const ea_field* f, int cx, int cy, int R, double dx,
+                       double dy, double eps, bool absolute, double* out);
+void launch_compact(ea_ctx* ctx, const float* map, unsigned long long count,
+                    SearchCtrl* ctrl, unsigned* cand, unsigned long long cap);
+
+struct ExactArgs {
+    const double* gx;
+    const double* gy;
+    const double* mag;
+    int W, H, R, ignore;
+    double eps;
+    const double* rot_exact;  // px|py|dx|dy, rows theta - it_begin, stride rot_stride
+    size_t rot_stride;
+    int n;
+    unsigned long long nx, ny, it_begin;
+    double x0, dx, y0, dy;
+};
+// Exact fp64 scores of candidate poses (index relative to it_begin * plane).
+void launch_rescore(ea_ctx* ctx, const ExactArgs& a, const unsigned* cand,
+                    const SearchCtrl* ctrl, unsigned long long cap, double* score);
+// Top k of the candidates by `better` (search.cpp:36-41) -> out_score/out_index
+// (global grid index).
+void launch_select(ea_ctx* ctx, const unsigned* cand, const double* score,
+                   SearchCtrl* ctrl, unsigned long long cap, int k,
+                   unsigned long long index_base, double* out_score,
+                   unsigned long long* out_index);
+// Dense exact map (score_map search.cpp:169-202).
+void launch_exact_map(ea_ctx* ctx, const ExactArgs& a, unsigned long long total, double* out);
+
+// Refinement: exact scores of an explicit pose list (ux, uy, rot slot).
+void launch_refine_score(ea_ctx* ctx, const ExactArgs& a, const double* poses /*ux,uy*/,
+                         const int* slot, int count, double* score, int* n_inb);
+// Stable sort by score desc + exact-duplicate removal + keep topk
+// (search.cpp:323-346).  entries: ux, uy, theta, parent; out beam rows.
+void launch_beam_select(ea_ctx* ctx, const double* poses3, const double* score,
+                        const int* parent, int count, int topk, double* beam_out,
+                        int* beam_parent, int* beam_count);
+
+}  // namespace eab

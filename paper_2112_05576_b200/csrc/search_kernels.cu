@@ -1,0 +1,746 @@
+// search_kernels.cu -- top-level exhaustive (x, y, theta) pose search and the
+// per-level refinement, as sm_100a kernels.
+//
+// Pipeline of one top-level search (reference: run_search search.cpp:95-140,
+// scan_range 72-93, score_rotated similarity.cpp:90-119):
+//
+//  1. rotate_kernel      rotate_model (similarity.cpp:68-88) for every theta of
+//                        the grid, exact fp64, plus an fp32 screening table.
+//  2. screen_*_kernel    fp32 screening score S_f of EVERY pose, written as a
+//                        map + a 4096-bin histogram.  Votes are max-reduced in
+//                        a fixed-point form (v + 3*2^e, summed as IEEE bit
+//                        patterns), so the sum is exact and order-free and
+//                        |S_f - S| <= delta for the reference fp64 score S.
+//  3. threshold_kernel   k-th largest S_f bin  ->  band threshold T - 2*delta.
+//  4. compact_kernel     candidates {S_f >= threshold}.
+//  5. rescore_kernel     exact fp64 score of each candidate, reference order.
+//  6. select_kernel      top k by `better` (score desc, index asc).
+//
+// Why this is exact: if |S_f - S| <= delta for every pose and T is at most
+// the k-th largest S_f, every pose of the true top k has S_f >= T - 2*delta,
+// so the exact pass sees all of them (and every pose tied with the k-th);
+// selecting by `better` over exact scores reproduces search_topk bit for bit.
+#include <cub/block/block_scan.cuh>
+
+#include "kernels.cuh"
+
+namespace eab {
+
+// ---- 1. rotation tables ------------------------------------------------------
+
+// floor(p + 0.5) for the lattice kernel: exact for every integer shift u with
+// |p + u| < 2^21 unless frac(p) lies within 2^-28 of 0.5 (then the two
+// roundings of (p + u) + 0.5 could cross an integer) -- such pairs are
+// counted and widen the screening bound instead.
+__device__ __forceinline__ int lattice_offset(double p, bool* amb) {
+    if (!(p > -1048576.0 && p < 1048576.0)) {
+        *amb = true;
+        return 0;
+    }
+    const double fl = floor(p);
+    const double fr = __dsub_rn(p, fl);  // exact
+    const double d = fabs(__dsub_rn(fr, 0.5));
+    if (d != 0.0 && d < 3.725290298461914e-09) *amb = true;  // 2^-28
+    return (int)floor(__dadd_rn(p, 0.5));
+}
+
+__global__ void rotate_kernel(const double* __restrict__ pts, int n,
+                              const double* __restrict__ cs, int nth,
+                              double* __restrict__ rot, int4* __restrict__ scr,
+                              int* __restrict__ flags) {
+    const size_t total = (size_t)nth * n;
+    const size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= total) return;
+    const int th = (int)(t / n), i = (int)(t % n);
+    const double c = cs[2 * th], s = cs[2 * th + 1];
+    const double x = pts[i], y = pts[n + i], dx = pts[2 * n + i], dy = pts[3 * n + i];
+    // similarity.cpp:79-86
+    const double px = __dsub_rn(__dmul_rn(c, x), __dmul_rn(s, y));
+    const double py = __dadd_rn(__dmul_rn(s, x), __dmul_rn(c, y));
+    const double rx = __dsub_rn(__dmul_rn(c, dx), __dmul_rn(s, dy));
+    const double ry = __dadd_rn(__dmul_rn(s, dx), __dmul_rn(c, dy));
+    const double norm = __dsqrt_rn(__dadd_rn(__dmul_rn(rx, rx), __dmul_rn(ry, ry)));
+    const double ndx = __ddiv_rn(rx, norm), ndy = __ddiv_rn(ry, norm);
+    rot[t] = px;
+    rot[total + t] = py;
+    rot[2 * total + t] = ndx;
+    rot[3 * total + t] = ndy;
+    if (scr) {
+        bool amb = false;
+        const int ox = lattice_offset(px, &amb);
+        const int oy = lattice_offset(py, &amb);
+        scr[t] = make_int4(ox, oy, __float_as_int((float)ndx), __float_as_int((float)ndy));
+        if (amb) atomicAdd(flags, 1);
+    }
+}
+
+void launch_rotate(ea_ctx* ctx, const double* pts_soa, int n, const double* cs, int nth,
+                   double* rot_exact, int4* rot_screen, int* flags) {
+    const size_t total = (size_t)nth * n;
+    if (total == 0) return;
+    rotate_kernel<<<(unsigned)((total + 255) / 256), 256, 0, ctx->stream>>>(
+        pts_soa, n, cs, nth, rot_exact, rot_screen, flags);
+    check_launch("rotate_kernel");
+    count_launch(ctx);
+}
+
+// ---- 2. screening ------------------------------------------------------------
+
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+    float r;
+    asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+    return r;
+}
+
+template <int K>
+__device__ __forceinline__ float max_run(const float* v) {
+    if constexpr (K == 1) {
+        return v[0];
+    } else if constexpr (K == 3) {
+        return fmax3(v[0], v[1], v[2]);
+    } else if constexpr (K == 5) {
+        return fmax3(fmax3(v[0], v[1], v[2]), v[3], v[4]);
+    } else {
+        float m = v[0];
+#pragma unroll
+        for (int i = 1; i < K; ++i) m = fmaxf(m, v[i]);
+        return m;
+    }
+}
+
+__device__ __forceinline__ int hist_bin(float s) {
+    int b = __float2int_rd((s + 1.0f) * 2048.0f);
+    return b < 0 ? 0 : (b >= kHistBins ? kHistBins - 1 : b);
+}
+
+constexpr int kScreenThreads = 256;
+constexpr int kTW = 8;  // poses per lane along x
+
+// The smem lattice kernel (integer top-level lattice with unit steps).
+//
+// A CTA is persistent (one per SM) and holds the whole padded screening
+// plane of the top level in shared memory.  Work items are (theta, warp
+// tile) pairs handed out by an atomic counter.  A warp tile is 32 x 8*S
+// poses; lane (xg = lane&3, yg = lane>>2) owns an 8 x S block and keeps its
+// 8*S fixed-point score accumulators in registers.  Per model point the lane
+// walks the S + 2R plane rows its windows touch: 8 + 2R float2 loads, two FMAs
+// per candidate, a horizontal (2R+1)-max (FMNMX3) and, once 2R+1 rows are in
+// flight, the vertical max -- i.e. each plane pixel loaded serves up to
+// (2R+1)^2 window slots.  Row skew (yp >> SHIFT) plus the 8-pose lane stride
+// make the 32 lanes' addresses hit every bank pair exactly twice: LDS.64 at
+// the 2-wavefront minimum.
+template <int R, int S, int SHIFT, bool IGNORE>
+__global__ void __launch_bounds__(kScreenThreads, 1)
+    screen_fast_kernel(const ScreenArgs a, const unsigned nwx, const unsigned nwy,
+                       const unsigned long long total_items, const int vec16) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    unsigned* hist = reinterpret_cast<unsigned*>(smem);
+    float2* P = reinterpret_cast<float2*>(smem + kHistBins * sizeof(unsigned));
+    {
+        const int4* src = reinterpret_cast<const int4*>(a.plane);
+        int4* dst = reinterpret_cast<int4*>(P);
+        for (int i = threadIdx.x; i < vec16; i += blockDim.x) dst[i] = __ldg(src + i);
+        for (int i = threadIdx.x; i < kHistBins; i += blockDim.x) hist[i] = 0u;
+    }
+    __syncthreads();
+
+    constexpr int NC = kTW + 2 * R;  // columns per row
+    constexpr int NR = S + 2 * R;    // rows per point
+    const int lane = threadIdx.x & 31;
+    const int xg = lane & 3, yg = lane >> 2;
+    const int W1 = a.geom.W + 1, H1 = a.geom.H + 1, PW = a.geom.PW;
+    const float K = a.K;
+    const int B3 = (int)a.B3;
+    const unsigned long long plane_poses = a.nx * a.ny;
+
+    for (;;) {
+        unsigned long long item = 0;
+        if (lane == 0) item = atomicAdd(&a.ctrl->work_counter, 1ull);
+        item = __shfl_sync(0xffffffffu, item, 0);
+        if (item >= total_items) break;
+        const unsigned wx = (unsigned)(item % nwx);
+        const unsigned long long rest = item / nwx;
+        const unsigned wy = (unsigned)(rest % nwy);
+        const unsigned long long itr = rest / nwy;
+        const int X = (int)wx * 32 + xg * kTW;
+        const int Y = (int)wy * (8 * S) + yg * S;
+        const int4* rot = a.rot_screen + (size_t)itr * a.n;
+
+        int acc[S][kTW];
+#pragma unroll
+        for (int s = 0; s < S; ++s)
+#pragma unroll
+            for (int j = 0; j < kTW; ++j) acc[s][j] = 0;
+
+        int4 p = __ldg(rot);
+        for (int i = 0; i < a.n; ++i) {
+            const int4 pn = __ldg(rot + (i + 1 < a.n ? i + 1 : i));
+            const float dxf = __int_as_float(p.z), dyf = __int_as_float(p.w);
+            const int cb = p.x + a.ix0 + X - R + 1;  // padded column of window start
+            const int rb = p.y + a.iy0 + Y - R + 1;  // padded row of window start
+            int col[NC];
+#pragma unroll
+            for (int m = 0; m < NC; ++m) col[m] = min(max(cb + m, 0), W1);
+            // For R <= 1 the zero ring makes an off-field centre vote exactly 0;
+            // a 5-wide window can reach real pixels, so mask those centres.
+            unsigned cmask = 0xffu;
+            if constexpr (R >= 2) {
+                cmask = 0u;
+#pragma unroll
+                for (int j = 0; j < kTW; ++j) {
+                    const int cxj = cb + R - 1 + j;
+                    cmask |= (cxj >= 0 && cxj < W1 - 1) ? (1u << j) : 0u;
+                }
+            }
+            float hprev[2 * R > 0 ? 2 * R : 1][kTW];
+#pragma unroll
+            for (int r = 0; r < NR; ++r) {
+                const int yp = min(max(rb + r, 0), H1);
+                const float2* row = P + yp * PW + (yp >> SHIFT);
+                float c[NC];
+#pragma unroll
+                for (int m = 0; m < NC; ++m) {
+                    const float2 v = row[col[m]];
+                    if constexpr (IGNORE) {
+                        c[m] = fabsf(fmaf(dyf, v.y, dxf * v.x));
+                    } else {
+                        c[m] = fmaf(dyf, v.y, fmaf(dxf, v.x, K));
+                    }
+                }
+                float h[kTW];
+#pragma unroll
+                for (int j = 0; j < kTW; ++j) h[j] = max_run<2 * R + 1>(c + j);
+                if (r >= 2 * R) {
+                    const int s = r - 2 * R;
+#pragma unroll
+                    for (int j = 0; j < kTW; ++j) {
+                        float col_v[2 * R + 1];
+#pragma unroll
+                        for (int q = 0; q < 2 * R; ++q) col_v[q] = hprev[q][j];
+                        col_v[2 * R] = h[j];
+                        float v = max_run<2 * R + 1>(col_v);
+                        if constexpr (IGNORE) v = v + K;
+                        if constexpr (R >= 2) {
+                            const int cys = rb + R - 1 + s;
+                            const bool in = ((cmask >> j) & 1u) && cys >= 0 && cys < H1 - 1;
+                            v = in ? v : K;
+                        }
+                        acc[s][j] += __float_as_int(v) - B3;
+                    }
+                }
+                if constexpr (R > 0) {
+#pragma unroll
+                    for (int q = 0; q + 1 < 2 * R; ++q)
+#pragma unroll
+                        for (int j = 0; j < kTW; ++j) hprev[q][j] = hprev[q + 1][j];
+#pragma unroll
+                    for (int j = 0; j < kTW; ++j) hprev[2 * R - 1][j] = h[j];
+                }
+            }
+            p = pn;
+        }
+        float* out = a.map + (size_t)itr * plane_poses;
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            const unsigned long long iy = (unsigned long long)(Y + s);
+#pragma unroll
+            for (int j = 0; j < kTW; ++j) {
+                const unsigned long long ix = (unsigned long long)(X + j);
+                if (ix < a.nx && iy < a.ny) {
+                    const float sc = (float)acc[s][j] * a.scale;
+                    out[iy * a.nx + ix] = sc;
+                    atomicAdd(&hist[hist_bin(sc)], 1u);
+                }
+            }
+        }
+    }
+    __syncthreads();
+    for (int b = threadIdx.x; b < kHistBins; b += blockDim.x) {
+        const unsigned v = hist[b];
+        if (v) atomicAdd(&a.hist[b], v);
+    }
+}
+
+template <int R, int S, int SHIFT, bool IGNORE>
+static void run_fast(ea_ctx* ctx, const ScreenArgs& a) {
+    const unsigned nwx = (unsigned)((a.nx + 31) / 32);
+    const unsigned nwy = (unsigned)((a.ny + 8 * S - 1) / (8 * S));
+    const unsigned long long items = (unsigned long long)nwx * nwy * a.it_count;
+    const size_t plane_bytes = ((a.geom.elems * sizeof(float2)) + 15) & ~(size_t)15;
+    const size_t smem = kHistBins * sizeof(unsigned) + plane_bytes;
+    auto kern = screen_fast_kernel<R, S, SHIFT, IGNORE>;
+    EAB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    unsigned long long warps_per_cta = kScreenThreads / 32;
+    unsigned long long ctas = (items + warps_per_cta - 1) / warps_per_cta;
+    if (ctas > (unsigned long long)ctx->sm_count) ctas = ctx->sm_count;
+    if (ctas == 0) ctas = 1;
+    kern<<<(unsigned)ctas, kScreenThreads, smem, ctx->stream>>>(a, nwx, nwy, items,
+                                                                (int)(plane_bytes / 16));
+    check_launch("screen_fast_kernel");
+    count_launch(ctx);
+}
+
+size_t fast_smem_bytes(const PlaneGeom& g) {
+    return kHistBins * sizeof(unsigned) + (((g.elems * sizeof(float2)) + 15) & ~(size_t)15);
+}
+
+bool launch_screen_fast(ea_ctx* ctx, const ScreenArgs& a) {
+    if (fast_smem_bytes(a.geom) > ctx->smem_optin) return false;
+    const bool ig = a.ignore != 0;
+    const int S = a.geom.shift == 3 ? 8 : 16;
+#define EAB_FAST(RR, SS, SH)                                        \
+    if (a.R == RR && S == SS) {                                     \
+        if (ig) run_fast<RR, SS, SH, true>(ctx, a);                 \
+        else run_fast<RR, SS, SH, false>(ctx, a);                   \
+        return true;                                                \
+    }
+    EAB_FAST(1, 16, 4)
+    EAB_FAST(1, 8, 3)
+    EAB_FAST(0, 16, 4)
+    EAB_FAST(0, 8, 3)
+    EAB_FAST(2, 16, 4)
+    EAB_FAST(2, 8, 3)
+#undef EAB_FAST
+    return false;
+}
+
+// General screening kernel: any grid (non-integer or non-unit steps), any
+// neighbourhood, any field border.  One thread per pose; projections are the
+// reference's exact fp64 ones, windows are clipped exactly; the candidate and
+// fixed-point arithmetic is the same as the lattice kernel's.
+template <bool IGNORE>
+__global__ void __launch_bounds__(256)
+    screen_general_kernel(const ScreenArgs a, const unsigned long long total) {
+    __shared__ unsigned hist[kHistBins];
+    for (int i = threadIdx.x; i < kHistBins; i += blockDim.x) hist[i] = 0u;
+    __syncthreads();
+    const unsigned long long plane_poses = a.nx * a.ny;
+    const int W = a.geom.W, H = a.geom.H, PW = a.geom.PW, SH = a.geom.shift;
+    const int R = a.R;
+    const float K = a.K;
+    const int B3 = (int)a.B3;
+    for (unsigned long long t = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+         t < total; t += (unsigned long long)gridDim.x * blockDim.x) {
+        const unsigned long long itr = t / plane_poses;
+        const unsigned long long rem = t % plane_poses;
+        const unsigned long long iy = rem / a.nx, ix = rem % a.nx;
+        const double ux = lattice(a.x0, ix, a.dx);
+        const double uy = lattice(a.y0, iy, a.dy);
+        const size_t base = (size_t)itr * a.n;
+        int acc = 0;
+        for (int i = 0; i < a.n; ++i) {
+            const double px = __dadd_rn(__ldg(a.rot_exact + base + i), ux);
+            const double py = __dadd_rn(__ldg(a.rot_exact + a.rot_stride + base + i), uy);
+            if (!(px > -kCoordGuard && px < kCoordGuard && py > -kCoordGuard &&
+                  py < kCoordGuard))
+                continue;
+            const int cx = (int)floor(__dadd_rn(px, 0.5));
+            const int cy = (int)floor(__dadd_rn(py, 0.5));
+            if (cx < 0 || cx >= W || cy < 0 || cy >= H) continue;
+            const int4 q = __ldg(a.rot_screen + base + i);
+            const float dxf = __int_as_float(q.z), dyf = __int_as_float(q.w);
+            const int x0 = max(cx - R, 0), x1 = min(cx + R, W - 1);
+            const int y0 = max(cy - R, 0), y1 = min(cy + R, H - 1);
+            float best = -INFINITY;
+            for (int y = y0; y <= y1; ++y) {
+                const int yp = y + 1;
+                const float2* row = a.plane + (size_t)yp * PW + (yp >> SH) + 1;
+                for (int x = x0; x <= x1; ++x) {
+                    const float2 v = __ldg(row + x);
+                    const float c = IGNORE ? fabsf(fmaf(dyf, v.y, dxf * v.x))
+                                           : fmaf(dyf, v.y, fmaf(dxf, v.x, K));
+                    best = fmaxf(best, c);
+                }
+            }
+            if constexpr (IGNORE) best = best + K;
+            acc += __float_as_int(best) - B3;
+        }
+        const float sc = (float)acc * a.scale;
+        a.map[t] = sc;
+        atomicAdd(&hist[hist_bin(sc)], 1u);
+    }
+    __syncthreads();
+    for (int b = threadIdx.x; b < kHistBins; b += blockDim.x) {
+        const unsigned v = hist[b];
+        if (v) atomicAdd(&a.hist[b], v);
+    }
+}
+
+void launch_screen_general(ea_ctx* ctx, const ScreenArgs& a) {
+    const unsigned long long total = a.nx * a.ny * a.it_count;
+    unsigned long long blocks = (total + 255) / 256;
+    const unsigned long long cap = (unsigned long long)ctx->sm_count * 8;
+    if (blocks > cap) blocks = cap;
+    if (blocks == 0) blocks = 1;
+    if (a.ignore)
+        screen_general_kernel<true><<<(unsigned)blocks, 256, 0, ctx->stream>>>(a, total);
+    else
+        screen_general_kernel<false><<<(unsigned)blocks, 256, 0, ctx->stream>>>(a, total);
+    check_launch("screen_general_kernel");
+    count_launch(ctx);
+}
+
+// ---- 3. threshold --------------------------------------------------------------
+// Finds bin b holding the k-th largest screening score (b = bin(T_f) because
+// fewer than k scores lie strictly above T_f), sets thr = lo(b) - 2*delta -
+// 2^-20 (the slack covers fp32 rounding inside hist_bin) and an upper bound
+// of the candidate count.
+__global__ void __launch_bounds__(1024) threshold_kernel(const unsigned* __restrict__ hist,
+                                                         int k, double delta, int flag_n,
+                                                         SearchCtrl* ctrl) {
+    using Scan = cub::BlockScan<unsigned long long, 1024>;
+    __shared__ typename Scan::TempStorage tmp;
+    __shared__ unsigned long long cum[kHistBins];  // cum[q] = #scores in bins >= 4095-q
+    __shared__ int kbin;
+    const int t = threadIdx.x;
+    unsigned long long local[4], sum = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        local[j] = hist[kHistBins - 1 - (4 * t + j)];
+        sum += local[j];
+    }
+    unsigned long long excl;
+    Scan(tmp).ExclusiveSum(sum, excl);
+    if (t == 0) kbin = -1;
+    __syncthreads();
+    unsigned long long run = excl;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const unsigned long long before = run;
+        run += local[j];
+        cum[4 * t + j] = run;
+        if (before < (unsigned long long)k && run >= (unsigned long long)k)
+            kbin = kHistBins - 1 - (4 * t + j);
+    }
+    __syncthreads();
+    if (t == 0) {
+        float thr;
+        unsigned long long needed;
+        if (kbin < 0) {  // fewer than k poses: every pose is a candidate
+            thr = -INFINITY;
+            needed = cum[kHistBins - 1];
+        } else {
+            if (flag_n > 0) delta += 2.0 * (double)ctrl->flags / (double)flag_n;
+            const double lo = (double)kbin / 2048.0 - 1.0;
+            const double th = lo - 2.0 * delta - 9.5367431640625e-07;  // 2^-20
+            thr = (float)th;
+            if ((double)thr > th) thr = nextafterf(thr, -INFINITY);
+            const int tb = hist_bin(thr);
+            needed = cum[kHistBins - 1 - tb];
+        }
+        ctrl->thr = thr;
+        ctrl->needed = needed;
+    }
+}
+
+void launch_threshold(ea_ctx* ctx, const unsigned* hist, int k, double delta, int flag_n,
+                      SearchCtrl* ctrl) {
+    threshold_kernel<<<1, 1024, 0, ctx->stream>>>(hist, k, delta, flag_n, ctrl);
+    check_launch("threshold_kernel");
+    count_launch(ctx);
+}
+
+// ---- 4. compaction -----------------------------------------------------------
+__global__ void __launch_bounds__(256) compact_kernel(const float* __restrict__ map,
+                                                      unsigned long long count,
+                                                      SearchCtrl* ctrl,
+                                                      unsigned* __restrict__ cand,
+                                                      unsigned long long cap) {
+    const float thr = ctrl->thr;
+    const int lane = threadIdx.x & 31;
+    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+    for (unsigned long long i0 = (unsigned long long)blockIdx.x * blockDim.x + (threadIdx.x & ~31);
+         i0 < count; i0 += stride) {
+        const unsigned long long i = i0 + lane;
+        const bool pred = i < count && __ldg(map + i) >= thr;
+        const unsigned mask = __ballot_sync(0xffffffffu, pred);
+        if (mask) {
+            const int leader = __ffs(mask) - 1;
+            unsigned long long base = 0;
+            if (lane == leader) base = atomicAdd(&ctrl->cand_count, (unsigned long long)__popc(mask));
+            base = __shfl_sync(0xffffffffu, base, leader);
+            if (pred) {
+                const unsigned long long slot = base + __popc(mask & ((1u << lane) - 1u));
+                if (slot < cap) cand[slot] = (unsigned)i;
+            }
+        }
+    }
+}
+
+void launch_compact(ea_ctx* ctx, const float* map, unsigned long long count, SearchCtrl* ctrl,
+                    unsigned* cand, unsigned long long cap) {
+    unsigned long long blocks = (count + 255) / 256;
+    const unsigned long long maxb = (unsigned long long)ctx->sm_count * 8;
+    if (blocks > maxb) blocks = maxb;
+    if (blocks == 0) blocks = 1;
+    compact_kernel<<<(unsigned)blocks, 256, 0, ctx->stream>>>(map, count, ctrl, cand, cap);
+    check_launch("compact_kernel");
+    count_launch(ctx);
+}
+
+// ---- 5. exact rescoring ------------------------------------------------------
+// One warp per pose: lanes evaluate points lane, lane+32, ...; the votes are
+// then added in model-point order (similarity.cpp:109-118) by a shuffle walk,
+// so the fp64 sum is the reference's to the last bit.
+__device__ __forceinline__ double warp_pose_score(const ExactArgs& a, size_t base, double ux,
+                                                  double uy, int lane, int* n_inb) {
+    const size_t S = a.rot_stride;
+    double sum = 0.0;
+    int inb_total = 0;
+    for (int q = 0; q < a.n; q += 32) {
+        const int i = q + lane;
+        double v = 0.0;
+        int inb = 0;
+        if (i < a.n) {
+            v = point_term_exact(__ldg(a.rot_exact + base + i), __ldg(a.rot_exact + S + base + i),
+                                 __ldg(a.rot_exact + 2 * S + base + i),
+                                 __ldg(a.rot_exact + 3 * S + base + i), ux, uy, a.gx, a.gy,
+                                 a.mag, a.W, a.H, a.R, a.eps, a.ignore != 0, &inb);
+        }
+        inb_total += __popc(__ballot_sync(0xffffffffu, inb));
+        const int lim = a.n - q < 32 ? a.n - q : 32;
+        for (int l = 0; l < lim; ++l) sum = __dadd_rn(sum, __shfl_sync(0xffffffffu, v, l));
+    }
+    if (n_inb) *n_inb = inb_total;
+    return __ddiv_rn(sum, (double)a.n);
+}
+
+__global__ void __launch_bounds__(256) rescore_kernel(const ExactArgs a,
+                                                      const unsigned* __restrict__ cand,
+                                                      const SearchCtrl* ctrl,
+                                                      unsigned long long cap,
+                                                      double* __restrict__ score) {
+    unsigned long long nc = ctrl->cand_count;
+    if (nc > cap) nc = cap;
+    const int lane = threadIdx.x & 31;
+    const unsigned long long warp = ((unsigned long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const unsigned long long nwarps = ((unsigned long long)gridDim.x * blockDim.x) >> 5;
+    const unsigned long long plane = a.nx * a.ny;
+    for (unsigned long long c = warp; c < nc; c += nwarps) {
+        const unsigned long long rel = cand[c];
+        const unsigned long long itl = rel / plane;  // theta row inside the slab
+        const unsigned long long rem = rel % plane;
+        const double ux = lattice(a.x0, rem % a.nx, a.dx);
+        const double uy = lattice(a.y0, rem / a.nx, a.dy);
+        const double s = warp_pose_score(a, (size_t)itl * a.n, ux, uy, lane, nullptr);
+        if (lane == 0) score[c] = s;
+    }
+}
+
+void launch_rescore(ea_ctx* ctx, const ExactArgs& a, const unsigned* cand,
+                    const SearchCtrl* ctrl, unsigned long long cap, double* score) {
+    unsigned long long warps = cap;
+    unsigned long long blocks = (warps * 32 + 255) / 256;
+    const unsigned long long maxb = (unsigned long long)ctx->sm_count * 16;
+    if (blocks > maxb) blocks = maxb;
+    if (blocks == 0) blocks = 1;
+    rescore_kernel<<<(unsigned)blocks, 256, 0, ctx->stream>>>(a, cand, ctrl, cap, score);
+    check_launch("rescore_kernel");
+    count_launch(ctx);
+}
+
+// ---- 6. top-k by `better` --------------------------------------------------------
+struct Best {
+    double s;
+    unsigned long long i;
+    int ok;
+};
+
+__device__ __forceinline__ bool better(double sa, unsigned long long ia, double sb,
+                                       unsigned long long ib) {  // search.cpp:36-41
+    if (sa != sb) return sa > sb;
+    return ia < ib;
+}
+
+__device__ __forceinline__ Best pick(Best x, Best y) {
+    if (!x.ok) return y;
+    if (!y.ok) return x;
+    return better(x.s, x.i, y.s, y.i) ? x : y;
+}
+
+__global__ void __launch_bounds__(1024) select_kernel(const unsigned* __restrict__ cand,
+                                                      const double* __restrict__ score,
+                                                      SearchCtrl* ctrl, unsigned long long cap,
+                                                      int k, unsigned long long index_base,
+                                                      double* out_score,
+                                                      unsigned long long* out_index) {
+    __shared__ Best warp_best[32];
+    __shared__ Best prev;
+    unsigned long long nc = ctrl->cand_count;
+    if (nc > cap) nc = cap;
+    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+    int r = 0;
+    for (; r < k; ++r) {
+        Best b{0.0, 0ull, 0};
+        for (unsigned long long c = t; c < nc; c += blockDim.x) {
+            const double s = score[c];
+            const unsigned long long idx = index_base + cand[c];
+            if (r > 0 && !better(prev.s, prev.i, s, idx)) continue;
+            b = pick(b, Best{s, idx, 1});
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            Best o;
+            o.s = __shfl_down_sync(0xffffffffu, b.s, off);
+            o.i = __shfl_down_sync(0xffffffffu, b.i, off);
+            o.ok = __shfl_down_sync(0xffffffffu, b.ok, off);
+            b = pick(b, o);
+        }
+        if (lane == 0) warp_best[w] = b;
+        __syncthreads();
+        if (t == 0) {
+            Best f{0.0, 0ull, 0};
+            for (int q = 0; q < (int)(blockDim.x >> 5); ++q) f = pick(f, warp_best[q]);
+            prev = f;
+            if (f.ok) {
+                out_score[r] = f.s;
+                out_index[r] = f.i;
+            }
+        }
+        __syncthreads();
+        if (!prev.ok) break;
+    }
+    if (t == 0) ctrl->n_out = r;
+}
+
+void launch_select(ea_ctx* ctx, const unsigned* cand, const double* score, SearchCtrl* ctrl,
+                   unsigned long long cap, int k, unsigned long long index_base,
+                   double* out_score, unsigned long long* out_index) {
+    select_kernel<<<1, 1024, 0, ctx->stream>>>(cand, score, ctrl, cap, k, index_base, out_score,
+                                               out_index);
+    check_launch("select_kernel");
+    count_launch(ctx);
+}
+
+// ---- dense exact map (score_map) -------------------------------------------------
+__global__ void __launch_bounds__(256) exact_map_kernel(const ExactArgs a,
+                                                        unsigned long long total,
+                                                        double* __restrict__ out) {
+    const int lane = threadIdx.x & 31;
+    const unsigned long long warp = ((unsigned long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const unsigned long long nwarps = ((unsigned long long)gridDim.x * blockDim.x) >> 5;
+    const unsigned long long plane = a.nx * a.ny;
+    for (unsigned long long t = warp; t < total; t += nwarps) {
+        const unsigned long long it = t / plane;
+        const unsigned long long rem = t % plane;
+        const double ux = lattice(a.x0, rem % a.nx, a.dx);
+        const double uy = lattice(a.y0, rem / a.nx, a.dy);
+        const double s = warp_pose_score(a, (size_t)it * a.n, ux, uy, lane, nullptr);
+        if (lane == 0) out[t] = s;
+    }
+}
+
+void launch_exact_map(ea_ctx* ctx, const ExactArgs& a, unsigned long long total, double* out) {
+    unsigned long long blocks = (total * 32 + 255) / 256;
+    const unsigned long long maxb = (unsigned long long)ctx->sm_count * 16;
+    if (blocks > maxb) blocks = maxb;
+    if (blocks == 0) blocks = 1;
+    exact_map_kernel<<<(unsigned)blocks, 256, 0, ctx->stream>>>(a, total, out);
+    check_launch("exact_map_kernel");
+    count_launch(ctx);
+}
+
+// ---- point_vote (similarity.cpp:58-64) ---------------------------------------------
+__global__ void point_vote_kernel(const double* gx, const double* gy, const double* mag, int W,
+                                  int H, int cx, int cy, int R, double dx, double dy, double eps,
+                                  int absolute, double* out) {
+    *out = vote_exact(gx, gy, mag, W, H, cx, cy, R, dx, dy, eps, absolute != 0);
+}
+
+void launch_point_vote(ea_ctx* ctx, const ea_field* f, int cx, int cy, int R, double dx,
+                       double dy, double eps, bool absolute, double* out) {
+    point_vote_kernel<<<1, 1, 0, ctx->stream>>>(f->gx(), f->gy(), f->mag(), f->width, f->height,
+                                                cx, cy, R, dx, dy, eps, absolute ? 1 : 0, out);
+    check_launch("point_vote_kernel");
+    count_launch(ctx);
+}
+
+// ---- refinement --------------------------------------------------------------------
+__global__ void __launch_bounds__(256) refine_score_kernel(const ExactArgs a,
+                                                           const double* __restrict__ poses,
+                                                           const int* __restrict__ slot,
+                                                           int count,
+                                                           double* __restrict__ score,
+                                                           int* __restrict__ n_inb) {
+    const int lane = threadIdx.x & 31;
+    const int warp = (int)(((unsigned long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+    const int nwarps = (int)(((unsigned long long)gridDim.x * blockDim.x) >> 5);
+    for (int e = warp; e < count; e += nwarps) {
+        int inb = 0;
+        const double s = warp_pose_score(a, (size_t)slot[e] * a.n, poses[2 * e], poses[2 * e + 1],
+                                         lane, &inb);
+        if (lane == 0) {
+            score[e] = s;
+            if (n_inb) n_inb[e] = inb;
+        }
+    }
+}
+
+void launch_refine_score(ea_ctx* ctx, const ExactArgs& a, const double* poses, const int* slot,
+                         int count, double* score, int* n_inb) {
+    if (count <= 0) return;
+    unsigned long long blocks = ((unsigned long long)count * 32 + 255) / 256;
+    const unsigned long long maxb = (unsigned long long)ctx->sm_count * 16;
+    if (blocks > maxb) blocks = maxb;
+    refine_score_kernel<<<(unsigned)blocks, 256, 0, ctx->stream>>>(a, poses, slot, count, score,
+                                                                  n_inb);
+    check_launch("refine_score_kernel");
+    count_launch(ctx);
+}
+
+// std::stable_sort(score desc) + exact-duplicate removal + keep topk
+// (search.cpp:323-346).  Stable rank = #{j : s_j > s_e or (s_j == s_e and j < e)}.
+__global__ void __launch_bounds__(1024) beam_select_kernel(const double* __restrict__ poses3,
+                                                           const double* __restrict__ score,
+                                                           const int* __restrict__ parent,
+                                                           int count, int topk,
+                                                           int* __restrict__ order,
+                                                           double* __restrict__ beam_out,
+                                                           int* __restrict__ beam_parent,
+                                                           int* __restrict__ beam_count) {
+    for (int e = threadIdx.x; e < count; e += blockDim.x) {
+        const double s = score[e];
+        int r = 0;
+        for (int j = 0; j < count; ++j) {
+            const double sj = score[j];
+            r += (sj > s) || (sj == s && j < e);
+        }
+        order[r] = e;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int kept = 0;
+        for (int r = 0; r < count && kept < topk; ++r) {
+            const int e = order[r];
+            const double ux = poses3[3 * e], uy = poses3[3 * e + 1], th = poses3[3 * e + 2];
+            bool dup = false;
+            for (int q = 0; q < kept; ++q) {
+                if (beam_out[4 * q] == ux && beam_out[4 * q + 1] == uy && beam_out[4 * q + 2] == th) {
+                    dup = true;
+                    break;
+                }
+            }
+            if (!dup) {
+                beam_out[4 * kept] = ux;
+                beam_out[4 * kept + 1] = uy;
+                beam_out[4 * kept + 2] = th;
+                beam_out[4 * kept + 3] = score[e];
+                beam_parent[kept] = parent[e];
+                ++kept;
+            }
+        }
+        *beam_count = kept;
+    }
+}
+
+void launch_beam_select(ea_ctx* ctx, const double* poses3, const double* score,
+                        const int* parent, int count, int topk, double* beam_out,
+                        int* beam_parent, int* beam_count) {
+    int* order = reinterpret_cast<int*>(ctx->work.ensure(sizeof(int) * (size_t)(count + 1)));
+    beam_select_kernel<<<1, 1024, 0, ctx->stream>>>(poses3, score, parent, count, topk, order,
+                                                    beam_out, beam_parent, beam_count);
+    check_launch("beam_select_kernel");
+    count_launch(ctx);
+}
+
+}  // namespace eab

@@ -1,0 +1,369 @@
+"""CUDA path vs the CPU oracle (oracle/edgealign_oracle.c, pinned to the
+reference in tests/test_oracle_ref.py): bit-exact poses, indices and scores.
+
+Cases follow the reference's own tests (proj/tests/test_search.cpp,
+test_similarity.cpp, test_edge_model.cpp, test_image.cpp) plus the lattice /
+general screening paths, theta slabs and the BASELINE configs' geometry.
+"""
+import math
+
+import numpy as np
+import pytest
+
+from paper_2112_05576_b200 import abi
+
+pytestmark = pytest.mark.gpu
+
+D = abi.deg_to_rad
+
+
+def rand_image(rng, w, h, real=False):
+    if real:
+        return rng.uniform(-40.0, 300.0, size=(h, w))
+    return rng.integers(0, 256, size=(h, w)).astype(np.float64)
+
+
+def rand_model(oracle, rng, size):
+    f = oracle.compute_gradients(rand_image(rng, size, size))
+    return oracle.extract_edge_model(f, (0.0, 0.0), 0)
+
+
+def keys(lst):
+    return [(s.score, int(s.grid_index), s.pose.astuple()) for s in lst]
+
+
+# ---- field side ----------------------------------------------------------------------
+@pytest.mark.parametrize("w,h", [(3, 3), (4, 5), (17, 9), (64, 48), (161, 123), (640, 480)])
+def test_gradients_bit_exact(ea, oracle, w, h):
+    rng = np.random.default_rng(w * 1000 + h)
+    for real in (False, True):
+        img = rand_image(rng, w, h, real)
+        got = ea.compute_gradients(img)
+        want = oracle.compute_gradients(img)
+        for a, b in zip(got, want):
+            assert np.array_equal(a, b)
+
+
+def test_gradient_kats(ea):
+    # test_edge_model.cpp:50-92: constant -> 0; vertical step -> gx = 32
+    f = ea.compute_gradients(np.full((7, 9), 123.25))
+    assert not f.gx.any() and not f.gy.any() and not f.mag.any()
+    img = np.zeros((7, 9))
+    img[:, 4:] = 8.0
+    f = ea.compute_gradients(img)
+    assert (f.gx[1:6, 3] == 32).all() and (f.gx[1:6, 4] == 32).all()
+    assert (f.gy[1:6, 3] == 0).all() and (f.mag[1:6, 3] == 32).all()
+    with pytest.raises(ea.SizeError):
+        ea.compute_gradients(np.zeros((8, 2)))
+
+
+@pytest.mark.parametrize("w,h,levels", [(2, 2, 1), (5, 5, 1), (812, 617, 3), (1280, 1024, 4),
+                                        (2592, 1944, 5), (33, 17, 2)])
+def test_pyramid_bit_exact(ea, oracle, w, h, levels):
+    rng = np.random.default_rng(7)
+    img = rand_image(rng, w, h, real=True)
+    if levels <= oracle.max_pyramid_levels(w, h):
+        got = ea.build_pyramid(img, levels)
+        want = oracle.build_pyramid(img, levels)
+        assert [g.shape for g in got] == [x.shape for x in want]
+        for a, b in zip(got, want):
+            assert np.array_equal(a, b)
+    assert np.array_equal(ea.downsample(img), oracle.downsample(img))
+
+
+def test_pyramid_errors(ea):
+    with pytest.raises(ea.SizeError, match="maximum feasible level count is 2"):
+        ea.build_pyramid(np.zeros((16, 16)), 4)
+    with pytest.raises(ea.SizeError):
+        ea.downsample(np.zeros((5, 1)))
+    assert ea.max_pyramid_levels(16, 16) == 2
+
+
+# ---- similarity ---------------------------------------------------------------------
+def test_point_vote_kats(ea):
+    # test_similarity.cpp:45-81
+    def field(w, h, sets):
+        gx, gy = np.zeros((h, w)), np.zeros((h, w))
+        for (x, y, a, b) in sets:
+            gx[y, x], gy[y, x] = a, b
+        return (gx, gy, np.sqrt(gx * gx + gy * gy))
+
+    P = ea.ScoreParams
+    assert ea.point_vote(1, 0, field(7, 7, [(3, 3, 5, 0)]), 3, 3, P(3)) == pytest.approx(1.0, abs=1e-12)
+    assert ea.point_vote(1, 0, field(7, 7, []), 3, 3, P(3)) == 0.0
+    f = field(7, 7, [(3, 3, -5, 0), (4, 3, 1e-4, 0)])
+    assert ea.point_vote(1, 0, f, 3, 3, P(3)) == pytest.approx(1.0, abs=1e-12)
+    assert ea.point_vote(1, 0, f, 3, 3, P(1)) == pytest.approx(-1.0, abs=1e-12)
+    z = field(5, 5, [])
+    assert ea.point_vote(0, 1, z, 40, 40, P(3)) == 0.0
+    assert ea.point_vote(0, 1, z, -9, 2, P(3)) == 0.0
+    assert ea.point_vote(1, 0, field(5, 5, [(2, 2, -7, 0)]), 2, 2,
+                         P(1, abi.POLARITY_IGNORE)) == pytest.approx(1.0)
+    with pytest.raises(ea.InvalidArgument, match="neighborhood must be odd"):
+        ea.point_vote(1, 0, z, 2, 2, P(2))
+    with pytest.raises(ea.InvalidArgument, match="eps_mag must be positive"):
+        ea.point_vote(1, 0, z, 2, 2, P(3, 0, 0.0))
+
+
+def test_rotate_model_bit_exact(ea, oracle):
+    rng = np.random.default_rng(5)
+    m = rand_model(oracle, rng, 14)
+    for theta in [0.0, 0.3, -2.0, D(30), D(359.75), 7.1]:
+        got = ea.rotate_model(m, theta)
+        want = oracle.rotate_model(m.points, theta)
+        for a, b in zip(got, want):
+            assert np.array_equal(a, b)
+
+
+def test_pose_score_bit_exact(ea, oracle):
+    rng = np.random.default_rng(37)
+    m = oracle.prepare_model(oracle.render_template("cross", 32))
+    f = oracle.compute_gradients(rand_image(rng, 48, 48))
+    for trial in range(60):
+        pose = (rng.uniform(-10, 58), rng.uniform(-10, 58), rng.uniform(-3.2, 3.2))
+        for params in (ea.ScoreParams(1), ea.ScoreParams(3), ea.ScoreParams(5),
+                       ea.ScoreParams(3, abi.POLARITY_IGNORE)):
+            assert ea.pose_score(m, pose, f, params) == oracle.pose_score(m.points, pose, f, params)
+    v, n = ea.pose_score(m, (500, 500, 0.3), f, ea.ScoreParams(3))
+    assert v == 0.0 and n == 0
+
+
+# ---- top-level search ------------------------------------------------------------------
+SEARCH_CASES = [
+    # (model size, field w, h, grid, nb, polarity)  -- test_search.cpp:55-98 shapes
+    (8, 32, 32, (4, 27, 1, 4, 27, 1, 0.0, D(30), D(15)), 3, 0),
+    (10, 32, 32, (4, 27, 1, 4, 27, 1, 0.0, D(30), D(15)), 1, 0),
+    (12, 40, 40, (0, 39, 1, 0, 39, 1, 0.0, D(20), D(10)), 3, 0),
+    (14, 32, 32, (4, 27, 1, 4, 27, 1, 0.0, D(30), D(15)), 5, 0),
+    (12, 40, 40, (0, 39, 1, 0, 39, 1, 0.0, D(20), D(10)), 3, 1),
+    (12, 40, 40, (-6, 45, 1, -7, 44, 1, 0.0, D(359), D(1)), 3, 0),   # off-image overhang
+    (10, 30, 30, (5, 24, 2, 5, 24, 3, 0.0, D(10), D(5)), 3, 0),      # integer, non-unit step
+    (10, 30, 30, (0.5, 24.5, 1, 2.25, 20, 0.75, 0.1, 0.9, 0.2), 3, 0),  # general grid
+    (20, 64, 48, (0, 63, 1, 0, 47, 1, 0.0, D(355), D(5)), 3, 0),
+]
+
+
+@pytest.mark.parametrize("case", range(len(SEARCH_CASES)))
+def test_search_topk_bit_exact(ea, oracle, case):
+    size, w, h, g, nb, pol = SEARCH_CASES[case]
+    rng = np.random.default_rng(100 + case)
+    m = rand_model(oracle, rng, size)
+    f = oracle.compute_gradients(rand_image(rng, w, h))
+    grid = ea.PoseGrid(*g)
+    params = ea.ScoreParams(nb, pol)
+    for k in (1, 5, 17):
+        got = ea.search_topk(m, f, grid, params, k=k)
+        want = oracle.search_topk(m.points, f, grid, params, k)
+        assert keys(got) == keys(want)
+    det = ea.exhaustive_search(m, f, grid, params)
+    ref = oracle.exhaustive_search(m.points, f, grid, params)
+    assert (det.score, det.grid_index) == (ref.score, ref.grid_index)
+
+
+def test_search_uploaded_field_with_border(ea, oracle):
+    """A field whose outer ring votes (not from compute_gradients) must take
+    the exactly-clipped general path."""
+    rng = np.random.default_rng(3)
+    m = rand_model(oracle, rng, 10)
+    gx = rng.normal(size=(30, 34))
+    gy = rng.normal(size=(30, 34))
+    f = (gx, gy, np.sqrt(gx * gx + gy * gy))
+    grid = ea.PoseGrid(0, 33, 1, 0, 29, 1, 0.0, D(40), D(10))
+    got = ea.search_topk(m, f, grid, ea.ScoreParams(3), k=5)
+    assert keys(got) == keys(oracle.search_topk(m.points, f, grid, ea.ScoreParams(3), 5))
+    assert ea.default_context().stats()["screen_path"] == 2
+
+
+def test_search_flat_field_ties(ea, oracle):
+    """All scores 0: the top k are the k smallest indices (search.cpp:36-41)."""
+    m = oracle.prepare_model(oracle.render_template("rectangle", 32))
+    z = np.zeros((40, 40))
+    f = (z, z, z)
+    grid = ea.PoseGrid(0, 39, 1, 0, 39, 1, 0.0, D(20), D(10))
+    got = ea.search_topk(m, f, grid, ea.ScoreParams(3), k=7)
+    assert keys(got) == keys(oracle.search_topk(m.points, f, grid, ea.ScoreParams(3), 7))
+    assert [int(s.grid_index) for s in got] == list(range(7))
+
+
+def test_search_k_exceeds_grid(ea, oracle):
+    rng = np.random.default_rng(11)
+    m = rand_model(oracle, rng, 10)
+    f = oracle.compute_gradients(rand_image(rng, 20, 20))
+    grid = ea.PoseGrid(3, 5, 1, 4, 4, 1, 0.0, 0.2, 0.1)
+    got = ea.search_topk(m, f, grid, ea.ScoreParams(3), k=50)
+    want = oracle.search_topk(m.points, f, grid, ea.ScoreParams(3), 50)
+    assert len(got) == 9 and keys(got) == keys(want)
+
+
+def test_search_errors(ea, oracle):
+    rng = np.random.default_rng(12)
+    m = rand_model(oracle, rng, 10)
+    f = oracle.compute_gradients(rand_image(rng, 20, 20))
+    grid = ea.PoseGrid(0, 19, 1, 0, 19, 1, 0.0, 0.0, 1.0)
+    with pytest.raises(ea.InvalidArgument, match="topk must be >= 1"):
+        ea.search_topk(m, f, grid, ea.ScoreParams(3), k=0)
+    empty = ea.EdgeModel(np.zeros((0, 5)))
+    with pytest.raises(ea.InvalidArgument, match="search needs a nonempty model"):
+        ea.search_topk(empty, f, grid, ea.ScoreParams(3), k=1)
+    with pytest.raises(ea.InvalidArgument, match="steps must be positive"):
+        ea.search_topk(m, f, ea.PoseGrid(0, 1, 0.0, 0, 1, 1, 0, 1, 1), ea.ScoreParams(3), k=1)
+    with pytest.raises(ea.BudgetError, match="900"):
+        ea.score_map(m, f, ea.PoseGrid(0, 29, 1, 0, 29, 1, 0, 0, 1), ea.ScoreParams(1), 100)
+
+
+def test_score_map_bit_exact(ea, oracle):
+    rng = np.random.default_rng(67)
+    m = rand_model(oracle, rng, 10)
+    f = oracle.compute_gradients(rand_image(rng, 30, 30))
+    for g in [(5, 24, 1, 5, 24, 1, 0.0, D(10), D(5)), (7, 7, 1, 7, 7, 1, 0.1, 0.1, 1.0),
+              (0.25, 20, 1.5, 1, 22, 2.5, -0.5, 0.5, 0.25)]:
+        grid = ea.PoseGrid(*g)
+        got = ea.score_map(m, f, grid, ea.ScoreParams(3), 1 << 20)
+        want = oracle.score_map(m.points, f, grid, ea.ScoreParams(3), 1 << 20)
+        assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("nb,pol,general", [(3, 0, False), (1, 0, False), (5, 0, False),
+                                            (3, 1, False), (3, 0, True), (7, 1, True)])
+def test_screen_bound(ea, oracle, nb, pol, general):
+    """|S_f - S| <= delta for every pose (the premise of exactness)."""
+    rng = np.random.default_rng(nb * 10 + pol)
+    tm = oracle.prepare_model(oracle.render_template("l_bracket", 48))
+    f = oracle.compute_gradients(rand_image(rng, 40, 36, real=True))
+    if general:
+        grid = ea.PoseGrid(-3.5, 40, 1, -2.5, 38, 1, 0.0, D(350), D(10))
+    else:
+        grid = ea.PoseGrid(-4, 43, 1, -3, 38, 1, 0.0, D(350), D(10))
+    params = ea.ScoreParams(nb, pol)
+    sf, delta = ea.screen_map(tm, f, grid, params)
+    s = oracle.score_map(tm.points, f, grid, params, 1 << 30)
+    err = np.abs(sf.astype(np.float64) - s).max()
+    assert err <= delta, (err, delta)
+    assert delta < 2e-6
+
+
+def test_theta_slabs_merge_to_full(ea, oracle):
+    """Theta-sharded search + `better` merge == the full search (the
+    multi-GPU exchange, search.cpp:116-139)."""
+    rng = np.random.default_rng(21)
+    m = oracle.prepare_model(oracle.render_template("l_bracket", 40))
+    f = oracle.compute_gradients(rand_image(rng, 48, 40))
+    grid = ea.PoseGrid(0, 47, 1, 0, 39, 1, 0.0, D(357), D(3))
+    params = ea.ScoreParams(3)
+    full = ea.search_topk(m, f, grid, params, k=5)
+    nt = ea.grid_counts(grid)[2]
+    for G in (2, 3, 8):
+        parts = []
+        for g in range(G):
+            parts += ea.search_topk_slab(m, f, grid, params, 5, nt * g // G, nt * (g + 1) // G)
+        assert keys(ea.merge_topk(parts, 5)) == keys(full)
+
+
+# ---- coarse to fine ------------------------------------------------------------------------
+def scene(ea, **kw):
+    spec = ea.SceneSpec(**kw)
+    img, tmpl, pose, occ = ea.compose_scene(spec)
+    return img, tmpl
+
+
+C2F_CASES = [
+    # test_search.cpp:162-262 geometries
+    dict(scene=dict(canvas_width=96, canvas_height=96, template_id="cross", template_size=32,
+                    true_pose=(48, 48, 0.0)),
+         cfg=dict(grid=(24, 72, 2, 24, 72, 2, 0.0, 0.0, 1.0), num_levels=1)),
+    dict(scene=dict(canvas_width=256, canvas_height=256, template_id="rectangle",
+                    template_size=64, true_pose=(100, 60, D(30))),
+         cfg=dict(grid=(40, 216, 8, 40, 216, 8, 0.0, D(88), D(4)), num_levels=2, min_score=0.4)),
+    dict(scene=dict(canvas_width=160, canvas_height=160, template_id="l_bracket",
+                    template_size=48, true_pose=(80, 76, D(22)), clutter_segments=14,
+                    clutter_seed=99),
+         cfg=dict(grid=(40, 120, 6, 40, 120, 6, 0.0, D(45), D(5)), num_levels=2, topk=6)),
+    dict(scene=dict(canvas_width=320, canvas_height=240, template_id="l_bracket",
+                    template_size=64, true_pose=(150, 110, D(200)), clutter_segments=30,
+                    clutter_seed=5, noise_sigma=2.0, noise_seed=3,
+                    illumination=(1.3, -10.0, 1.1)),
+         cfg=dict(grid=(0, 319, 4, 0, 239, 4, 0.0, D(358), D(2)), num_levels=3)),
+]
+
+
+@pytest.mark.parametrize("case", range(len(C2F_CASES)))
+def test_coarse_to_fine_bit_exact(ea, oracle, case):
+    c = C2F_CASES[case]
+    img, tmpl = scene(ea, **c["scene"])
+    cfgd = dict(c["cfg"])
+    L = cfgd["num_levels"]
+    cfg = ea.SearchConfig(grid=ea.PoseGrid(*cfgd.pop("grid")), score_params=ea.ScoreParams(3),
+                          **cfgd)
+    tp, wp = oracle.build_pyramid(tmpl, L), oracle.build_pyramid(img, L)
+    want = oracle.coarse_to_fine(tp, wp, cfg)
+    got = ea.coarse_to_fine(tp, wp, cfg)
+    assert got.key() == want.key()
+    det = ea.Detector(tmpl, cfg).detect(img)
+    assert det.key() == want.key()
+
+
+def test_flat_scene_no_detection(ea, oracle):
+    flat = np.full((96, 96), 180.0)
+    tmpl = oracle.render_template("rectangle", 32)
+    cfg = ea.SearchConfig(grid=ea.PoseGrid(16, 80, 4, 16, 80, 4, 0.0, 0.0, 1.0), num_levels=2,
+                          score_params=ea.ScoreParams(3))
+    tp, wp = oracle.build_pyramid(tmpl, 2), oracle.build_pyramid(flat, 2)
+    got = ea.coarse_to_fine(tp, wp, cfg)
+    assert not got.found and got.score < cfg.min_score
+    assert got.key() == oracle.coarse_to_fine(tp, wp, cfg).key()
+
+
+def test_prepare_levels_errors(ea):
+    flat = np.full((64, 64), 127.0)
+    cfg = ea.SearchConfig(grid=ea.PoseGrid(0, 63, 4, 0, 63, 4, 0, 0, 1), num_levels=2)
+    pyr = ea.build_pyramid(flat, 2)
+    with pytest.raises(ea.EmptyModelError, match="level 0"):
+        ea.prepare_levels(pyr, pyr, cfg)
+    cfg.num_levels = 3
+    with pytest.raises(ea.InvalidArgument, match="pyramids must provide 3 levels"):
+        ea.prepare_levels(pyr, pyr, cfg)
+
+
+def test_prepare_levels_models_and_fields(ea, oracle):
+    img, tmpl = scene(ea, canvas_width=160, canvas_height=160, template_id="l_bracket",
+                      template_size=48, true_pose=(80, 76, D(22)), clutter_segments=14,
+                      clutter_seed=99)
+    cfg = ea.SearchConfig(grid=ea.PoseGrid(0, 159, 2, 0, 159, 2, 0, D(10), D(5)), num_levels=2)
+    tp, wp = oracle.build_pyramid(tmpl, 2), oracle.build_pyramid(img, 2)
+    lv = ea.prepare_levels(tp, wp, cfg)
+    models, fields = oracle.prepare_levels(tp, wp, cfg)
+    for l in range(2):
+        got = lv.model(l)
+        assert np.array_equal(got.points, models[l].points)
+        assert (got.centroid_x, got.centroid_y) == (models[l].centroid_x, models[l].centroid_y)
+        for a, b in zip(lv.field(l), fields[l]):
+            assert np.array_equal(a, b)
+
+
+@pytest.mark.slow
+def test_config1_detect_bit_exact(ea, oracle):
+    """BASELINE configs[0]: 640x480, 128 px model, 1 deg over 360, 3 levels."""
+    img, tmpl = scene(ea, canvas_width=640, canvas_height=480, template_id="l_bracket",
+                      template_size=128, true_pose=(320, 240, D(30)), clutter_segments=40,
+                      clutter_seed=7)
+    cfg = ea.SearchConfig(grid=ea.PoseGrid(0, 639, 4, 0, 479, 4, 0.0, D(359), D(1)),
+                          num_levels=3, score_params=ea.ScoreParams(3))
+    tp, wp = oracle.build_pyramid(tmpl, 3), oracle.build_pyramid(img, 3)
+    want = oracle.coarse_to_fine(tp, wp, cfg)
+    got = ea.Detector(tmpl, cfg).detect(img)
+    assert got.key() == want.key()
+    assert got.found
+    assert abs(got.pose.ux - 320) <= 2 and abs(got.pose.uy - 240) <= 2
+
+
+@pytest.mark.slow
+def test_config2_detect_bit_exact(ea, oracle):
+    """BASELINE configs[1] (the bench workload): 1280x1024, 200 px model,
+    0.5 deg over 360, 4 levels, occluder + illumination + noise."""
+    import bench
+    img, tmpl, cfg, truth = bench.make_inputs("cfg2")
+    L = cfg.num_levels
+    tp, wp = oracle.build_pyramid(tmpl, L), oracle.build_pyramid(img, L)
+    want = oracle.coarse_to_fine(tp, wp, cfg)
+    got = ea.Detector(tmpl, cfg).detect(img)
+    assert got.key() == want.key()
