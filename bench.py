@@ -310,7 +310,7 @@ def bench_ours(args, rank, world, local_rank):
     kernel_ms = statistics.median(screen_ms)
     local_evals = nx * ny * (it1 - it0) * n_top
     achieved = local_evals * ALG_BYTES_PER_EVAL / (kernel_ms / 1e3) / 1e9
-    S = 16 if ((ny + 127) // 128) * 128 * 18 <= ((ny + 63) // 64) * 64 * 20 else 8
+    S = 16 if os.environ.get("EAB_SCREEN_ROWS") == "16" else 8
     actual_b = (S + 2) / S * (10 / 8) * 8  # smem bytes the lattice kernel really loads / eval
     line = {
         "metric": "pose-evals/sec", "value": value, "unit": "pose-evals/s", "n_gpus": world,

@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -296,14 +297,30 @@ ScreenPlan screen(ea_ctx* ctx, const ea_model* m, const ea_field* f, const ea_po
     const bool lattice = is_int(g.x0) && is_int(g.y0) && std::fabs(g.x1) <= 1048576.0 &&
                          std::fabs(g.y1) <= 1048576.0 && g.dx == 1.0 && g.dy == 1.0 && R <= 2 &&
                          f->ring_max < p.eps_mag;
-    int shift = 4;
-    {
-        const uint64_t ny = plan.c.ny;
-        const uint64_t cost16 = ((ny + 127) / 128) * 128 * 18;
-        const uint64_t cost8 = ((ny + 63) / 64) * 64 * 20;
-        shift = cost16 <= cost8 ? 4 : 3;
+    // Lane strips of 8 rows (64 accumulators, 12 warps/SM) measured faster
+    // than 16 rows (128 accumulators, 8 warps/SM, spills) on B200.
+    int shift = 3;
+    if (const char* e = std::getenv("EAB_SCREEN_ROWS")) shift = std::atoi(e) == 16 ? 4 : 3;
+    // Zero columns beyond the ring so no lattice window needs clamping:
+    // |offset| <= ceil(max |p_i|) + 1 for every rotation of the model.
+    int PL = 0, PR = 0;
+    if (lattice) {
+        double rmax = 0.0;
+        for (const ea_edge_point& q : m->host)
+            rmax = std::max(rmax, std::sqrt(q.x_rel * q.x_rel + q.y_rel * q.y_rel));
+        const long ro = (long)std::ceil(rmax) + 2;
+        const long ix0 = (long)g.x0, span = (long)((plan.c.nx + 31) / 32) * 32;
+        PL = (int)std::max(0L, ro + R - 1 - ix0);
+        PR = (int)std::max(0L, ix0 + span + ro + R - f->width - 1);
+        const size_t budget = ctx->smem_optin;  // hist + plane must fit one CTA
+        auto bytes = [&](int l, int r) {
+            return fast_smem_bytes(plane_geom(f->width, f->height, shift, l, r));
+        };
+        while ((PL > 0 || PR > 0) && bytes(PL, PR) > budget) {  // shrink: clamp path covers
+            if (PL >= PR) --PL; else --PR;
+        }
     }
-    const PlaneGeom geom = plane_geom(f->width, f->height, shift);
+    const PlaneGeom geom = plane_geom(f->width, f->height, shift, PL, PR);
     float2* plane = (float2*)ctx->plane.ensure(sizeof(float2) * geom.elems);
     EAB_CUDA(cudaMemsetAsync(plane, 0, sizeof(float2) * geom.elems, ctx->stream));
     launch_plane(ctx, f, p.eps_mag, geom, plane, &ctrl->ring_bad);

@@ -62,13 +62,13 @@ __global__ void sobel_kernel(const double* __restrict__ img, int w, int h,
 // is what makes the zero ring equivalent to the reference's window clipping.
 __global__ void plane_kernel(const double* __restrict__ gx, const double* __restrict__ gy,
                              const double* __restrict__ mag, int W, int H, double eps,
-                             int PW, int shift, float2* __restrict__ plane,
+                             int PW, int PL, int shift, float2* __restrict__ plane,
                              int* __restrict__ ring_bad) {
     const int xp = blockIdx.x * blockDim.x + threadIdx.x;
     const int yp = blockIdx.y;
     if (xp >= PW || yp >= H + 2) return;
     float2 v = make_float2(0.f, 0.f);
-    const int x = xp - 1, y = yp - 1;
+    const int x = xp - 1 - PL, y = yp - 1;
     if (x >= 0 && x < W && y >= 0 && y < H) {
         const size_t o = (size_t)y * W + x;
         const double m = mag[o];
@@ -102,7 +102,7 @@ void launch_plane(ea_ctx* ctx, const ea_field* f, double eps, const PlaneGeom& g
                   float2* plane, int* ring_bad) {
     dim3 grid((g.PW + 127) / 128, g.H + 2);
     plane_kernel<<<grid, 128, 0, ctx->stream>>>(f->gx(), f->gy(), f->mag(), g.W, g.H, eps,
-                                                g.PW, g.shift, plane, ring_bad);
+                                                g.PW, g.PL, g.shift, plane, ring_bad);
     check_launch("plane_kernel");
     count_launch(ctx);
 }

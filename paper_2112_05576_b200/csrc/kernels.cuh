@@ -12,20 +12,30 @@ constexpr int kHistBins = 4096;           // screening-score histogram, [-1,1] i
 constexpr double kCoordGuard = 1e9;       // similarity.cpp:28
 
 // Geometry of the padded, row-skewed screening plane.
+// Field pixel (x, y) lives at padded (xp, yp) = (x + 1 + PL, y + 1): a one-
+// pixel zero ring plus PL / PR extra zero columns, so that the lattice
+// kernel's windows never need column clamping.
 struct PlaneGeom {
     int W = 0, H = 0;   // unpadded field dims
-    int PW = 0;         // row pitch in float2 (>= W + 2)
+    int PL = 0, PR = 0; // extra zero columns left / right of the ring
+    int PW = 0;         // row pitch in float2 (= W + 2 + PL + PR)
     int shift = 4;      // row skew: element (xp, yp) at yp*PW + (yp >> shift) + xp
-    size_t elems = 0;   // float2 count of the whole plane (rounded to 2 for 16 B copies)
+    int zero = 0;       // offset of a PW + 16 zero strip standing in for off-plane rows
+    size_t elems = 0;   // float2 count incl. the strip (rounded to 2 for 16 B copies)
 };
 
-inline PlaneGeom plane_geom(int W, int H, int shift) {
+inline PlaneGeom plane_geom(int W, int H, int shift, int PL = 0, int PR = 0) {
     PlaneGeom g;
     g.W = W;
     g.H = H;
-    g.PW = W + 2;
+    g.PL = PL;
+    g.PR = PR;
+    g.PW = W + 2 + PL + PR;
     g.shift = shift;
     size_t e = (size_t)(H + 2) * g.PW + (size_t)((H + 1) >> shift) + 1;
+    e = (e + 15) & ~(size_t)15;
+    g.zero = (int)e;
+    e += (size_t)g.PW + 16;
     g.elems = (e + 1) & ~(size_t)1;
     return g;
 }
@@ -134,6 +144,8 @@ struct ScreenArgs {
     SearchCtrl* ctrl;
 };
 
+// Dynamic shared memory the lattice kernel needs for a plane.
+size_t fast_smem_bytes(const PlaneGeom& g);
 // Returns true if the smem lattice kernel handled the launch.
 bool launch_screen_fast(ea_ctx* ctx, const ScreenArgs& a);
 void launch_screen_general(ea_ctx* ctx, const ScreenArgs& a);

@@ -113,24 +113,107 @@ __device__ __forceinline__ int hist_bin(float s) {
     return b < 0 ? 0 : (b >= kHistBins ? kHistBins - 1 : b);
 }
 
-constexpr int kScreenThreads = 256;
+// 12 warps per SM for 8-row lane strips (<= 168 registers), 8 warps for 16.
+template <int S>
+constexpr int screen_threads() { return S <= 8 ? 384 : 256; }
 constexpr int kTW = 8;  // poses per lane along x
+
+// One model point over a lane's 8 x S pose block: walk the S + 2R plane rows
+// its windows touch.  CLAMP=false is the warp-uniform interior case (every
+// column of the warp's windows lies inside the padded plane): loads address
+// [row + immediate].  CLAMP=true clamps each column into the zero ring.
+template <int R, int S, int SHIFT, bool IGNORE, bool CLAMP>
+__device__ __forceinline__ void point_rows(const float2* __restrict__ P, const int PW,
+                                           const int XL, const int cx_lo, const int cx_hi,
+                                           const int H1, const int Z, const int cb,
+                                           const int rb, const float dxf, const float dyf,
+                                           const float K, const int B3, int (&acc)[S][kTW]) {
+    constexpr int NC = kTW + 2 * R;  // columns per row
+    constexpr int NR = S + 2 * R;    // rows per point
+    int col[CLAMP ? NC : 1];
+    if constexpr (CLAMP) {
+#pragma unroll
+        for (int m = 0; m < NC; ++m) col[m] = min(max(cb + m, 0), XL);
+    }
+    // For R <= 1 the zero ring makes an off-field centre vote exactly 0; a
+    // 5-wide window can reach real pixels, so R >= 2 masks those centres.
+    unsigned cmask = 0xffu;
+    if constexpr (R >= 2) {
+        cmask = 0u;
+#pragma unroll
+        for (int j = 0; j < kTW; ++j) {
+            const int cxj = cb + R + j;  // padded column of the window centre
+            cmask |= (cxj >= cx_lo && cxj <= cx_hi) ? (1u << j) : 0u;
+        }
+    }
+    float hprev[2 * R > 0 ? 2 * R : 1][kTW];
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+        // Rows off the plane read the zero strip at an offset congruent (mod
+        // 16 float2 slots) to where the row would be, so the lanes' bank
+        // spacing survives at the top/bottom edges.
+        const int yv = rb + r;
+        const int va = yv * PW + (yv >> SHIFT);
+        const float2* row = P + (((unsigned)yv <= (unsigned)H1) ? va : Z + (va & 15));
+        if constexpr (!CLAMP) row += cb;
+        float c[NC];
+#pragma unroll
+        for (int m = 0; m < NC; ++m) {
+            const float2 v = CLAMP ? row[col[m]] : row[m];
+            if constexpr (IGNORE) {
+                c[m] = fabsf(fmaf(dyf, v.y, dxf * v.x));
+            } else {
+                c[m] = fmaf(dyf, v.y, fmaf(dxf, v.x, K));
+            }
+        }
+        float h[kTW];
+#pragma unroll
+        for (int j = 0; j < kTW; ++j) h[j] = max_run<2 * R + 1>(c + j);
+        if (r >= 2 * R) {
+            const int s = r - 2 * R;
+#pragma unroll
+            for (int j = 0; j < kTW; ++j) {
+                float col_v[2 * R + 1];
+#pragma unroll
+                for (int q = 0; q < 2 * R; ++q) col_v[q] = hprev[q][j];
+                col_v[2 * R] = h[j];
+                float v = max_run<2 * R + 1>(col_v);
+                if constexpr (IGNORE) v = v + K;
+                if constexpr (R >= 2) {
+                    const int cys = rb + R + s;  // padded row of the window centre
+                    const bool in = ((cmask >> j) & 1u) && cys >= 1 && cys <= H1 - 1;
+                    v = in ? v : K;
+                }
+                acc[s][j] += __float_as_int(v) - B3;
+            }
+        }
+        if constexpr (R > 0) {
+#pragma unroll
+            for (int q = 0; q + 1 < 2 * R; ++q)
+#pragma unroll
+                for (int j = 0; j < kTW; ++j) hprev[q][j] = hprev[q + 1][j];
+#pragma unroll
+            for (int j = 0; j < kTW; ++j) hprev[2 * R - 1][j] = h[j];
+        }
+    }
+}
 
 // The smem lattice kernel (integer top-level lattice with unit steps).
 //
 // A CTA is persistent (one per SM) and holds the whole padded screening
 // plane of the top level in shared memory.  Work items are (theta, warp
 // tile) pairs handed out by an atomic counter.  A warp tile is 32 x 8*S
-// poses; lane (xg = lane&3, yg = lane>>2) owns an 8 x S block and keeps its
+// poses; lane (yg = lane&7, xg = lane>>3) owns an 8 x S block and keeps its
 // 8*S fixed-point score accumulators in registers.  Per model point the lane
 // walks the S + 2R plane rows its windows touch: 8 + 2R float2 loads, two FMAs
 // per candidate, a horizontal (2R+1)-max (FMNMX3) and, once 2R+1 rows are in
-// flight, the vertical max -- i.e. each plane pixel loaded serves up to
-// (2R+1)^2 window slots.  Row skew (yp >> SHIFT) plus the 8-pose lane stride
-// make the 32 lanes' addresses hit every bank pair exactly twice: LDS.64 at
-// the 2-wavefront minimum.
+// flight, the vertical max -- each plane pixel loaded serves up to (2R+1)^2
+// window slots.  Bank mapping: a lane's float2 slot (mod 16) is
+// yg*(2^SHIFT*PW + 1) + 8*xg = yg + 8*xg thanks to the row skew (yp >> SHIFT),
+// so each half-warp (yg 0..7 x two xg) covers all 16 bank pairs once: LDS.64
+// at the 2-wavefront minimum.
 template <int R, int S, int SHIFT, bool IGNORE>
-__global__ void __launch_bounds__(kScreenThreads, 1)
+__global__ void __launch_bounds__(screen_threads<S>(), 1)
     screen_fast_kernel(const ScreenArgs a, const unsigned nwx, const unsigned nwy,
                        const unsigned long long total_items, const int vec16) {
     extern __shared__ __align__(16) unsigned char smem[];
@@ -144,11 +227,11 @@ __global__ void __launch_bounds__(kScreenThreads, 1)
     }
     __syncthreads();
 
-    constexpr int NC = kTW + 2 * R;  // columns per row
-    constexpr int NR = S + 2 * R;    // rows per point
+    constexpr int NC = kTW + 2 * R;
     const int lane = threadIdx.x & 31;
-    const int xg = lane & 3, yg = lane >> 2;
-    const int W1 = a.geom.W + 1, H1 = a.geom.H + 1, PW = a.geom.PW;
+    const int yg = lane & 7, xg = lane >> 3;
+    const int H1 = a.geom.H + 1, PW = a.geom.PW, XL = a.geom.PW - 1;
+    const int cx_lo = 1 + a.geom.PL, cx_hi = a.geom.W + a.geom.PL, Z = a.geom.zero;
     const float K = a.K;
     const int B3 = (int)a.B3;
     const unsigned long long plane_poses = a.nx * a.ny;
@@ -162,7 +245,8 @@ __global__ void __launch_bounds__(kScreenThreads, 1)
         const unsigned long long rest = item / nwx;
         const unsigned wy = (unsigned)(rest % nwy);
         const unsigned long long itr = rest / nwy;
-        const int X = (int)wx * 32 + xg * kTW;
+        const int X0 = (int)wx * 32;
+        const int X = X0 + xg * kTW;
         const int Y = (int)wy * (8 * S) + yg * S;
         const int4* rot = a.rot_screen + (size_t)itr * a.n;
 
@@ -176,66 +260,15 @@ __global__ void __launch_bounds__(kScreenThreads, 1)
         for (int i = 0; i < a.n; ++i) {
             const int4 pn = __ldg(rot + (i + 1 < a.n ? i + 1 : i));
             const float dxf = __int_as_float(p.z), dyf = __int_as_float(p.w);
-            const int cb = p.x + a.ix0 + X - R + 1;  // padded column of window start
-            const int rb = p.y + a.iy0 + Y - R + 1;  // padded row of window start
-            int col[NC];
-#pragma unroll
-            for (int m = 0; m < NC; ++m) col[m] = min(max(cb + m, 0), W1);
-            // For R <= 1 the zero ring makes an off-field centre vote exactly 0;
-            // a 5-wide window can reach real pixels, so mask those centres.
-            unsigned cmask = 0xffu;
-            if constexpr (R >= 2) {
-                cmask = 0u;
-#pragma unroll
-                for (int j = 0; j < kTW; ++j) {
-                    const int cxj = cb + R - 1 + j;
-                    cmask |= (cxj >= 0 && cxj < W1 - 1) ? (1u << j) : 0u;
-                }
-            }
-            float hprev[2 * R > 0 ? 2 * R : 1][kTW];
-#pragma unroll
-            for (int r = 0; r < NR; ++r) {
-                const int yp = min(max(rb + r, 0), H1);
-                const float2* row = P + yp * PW + (yp >> SHIFT);
-                float c[NC];
-#pragma unroll
-                for (int m = 0; m < NC; ++m) {
-                    const float2 v = row[col[m]];
-                    if constexpr (IGNORE) {
-                        c[m] = fabsf(fmaf(dyf, v.y, dxf * v.x));
-                    } else {
-                        c[m] = fmaf(dyf, v.y, fmaf(dxf, v.x, K));
-                    }
-                }
-                float h[kTW];
-#pragma unroll
-                for (int j = 0; j < kTW; ++j) h[j] = max_run<2 * R + 1>(c + j);
-                if (r >= 2 * R) {
-                    const int s = r - 2 * R;
-#pragma unroll
-                    for (int j = 0; j < kTW; ++j) {
-                        float col_v[2 * R + 1];
-#pragma unroll
-                        for (int q = 0; q < 2 * R; ++q) col_v[q] = hprev[q][j];
-                        col_v[2 * R] = h[j];
-                        float v = max_run<2 * R + 1>(col_v);
-                        if constexpr (IGNORE) v = v + K;
-                        if constexpr (R >= 2) {
-                            const int cys = rb + R - 1 + s;
-                            const bool in = ((cmask >> j) & 1u) && cys >= 0 && cys < H1 - 1;
-                            v = in ? v : K;
-                        }
-                        acc[s][j] += __float_as_int(v) - B3;
-                    }
-                }
-                if constexpr (R > 0) {
-#pragma unroll
-                    for (int q = 0; q + 1 < 2 * R; ++q)
-#pragma unroll
-                        for (int j = 0; j < kTW; ++j) hprev[q][j] = hprev[q + 1][j];
-#pragma unroll
-                    for (int j = 0; j < kTW; ++j) hprev[2 * R - 1][j] = h[j];
-                }
+            const int cb = p.x + a.ix0 + X - R + cx_lo;   // padded column of window start
+            const int rb = p.y + a.iy0 + Y - R + 1;       // padded row of window start
+            const int cw = p.x + a.ix0 + X0 - R + cx_lo;  // warp's first column (uniform)
+            if (cw >= 0 && cw + 24 + NC - 1 <= XL) {
+                point_rows<R, S, SHIFT, IGNORE, false>(P, PW, XL, cx_lo, cx_hi, H1, Z, cb, rb,
+                                                      dxf, dyf, K, B3, acc);
+            } else {
+                point_rows<R, S, SHIFT, IGNORE, true>(P, PW, XL, cx_lo, cx_hi, H1, Z, cb, rb,
+                                                     dxf, dyf, K, B3, acc);
             }
             p = pn;
         }
@@ -270,11 +303,12 @@ static void run_fast(ea_ctx* ctx, const ScreenArgs& a) {
     const size_t smem = kHistBins * sizeof(unsigned) + plane_bytes;
     auto kern = screen_fast_kernel<R, S, SHIFT, IGNORE>;
     EAB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    unsigned long long warps_per_cta = kScreenThreads / 32;
+    constexpr int threads = screen_threads<S>();
+    unsigned long long warps_per_cta = threads / 32;
     unsigned long long ctas = (items + warps_per_cta - 1) / warps_per_cta;
     if (ctas > (unsigned long long)ctx->sm_count) ctas = ctx->sm_count;
     if (ctas == 0) ctas = 1;
-    kern<<<(unsigned)ctas, kScreenThreads, smem, ctx->stream>>>(a, nwx, nwy, items,
+    kern<<<(unsigned)ctas, threads, smem, ctx->stream>>>(a, nwx, nwy, items,
                                                                 (int)(plane_bytes / 16));
     check_launch("screen_fast_kernel");
     count_launch(ctx);
@@ -344,7 +378,7 @@ __global__ void __launch_bounds__(256)
             float best = -INFINITY;
             for (int y = y0; y <= y1; ++y) {
                 const int yp = y + 1;
-                const float2* row = a.plane + (size_t)yp * PW + (yp >> SH) + 1;
+                const float2* row = a.plane + (size_t)yp * PW + (yp >> SH) + 1 + a.geom.PL;
                 for (int x = x0; x <= x1; ++x) {
                     const float2 v = __ldg(row + x);
                     const float c = IGNORE ? fabsf(fmaf(dyf, v.y, dxf * v.x))
