@@ -31,7 +31,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 import paper_2112_05576_b200 as ea  # noqa: E402
-from paper_2112_05576_b200 import abi  # noqa: E402
+from paper_2112_05576_b200 import abi, parallel  # noqa: E402
 
 D = abi.deg_to_rad
 
@@ -213,23 +213,13 @@ def bench_ours(args, rank, world, local_rank):
     nx, ny, nt = ea.grid_counts(tg)
     L = cfg.num_levels
     n_top = len(det.levels.model(L - 1).points)
-    it0, it1 = nt * rank // world, nt * (rank + 1) // world
+    it0, it1 = parallel.theta_slab(nt, rank, world)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
 
     def gather(seeds):
         if world == 1:
             return seeds
-        t = torch.zeros((cfg.topk, 5), dtype=torch.float64, device=dev)
-        for i, s in enumerate(seeds):
-            t[i] = torch.tensor([s.score, float(s.grid_index), s.pose.ux, s.pose.uy,
-                                 s.pose.theta], dtype=torch.float64)
-        t[len(seeds):, 0] = float("nan")
-        out = torch.empty((world * cfg.topk, 5), dtype=torch.float64, device=dev)
-        dist.all_gather_into_tensor(out, t)
-        rows = out.cpu().numpy()
-        cands = [ea.ScoredPose(r[0], int(r[1]), ea.Pose(r[2], r[3], r[4]))
-                 for r in rows if not np.isnan(r[0])]
-        return ea.merge_topk(cands, cfg.topk)
+        return parallel.gather_topk(seeds, cfg.topk, device=dev)
 
     def top_step():
         seeds = ea.search_top_slab(det.levels, cfg, it0, it1)
