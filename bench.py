@@ -275,6 +275,7 @@ def bench_ours(args, rank, world, local_rank):
     for _ in range(args.warmup):
         detect_step()
     barrier()
+    phases = []
     eev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for _ in range(args.steps)]
     outcome = None
@@ -283,6 +284,8 @@ def bench_ours(args, rank, world, local_rank):
         eev[i][0].record(stream)
         outcome = detect_step()
         eev[i][1].record(stream)
+        st_d = ctx.stats()
+        phases.append((st_d["image_ms"], st_d["top_ms"], st_d["refine_ms"]))
     barrier()
     e2e_ms = sum(a.elapsed_time(b) for a, b in eev)
     if world > 1:
@@ -312,7 +315,10 @@ def bench_ours(args, rank, world, local_rank):
                    "pose_evals_per_step": pose_pts, "l2": "flushed (256 MiB write) between steps",
                    "parallelism": f"theta-slab x{world}" if world > 1 else "single GPU"},
         "e2e": {"value": e2e, "unit": "pose-evals/s", "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h, "detect_latency_ms": e2e_ms / args.steps},
+                "d2h_bytes_per_step": d2h, "detect_latency_ms": e2e_ms / args.steps,
+                "phases_ms_median": {k: statistics.median(p[i] for p in phases)
+                                     for i, k in enumerate(("h2d_pyramid_gradients",
+                                                            "top_level_search", "refinement"))}},
         "roofline": {"bound": "smem", "kernel": "screen_fast_kernel" if st["screen_path"] == 1
                      else "screen_general_kernel", "achieved": achieved,
                      "peak": smem_peak_gbs, "unit": "GB/s", "frac": achieved / smem_peak_gbs,

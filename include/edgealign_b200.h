@@ -166,6 +166,8 @@ typedef struct {
     int32_t _pad;
     double screen_ms;          /* CUDA-event time of the screening kernel        */
     double top_ms;             /* CUDA-event time of the whole top-level search  */
+    double image_ms;           /* ea_detect: H2D + pyramid + gradients           */
+    double refine_ms;          /* refinement down the pyramid (incl. host prep)  */
 } ea_search_stats;
 
 /* ---- context ------------------------------------------------------------ */

@@ -164,7 +164,8 @@ class SearchStats(C.Structure):
                 ("candidates_needed", C.c_uint64), ("screen_delta", C.c_double),
                 ("threshold", C.c_double), ("screen_path", C.c_int32),
                 ("flagged_points", C.c_int32), ("kernels_launched", C.c_int32),
-                ("_pad", C.c_int32), ("screen_ms", C.c_double), ("top_ms", C.c_double)]
+                ("_pad", C.c_int32), ("screen_ms", C.c_double), ("top_ms", C.c_double),
+                ("image_ms", C.c_double), ("refine_ms", C.c_double)]
 
 
 def isfinite_grid(g):

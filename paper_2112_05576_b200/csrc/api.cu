@@ -8,12 +8,14 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <mutex>
 #include <string>
 #include <vector>
 
 #include "host_model.h"
 #include "kernels.cuh"
+#include "refine.cuh"
 
 using namespace eab;
 
@@ -247,6 +249,7 @@ struct ScreenPlan {
     int fold_e = 0;
     double delta = 0.0;
     bool fast = false;
+    ItemGeom items{};
 };
 
 ScreenPlan screen(ea_ctx* ctx, const ea_model* m, const ea_field* f, const ea_pose_grid& g,
@@ -265,10 +268,15 @@ ScreenPlan screen(ea_ctx* ctx, const ea_model* m, const ea_field* f, const ea_po
     const int R = (p.neighborhood - 1) / 2;
 
     // Tables for the slab's thetas.
-    const std::vector<double>& cs_all = theta_cs(ctx, g.t0, g.dt, plan.c.nt);
     const size_t nth = plan.it_count;
     double* d_cs = (double*)ctx->cs.ensure(sizeof(double) * 2 * (nth ? nth : 1));
-    h2d_staged(ctx, d_cs, cs_all.data() + 2 * it_begin, sizeof(double) * 2 * nth);
+    const std::vector<double> key{g.t0, g.dt, (double)plan.c.nt, (double)it_begin, (double)nth};
+    if (key != ctx->cs_dev_key) {  // device copy of the slab's cos/sin, reused across calls
+        const std::vector<double>& cs_all = theta_cs(ctx, g.t0, g.dt, plan.c.nt);
+        ctx->cs_dev_key.clear();
+        h2d_staged(ctx, d_cs, cs_all.data() + 2 * it_begin, sizeof(double) * 2 * nth);
+        ctx->cs_dev_key = key;
+    }
     // Slab-relative rotation tables: row (it - it_begin) of px|py|dx|dy and of
     // the lattice table.
     const size_t slab_pairs = nth * (size_t)n;
@@ -289,6 +297,8 @@ ScreenPlan screen(ea_ctx* ctx, const ea_model* m, const ea_field* f, const ea_po
     std::memcpy(&B3, &K, sizeof B3);
     // |S_f - S| <= 2^(e-20) (candidate + fold rounding) + 2^-23 (final fp32 store)
     plan.delta = std::ldexp(1.0, e - 20) + std::ldexp(1.0, -23);
+    // fp16 plane (lattice path): |n_h - n| <= 2^-11 |n| per component, so a
+    // candidate moves by at most sqrt(2) * 2^-11 (+ subnormal slack 2^-24).
 
     // Path choice.
     // Integer origin + unit steps: every translation is an exact integer,
@@ -299,8 +309,12 @@ ScreenPlan screen(ea_ctx* ctx, const ea_model* m, const ea_field* f, const ea_po
                          f->ring_max < p.eps_mag;
     // Lane strips of 8 rows (64 accumulators, 12 warps/SM) measured faster
     // than 16 rows (128 accumulators, 8 warps/SM, spills) on B200.
-    int shift = 3;
-    if (const char* e = std::getenv("EAB_SCREEN_ROWS")) shift = std::atoi(e) == 16 ? 4 : 3;
+    const int shift = 3;
+    int elem = 8;  // float2 plane
+    if (lattice) {
+        const char* pe = std::getenv("EAB_PLANE");
+        elem = (pe && std::strcmp(pe, "f16") == 0) ? 4 : 8;  // fp32 plane unless asked
+    }
     // Zero columns beyond the ring so no lattice window needs clamping:
     // |offset| <= ceil(max |p_i|) + 1 for every rotation of the model.
     int PL = 0, PR = 0;
@@ -314,17 +328,23 @@ ScreenPlan screen(ea_ctx* ctx, const ea_model* m, const ea_field* f, const ea_po
         PR = (int)std::max(0L, ix0 + span + ro + R - f->width - 1);
         const size_t budget = ctx->smem_optin;  // hist + plane must fit one CTA
         auto bytes = [&](int l, int r) {
-            return fast_smem_bytes(plane_geom(f->width, f->height, shift, l, r));
+            return fast_smem_bytes(plane_geom(f->width, f->height, shift, l, r, elem));
         };
         while ((PL > 0 || PR > 0) && bytes(PL, PR) > budget) {  // shrink: clamp path covers
             if (PL >= PR) --PL; else --PR;
         }
     }
-    const PlaneGeom geom = plane_geom(f->width, f->height, shift, PL, PR);
-    float2* plane = (float2*)ctx->plane.ensure(sizeof(float2) * geom.elems);
-    EAB_CUDA(cudaMemsetAsync(plane, 0, sizeof(float2) * geom.elems, ctx->stream));
+    PlaneGeom geom = plane_geom(f->width, f->height, shift, PL, PR, elem);
+    if (elem == 4 && fast_smem_bytes(geom) > ctx->smem_optin) {  // whole plane must fit
+        elem = 8;
+        geom = plane_geom(f->width, f->height, shift, PL, PR, elem);
+    }
+    void* plane = ctx->plane.ensure(geom.bytes());
+    EAB_CUDA(cudaMemsetAsync(plane, 0, geom.bytes(), ctx->stream));
     launch_plane(ctx, f, p.eps_mag, geom, plane, &ctrl->ring_bad);
     float* map = (float*)ctx->map.ensure(sizeof(float) * (plan.slab_poses ? plan.slab_poses : 1));
+    float* item_max =
+        (float*)ctx->item_max.ensure(sizeof(float) * (plan.slab_poses / 32 + plan.it_count * 64 + 64));
 
     ScreenArgs a{};
     a.plane = plane;
@@ -349,6 +369,7 @@ ScreenPlan screen(ea_ctx* ctx, const ea_model* m, const ea_field* f, const ea_po
     a.B3 = B3;
     a.scale = (float)(std::ldexp(1.0, e - 22) / (double)n);
     a.map = map;
+    a.item_max = item_max;
     a.hist = hist;
     a.ctrl = ctrl;
     plan.fast = false;
@@ -359,6 +380,9 @@ ScreenPlan screen(ea_ctx* ctx, const ea_model* m, const ea_field* f, const ea_po
     }
     if (ctx->timing) EAB_CUDA(cudaEventRecord(ctx->ev[2], ctx->stream));
     ctx->stats.screen_path = plan.fast ? 1 : 2;
+    if (plan.fast && geom.elem_bytes == 4)
+        plan.delta += std::sqrt(2.0) * std::ldexp(1.0, -11) + std::ldexp(1.0, -24);
+    plan.items = screen_items(a, plan.fast);
     return plan;
 }
 
@@ -418,7 +442,8 @@ std::vector<ea_scored_pose> top_search(ea_ctx* ctx, const ea_model* m, const ea_
             EAB_CUDA(cudaMemsetAsync(&ctrl->cand_count, 0, sizeof(unsigned long long),
                                      ctx->stream));
         }
-        launch_compact(ctx, ctx->map.as<float>(), plan.slab_poses, ctrl, cand, cap);
+        launch_compact(ctx, ctx->map.as<float>(), ctx->item_max.as<float>(), plan.items, ctrl,
+                       cand, cap);
         launch_rescore(ctx, x, cand, ctrl, cap, cs);
         launch_select(ctx, cand, cs, ctrl, cap, k, plan.it_begin * plan.c.nx * plan.c.ny, tk, tki);
         const size_t res_bytes = (sizeof(double) + sizeof(unsigned long long)) * (size_t)k;
@@ -436,6 +461,16 @@ std::vector<ea_scored_pose> top_search(ea_ctx* ctx, const ea_model* m, const ea_
         }
         SearchCtrl hc;
         std::memcpy(&hc, h, sizeof hc);
+        if (std::getenv("EAB_DEBUG_ITEMS")) {
+            std::vector<float> im(plan.items.n_items);
+            d2h(ctx, im.data(), ctx->item_max.p, sizeof(float) * im.size());
+            sync(ctx);
+            size_t pass = 0;
+            for (float v : im) pass += v >= hc.thr;
+            std::fprintf(stderr, "[eab] items=%llu pass=%zu thr=%g first=%g lattice=%d rows=%u\n",
+                         (unsigned long long)plan.items.n_items, pass, (double)hc.thr,
+                         (double)im[0], plan.items.lattice, plan.items.rows);
+        }
         ctx->stats.candidates = hc.cand_count;
         ctx->stats.candidates_needed = hc.needed;
         ctx->stats.threshold = hc.thr;
@@ -462,8 +497,8 @@ struct Beam {
     uint64_t top_index;
 };
 
-void refine_levels(ea_ctx* ctx, const ea_levels* lv, const ea_search_config& cfg,
-                   const ea_pose_grid& top_grid, std::vector<Beam> beam, ea_outcome* out) {
+void refine_levels_host(ea_ctx* ctx, const ea_levels* lv, const ea_search_config& cfg,
+                        const ea_pose_grid& top_grid, std::vector<Beam> beam, ea_outcome* out) {
     const int top = cfg.num_levels - 1;
     std::memset(out, 0, sizeof(*out));
     int nt = 0;
@@ -568,6 +603,131 @@ void refine_levels(ea_ctx* ctx, const ea_levels* lv, const ea_search_config& cfg
     out->score = beam[0].score;
     out->grid_index = beam[0].top_index;
     out->found = beam[0].score >= cfg.min_score ? 1 : 0;
+}
+
+// Device-resident refinement (refine_kernels.cu): host glibc cos/sin of every
+// theta reachable from the seeds, then one votes + one select kernel per level
+// and a single D2H of the outcome.
+void refine_levels(ea_ctx* ctx, const ea_levels* lv, const ea_search_config& cfg,
+                   const ea_pose_grid& top_grid, std::vector<Beam> seeds, ea_outcome* out) {
+    const int top = cfg.num_levels - 1;
+    const int R = cfg.refine_radius, side = 2 * R + 1, k = cfg.topk;
+    const int ns = (int)seeds.size();
+    const long e_max = (long)k * side * side * side;
+    if (top == 0 || e_max > 4096) {
+        refine_levels_host(ctx, lv, cfg, top_grid, std::move(seeds), out);
+        return;
+    }
+    // per-level steps (search.cpp:286-295) and theta tables
+    const double theta_floor = 0.25 * (3.14159265358979323846 / 180.0);
+    std::vector<double> sx(top + 1), sy(top + 1), st(top + 1);
+    std::vector<size_t> toff(top + 1, 0);
+    double step_x = top_grid.dx, step_y = top_grid.dy, step_t = top_grid.dt;
+    size_t tsize = 0, paths = (size_t)ns;
+    for (int d = 1; d <= top; ++d) {
+        step_x /= 2.0;
+        step_y /= 2.0;
+        step_t = std::max(step_t / 2.0, theta_floor);
+        sx[d] = step_x;
+        sy[d] = step_y;
+        st[d] = step_t;
+        paths *= (size_t)side;
+        toff[d] = tsize;
+        tsize += 3 * paths;
+    }
+    int n_max = 0;
+    for (int l = 0; l < top; ++l) n_max = std::max(n_max, lv->models[l]->n);
+    const size_t beam_bytes = sizeof(BeamDev) * (size_t)k;
+    const size_t head = sizeof(ea_outcome) + 2 * beam_bytes + 2 * sizeof(int);
+    const size_t host_bytes = head + sizeof(double) * tsize;
+    sync(ctx);
+    char* hb = (char*)ctx->h_stage.ensure(host_bytes);
+    ea_outcome* hout = (ea_outcome*)hb;
+    std::memset(hout, 0, sizeof(ea_outcome));
+    hout->trace[0].level = top;
+    hout->trace[0].pose = seeds[0].pose;
+    hout->trace[0].score = seeds[0].score;
+    hout->n_trace = 1;
+    BeamDev* hbeam = (BeamDev*)(hb + sizeof(ea_outcome));
+    for (int i = 0; i < ns; ++i) {
+        hbeam[i] = BeamDev{seeds[i].pose.ux, seeds[i].pose.uy, seeds[i].pose.theta,
+                           seeds[i].score, seeds[i].top_index, i, 0};
+    }
+    int* hcnt = (int*)(hb + sizeof(ea_outcome) + 2 * beam_bytes);
+    hcnt[0] = ns;
+    hcnt[1] = 0;
+    double* htab = (double*)(hb + head);
+    {
+        std::vector<double> prev(ns);
+        for (int i = 0; i < ns; ++i) prev[i] = seeds[i].pose.theta;
+        for (int d = 1; d <= top; ++d) {
+            std::vector<double> cur(prev.size() * side);
+            double* t = htab + toff[d];
+            for (size_t q = 0; q < prev.size(); ++q) {
+                for (int kt = -R; kt <= R; ++kt) {
+                    const size_t path = q * side + (size_t)(kt + R);
+                    const double theta = prev[q] + (double)kt * st[d];  // search.cpp:305
+                    cur[path] = theta;
+                    t[3 * path] = theta;
+                    t[3 * path + 1] = std::cos(theta);
+                    t[3 * path + 2] = std::sin(theta);
+                }
+            }
+            prev.swap(cur);
+        }
+    }
+    const size_t ss = (size_t)side * side;
+    const size_t E = (size_t)k * side * ss;
+    char* db = (char*)ctx->refine_poses.ensure(host_bytes);
+    h2d(ctx, db, hb, host_bytes);
+    ea_outcome* dout = (ea_outcome*)db;
+    BeamDev* dbeam[2] = {(BeamDev*)(db + sizeof(ea_outcome)),
+                         (BeamDev*)(db + sizeof(ea_outcome) + beam_bytes)};
+    int* dcnt[2] = {(int*)(db + sizeof(ea_outcome) + 2 * beam_bytes),
+                    (int*)(db + sizeof(ea_outcome) + 2 * beam_bytes) + 1};
+    const double* dtab = (const double*)(db + head);
+    double* votes = (double*)ctx->refine_scores.ensure(sizeof(double) * (size_t)n_max * E);
+    double* entries = (double*)ctx->beam.ensure(sizeof(double) * 4 * E);
+    const ea_score_params& sp = cfg.score_params;
+    int cur = 0;
+    for (int d = 1; d <= top; ++d) {
+        const int level = top - d;
+        const ea_model* m = lv->models[level];
+        const ea_field* f = lv->fields[level];
+        RefineArgs a{};
+        a.pts = m->pts.as<double>();
+        a.n = m->n;
+        a.gx = f->gx();
+        a.gy = f->gy();
+        a.mag = f->mag();
+        a.W = f->width;
+        a.H = f->height;
+        a.vote_R = (sp.neighborhood - 1) / 2;
+        a.ignore = sp.polarity == EA_POLARITY_IGNORE;
+        a.eps = sp.eps_mag;
+        a.R = R;
+        a.side = side;
+        a.topk = k;
+        a.max_parents = k;
+        a.chunk = 16;
+        a.level = level;
+        a.trace_slot = d;
+        a.step_x = sx[d];
+        a.step_y = sy[d];
+        a.min_score = cfg.min_score;
+        a.table = dtab + toff[d];
+        a.beam = dbeam[cur];
+        a.beam_count = dcnt[cur];
+        a.beam_out = dbeam[cur ^ 1];
+        a.beam_count_out = dcnt[cur ^ 1];
+        a.votes = votes;
+        a.entries = entries;
+        a.outcome = dout;
+        launch_refine_level(ctx, a);
+        cur ^= 1;
+    }
+    d2h(ctx, out, dout, sizeof(ea_outcome));
+    sync(ctx);
 }
 
 ea_pose_grid top_grid_of(const ea_search_config& cfg) {  // search.cpp:264-273
@@ -722,6 +882,7 @@ void ea_ctx_destroy(ea_ctx* ctx) {
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
     for (DevBuf* b : {&ctx->cs, &ctx->rot_exact, &ctx->rot_screen, &ctx->plane, &ctx->map,
+                      &ctx->item_max, &ctx->tail,
                       &ctx->hist, &ctx->ctrl, &ctx->cand, &ctx->cand_score, &ctx->topk,
                       &ctx->refine_poses, &ctx->refine_scores, &ctx->beam, &ctx->accum64,
                       &ctx->work})
@@ -1056,6 +1217,7 @@ ea_status ea_rotate_model(ea_ctx* ctx, const ea_model* m, double theta, double* 
         const int n = m->n;
         if (n == 0) return;
         const double hcs[2] = {std::cos(theta), std::sin(theta)};
+        ctx->cs_dev_key.clear();
         double* dcs = (double*)ctx->cs.ensure(sizeof(double) * 2);
         h2d_staged(ctx, dcs, hcs, sizeof hcs);
         double* rot = (double*)ctx->rot_exact.ensure(sizeof(double) * 4 * n);
@@ -1184,6 +1346,7 @@ ea_status ea_score_map(ea_ctx* ctx, const ea_model* m, const ea_field* f, const 
         DeviceGuard dg(ctx->device);
         const int n = m->n;
         const std::vector<double>& cs = theta_cs(ctx, g->t0, g->dt, c.nt);
+        ctx->cs_dev_key.clear();
         double* dcs = (double*)ctx->cs.ensure(sizeof(double) * 2 * c.nt);
         h2d_staged(ctx, dcs, cs.data(), sizeof(double) * 2 * c.nt);
         const size_t pairs = (size_t)c.nt * n;
@@ -1428,17 +1591,29 @@ ea_status ea_detect(ea_ctx* ctx, ea_levels* lv, const double* image, int w, int 
         DeviceGuard dg(ctx->device);
         if ((int)lv->models.size() < cfg->num_levels)
             fail(EA_ERR_INVALID_ARGUMENT, "prepared levels do not cover num_levels");
+        if (ctx->timing) EAB_CUDA(cudaEventRecord(ctx->ev[4], ctx->stream));
         set_working_image(ctx, lv, image, w, h, cfg->num_levels);
+        if (ctx->timing) EAB_CUDA(cudaEventRecord(ctx->ev[5], ctx->stream));
         check_search_config(lv, *cfg);
         const int top = cfg->num_levels - 1;
         const ea_pose_grid tg = top_grid_of(*cfg);
+        const int launched0 = ctx->stats.kernels_launched;
         const auto seeds = top_search(ctx, lv->models[top], lv->fields[top], tg,
                                       cfg->score_params, cfg->topk, 0, 0);
-        const ea_search_stats keep = ctx->stats;
+        ea_search_stats keep = ctx->stats;
+        if (ctx->timing) EAB_CUDA(cudaEventRecord(ctx->ev[6], ctx->stream));
         refine_levels(ctx, lv, *cfg, tg, seeds_to_beam(seeds), out);
-        const int launched = ctx->stats.kernels_launched;
+        if (ctx->timing) {
+            EAB_CUDA(cudaEventRecord(ctx->ev[7], ctx->stream));
+            EAB_CUDA(cudaEventSynchronize(ctx->ev[7]));
+            float ms = 0.f;
+            EAB_CUDA(cudaEventElapsedTime(&ms, ctx->ev[4], ctx->ev[5]));
+            keep.image_ms = ms;
+            EAB_CUDA(cudaEventElapsedTime(&ms, ctx->ev[6], ctx->ev[7]));
+            keep.refine_ms = ms;
+        }
+        keep.kernels_launched = launched0 + ctx->stats.kernels_launched;
         ctx->stats = keep;
-        ctx->stats.kernels_launched = launched;
     });
 }
 

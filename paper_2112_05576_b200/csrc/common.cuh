@@ -105,13 +105,14 @@ struct ea_ctx {
     uint64_t launches = 0;
     ea_search_stats stats{};
     bool timing = false;
-    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    cudaEvent_t ev[8] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
     // scratch
-    eab::DevBuf cs, rot_exact, rot_screen, plane, map, hist, ctrl, cand, cand_score, topk,
+    eab::DevBuf cs, rot_exact, rot_screen, plane, map, item_max, tail, hist, ctrl, cand, cand_score, topk,
         refine_poses, refine_scores, beam, accum64, work;
     eab::HostBuf h_stage, h_out;
     // glibc cos/sin tables of theta grids, cached per (t0, dt, nt)
     std::map<std::vector<double>, std::vector<double>> cs_cache;
+    std::vector<double> cs_dev_key;  // what ctx->cs currently holds on the device
 };
 
 namespace eab {

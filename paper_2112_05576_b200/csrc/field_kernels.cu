@@ -60,25 +60,39 @@ __global__ void sobel_kernel(const double* __restrict__ img, int w, int h,
 // latter gives exactly the reference's neutral 0 vote (kernels_scalar.cpp:44-47).
 // Also records whether the field's own outer ring votes 0 everywhere, which
 // is what makes the zero ring equivalent to the reference's window clipping.
+// The fp16 variant rounds g/|g| from fp64 directly to half (one rounding,
+// |error| <= 2^-11 |n| per component; the screening bound accounts for it).
+template <typename PX>
+__device__ __forceinline__ PX make_px(double nx, double ny);
+template <>
+__device__ __forceinline__ float2 make_px<float2>(double nx, double ny) {
+    return make_float2((float)nx, (float)ny);
+}
+template <>
+__device__ __forceinline__ __half2 make_px<__half2>(double nx, double ny) {
+    return __halves2half2(__double2half(nx), __double2half(ny));
+}
+
+template <typename PX>
 __global__ void plane_kernel(const double* __restrict__ gx, const double* __restrict__ gy,
                              const double* __restrict__ mag, int W, int H, double eps,
-                             int PW, int PL, int shift, float2* __restrict__ plane,
+                             int PW, int PL, int shift, PX* __restrict__ plane,
                              int* __restrict__ ring_bad) {
     const int xp = blockIdx.x * blockDim.x + threadIdx.x;
     const int yp = blockIdx.y;
     if (xp >= PW || yp >= H + 2) return;
-    float2 v = make_float2(0.f, 0.f);
+    double nx = 0.0, ny = 0.0;
     const int x = xp - 1 - PL, y = yp - 1;
     if (x >= 0 && x < W && y >= 0 && y < H) {
         const size_t o = (size_t)y * W + x;
         const double m = mag[o];
         if (m >= eps) {
-            v.x = (float)__ddiv_rn(gx[o], m);
-            v.y = (float)__ddiv_rn(gy[o], m);
+            nx = __ddiv_rn(gx[o], m);
+            ny = __ddiv_rn(gy[o], m);
             if (x == 0 || y == 0 || x == W - 1 || y == H - 1) atomicOr(ring_bad, 1);
         }
     }
-    plane[(size_t)yp * PW + (yp >> shift) + xp] = v;
+    plane[(size_t)yp * PW + (yp >> shift) + xp] = make_px<PX>(nx, ny);
 }
 
 void launch_downsample(ea_ctx* ctx, const double* in, int w, int h, double* out) {
@@ -99,10 +113,17 @@ void launch_sobel(ea_ctx* ctx, const double* img, int w, int h, double* gx, doub
 }
 
 void launch_plane(ea_ctx* ctx, const ea_field* f, double eps, const PlaneGeom& g,
-                  float2* plane, int* ring_bad) {
+                  void* plane, int* ring_bad) {
     dim3 grid((g.PW + 127) / 128, g.H + 2);
-    plane_kernel<<<grid, 128, 0, ctx->stream>>>(f->gx(), f->gy(), f->mag(), g.W, g.H, eps,
-                                                g.PW, g.PL, g.shift, plane, ring_bad);
+    if (g.elem_bytes == 4) {
+        plane_kernel<__half2><<<grid, 128, 0, ctx->stream>>>(
+            f->gx(), f->gy(), f->mag(), g.W, g.H, eps, g.PW, g.PL, g.shift,
+            static_cast<__half2*>(plane), ring_bad);
+    } else {
+        plane_kernel<float2><<<grid, 128, 0, ctx->stream>>>(
+            f->gx(), f->gy(), f->mag(), g.W, g.H, eps, g.PW, g.PL, g.shift,
+            static_cast<float2*>(plane), ring_bad);
+    }
     check_launch("plane_kernel");
     count_launch(ctx);
 }

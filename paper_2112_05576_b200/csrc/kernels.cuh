@@ -2,6 +2,7 @@
 // shared by the device kernels.
 #pragma once
 
+#include <cuda_fp16.h>
 #include <math.h>
 
 #include "common.cuh"
@@ -20,23 +21,33 @@ struct PlaneGeom {
     int PL = 0, PR = 0; // extra zero columns left / right of the ring
     int PW = 0;         // row pitch in float2 (= W + 2 + PL + PR)
     int shift = 4;      // row skew: element (xp, yp) at yp*PW + (yp >> shift) + xp
-    int zero = 0;       // offset of a PW + 16 zero strip standing in for off-plane rows
-    size_t elems = 0;   // float2 count incl. the strip (rounded to 2 for 16 B copies)
+    int zero = 0;       // offset of a PW + banks zero strip standing in for off-plane rows
+    int elem_bytes = 8; // 8: float2 (nx, ny); 4: __half2 (nx, ny)
+    size_t elems = 0;   // element count incl. the strip (whole 16 B chunks)
+    size_t bytes() const { return elems * (size_t)elem_bytes; }
+    int banks() const { return 128 / elem_bytes; }  // elements per 128 B wavefront
 };
 
-inline PlaneGeom plane_geom(int W, int H, int shift, int PL = 0, int PR = 0) {
+inline PlaneGeom plane_geom(int W, int H, int shift, int PL = 0, int PR = 0, int elem_bytes = 8) {
     PlaneGeom g;
     g.W = W;
     g.H = H;
     g.PL = PL;
-    g.PR = PR;
+    g.elem_bytes = elem_bytes;
+    // pitch: 2^shift * PW must be a multiple of the wavefront's element count
+    // so that lanes' slots are yg + 8*xg exactly
+    const int mult = g.banks() >> shift > 1 ? g.banks() >> shift : 1;
     g.PW = W + 2 + PL + PR;
+    g.PW = (g.PW + mult - 1) / mult * mult;
+    g.PR = g.PW - (W + 2 + PL);
     g.shift = shift;
+    const size_t B = (size_t)g.banks();
     size_t e = (size_t)(H + 2) * g.PW + (size_t)((H + 1) >> shift) + 1;
-    e = (e + 15) & ~(size_t)15;
+    e = (e + B - 1) / B * B;
     g.zero = (int)e;
-    e += (size_t)g.PW + 16;
-    g.elems = (e + 1) & ~(size_t)1;
+    e += (size_t)g.PW + B;
+    const size_t per16 = 16 / (size_t)elem_bytes;
+    g.elems = (e + per16 - 1) / per16 * per16;
     return g;
 }
 
@@ -104,6 +115,17 @@ __device__ __forceinline__ double point_term_exact(double rpx, double rpy, doubl
     return 0.0;
 }
 
+// Monotone integer image of a double under fp64 comparison (-0 == +0; the
+// scores compared are never NaN): ranks and maxima run on the integer pipe,
+// which on B200 is far wider than the fp64 compare path.
+__device__ __forceinline__ long long order_key(double v) {
+    const long long b = __double_as_longlong(v == 0.0 ? 0.0 : v);
+    return b < 0 ? (b ^ 0x7FFFFFFFFFFFFFFFLL) : b;
+}
+__device__ __forceinline__ double from_order_key(long long k) {
+    return __longlong_as_double(k < 0 ? (k ^ 0x7FFFFFFFFFFFFFFFLL) : k);
+}
+
 // pose_at arithmetic (pose.h:84-91): base + (double)i * step, no contraction.
 __device__ __forceinline__ double lattice(double base, unsigned long long i, double step) {
     return __dadd_rn(base, __dmul_rn((double)i, step));
@@ -114,7 +136,7 @@ void launch_downsample(ea_ctx* ctx, const double* in, int w, int h, double* out)
 void launch_sobel(ea_ctx* ctx, const double* img, int w, int h, double* gx, double* gy,
                   double* mag);
 void launch_plane(ea_ctx* ctx, const ea_field* f, double eps, const PlaneGeom& g,
-                  float2* plane, int* ring_bad);
+                  void* plane, int* ring_bad);
 
 // rotate_model for many thetas: rot_exact = px|py|dx|dy (each nth*n doubles),
 // rot_screen = {ox, oy, dxf, dyf} per (theta, point) for the lattice kernel.
@@ -122,7 +144,7 @@ void launch_rotate(ea_ctx* ctx, const double* pts_soa, int n, const double* cs, 
                    double* rot_exact, int4* rot_screen, int* flags);
 
 struct ScreenArgs {
-    const float2* plane;
+    const void* plane;        // float2 or __half2 elements (geom.elem_bytes)
     PlaneGeom geom;
     const int4* rot_screen;     // [theta - it_begin][point]
     const double* rot_exact;    // px | py | dx | dy, rows theta - it_begin
@@ -140,6 +162,7 @@ struct ScreenArgs {
     unsigned B3;      // bits of K
     float scale;      // 2^(e-22) / n
     float* map;       // (it - it_begin) * nx * ny + iy * nx + ix
+    float* item_max;  // best screen score per work item (lattice tile / 32 poses)
     unsigned* hist;   // kHistBins
     SearchCtrl* ctrl;
 };
@@ -155,7 +178,15 @@ void launch_threshold(ea_ctx* ctx, const unsigned* hist, int k, double delta, in
                       SearchCtrl* ctrl);
 void launch_point_vote(ea_ctx* ctx, const ea_field* f, int cx, int cy, int R, double dx,
                        double dy, double eps, bool absolute, double* out);
-void launch_compact(ea_ctx* ctx, const float* map, unsigned long long count,
+// Work-item geometry of the screening map, for the compaction pass.
+struct ItemGeom {
+    unsigned long long n_items;
+    int lattice;           // 1: items are (theta, wy, wx) tiles of 32 x rows poses
+    unsigned nwx, nwy, rows;
+    unsigned long long nx, ny, total;
+};
+ItemGeom screen_items(const ScreenArgs& a, bool fast);
+void launch_compact(ea_ctx* ctx, const float* map, const float* item_max, const ItemGeom& g,
                     SearchCtrl* ctrl, unsigned* cand, unsigned long long cap);
 
 struct ExactArgs {

@@ -1,0 +1,40 @@
+// refine.cuh -- device-resident beam refinement (search.cpp:254-357).
+#pragma once
+
+#include "common.cuh"
+
+namespace eab {
+
+// One beam entry: pose in the current level's coordinates (BeamEntry,
+// search.cpp:242-246) + the kt path that indexes its theta table.
+struct BeamDev {
+    double ux, uy, theta, score;
+    unsigned long long top_index;
+    int path;
+    int _pad;
+};
+
+struct RefineArgs {
+    const double* pts;  // model SoA x|y|dx|dy at this level
+    int n;
+    const double* gx;
+    const double* gy;
+    const double* mag;
+    int W, H;
+    int vote_R, ignore;
+    double eps;
+    int R, side, topk, max_parents, chunk, level, trace_slot;
+    double step_x, step_y, min_score;
+    const double* table;  // (theta, cos, sin) per path of this level
+    const BeamDev* beam;  // parents
+    const int* beam_count;
+    BeamDev* beam_out;
+    int* beam_count_out;
+    double* votes;        // [entry][point], pose-major
+    double* entries;      // [entry] score, ux, uy, theta
+    ea_outcome* outcome;  // device copy of the result
+};
+
+void launch_refine_level(ea_ctx* ctx, const RefineArgs& a);
+
+}  // namespace eab

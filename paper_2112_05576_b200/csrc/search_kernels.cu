@@ -20,6 +20,10 @@
 // the k-th largest S_f, every pose of the true top k has S_f >= T - 2*delta,
 // so the exact pass sees all of them (and every pose tied with the k-th);
 // selecting by `better` over exact scores reproduces search_topk bit for bit.
+#include <algorithm>
+#include <climits>
+#include <cstdlib>
+
 #include <cub/block/block_scan.cuh>
 
 #include "kernels.cuh"
@@ -122,8 +126,11 @@ constexpr int kTW = 8;  // poses per lane along x
 // its windows touch.  CLAMP=false is the warp-uniform interior case (every
 // column of the warp's windows lies inside the padded plane): loads address
 // [row + immediate].  CLAMP=true clamps each column into the zero ring.
-template <int R, int S, int SHIFT, bool IGNORE, bool CLAMP>
-__device__ __forceinline__ void point_rows(const float2* __restrict__ P, const int PW,
+__device__ __forceinline__ float2 px_f32(float2 v) { return v; }
+__device__ __forceinline__ float2 px_f32(__half2 v) { return __half22float2(v); }
+
+template <int R, int S, int SHIFT, bool IGNORE, bool CLAMP, typename PX>
+__device__ __forceinline__ void point_rows(const PX* __restrict__ P, const int PW,
                                            const int XL, const int cx_lo, const int cx_hi,
                                            const int H1, const int Z, const int cb,
                                            const int rb, const float dxf, const float dyf,
@@ -150,16 +157,17 @@ __device__ __forceinline__ void point_rows(const float2* __restrict__ P, const i
 #pragma unroll
     for (int r = 0; r < NR; ++r) {
         // Rows off the plane read the zero strip at an offset congruent (mod
-        // 16 float2 slots) to where the row would be, so the lanes' bank
-        // spacing survives at the top/bottom edges.
+        // one wavefront of elements) to where the row would be, so the lanes'
+        // bank spacing survives at the top/bottom edges.
+        constexpr int kBankMask = 128 / (int)sizeof(PX) - 1;
         const int yv = rb + r;
         const int va = yv * PW + (yv >> SHIFT);
-        const float2* row = P + (((unsigned)yv <= (unsigned)H1) ? va : Z + (va & 15));
+        const PX* row = P + (((unsigned)yv <= (unsigned)H1) ? va : Z + (va & kBankMask));
         if constexpr (!CLAMP) row += cb;
         float c[NC];
 #pragma unroll
         for (int m = 0; m < NC; ++m) {
-            const float2 v = CLAMP ? row[col[m]] : row[m];
+            const float2 v = px_f32(CLAMP ? row[col[m]] : row[m]);
             if constexpr (IGNORE) {
                 c[m] = fabsf(fmaf(dyf, v.y, dxf * v.x));
             } else {
@@ -212,13 +220,25 @@ __device__ __forceinline__ void point_rows(const float2* __restrict__ P, const i
 // yg*(2^SHIFT*PW + 1) + 8*xg = yg + 8*xg thanks to the row skew (yp >> SHIFT),
 // so each half-warp (yg 0..7 x two xg) covers all 16 bank pairs once: LDS.64
 // at the 2-wavefront minimum.
-template <int R, int S, int SHIFT, bool IGNORE>
+// Tail split: N items on P warps leave a last partial round of N mod P items;
+// those are cut into f point-chunks (micro-items) so every warp ends with a
+// short piece.  Chunk partial sums are exact int32, merged with coalesced
+// reductions in L2; the chunk that arrives last finalises the tile.
+struct TailPlan {
+    unsigned long long n_main;  // items processed whole
+    unsigned long long n_tail;  // items split into f point-chunks
+    int f;
+    int* part;                  // [n_tail][S*8][32] partial sums
+    unsigned* done;             // [n_tail] arrival counters
+};
+
+template <int R, int S, int SHIFT, bool IGNORE, typename PX>
 __global__ void __launch_bounds__(screen_threads<S>(), 1)
     screen_fast_kernel(const ScreenArgs a, const unsigned nwx, const unsigned nwy,
-                       const unsigned long long total_items, const int vec16) {
+                       const TailPlan tp, const int vec16) {
     extern __shared__ __align__(16) unsigned char smem[];
     unsigned* hist = reinterpret_cast<unsigned*>(smem);
-    float2* P = reinterpret_cast<float2*>(smem + kHistBins * sizeof(unsigned));
+    PX* P = reinterpret_cast<PX*>(smem + kHistBins * sizeof(unsigned));
     {
         const int4* src = reinterpret_cast<const int4*>(a.plane);
         int4* dst = reinterpret_cast<int4*>(P);
@@ -228,6 +248,7 @@ __global__ void __launch_bounds__(screen_threads<S>(), 1)
     __syncthreads();
 
     constexpr int NC = kTW + 2 * R;
+    constexpr int NACC = S * kTW;
     const int lane = threadIdx.x & 31;
     const int yg = lane & 7, xg = lane >> 3;
     const int H1 = a.geom.H + 1, PW = a.geom.PW, XL = a.geom.PW - 1;
@@ -235,12 +256,24 @@ __global__ void __launch_bounds__(screen_threads<S>(), 1)
     const float K = a.K;
     const int B3 = (int)a.B3;
     const unsigned long long plane_poses = a.nx * a.ny;
+    const unsigned long long total = tp.n_main + tp.n_tail * (unsigned long long)tp.f;
 
     for (;;) {
-        unsigned long long item = 0;
-        if (lane == 0) item = atomicAdd(&a.ctrl->work_counter, 1ull);
-        item = __shfl_sync(0xffffffffu, item, 0);
-        if (item >= total_items) break;
+        unsigned long long work = 0;
+        if (lane == 0) work = atomicAdd(&a.ctrl->work_counter, 1ull);
+        work = __shfl_sync(0xffffffffu, work, 0);
+        if (work >= total) break;
+        unsigned long long item = work;
+        long long tslot = -1;
+        int p0 = 0, p1 = a.n;
+        if (work >= tp.n_main) {
+            const unsigned long long m = work - tp.n_main;
+            tslot = (long long)(m / (unsigned)tp.f);
+            const int ch = (int)(m % (unsigned)tp.f);
+            item = tp.n_main + (unsigned long long)tslot;
+            p0 = (int)((long long)ch * a.n / tp.f);
+            p1 = (int)((long long)(ch + 1) * a.n / tp.f);
+        }
         const unsigned wx = (unsigned)(item % nwx);
         const unsigned long long rest = item / nwx;
         const unsigned wy = (unsigned)(rest % nwy);
@@ -256,23 +289,43 @@ __global__ void __launch_bounds__(screen_threads<S>(), 1)
 #pragma unroll
             for (int j = 0; j < kTW; ++j) acc[s][j] = 0;
 
-        int4 p = __ldg(rot);
-        for (int i = 0; i < a.n; ++i) {
-            const int4 pn = __ldg(rot + (i + 1 < a.n ? i + 1 : i));
-            const float dxf = __int_as_float(p.z), dyf = __int_as_float(p.w);
-            const int cb = p.x + a.ix0 + X - R + cx_lo;   // padded column of window start
-            const int rb = p.y + a.iy0 + Y - R + 1;       // padded row of window start
-            const int cw = p.x + a.ix0 + X0 - R + cx_lo;  // warp's first column (uniform)
-            if (cw >= 0 && cw + 24 + NC - 1 <= XL) {
-                point_rows<R, S, SHIFT, IGNORE, false>(P, PW, XL, cx_lo, cx_hi, H1, Z, cb, rb,
-                                                      dxf, dyf, K, B3, acc);
-            } else {
-                point_rows<R, S, SHIFT, IGNORE, true>(P, PW, XL, cx_lo, cx_hi, H1, Z, cb, rb,
-                                                     dxf, dyf, K, B3, acc);
+        if (p0 < p1) {
+            int4 p = __ldg(rot + p0);
+            for (int i = p0; i < p1; ++i) {
+                const int4 pn = __ldg(rot + (i + 1 < p1 ? i + 1 : i));
+                const float dxf = __int_as_float(p.z), dyf = __int_as_float(p.w);
+                const int cb = p.x + a.ix0 + X - R + cx_lo;   // padded column of window start
+                const int rb = p.y + a.iy0 + Y - R + 1;       // padded row of window start
+                const int cw = p.x + a.ix0 + X0 - R + cx_lo;  // warp's first column (uniform)
+                if (cw >= 0 && cw + 24 + NC - 1 <= XL) {
+                    point_rows<R, S, SHIFT, IGNORE, false, PX>(P, PW, XL, cx_lo, cx_hi, H1, Z,
+                                                              cb, rb, dxf, dyf, K, B3, acc);
+                } else {
+                    point_rows<R, S, SHIFT, IGNORE, true, PX>(P, PW, XL, cx_lo, cx_hi, H1, Z,
+                                                             cb, rb, dxf, dyf, K, B3, acc);
+                }
+                p = pn;
             }
-            p = pn;
+        }
+        if (tslot >= 0) {  // micro-item: merge, last arrival finalises
+            int* part = tp.part + (size_t)tslot * NACC * 32;
+#pragma unroll
+            for (int s = 0; s < S; ++s)
+#pragma unroll
+                for (int j = 0; j < kTW; ++j) atomicAdd(part + (s * kTW + j) * 32 + lane, acc[s][j]);
+            __threadfence();
+            unsigned old = 0;
+            if (lane == 0) old = atomicAdd(tp.done + tslot, 1u);
+            old = __shfl_sync(0xffffffffu, old, 0);
+            if (old != (unsigned)tp.f - 1u) continue;
+            __threadfence();
+#pragma unroll
+            for (int s = 0; s < S; ++s)
+#pragma unroll
+                for (int j = 0; j < kTW; ++j) acc[s][j] = __ldcg(part + (s * kTW + j) * 32 + lane);
         }
         float* out = a.map + (size_t)itr * plane_poses;
+        float best = -INFINITY;
 #pragma unroll
         for (int s = 0; s < S; ++s) {
             const unsigned long long iy = (unsigned long long)(Y + s);
@@ -282,10 +335,14 @@ __global__ void __launch_bounds__(screen_threads<S>(), 1)
                 if (ix < a.nx && iy < a.ny) {
                     const float sc = (float)acc[s][j] * a.scale;
                     out[iy * a.nx + ix] = sc;
+                    best = fmaxf(best, sc);
                     atomicAdd(&hist[hist_bin(sc)], 1u);
                 }
             }
         }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) best = fmaxf(best, __shfl_xor_sync(0xffffffffu, best, o));
+        if (lane == 0) a.item_max[item] = best;
     }
     __syncthreads();
     for (int b = threadIdx.x; b < kHistBins; b += blockDim.x) {
@@ -294,46 +351,66 @@ __global__ void __launch_bounds__(screen_threads<S>(), 1)
     }
 }
 
-template <int R, int S, int SHIFT, bool IGNORE>
+template <int R, int S, int SHIFT, bool IGNORE, typename PX>
 static void run_fast(ea_ctx* ctx, const ScreenArgs& a) {
     const unsigned nwx = (unsigned)((a.nx + 31) / 32);
     const unsigned nwy = (unsigned)((a.ny + 8 * S - 1) / (8 * S));
     const unsigned long long items = (unsigned long long)nwx * nwy * a.it_count;
-    const size_t plane_bytes = ((a.geom.elems * sizeof(float2)) + 15) & ~(size_t)15;
+    const size_t plane_bytes = (a.geom.bytes() + 15) & ~(size_t)15;
     const size_t smem = kHistBins * sizeof(unsigned) + plane_bytes;
-    auto kern = screen_fast_kernel<R, S, SHIFT, IGNORE>;
+    auto kern = screen_fast_kernel<R, S, SHIFT, IGNORE, PX>;
     EAB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     constexpr int threads = screen_threads<S>();
     unsigned long long warps_per_cta = threads / 32;
     unsigned long long ctas = (items + warps_per_cta - 1) / warps_per_cta;
     if (ctas > (unsigned long long)ctx->sm_count) ctas = ctx->sm_count;
     if (ctas == 0) ctas = 1;
-    kern<<<(unsigned)ctas, threads, smem, ctx->stream>>>(a, nwx, nwy, items,
-                                                                (int)(plane_bytes / 16));
+    // tail split (see TailPlan)
+    TailPlan tp{items, 0, 1, nullptr, nullptr};
+    const unsigned long long P = ctas * warps_per_cta;
+    const unsigned long long rem = items % P;
+    const bool split = std::getenv("EAB_NO_TAIL_SPLIT") == nullptr;
+    if (split && rem > 0 && a.n >= 8) {
+        int f = (int)std::min<unsigned long long>(P / rem, (unsigned long long)(a.n / 4));
+        if (f >= 2) {
+            tp.n_main = items - rem;
+            tp.n_tail = rem;
+            tp.f = f;
+            const size_t part_bytes = rem * (size_t)S * kTW * 32 * sizeof(int);
+            char* buf = (char*)ctx->tail.ensure(part_bytes + rem * sizeof(unsigned));
+            tp.part = (int*)buf;
+            tp.done = (unsigned*)(buf + part_bytes);
+            EAB_CUDA(cudaMemsetAsync(buf, 0, part_bytes + rem * sizeof(unsigned), ctx->stream));
+        }
+    }
+    kern<<<(unsigned)ctas, threads, smem, ctx->stream>>>(a, nwx, nwy, tp, (int)(plane_bytes / 16));
     check_launch("screen_fast_kernel");
     count_launch(ctx);
 }
 
 size_t fast_smem_bytes(const PlaneGeom& g) {
-    return kHistBins * sizeof(unsigned) + (((g.elems * sizeof(float2)) + 15) & ~(size_t)15);
+    return kHistBins * sizeof(unsigned) + ((g.bytes() + 15) & ~(size_t)15);
 }
 
 bool launch_screen_fast(ea_ctx* ctx, const ScreenArgs& a) {
     if (fast_smem_bytes(a.geom) > ctx->smem_optin) return false;
+    if (a.geom.shift != 3) return false;  // 8-row lane strips
     const bool ig = a.ignore != 0;
-    const int S = a.geom.shift == 3 ? 8 : 16;
-#define EAB_FAST(RR, SS, SH)                                        \
-    if (a.R == RR && S == SS) {                                     \
-        if (ig) run_fast<RR, SS, SH, true>(ctx, a);                 \
-        else run_fast<RR, SS, SH, false>(ctx, a);                   \
-        return true;                                                \
+    const bool half = a.geom.elem_bytes == 4;
+#define EAB_FAST(RR)                                                        \
+    if (a.R == RR) {                                                        \
+        if (half) {                                                         \
+            if (ig) run_fast<RR, 8, 3, true, __half2>(ctx, a);              \
+            else run_fast<RR, 8, 3, false, __half2>(ctx, a);                \
+        } else {                                                            \
+            if (ig) run_fast<RR, 8, 3, true, float2>(ctx, a);               \
+            else run_fast<RR, 8, 3, false, float2>(ctx, a);                 \
+        }                                                                   \
+        return true;                                                        \
     }
-    EAB_FAST(1, 16, 4)
-    EAB_FAST(1, 8, 3)
-    EAB_FAST(0, 16, 4)
-    EAB_FAST(0, 8, 3)
-    EAB_FAST(2, 16, 4)
-    EAB_FAST(2, 8, 3)
+    EAB_FAST(1)
+    EAB_FAST(0)
+    EAB_FAST(2)
 #undef EAB_FAST
     return false;
 }
@@ -353,8 +430,12 @@ __global__ void __launch_bounds__(256)
     const int R = a.R;
     const float K = a.K;
     const int B3 = (int)a.B3;
-    for (unsigned long long t = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
-         t < total; t += (unsigned long long)gridDim.x * blockDim.x) {
+    const int lane = threadIdx.x & 31;
+    for (unsigned long long t0 = (unsigned long long)blockIdx.x * blockDim.x + (threadIdx.x & ~31u);
+         t0 < total; t0 += (unsigned long long)gridDim.x * blockDim.x) {
+        const unsigned long long t = t0 + lane;
+        float sc = -INFINITY;
+        if (t < total) {
         const unsigned long long itr = t / plane_poses;
         const unsigned long long rem = t % plane_poses;
         const unsigned long long iy = rem / a.nx, ix = rem % a.nx;
@@ -378,7 +459,8 @@ __global__ void __launch_bounds__(256)
             float best = -INFINITY;
             for (int y = y0; y <= y1; ++y) {
                 const int yp = y + 1;
-                const float2* row = a.plane + (size_t)yp * PW + (yp >> SH) + 1 + a.geom.PL;
+                const float2* row = static_cast<const float2*>(a.plane) + (size_t)yp * PW +
+                                    (yp >> SH) + 1 + a.geom.PL;
                 for (int x = x0; x <= x1; ++x) {
                     const float2 v = __ldg(row + x);
                     const float c = IGNORE ? fabsf(fmaf(dyf, v.y, dxf * v.x))
@@ -389,9 +471,14 @@ __global__ void __launch_bounds__(256)
             if constexpr (IGNORE) best = best + K;
             acc += __float_as_int(best) - B3;
         }
-        const float sc = (float)acc * a.scale;
+        sc = (float)acc * a.scale;
         a.map[t] = sc;
         atomicAdd(&hist[hist_bin(sc)], 1u);
+        }
+        float best = sc;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) best = fmaxf(best, __shfl_xor_sync(0xffffffffu, best, o));
+        if (lane == 0) a.item_max[t0 >> 5] = best;
     }
     __syncthreads();
     for (int b = threadIdx.x; b < kHistBins; b += blockDim.x) {
@@ -475,39 +562,95 @@ void launch_threshold(ea_ctx* ctx, const unsigned* hist, int k, double delta, in
 }
 
 // ---- 4. compaction -----------------------------------------------------------
+// One warp per screening work item; items whose best score is below the band
+// threshold are skipped without touching the map (typically all but the few
+// tiles around the peaks).
 __global__ void __launch_bounds__(256) compact_kernel(const float* __restrict__ map,
-                                                      unsigned long long count,
-                                                      SearchCtrl* ctrl,
+                                                      const float* __restrict__ item_max,
+                                                      const ItemGeom g, SearchCtrl* ctrl,
                                                       unsigned* __restrict__ cand,
                                                       unsigned long long cap) {
     const float thr = ctrl->thr;
     const int lane = threadIdx.x & 31;
-    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
-    for (unsigned long long i0 = (unsigned long long)blockIdx.x * blockDim.x + (threadIdx.x & ~31);
-         i0 < count; i0 += stride) {
-        const unsigned long long i = i0 + lane;
-        const bool pred = i < count && __ldg(map + i) >= thr;
-        const unsigned mask = __ballot_sync(0xffffffffu, pred);
-        if (mask) {
-            const int leader = __ffs(mask) - 1;
-            unsigned long long base = 0;
-            if (lane == leader) base = atomicAdd(&ctrl->cand_count, (unsigned long long)__popc(mask));
-            base = __shfl_sync(0xffffffffu, base, leader);
-            if (pred) {
-                const unsigned long long slot = base + __popc(mask & ((1u << lane) - 1u));
-                if (slot < cap) cand[slot] = (unsigned)i;
+    const unsigned long long warp = ((unsigned long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const unsigned long long nwarps = ((unsigned long long)gridDim.x * blockDim.x) >> 5;
+    const unsigned long long plane = g.nx * g.ny;
+    for (unsigned long long it = warp; it < g.n_items; it += nwarps) {
+        if (!(__ldg(item_max + it) >= thr)) continue;
+        const unsigned steps = g.lattice ? g.rows : 1u;
+        unsigned long long base = 0, x = 0, y0 = 0;
+        if (g.lattice) {
+            const unsigned long long wx = it % g.nwx, rest = it / g.nwx;
+            const unsigned long long wy = rest % g.nwy, itr = rest / g.nwy;
+            base = itr * plane;
+            x = wx * 32 + lane;
+            y0 = wy * g.rows;
+        }
+        for (unsigned r0 = 0; r0 < steps; r0 += 16) {
+            // 16 rows of loads in flight before any ballot/atomic
+            float v[16];
+            unsigned long long idx[16];
+            bool okk[16];
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {
+                const unsigned r = r0 + q;
+                if (g.lattice) {
+                    const unsigned long long y = y0 + r;
+                    okk[q] = r < steps && x < g.nx && y < g.ny;
+                    idx[q] = base + y * g.nx + x;
+                } else {
+                    idx[q] = it * 32 + lane;
+                    okk[q] = q == 0 && idx[q] < g.total;
+                }
+                v[q] = okk[q] ? __ldg(map + idx[q]) : -INFINITY;
+            }
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {
+            const unsigned long long i = idx[q];
+            const bool pred = okk[q] && v[q] >= thr;
+            const unsigned mask = __ballot_sync(0xffffffffu, pred);
+            if (mask) {
+                const int leader = __ffs(mask) - 1;
+                unsigned long long slot0 = 0;
+                if (lane == leader)
+                    slot0 = atomicAdd(&ctrl->cand_count, (unsigned long long)__popc(mask));
+                slot0 = __shfl_sync(0xffffffffu, slot0, leader);
+                if (pred) {
+                    const unsigned long long slot = slot0 + __popc(mask & ((1u << lane) - 1u));
+                    if (slot < cap) cand[slot] = (unsigned)i;
+                }
+            }
             }
         }
     }
 }
 
-void launch_compact(ea_ctx* ctx, const float* map, unsigned long long count, SearchCtrl* ctrl,
-                    unsigned* cand, unsigned long long cap) {
-    unsigned long long blocks = (count + 255) / 256;
-    const unsigned long long maxb = (unsigned long long)ctx->sm_count * 8;
+ItemGeom screen_items(const ScreenArgs& a, bool fast) {
+    ItemGeom g{};
+    g.nx = a.nx;
+    g.ny = a.ny;
+    g.total = a.nx * a.ny * a.it_count;
+    if (fast) {
+        const unsigned S = a.geom.shift == 3 ? 8u : 16u;
+        g.lattice = 1;
+        g.rows = 8 * S;
+        g.nwx = (unsigned)((a.nx + 31) / 32);
+        g.nwy = (unsigned)((a.ny + g.rows - 1) / g.rows);
+        g.n_items = (unsigned long long)g.nwx * g.nwy * a.it_count;
+    } else {
+        g.lattice = 0;
+        g.n_items = (g.total + 31) / 32;
+    }
+    return g;
+}
+
+void launch_compact(ea_ctx* ctx, const float* map, const float* item_max, const ItemGeom& g,
+                    SearchCtrl* ctrl, unsigned* cand, unsigned long long cap) {
+    unsigned long long blocks = (g.n_items * 32 + 255) / 256;
+    const unsigned long long maxb = (unsigned long long)ctx->sm_count;
     if (blocks > maxb) blocks = maxb;
     if (blocks == 0) blocks = 1;
-    compact_kernel<<<(unsigned)blocks, 256, 0, ctx->stream>>>(map, count, ctrl, cand, cap);
+    compact_kernel<<<(unsigned)blocks, 256, 0, ctx->stream>>>(map, item_max, g, ctrl, cand, cap);
     check_launch("compact_kernel");
     count_launch(ctx);
 }
@@ -539,33 +682,83 @@ __device__ __forceinline__ double warp_pose_score(const ExactArgs& a, size_t bas
     return __ddiv_rn(sum, (double)a.n);
 }
 
+// One CTA per candidate pose: every (model point, window pixel) candidate of
+// the pose is evaluated in parallel in exact fp64 (kernels_scalar.cpp:43-54),
+// the per-point window maximum is taken with integer-key shared atomics (max
+// is order-free), and thread 0 adds the votes in model-point order
+// (similarity.cpp:109-118) -- the reference's fp64 score to the last bit.
+constexpr int kRescoreChunk = 256;
+
 __global__ void __launch_bounds__(256) rescore_kernel(const ExactArgs a,
                                                       const unsigned* __restrict__ cand,
                                                       const SearchCtrl* ctrl,
                                                       unsigned long long cap,
                                                       double* __restrict__ score) {
+    __shared__ long long vmax[kRescoreChunk];
+    __shared__ int2 centre[kRescoreChunk];
     unsigned long long nc = ctrl->cand_count;
     if (nc > cap) nc = cap;
-    const int lane = threadIdx.x & 31;
-    const unsigned long long warp = ((unsigned long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const unsigned long long nwarps = ((unsigned long long)gridDim.x * blockDim.x) >> 5;
     const unsigned long long plane = a.nx * a.ny;
-    for (unsigned long long c = warp; c < nc; c += nwarps) {
+    const int side = 2 * a.R + 1, W2 = side * side;
+    const size_t S = a.rot_stride;
+    const bool absolute = a.ignore != 0;
+    for (unsigned long long c = blockIdx.x; c < nc; c += gridDim.x) {
         const unsigned long long rel = cand[c];
-        const unsigned long long itl = rel / plane;  // theta row inside the slab
-        const unsigned long long rem = rel % plane;
+        const unsigned long long itl = rel / plane, rem = rel % plane;
         const double ux = lattice(a.x0, rem % a.nx, a.dx);
         const double uy = lattice(a.y0, rem / a.nx, a.dy);
-        const double s = warp_pose_score(a, (size_t)itl * a.n, ux, uy, lane, nullptr);
-        if (lane == 0) score[c] = s;
+        const size_t base = (size_t)itl * a.n;
+        double sum = 0.0;
+        for (int p0 = 0; p0 < a.n; p0 += kRescoreChunk) {
+            const int cn = min(kRescoreChunk, a.n - p0);
+            for (int t = threadIdx.x; t < cn; t += blockDim.x) {
+                const size_t q = base + p0 + t;
+                const double px = __dadd_rn(__ldg(a.rot_exact + q), ux);
+                const double py = __dadd_rn(__ldg(a.rot_exact + S + q), uy);
+                int2 cc = make_int2(-1, -1);  // (-1,-1): centre off the field, vote 0
+                if (px > -kCoordGuard && px < kCoordGuard && py > -kCoordGuard &&
+                    py < kCoordGuard) {
+                    const int cx = (int)floor(__dadd_rn(px, 0.5));
+                    const int cy = (int)floor(__dadd_rn(py, 0.5));
+                    if (cx >= 0 && cx < a.W && cy >= 0 && cy < a.H) cc = make_int2(cx, cy);
+                }
+                centre[t] = cc;
+                vmax[t] = LLONG_MIN;
+            }
+            __syncthreads();
+            for (int t = threadIdx.x; t < cn * W2; t += blockDim.x) {
+                const int i = t / W2, w = t % W2;
+                const int2 cc = centre[i];
+                if (cc.x < 0) continue;
+                const int x = cc.x + w % side - a.R, y = cc.y + w / side - a.R;
+                if (x < 0 || x >= a.W || y < 0 || y >= a.H) continue;  // clipped window
+                const size_t o = (size_t)y * a.W + x;
+                const size_t q = base + p0 + i;
+                const double m = __ldg(a.mag + o);
+                double cnd = 0.0;
+                if (m >= a.eps) {
+                    cnd = __ddiv_rn(__dadd_rn(__dmul_rn(__ldg(a.rot_exact + 2 * S + q), __ldg(a.gx + o)),
+                                              __dmul_rn(__ldg(a.rot_exact + 3 * S + q), __ldg(a.gy + o))),
+                                    m);
+                }
+                if (absolute) cnd = fabs(cnd);
+                atomicMax(&vmax[i], order_key(cnd));
+            }
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                for (int i = 0; i < cn; ++i)
+                    sum = __dadd_rn(sum, centre[i].x < 0 ? 0.0 : from_order_key(vmax[i]));
+            }
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) score[c] = __ddiv_rn(sum, (double)a.n);
     }
 }
 
 void launch_rescore(ea_ctx* ctx, const ExactArgs& a, const unsigned* cand,
                     const SearchCtrl* ctrl, unsigned long long cap, double* score) {
-    unsigned long long warps = cap;
-    unsigned long long blocks = (warps * 32 + 255) / 256;
-    const unsigned long long maxb = (unsigned long long)ctx->sm_count * 16;
+    unsigned long long blocks = cap;
+    const unsigned long long maxb = (unsigned long long)ctx->sm_count * 8;
     if (blocks > maxb) blocks = maxb;
     if (blocks == 0) blocks = 1;
     rescore_kernel<<<(unsigned)blocks, 256, 0, ctx->stream>>>(a, cand, ctrl, cap, score);
@@ -575,24 +768,25 @@ void launch_rescore(ea_ctx* ctx, const ExactArgs& a, const unsigned* cand,
 
 // ---- 6. top-k by `better` --------------------------------------------------------
 struct Best {
-    double s;
+    long long k;
     unsigned long long i;
     int ok;
 };
 
-__device__ __forceinline__ bool better(double sa, unsigned long long ia, double sb,
-                                       unsigned long long ib) {  // search.cpp:36-41
-    if (sa != sb) return sa > sb;
+// better (search.cpp:36-41) on order keys: score desc, then index asc.
+__device__ __forceinline__ bool better_k(long long ka, unsigned long long ia, long long kb,
+                                         unsigned long long ib) {
+    if (ka != kb) return ka > kb;
     return ia < ib;
 }
 
 __device__ __forceinline__ Best pick(Best x, Best y) {
     if (!x.ok) return y;
     if (!y.ok) return x;
-    return better(x.s, x.i, y.s, y.i) ? x : y;
+    return better_k(x.k, x.i, y.k, y.i) ? x : y;
 }
 
-__global__ void __launch_bounds__(1024) select_kernel(const unsigned* __restrict__ cand,
+__global__ void __launch_bounds__(256) select_kernel(const unsigned* __restrict__ cand,
                                                       const double* __restrict__ score,
                                                       SearchCtrl* ctrl, unsigned long long cap,
                                                       int k, unsigned long long index_base,
@@ -600,22 +794,33 @@ __global__ void __launch_bounds__(1024) select_kernel(const unsigned* __restrict
                                                       unsigned long long* out_index) {
     __shared__ Best warp_best[32];
     __shared__ Best prev;
+    constexpr int kStage = 2048;  // candidates staged in shared memory
+    __shared__ long long skey[kStage];
+    __shared__ unsigned long long sidx[kStage];
     unsigned long long nc = ctrl->cand_count;
     if (nc > cap) nc = cap;
     const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+    const bool staged = nc <= kStage;
+    if (staged) {
+        for (unsigned long long c = t; c < nc; c += blockDim.x) {
+            skey[c] = order_key(score[c]);
+            sidx[c] = index_base + cand[c];
+        }
+        __syncthreads();
+    }
     int r = 0;
     for (; r < k; ++r) {
-        Best b{0.0, 0ull, 0};
+        Best b{0, 0ull, 0};
         for (unsigned long long c = t; c < nc; c += blockDim.x) {
-            const double s = score[c];
-            const unsigned long long idx = index_base + cand[c];
-            if (r > 0 && !better(prev.s, prev.i, s, idx)) continue;
-            b = pick(b, Best{s, idx, 1});
+            const long long kk = staged ? skey[c] : order_key(score[c]);
+            const unsigned long long idx = staged ? sidx[c] : index_base + cand[c];
+            if (r > 0 && !better_k(prev.k, prev.i, kk, idx)) continue;
+            b = pick(b, Best{kk, idx, 1});
         }
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) {
             Best o;
-            o.s = __shfl_down_sync(0xffffffffu, b.s, off);
+            o.k = __shfl_down_sync(0xffffffffu, b.k, off);
             o.i = __shfl_down_sync(0xffffffffu, b.i, off);
             o.ok = __shfl_down_sync(0xffffffffu, b.ok, off);
             b = pick(b, o);
@@ -623,11 +828,11 @@ __global__ void __launch_bounds__(1024) select_kernel(const unsigned* __restrict
         if (lane == 0) warp_best[w] = b;
         __syncthreads();
         if (t == 0) {
-            Best f{0.0, 0ull, 0};
+            Best f{0, 0ull, 0};
             for (int q = 0; q < (int)(blockDim.x >> 5); ++q) f = pick(f, warp_best[q]);
             prev = f;
             if (f.ok) {
-                out_score[r] = f.s;
+                out_score[r] = from_order_key(f.k);
                 out_index[r] = f.i;
             }
         }
@@ -640,7 +845,7 @@ __global__ void __launch_bounds__(1024) select_kernel(const unsigned* __restrict
 void launch_select(ea_ctx* ctx, const unsigned* cand, const double* score, SearchCtrl* ctrl,
                    unsigned long long cap, int k, unsigned long long index_base,
                    double* out_score, unsigned long long* out_index) {
-    select_kernel<<<1, 1024, 0, ctx->stream>>>(cand, score, ctrl, cap, k, index_base, out_score,
+    select_kernel<<<1, 256, 0, ctx->stream>>>(cand, score, ctrl, cap, k, index_base, out_score,
                                                out_index);
     check_launch("select_kernel");
     count_launch(ctx);
