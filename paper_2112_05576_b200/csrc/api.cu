@@ -403,53 +403,85 @@ ExactArgs exact_args(const ea_field* f, const ea_score_params& p, const double* 
     return x;
 }
 
-// run_search (search.cpp:95-140) on theta indices [it_begin, it_end).
-std::vector<ea_scored_pose> top_search(ea_ctx* ctx, const ea_model* m, const ea_field* f,
-                                       const ea_pose_grid& g, const ea_score_params& p, int k,
-                                       uint64_t it_begin, uint64_t it_end) {
+// run_search (search.cpp:95-140) on theta indices [it_begin, it_end), split in
+// an enqueue half (everything up to the top-k select, results stay on the
+// device in ctx->topk) and a collect half (one D2H + sync).
+struct TopLaunch {
+    ScreenPlan plan;
+    unsigned long long cap = 0;
+    int k = 0, n = 0;
+    double* top_score = nullptr;
+    unsigned long long* top_index = nullptr;
+};
+
+TopLaunch top_enqueue(ea_ctx* ctx, const ea_model* m, const ea_field* f, const ea_pose_grid& g,
+                      const ea_score_params& p, int k, uint64_t it_begin, uint64_t it_end,
+                      unsigned long long cap) {
     validate_params(p);
     if (m->n == 0) fail(EA_ERR_INVALID_ARGUMENT, "search needs a nonempty model");
     if (k < 1) fail(EA_ERR_INVALID_ARGUMENT, "topk must be >= 1");
     ctx->stats = ea_search_stats{};
     if (ctx->timing) EAB_CUDA(cudaEventRecord(ctx->ev[0], ctx->stream));
-    const ScreenPlan plan = screen(ctx, m, f, g, p, it_begin, it_end);
-    std::vector<ea_scored_pose> out;
-    ctx->stats.poses = plan.slab_poses;
-    ctx->stats.pose_points = plan.slab_poses * (uint64_t)m->n;
-    if (plan.slab_poses == 0) return out;
-    const int n = m->n;
+    TopLaunch t;
+    t.plan = screen(ctx, m, f, g, p, it_begin, it_end);
+    t.k = k;
+    t.n = m->n;
+    t.cap = cap;
+    ctx->stats.poses = t.plan.slab_poses;
+    ctx->stats.pose_points = t.plan.slab_poses * (uint64_t)m->n;
     SearchCtrl* ctrl = ctx->ctrl.as<SearchCtrl>();
-    // delta widened on device by the rounding-ambiguous pairs (lattice path only)
-    launch_threshold(ctx, ctx->hist.as<unsigned>(), k, plan.delta, plan.fast ? n : 0, ctrl);
+    double* tk = (double*)ctx->topk.ensure((sizeof(double) + sizeof(unsigned long long)) * (size_t)k);
+    t.top_score = tk;
+    t.top_index = reinterpret_cast<unsigned long long*>(tk + k);
+    if (t.plan.slab_poses == 0) return t;
 
-    unsigned long long cap = std::max<size_t>(ctx->cand.cap / sizeof(unsigned), 1u << 16);
-    const size_t slab_pairs = plan.it_count * (size_t)n;
-    ExactArgs x = exact_args(f, p, ctx->rot_exact.as<double>(), slab_pairs, n);
-    x.nx = plan.c.nx;
-    x.ny = plan.c.ny;
-    x.it_begin = plan.it_begin;
+    const size_t slab_pairs = t.plan.it_count * (size_t)t.n;
+    ExactArgs x = exact_args(f, p, ctx->rot_exact.as<double>(), slab_pairs, t.n);
+    x.nx = t.plan.c.nx;
+    x.ny = t.plan.c.ny;
+    x.it_begin = t.plan.it_begin;
     x.x0 = g.x0;
     x.dx = g.dx;
     x.y0 = g.y0;
     x.dy = g.dy;
-    for (int attempt = 0; attempt < 2; ++attempt) {
-        unsigned* cand = (unsigned*)ctx->cand.ensure(sizeof(unsigned) * cap);
-        double* cs = (double*)ctx->cand_score.ensure(sizeof(double) * cap);
-        double* tk = (double*)ctx->topk.ensure((sizeof(double) + sizeof(unsigned long long)) *
-                                               (size_t)k);
-        unsigned long long* tki = reinterpret_cast<unsigned long long*>(tk + k);
-        if (attempt > 0) {
-            EAB_CUDA(cudaMemsetAsync(&ctrl->cand_count, 0, sizeof(unsigned long long),
-                                     ctx->stream));
-        }
-        launch_compact(ctx, ctx->map.as<float>(), ctx->item_max.as<float>(), plan.items, ctrl,
-                       cand, cap);
-        launch_rescore(ctx, x, cand, ctrl, cap, cs);
-        launch_select(ctx, cand, cs, ctrl, cap, k, plan.it_begin * plan.c.nx * plan.c.ny, tk, tki);
+    unsigned* cand = (unsigned*)ctx->cand.ensure(sizeof(unsigned) * cap);
+    double* cs = (double*)ctx->cand_score.ensure(sizeof(double) * cap);
+    // band threshold from the histogram (delta widened on the device by the
+    // rounding-ambiguous pairs, lattice path only), then the compaction
+    launch_compact(ctx, ctx->map.as<float>(), ctx->item_max.as<float>(), t.plan.items, ctrl, cand,
+                   cap, ctx->hist.as<unsigned>(), k, t.plan.delta, t.plan.fast ? t.n : 0);
+    launch_rescore(ctx, x, cand, ctrl, cap, cs);
+    launch_select(ctx, cand, cs, ctrl, cap, k, t.plan.it_begin * t.plan.c.nx * t.plan.c.ny,
+                  t.top_score, t.top_index);
+    return t;
+}
+
+// Stats from the control block; false when the band overflowed the buffer.
+bool top_stats(ea_ctx* ctx, const TopLaunch& t, const SearchCtrl& hc) {
+    ctx->stats.candidates = hc.cand_count;
+    ctx->stats.candidates_needed = hc.needed;
+    ctx->stats.threshold = hc.thr;
+    ctx->stats.flagged_points = hc.flags;
+    ctx->stats.screen_delta = t.plan.delta + (t.plan.fast ? 2.0 * hc.flags / t.n : 0.0);
+    return hc.cand_count <= t.cap;
+}
+
+unsigned long long initial_cap(ea_ctx* ctx) {
+    return std::max<size_t>(ctx->cand.cap / sizeof(unsigned), 1u << 16);
+}
+
+std::vector<ea_scored_pose> top_search(ea_ctx* ctx, const ea_model* m, const ea_field* f,
+                                       const ea_pose_grid& g, const ea_score_params& p, int k,
+                                       uint64_t it_begin, uint64_t it_end) {
+    unsigned long long cap = initial_cap(ctx);
+    for (int attempt = 0; attempt < 3; ++attempt) {
+        const TopLaunch t = top_enqueue(ctx, m, f, g, p, k, it_begin, it_end, cap);
+        std::vector<ea_scored_pose> out;
+        if (t.plan.slab_poses == 0) return out;
         const size_t res_bytes = (sizeof(double) + sizeof(unsigned long long)) * (size_t)k;
         char* h = (char*)ctx->h_out.ensure(sizeof(SearchCtrl) + res_bytes);
-        d2h(ctx, h, ctrl, sizeof(SearchCtrl));
-        d2h(ctx, h + sizeof(SearchCtrl), tk, res_bytes);
+        d2h(ctx, h, ctx->ctrl.p, sizeof(SearchCtrl));
+        d2h(ctx, h + sizeof(SearchCtrl), t.top_score, res_bytes);
         if (ctx->timing) EAB_CUDA(cudaEventRecord(ctx->ev[3], ctx->stream));
         sync(ctx);
         if (ctx->timing) {
@@ -461,29 +493,14 @@ std::vector<ea_scored_pose> top_search(ea_ctx* ctx, const ea_model* m, const ea_
         }
         SearchCtrl hc;
         std::memcpy(&hc, h, sizeof hc);
-        if (std::getenv("EAB_DEBUG_ITEMS")) {
-            std::vector<float> im(plan.items.n_items);
-            d2h(ctx, im.data(), ctx->item_max.p, sizeof(float) * im.size());
-            sync(ctx);
-            size_t pass = 0;
-            for (float v : im) pass += v >= hc.thr;
-            std::fprintf(stderr, "[eab] items=%llu pass=%zu thr=%g first=%g lattice=%d rows=%u\n",
-                         (unsigned long long)plan.items.n_items, pass, (double)hc.thr,
-                         (double)im[0], plan.items.lattice, plan.items.rows);
-        }
-        ctx->stats.candidates = hc.cand_count;
-        ctx->stats.candidates_needed = hc.needed;
-        ctx->stats.threshold = hc.thr;
-        ctx->stats.flagged_points = hc.flags;
-        ctx->stats.screen_delta = plan.delta + (plan.fast ? 2.0 * hc.flags / n : 0.0);
-        if (hc.cand_count > cap) {  // band admitted more than the buffer: grow, redo
+        if (!top_stats(ctx, t, hc)) {  // band admitted more than the buffer: grow, redo
             cap = hc.cand_count;
             continue;
         }
         const double* hs = reinterpret_cast<const double*>(h + sizeof(SearchCtrl));
         const unsigned long long* hi = reinterpret_cast<const unsigned long long*>(hs + k);
         for (int r = 0; r < hc.n_out; ++r) {
-            out.push_back(ea_scored_pose{hs[r], hi[r], pose_of(g, plan.c, hi[r])});
+            out.push_back(ea_scored_pose{hs[r], hi[r], pose_of(g, t.plan.c, hi[r])});
         }
         return out;
     }
@@ -730,6 +747,141 @@ void refine_levels(ea_ctx* ctx, const ea_levels* lv, const ea_search_config& cfg
     sync(ctx);
 }
 
+// glibc (theta, cos, sin) for every refinement path of every top-level theta:
+// level d holds nt * side^d entries, path = ((it*side + k1)*side + k2)...,
+// theta_d = theta_{d-1} + (double)kt * step_t(d) (search.cpp:286-305).
+// Cached per grid; nullptr when the tables would be too large.
+const double* theta_tables(ea_ctx* ctx, const ea_pose_grid& tg, uint64_t nt, int top, int R) {
+    std::vector<double> key{tg.t0, tg.dt, (double)nt, (double)top, (double)R};
+    if (key == ctx->ttab_key) return ctx->ttab.as<double>();
+    const int side = 2 * R + 1;
+    size_t total = 0, level = nt;
+    std::vector<size_t> off(top + 1, 0);
+    for (int d = 1; d <= top; ++d) {
+        level *= (size_t)side;
+        off[d] = total;
+        total += level;
+        if (total > (16u << 20)) return nullptr;
+    }
+    std::vector<double> h(3 * (total ? total : 1));
+    const double theta_floor = 0.25 * (3.14159265358979323846 / 180.0);
+    std::vector<double> prev(nt), cur;
+    for (uint64_t i = 0; i < nt; ++i) prev[i] = tg.t0 + (double)i * tg.dt;  // pose.h:91
+    double st = tg.dt;
+    for (int d = 1; d <= top; ++d) {
+        st = std::max(st / 2.0, theta_floor);
+        cur.assign(prev.size() * side, 0.0);
+        double* t = h.data() + 3 * off[d];
+        for (size_t q = 0; q < prev.size(); ++q) {
+            for (int kt = -R; kt <= R; ++kt) {
+                const size_t path = q * side + (size_t)(kt + R);
+                const double theta = prev[q] + (double)kt * st;
+                cur[path] = theta;
+                t[3 * path] = theta;
+                t[3 * path + 1] = std::cos(theta);
+                t[3 * path + 2] = std::sin(theta);
+            }
+        }
+        prev.swap(cur);
+    }
+    ctx->ttab_key.clear();
+    double* d = (double*)ctx->ttab.ensure(sizeof(double) * h.size());
+    h2d_staged(ctx, d, h.data(), sizeof(double) * h.size());
+    sync(ctx);
+    ctx->ttab_off = off;
+    ctx->ttab_key = key;
+    return d;
+}
+
+// Device refinement state: outcome | beam A | beam B | counts A, B.
+struct RefineState {
+    ea_outcome* out;
+    BeamDev* beam[2];
+    int* cnt[2];
+};
+
+RefineState refine_state(ea_ctx* ctx, int k) {
+    const size_t beam_bytes = sizeof(BeamDev) * (size_t)k;
+    char* b = (char*)ctx->rstate.ensure(sizeof(ea_outcome) + 2 * beam_bytes + 4 * sizeof(int));
+    RefineState r;
+    r.out = (ea_outcome*)b;
+    r.beam[0] = (BeamDev*)(b + sizeof(ea_outcome));
+    r.beam[1] = (BeamDev*)(b + sizeof(ea_outcome) + beam_bytes);
+    r.cnt[0] = (int*)(b + sizeof(ea_outcome) + 2 * beam_bytes);
+    r.cnt[1] = r.cnt[0] + 1;
+    return r;
+}
+
+// Enqueue the refinement levels on a device beam (beam[0], cnt[0]).
+void refine_enqueue(ea_ctx* ctx, const ea_levels* lv, const ea_search_config& cfg,
+                    const ea_pose_grid& tg, const double* tables, const RefineState& st) {
+    const int top = cfg.num_levels - 1;
+    const int R = cfg.refine_radius, side = 2 * R + 1, k = cfg.topk;
+    const size_t E = (size_t)k * side * side * side;
+    int n_max = 0;
+    for (int l = 0; l < top; ++l) n_max = std::max(n_max, lv->models[l]->n);
+    double* votes = (double*)ctx->refine_scores.ensure(sizeof(double) * (size_t)std::max(n_max, 1) * E);
+    double* entries = (double*)ctx->beam.ensure((sizeof(double) * 4 + sizeof(int)) * E);
+    int* dup = (int*)(entries + 4 * E);
+    const ea_score_params& sp = cfg.score_params;
+    double step_x = tg.dx, step_y = tg.dy;
+    int cur = 0;
+    for (int d = 1; d <= top; ++d) {
+        step_x /= 2.0;  // search.cpp:293-294
+        step_y /= 2.0;
+        const int level = top - d;
+        const ea_model* m = lv->models[level];
+        const ea_field* f = lv->fields[level];
+        RefineArgs a{};
+        a.pts = m->pts.as<double>();
+        a.n = m->n;
+        a.gx = f->gx();
+        a.gy = f->gy();
+        a.mag = f->mag();
+        a.W = f->width;
+        a.H = f->height;
+        a.vote_R = (sp.neighborhood - 1) / 2;
+        a.ignore = sp.polarity == EA_POLARITY_IGNORE;
+        a.eps = sp.eps_mag;
+        a.R = R;
+        a.side = side;
+        a.topk = k;
+        a.max_parents = k;
+        a.chunk = 16;
+        a.level = level;
+        a.trace_slot = d;
+        a.step_x = step_x;
+        a.step_y = step_y;
+        a.min_score = cfg.min_score;
+        a.table = tables + 3 * ctx->ttab_off[d];
+        a.beam = st.beam[cur];
+        a.beam_count = st.cnt[cur];
+        a.beam_out = st.beam[cur ^ 1];
+        a.beam_count_out = st.cnt[cur ^ 1];
+        a.votes = votes;
+        a.entries = entries;
+        a.dup = dup;
+        a.outcome = st.out;
+        launch_refine_level(ctx, a);
+        cur ^= 1;
+    }
+}
+
+SeedArgs seed_args(const ea_pose_grid& tg, const ea_grid_counts& c, const ea_search_config& cfg) {
+    SeedArgs s{};
+    s.x0 = tg.x0;
+    s.dx = tg.dx;
+    s.y0 = tg.y0;
+    s.dy = tg.dy;
+    s.t0 = tg.t0;
+    s.dt = tg.dt;
+    s.nx = c.nx;
+    s.ny = c.ny;
+    s.top_level = cfg.num_levels - 1;
+    s.min_score = cfg.min_score;
+    return s;
+}
+
 ea_pose_grid top_grid_of(const ea_search_config& cfg) {  // search.cpp:264-273
     const int top = cfg.num_levels - 1;
     const double scale = (double)(1 << top);
@@ -759,6 +911,61 @@ std::vector<Beam> seeds_to_beam(const std::vector<ea_scored_pose>& seeds) {
     std::vector<Beam> beam;
     for (const auto& s : seeds) beam.push_back(Beam{s.pose, s.score, s.grid_index});
     return beam;
+}
+
+// search_levels (search.cpp:254-357) with the whole pipeline on the device:
+// top-level search -> seed beam -> refinement levels, one D2H at the end.
+void search_levels_device(ea_ctx* ctx, const ea_levels* lv, const ea_search_config& cfg,
+                          ea_outcome* out) {
+    const int top = cfg.num_levels - 1;
+    const int k = cfg.topk, R = cfg.refine_radius, side = 2 * R + 1;
+    const ea_pose_grid tg = top_grid_of(cfg);
+    const ea_grid_counts c = counts_of(tg);
+    const size_t E = (size_t)k * side * side * side;
+    const double* tables = nullptr;
+    if (top > 0) {
+        if (E <= 4096 && k <= 64) tables = theta_tables(ctx, tg, c.nt, top, R);
+        if (!tables) {  // very wide beams: host-assisted refinement
+            const auto seeds = top_search(ctx, lv->models[top], lv->fields[top], tg,
+                                          cfg.score_params, k, 0, 0);
+            const ea_search_stats keep = ctx->stats;
+            refine_levels(ctx, lv, cfg, tg, seeds_to_beam(seeds), out);
+            const int launched = ctx->stats.kernels_launched;
+            ctx->stats = keep;
+            ctx->stats.kernels_launched = launched;
+            return;
+        }
+    }
+    unsigned long long cap = initial_cap(ctx);
+    for (int attempt = 0; attempt < 3; ++attempt) {
+        const TopLaunch t = top_enqueue(ctx, lv->models[top], lv->fields[top], tg,
+                                        cfg.score_params, k, 0, 0, cap);
+        if (ctx->timing) EAB_CUDA(cudaEventRecord(ctx->ev[3], ctx->stream));
+        const RefineState st = refine_state(ctx, k);
+        EAB_CUDA(cudaMemsetAsync(st.out, 0, sizeof(ea_outcome), ctx->stream));
+        launch_seed_beam(ctx, t.top_score, t.top_index, &ctx->ctrl.as<SearchCtrl>()->n_out,
+                         seed_args(tg, c, cfg), st.beam[0], st.cnt[0], st.out);
+        if (top > 0) refine_enqueue(ctx, lv, cfg, tg, tables, st);
+        char* h = (char*)ctx->h_out.ensure(sizeof(SearchCtrl));
+        d2h(ctx, h, ctx->ctrl.p, sizeof(SearchCtrl));
+        d2h(ctx, out, st.out, sizeof(ea_outcome));
+        if (ctx->timing) EAB_CUDA(cudaEventRecord(ctx->ev[7], ctx->stream));
+        sync(ctx);
+        if (ctx->timing) {
+            float ms = 0.f;
+            EAB_CUDA(cudaEventElapsedTime(&ms, ctx->ev[1], ctx->ev[2]));
+            ctx->stats.screen_ms = ms;
+            EAB_CUDA(cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[3]));
+            ctx->stats.top_ms = ms;
+            EAB_CUDA(cudaEventElapsedTime(&ms, ctx->ev[3], ctx->ev[7]));
+            ctx->stats.refine_ms = ms;
+        }
+        SearchCtrl hc;
+        std::memcpy(&hc, h, sizeof hc);
+        if (top_stats(ctx, t, hc)) return;
+        cap = hc.cand_count;  // band admitted more than the buffer: grow, redo
+    }
+    fail(EA_ERR_INTERNAL, "candidate buffer did not converge");
 }
 
 // Template side of prepare_levels (search.cpp:222-234) for one level.
@@ -1522,15 +1729,7 @@ ea_status ea_search_levels(ea_ctx* ctx, const ea_levels* lv, const ea_search_con
         need(out, "out");
         check_search_config(lv, *cfg);
         DeviceGuard dg(ctx->device);
-        const int top = cfg->num_levels - 1;
-        const ea_pose_grid tg = top_grid_of(*cfg);
-        const auto seeds = top_search(ctx, lv->models[top], lv->fields[top], tg,
-                                      cfg->score_params, cfg->topk, 0, 0);
-        const ea_search_stats keep = ctx->stats;
-        refine_levels(ctx, lv, *cfg, tg, seeds_to_beam(seeds), out);
-        const int launched = ctx->stats.kernels_launched;
-        ctx->stats = keep;
-        ctx->stats.kernels_launched = launched;
+        search_levels_device(ctx, lv, *cfg, out);
     });
 }
 
@@ -1564,8 +1763,50 @@ ea_status ea_refine(ea_ctx* ctx, const ea_levels* lv, const ea_search_config* cf
         if (n_seeds < 1) fail(EA_ERR_INVALID_ARGUMENT, "refinement needs at least one seed");
         need(seeds, "seeds");
         DeviceGuard dg(ctx->device);
-        std::vector<ea_scored_pose> v(seeds, seeds + std::min(n_seeds, cfg->topk));
-        refine_levels(ctx, lv, *cfg, top_grid_of(*cfg), seeds_to_beam(v), out);
+        const int k = cfg->topk, top = cfg->num_levels - 1, R = cfg->refine_radius;
+        const int side = 2 * R + 1;
+        std::vector<ea_scored_pose> v(seeds, seeds + std::min(n_seeds, k));
+        const ea_pose_grid tg = top_grid_of(*cfg);
+        const ea_grid_counts c = counts_of(tg);
+        const double* tables = nullptr;
+        if (top > 0 && (size_t)k * side * side * side <= 4096 && k <= 64)
+            tables = theta_tables(ctx, tg, c.nt, top, R);
+        if (top > 0 && !tables) {
+            refine_levels(ctx, lv, *cfg, tg, seeds_to_beam(v), out);
+            return;
+        }
+        // seeds -> device beam (theta path = the seed's theta index)
+        const RefineState st = refine_state(ctx, k);
+        const size_t bytes = sizeof(ea_outcome) + sizeof(BeamDev) * v.size() + sizeof(int);
+        sync(ctx);
+        char* hb = (char*)ctx->h_stage.ensure(bytes);
+        ea_outcome* ho = (ea_outcome*)hb;
+        std::memset(ho, 0, sizeof(ea_outcome));
+        ho->trace[0].level = top;
+        ho->trace[0].pose = v[0].pose;
+        ho->trace[0].score = v[0].score;
+        ho->n_trace = 1;
+        if (top == 0) {
+            ho->pose = v[0].pose;
+            ho->score = v[0].score;
+            ho->grid_index = v[0].grid_index;
+            ho->found = v[0].score >= cfg->min_score ? 1 : 0;
+            *out = *ho;
+            return;
+        }
+        BeamDev* hbeam = (BeamDev*)(hb + sizeof(ea_outcome));
+        const uint64_t plane = c.nx * c.ny;
+        for (size_t i = 0; i < v.size(); ++i) {
+            hbeam[i] = BeamDev{v[i].pose.ux, v[i].pose.uy, v[i].pose.theta, v[i].score,
+                               v[i].grid_index, (int)(v[i].grid_index / plane), 0};
+        }
+        *(int*)(hb + sizeof(ea_outcome) + sizeof(BeamDev) * v.size()) = (int)v.size();
+        h2d(ctx, st.out, ho, sizeof(ea_outcome));
+        h2d(ctx, st.beam[0], hbeam, sizeof(BeamDev) * v.size());
+        h2d(ctx, st.cnt[0], hb + sizeof(ea_outcome) + sizeof(BeamDev) * v.size(), sizeof(int));
+        refine_enqueue(ctx, lv, *cfg, tg, tables, st);
+        d2h(ctx, out, st.out, sizeof(ea_outcome));
+        sync(ctx);
     });
 }
 
@@ -1595,25 +1836,14 @@ ea_status ea_detect(ea_ctx* ctx, ea_levels* lv, const double* image, int w, int 
         set_working_image(ctx, lv, image, w, h, cfg->num_levels);
         if (ctx->timing) EAB_CUDA(cudaEventRecord(ctx->ev[5], ctx->stream));
         check_search_config(lv, *cfg);
-        const int top = cfg->num_levels - 1;
-        const ea_pose_grid tg = top_grid_of(*cfg);
-        const int launched0 = ctx->stats.kernels_launched;
-        const auto seeds = top_search(ctx, lv->models[top], lv->fields[top], tg,
-                                      cfg->score_params, cfg->topk, 0, 0);
-        ea_search_stats keep = ctx->stats;
-        if (ctx->timing) EAB_CUDA(cudaEventRecord(ctx->ev[6], ctx->stream));
-        refine_levels(ctx, lv, *cfg, tg, seeds_to_beam(seeds), out);
+        const int launched0 = ctx->launches;
+        search_levels_device(ctx, lv, *cfg, out);
         if (ctx->timing) {
-            EAB_CUDA(cudaEventRecord(ctx->ev[7], ctx->stream));
-            EAB_CUDA(cudaEventSynchronize(ctx->ev[7]));
             float ms = 0.f;
             EAB_CUDA(cudaEventElapsedTime(&ms, ctx->ev[4], ctx->ev[5]));
-            keep.image_ms = ms;
-            EAB_CUDA(cudaEventElapsedTime(&ms, ctx->ev[6], ctx->ev[7]));
-            keep.refine_ms = ms;
+            ctx->stats.image_ms = ms;
         }
-        keep.kernels_launched = launched0 + ctx->stats.kernels_launched;
-        ctx->stats = keep;
+        ctx->stats.kernels_launched = (int)(ctx->launches - launched0);
     });
 }
 

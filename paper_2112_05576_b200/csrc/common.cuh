@@ -113,6 +113,10 @@ struct ea_ctx {
     // glibc cos/sin tables of theta grids, cached per (t0, dt, nt)
     std::map<std::vector<double>, std::vector<double>> cs_cache;
     std::vector<double> cs_dev_key;  // what ctx->cs currently holds on the device
+    // glibc (theta, cos, sin) of every refinement path of every top-level theta
+    std::vector<double> ttab_key;
+    std::vector<size_t> ttab_off;
+    eab::DevBuf ttab, rstate;
 };
 
 namespace eab {

@@ -186,8 +186,10 @@ struct ItemGeom {
     unsigned long long nx, ny, total;
 };
 ItemGeom screen_items(const ScreenArgs& a, bool fast);
+// Compaction with the band threshold (see launch_threshold) computed in-kernel.
 void launch_compact(ea_ctx* ctx, const float* map, const float* item_max, const ItemGeom& g,
-                    SearchCtrl* ctrl, unsigned* cand, unsigned long long cap);
+                    SearchCtrl* ctrl, unsigned* cand, unsigned long long cap,
+                    const unsigned* hist, int k, double delta, int flag_n);
 
 struct ExactArgs {
     const double* gx;

@@ -32,9 +32,21 @@ struct RefineArgs {
     int* beam_count_out;
     double* votes;        // [entry][point], pose-major
     double* entries;      // [entry] score, ux, uy, theta
+    int* dup;             // [entry] an earlier entry has the same pose
     ea_outcome* outcome;  // device copy of the result
 };
 
 void launch_refine_level(ea_ctx* ctx, const RefineArgs& a);
+
+// Top-level grid + search params the seed kernel needs.
+struct SeedArgs {
+    double x0, dx, y0, dy, t0, dt;
+    unsigned long long nx, ny;
+    int top_level;
+    double min_score;
+};
+void launch_seed_beam(ea_ctx* ctx, const double* top_score, const unsigned long long* top_index,
+                      const int* n_top, const SeedArgs& s, BeamDev* beam, int* beam_count,
+                      ea_outcome* out);
 
 }  // namespace eab

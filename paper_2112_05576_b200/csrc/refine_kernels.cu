@@ -10,9 +10,13 @@
 //                         chunk exactly (similarity.cpp:79-86), then every
 //                         thread computes exact fp64 votes of (pose, point)
 //                         pairs for the side^2 lattice poses.  votes[i][e].
-//   refine_select_kernel  one CTA: ordered sums (model-point order, then /n),
-//                         std::stable_sort rank by score, exact-duplicate
-//                         removal, keep topk, level trace / final outcome.
+//   refine_sum_kernel     one warp per pose: ordered fp64 sum (model-point
+//                         order, then /n) + "an earlier entry has this pose".
+//   refine_rank_kernel    one warp per pose: rank among first occurrences in
+//                         the stable-sort order -> new beam slot, trace,
+//                         final outcome.
+#include <climits>
+
 #include "kernels.cuh"
 #include "refine.cuh"
 
@@ -58,6 +62,17 @@ __global__ void __launch_bounds__(256) refine_votes_kernel(const RefineArgs a) {
     }
 }
 
+__device__ __forceinline__ void entry_pose(const RefineArgs& a, int e, double* ux, double* uy,
+                                           double* th) {
+    const int side = a.side, ss = side * side;
+    const int pk = e / ss, j = e % ss;
+    const BeamDev& parent = a.beam[pk / side];
+    const int ky = j / side - a.R, kx = j % side - a.R;
+    *ux = __dadd_rn(__dmul_rn(parent.ux, 2.0), __dmul_rn((double)kx, a.step_x));
+    *uy = __dadd_rn(__dmul_rn(parent.uy, 2.0), __dmul_rn((double)ky, a.step_y));
+    *th = a.table[3 * (parent.path * side + (pk % side))];
+}
+
 // Ordered fp64 sum of each lattice pose's votes (model-point order, then /n,
 // similarity.cpp:109-118): one warp per pose; lanes load 32 consecutive votes,
 // every lane walks them in order through shuffles (the chain is the
@@ -80,16 +95,30 @@ __global__ void __launch_bounds__(256) refine_sum_kernel(const RefineArgs a) {
         for (int l = 0; l < 32; ++l)
             if (l < lim) sum = __dadd_rn(sum, t[l]);
     }
+    // The pose of entry e (search.cpp:305-312) and whether an earlier entry in
+    // generation order has the identical pose: identical poses score
+    // identically, so after the stable sort the first occurrence is the one
+    // kept (search.cpp:330-345).
+    double px, py, pt;
+    entry_pose(a, e, &px, &py, &pt);
+    int dup = 0;
+    for (int q0 = 0; q0 < e; q0 += 32) {  // warp-uniform trip count
+        const int q = q0 + lane;
+        if (q < e) {
+            double qx, qy, qt;
+            entry_pose(a, q, &qx, &qy, &qt);
+            dup |= (qx == px && qy == py && qt == pt) ? 1 : 0;
+        }
+        if (__any_sync(0xffffffffu, dup)) break;
+    }
+    dup = __any_sync(0xffffffffu, dup);
     if (lane == 0) {
-        const int pk = e / ss, j = e % ss;
-        const BeamDev parent = a.beam[pk / side];
-        const int path = parent.path * side + (pk % side);
-        const int ky = j / side - R, kx = j % side - R;
         double* out = a.entries + 4 * (size_t)e;
         out[0] = __ddiv_rn(sum, (double)a.n);
-        out[1] = __dadd_rn(__dmul_rn(parent.ux, 2.0), __dmul_rn((double)kx, a.step_x));
-        out[2] = __dadd_rn(__dmul_rn(parent.uy, 2.0), __dmul_rn((double)ky, a.step_y));
-        out[3] = a.table[3 * path];
+        out[1] = px;
+        out[2] = py;
+        out[3] = pt;
+        a.dup[e] = dup;
     }
 }
 
@@ -97,71 +126,109 @@ __device__ __forceinline__ unsigned long long eq_key(double v) {
     return (unsigned long long)__double_as_longlong(v == 0.0 ? 0.0 : v);
 }
 
-__global__ void __launch_bounds__(1024) refine_select_kernel(const RefineArgs a) {
-    extern __shared__ long long smk[];
+// std::stable_sort by score (search.cpp:326-329) + exact-duplicate removal +
+// keep topk (search.cpp:330-345), as a one-warp selection: each round takes
+// the next entry in (score desc, generation order asc) -- the stable order --
+// and keeps it unless a kept entry has the same pose.
+// New beam (search.cpp:323-346): among first occurrences, the rank of entry e
+// in (score desc, generation index asc) -- the stable-sort order -- decides
+// its slot; one warp per entry, no serial walk.
+__global__ void __launch_bounds__(256) refine_rank_kernel(const RefineArgs a) {
     const int side = a.side, ss = side * side;
-    const int P = *a.beam_count;
-    const int E = P * side * ss;
-    const int Emax = a.max_parents * side * ss;
-    long long* key = smk;
-    int* order = reinterpret_cast<int*>(key + Emax);
-    for (int e = threadIdx.x; e < E; e += blockDim.x) key[e] = order_key(a.entries[4 * (size_t)e]);
-    __syncthreads();
-    // stable rank by score descending (std::stable_sort, search.cpp:326-329)
-    for (int e = threadIdx.x; e < E; e += blockDim.x) {
-        const long long k = key[e];
-        int r = 0;
-        for (int j = 0; j < E; ++j) {
-            const long long kj = key[j];
-            r += (kj > k) | ((kj == k) & (j < e));
-        }
-        order[r] = e;
+    const int E = *a.beam_count * side * ss;
+    const int lane = threadIdx.x & 31;
+    const int e = (int)(((unsigned)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+    if (e >= E) return;
+    const long long ke = order_key(a.entries[4 * (size_t)e]);
+    const bool mine = a.dup[e] == 0;
+    int rank = 0, distinct = 0;
+    for (int q = lane; q < E; q += 32) {
+        if (a.dup[q]) continue;
+        ++distinct;
+        const long long kq = order_key(a.entries[4 * (size_t)q]);
+        rank += (kq > ke) || (kq == ke && q < e);
     }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        // walk in rank order, drop exact duplicates of kept poses, keep topk
-        // (search.cpp:330-345)
-        unsigned long long kx[64], ky[64], kt[64];
-        const int cap = a.topk < 64 ? a.topk : 64;
-        int kept = 0;
-        for (int r = 0; r < E && kept < cap; ++r) {
-            const int e = order[r];
-            const double* in = a.entries + 4 * (size_t)e;
-            const unsigned long long x = eq_key(in[1]), y = eq_key(in[2]), t = eq_key(in[3]);
-            bool dup = false;
-            for (int q = 0; q < kept && !dup; ++q) dup = kx[q] == x && ky[q] == y && kt[q] == t;
-            if (dup) continue;
-            kx[kept] = x;
-            ky[kept] = y;
-            kt[kept] = t;
-            const int pk = e / ss;
-            const BeamDev parent = a.beam[pk / side];
-            BeamDev b;
-            b.score = in[0];
-            b.ux = in[1];
-            b.uy = in[2];
-            b.theta = in[3];
-            b.top_index = parent.top_index;
-            b.path = parent.path * side + (pk % side);
-            b._pad = 0;
-            a.beam_out[kept++] = b;
-        }
-        *a.beam_count_out = kept;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        rank += __shfl_xor_sync(0xffffffffu, rank, o);
+        distinct += __shfl_xor_sync(0xffffffffu, distinct, o);
+    }
+    if (!mine || rank >= a.topk || lane != 0) return;
+    const double* in = a.entries + 4 * (size_t)e;
+    const int pk = e / ss;
+    const BeamDev& parent = a.beam[pk / side];
+    BeamDev b;
+    b.score = in[0];
+    b.ux = in[1];
+    b.uy = in[2];
+    b.theta = in[3];
+    b.top_index = parent.top_index;
+    b.path = parent.path * side + (pk % side);
+    b._pad = 0;
+    a.beam_out[rank] = b;
+    if (rank == 0) {
+        *a.beam_count_out = distinct < a.topk ? distinct : a.topk;
         ea_outcome* o = a.outcome;
-        const BeamDev b0 = a.beam_out[0];
         if (a.trace_slot < EA_MAX_LEVELS) {
             o->trace[a.trace_slot].level = a.level;
-            o->trace[a.trace_slot].pose = ea_pose{b0.ux, b0.uy, b0.theta};
-            o->trace[a.trace_slot].score = b0.score;
+            o->trace[a.trace_slot].pose = ea_pose{b.ux, b.uy, b.theta};
+            o->trace[a.trace_slot].score = b.score;
             o->n_trace = a.trace_slot + 1;
         }
         if (a.level == 0) {
-            o->pose = ea_pose{b0.ux, b0.uy, b0.theta};
-            o->score = b0.score;
-            o->grid_index = b0.top_index;
-            o->found = b0.score >= a.min_score ? 1 : 0;
+            o->pose = ea_pose{b.ux, b.uy, b.theta};
+            o->score = b.score;
+            o->grid_index = b.top_index;
+            o->found = b.score >= a.min_score ? 1 : 0;
         }
     }
+}
+
+// Beam seeds straight from the top-level top-k on the device (search.cpp:
+// 276-284): pose_at of each index (pose.h:84-91), theta path = theta index.
+__global__ void seed_beam_kernel(const double* __restrict__ top_score,
+                                 const unsigned long long* __restrict__ top_index,
+                                 const int* __restrict__ n_top, SeedArgs s, BeamDev* beam,
+                                 int* beam_count, ea_outcome* out) {
+    const int n = *n_top;
+    const unsigned long long plane = s.nx * s.ny;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const unsigned long long idx = top_index[i];
+        const unsigned long long it = idx / plane, rem = idx % plane;
+        BeamDev b;
+        b.ux = __dadd_rn(s.x0, __dmul_rn((double)(rem % s.nx), s.dx));
+        b.uy = __dadd_rn(s.y0, __dmul_rn((double)(rem / s.nx), s.dy));
+        b.theta = __dadd_rn(s.t0, __dmul_rn((double)it, s.dt));
+        b.score = top_score[i];
+        b.top_index = idx;
+        b.path = (int)it;
+        b._pad = 0;
+        beam[i] = b;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        *beam_count = n;
+        const BeamDev b0 = beam[0];
+        out->trace[0].level = s.top_level;
+        out->trace[0].pose = ea_pose{b0.ux, b0.uy, b0.theta};
+        out->trace[0].score = b0.score;
+        out->n_trace = 1;
+        if (s.top_level == 0) {  // no refinement: the seed is the answer
+            out->pose = ea_pose{b0.ux, b0.uy, b0.theta};
+            out->score = b0.score;
+            out->grid_index = b0.top_index;
+            out->found = b0.score >= s.min_score ? 1 : 0;
+        }
+    }
+}
+
+void launch_seed_beam(ea_ctx* ctx, const double* top_score, const unsigned long long* top_index,
+                      const int* n_top, const SeedArgs& s, BeamDev* beam, int* beam_count,
+                      ea_outcome* out) {
+    seed_beam_kernel<<<1, 64, 0, ctx->stream>>>(top_score, top_index, n_top, s, beam,
+                                                beam_count, out);
+    check_launch("seed_beam_kernel");
+    count_launch(ctx);
 }
 
 void launch_refine_level(ea_ctx* ctx, const RefineArgs& a) {
@@ -173,12 +240,8 @@ void launch_refine_level(ea_ctx* ctx, const RefineArgs& a) {
     const int e_max = a.max_parents * a.side * a.side * a.side;
     refine_sum_kernel<<<(e_max * 32 + 255) / 256, 256, 0, ctx->stream>>>(a);
     check_launch("refine_sum_kernel");
-    const size_t Emax = (size_t)a.max_parents * a.side * a.side * a.side;
-    const size_t smem = Emax * (sizeof(long long) + sizeof(int));
-    EAB_CUDA(cudaFuncSetAttribute(refine_select_kernel,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    refine_select_kernel<<<1, 1024, smem, ctx->stream>>>(a);
-    check_launch("refine_select_kernel");
+    refine_rank_kernel<<<(e_max * 32 + 255) / 256, 256, 0, ctx->stream>>>(a);
+    check_launch("refine_rank_kernel");
     count_launch(ctx, 3);
 }
 

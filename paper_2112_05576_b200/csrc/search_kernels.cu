@@ -506,18 +506,20 @@ void launch_screen_general(ea_ctx* ctx, const ScreenArgs& a) {
 // fewer than k scores lie strictly above T_f), sets thr = lo(b) - 2*delta -
 // 2^-20 (the slack covers fp32 rounding inside hist_bin) and an upper bound
 // of the candidate count.
-__global__ void __launch_bounds__(1024) threshold_kernel(const unsigned* __restrict__ hist,
-                                                         int k, double delta, int flag_n,
-                                                         SearchCtrl* ctrl) {
-    using Scan = cub::BlockScan<unsigned long long, 1024>;
+template <int BLOCK>
+__device__ __forceinline__ float block_threshold(const unsigned* __restrict__ hist, int k,
+                                                 double delta, int flag_n,
+                                                 SearchCtrl* ctrl, bool write) {
+    using Scan = cub::BlockScan<unsigned long long, BLOCK>;
+    constexpr int PER = kHistBins / BLOCK;
     __shared__ typename Scan::TempStorage tmp;
-    __shared__ unsigned long long cum[kHistBins];  // cum[q] = #scores in bins >= 4095-q
     __shared__ int kbin;
+    __shared__ float thr_s;
     const int t = threadIdx.x;
-    unsigned long long local[4], sum = 0;
+    unsigned long long local[PER], sum = 0;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        local[j] = hist[kHistBins - 1 - (4 * t + j)];
+    for (int j = 0; j < PER; ++j) {
+        local[j] = __ldcg(hist + kHistBins - 1 - (PER * t + j));
         sum += local[j];
     }
     unsigned long long excl;
@@ -526,37 +528,41 @@ __global__ void __launch_bounds__(1024) threshold_kernel(const unsigned* __restr
     __syncthreads();
     unsigned long long run = excl;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+    for (int j = 0; j < PER; ++j) {
         const unsigned long long before = run;
         run += local[j];
-        cum[4 * t + j] = run;
         if (before < (unsigned long long)k && run >= (unsigned long long)k)
-            kbin = kHistBins - 1 - (4 * t + j);
+            kbin = kHistBins - 1 - (PER * t + j);
     }
     __syncthreads();
     if (t == 0) {
-        float thr;
-        unsigned long long needed;
-        if (kbin < 0) {  // fewer than k poses: every pose is a candidate
-            thr = -INFINITY;
-            needed = cum[kHistBins - 1];
-        } else {
+        float thr = -INFINITY;
+        if (kbin >= 0) {  // else fewer than k poses: every pose is a candidate
             if (flag_n > 0) delta += 2.0 * (double)ctrl->flags / (double)flag_n;
             const double lo = (double)kbin / 2048.0 - 1.0;
             const double th = lo - 2.0 * delta - 9.5367431640625e-07;  // 2^-20
             thr = (float)th;
             if ((double)thr > th) thr = nextafterf(thr, -INFINITY);
-            const int tb = hist_bin(thr);
-            needed = cum[kHistBins - 1 - tb];
         }
-        ctrl->thr = thr;
-        ctrl->needed = needed;
+        thr_s = thr;
+        if (write) ctrl->thr = thr;
     }
+    __syncthreads();
+    return thr_s;
+}
+
+// Finds bin b holding the k-th largest screening score (b = bin(T_f) because
+// fewer than k scores lie strictly above T_f) and sets thr = lo(b) - 2*delta -
+// 2^-20 (the slack covers fp32 rounding inside hist_bin).
+__global__ void __launch_bounds__(256) threshold_kernel(const unsigned* __restrict__ hist, int k,
+                                                        double delta, int flag_n,
+                                                        SearchCtrl* ctrl) {
+    block_threshold<256>(hist, k, delta, flag_n, ctrl, true);
 }
 
 void launch_threshold(ea_ctx* ctx, const unsigned* hist, int k, double delta, int flag_n,
                       SearchCtrl* ctrl) {
-    threshold_kernel<<<1, 1024, 0, ctx->stream>>>(hist, k, delta, flag_n, ctrl);
+    threshold_kernel<<<1, 256, 0, ctx->stream>>>(hist, k, delta, flag_n, ctrl);
     check_launch("threshold_kernel");
     count_launch(ctx);
 }
@@ -564,19 +570,31 @@ void launch_threshold(ea_ctx* ctx, const unsigned* hist, int k, double delta, in
 // ---- 4. compaction -----------------------------------------------------------
 // One warp per screening work item; items whose best score is below the band
 // threshold are skipped without touching the map (typically all but the few
-// tiles around the peaks).
+// tiles around the peaks).  Every block derives the band threshold from the
+// histogram itself (block 0 publishes it), so no separate threshold launch.
 __global__ void __launch_bounds__(256) compact_kernel(const float* __restrict__ map,
                                                       const float* __restrict__ item_max,
                                                       const ItemGeom g, SearchCtrl* ctrl,
                                                       unsigned* __restrict__ cand,
-                                                      unsigned long long cap) {
-    const float thr = ctrl->thr;
+                                                      unsigned long long cap,
+                                                      const unsigned* __restrict__ hist, int k,
+                                                      double delta, int flag_n) {
+    const float thr = block_threshold<256>(hist, k, delta, flag_n, ctrl, blockIdx.x == 0);
     const int lane = threadIdx.x & 31;
     const unsigned long long warp = ((unsigned long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const unsigned long long nwarps = ((unsigned long long)gridDim.x * blockDim.x) >> 5;
     const unsigned long long plane = g.nx * g.ny;
-    for (unsigned long long it = warp; it < g.n_items; it += nwarps) {
-        if (!(__ldg(item_max + it) >= thr)) continue;
+    for (unsigned long long it0 = warp; it0 < g.n_items; it0 += 8 * nwarps) {
+        float best[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const unsigned long long it = it0 + q * nwarps;
+            best[q] = it < g.n_items ? __ldg(item_max + it) : -INFINITY;
+        }
+#pragma unroll 1
+        for (int q = 0; q < 8; ++q) {
+        const unsigned long long it = it0 + q * nwarps;
+        if (it >= g.n_items || !(best[q] >= thr)) continue;
         const unsigned steps = g.lattice ? g.rows : 1u;
         unsigned long long base = 0, x = 0, y0 = 0;
         if (g.lattice) {
@@ -592,35 +610,36 @@ __global__ void __launch_bounds__(256) compact_kernel(const float* __restrict__ 
             unsigned long long idx[16];
             bool okk[16];
 #pragma unroll
-            for (int q = 0; q < 16; ++q) {
-                const unsigned r = r0 + q;
+            for (int qq = 0; qq < 16; ++qq) {
+                const unsigned r = r0 + qq;
                 if (g.lattice) {
                     const unsigned long long y = y0 + r;
-                    okk[q] = r < steps && x < g.nx && y < g.ny;
-                    idx[q] = base + y * g.nx + x;
+                    okk[qq] = r < steps && x < g.nx && y < g.ny;
+                    idx[qq] = base + y * g.nx + x;
                 } else {
-                    idx[q] = it * 32 + lane;
-                    okk[q] = q == 0 && idx[q] < g.total;
+                    idx[qq] = it * 32 + lane;
+                    okk[qq] = qq == 0 && idx[qq] < g.total;
                 }
-                v[q] = okk[q] ? __ldg(map + idx[q]) : -INFINITY;
+                v[qq] = okk[qq] ? __ldg(map + idx[qq]) : -INFINITY;
             }
 #pragma unroll
-            for (int q = 0; q < 16; ++q) {
-            const unsigned long long i = idx[q];
-            const bool pred = okk[q] && v[q] >= thr;
-            const unsigned mask = __ballot_sync(0xffffffffu, pred);
-            if (mask) {
-                const int leader = __ffs(mask) - 1;
-                unsigned long long slot0 = 0;
-                if (lane == leader)
-                    slot0 = atomicAdd(&ctrl->cand_count, (unsigned long long)__popc(mask));
-                slot0 = __shfl_sync(0xffffffffu, slot0, leader);
-                if (pred) {
-                    const unsigned long long slot = slot0 + __popc(mask & ((1u << lane) - 1u));
-                    if (slot < cap) cand[slot] = (unsigned)i;
+            for (int qq = 0; qq < 16; ++qq) {
+                const unsigned long long i = idx[qq];
+                const bool pred = okk[qq] && v[qq] >= thr;
+                const unsigned mask = __ballot_sync(0xffffffffu, pred);
+                if (mask) {
+                    const int leader = __ffs(mask) - 1;
+                    unsigned long long slot0 = 0;
+                    if (lane == leader)
+                        slot0 = atomicAdd(&ctrl->cand_count, (unsigned long long)__popc(mask));
+                    slot0 = __shfl_sync(0xffffffffu, slot0, leader);
+                    if (pred) {
+                        const unsigned long long slot = slot0 + __popc(mask & ((1u << lane) - 1u));
+                        if (slot < cap) cand[slot] = (unsigned)i;
+                    }
                 }
             }
-            }
+        }
         }
     }
 }
@@ -645,12 +664,14 @@ ItemGeom screen_items(const ScreenArgs& a, bool fast) {
 }
 
 void launch_compact(ea_ctx* ctx, const float* map, const float* item_max, const ItemGeom& g,
-                    SearchCtrl* ctrl, unsigned* cand, unsigned long long cap) {
+                    SearchCtrl* ctrl, unsigned* cand, unsigned long long cap,
+                    const unsigned* hist, int k, double delta, int flag_n) {
     unsigned long long blocks = (g.n_items * 32 + 255) / 256;
     const unsigned long long maxb = (unsigned long long)ctx->sm_count;
     if (blocks > maxb) blocks = maxb;
     if (blocks == 0) blocks = 1;
-    compact_kernel<<<(unsigned)blocks, 256, 0, ctx->stream>>>(map, item_max, g, ctrl, cand, cap);
+    compact_kernel<<<(unsigned)blocks, 256, 0, ctx->stream>>>(map, item_max, g, ctrl, cand, cap,
+                                                              hist, k, delta, flag_n);
     check_launch("compact_kernel");
     count_launch(ctx);
 }
@@ -787,33 +808,61 @@ __device__ __forceinline__ Best pick(Best x, Best y) {
 }
 
 __global__ void __launch_bounds__(256) select_kernel(const unsigned* __restrict__ cand,
-                                                      const double* __restrict__ score,
-                                                      SearchCtrl* ctrl, unsigned long long cap,
-                                                      int k, unsigned long long index_base,
-                                                      double* out_score,
-                                                      unsigned long long* out_index) {
-    __shared__ Best warp_best[32];
-    __shared__ Best prev;
+                                                     const double* __restrict__ score,
+                                                     SearchCtrl* ctrl, unsigned long long cap,
+                                                     int k, unsigned long long index_base,
+                                                     double* out_score,
+                                                     unsigned long long* out_index) {
     constexpr int kStage = 2048;  // candidates staged in shared memory
     __shared__ long long skey[kStage];
     __shared__ unsigned long long sidx[kStage];
+    __shared__ Best warp_best[8];
+    __shared__ Best prev;
     unsigned long long nc = ctrl->cand_count;
     if (nc > cap) nc = cap;
     const int t = threadIdx.x, lane = t & 31, w = t >> 5;
-    const bool staged = nc <= kStage;
-    if (staged) {
+    if (nc <= kStage) {
+        // the block stages (score key, global index); one warp selects
         for (unsigned long long c = t; c < nc; c += blockDim.x) {
             skey[c] = order_key(score[c]);
             sidx[c] = index_base + cand[c];
         }
         __syncthreads();
+        if (w != 0) return;
+        Best p{0, 0ull, 0};
+        int r = 0;
+        for (; r < k; ++r) {
+            Best b{0, 0ull, 0};
+            for (int c = lane; c < (int)nc; c += 32) {
+                const Best x{skey[c], sidx[c], 1};
+                if (p.ok && !better_k(p.k, p.i, x.k, x.i)) continue;
+                b = pick(b, x);
+            }
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) {
+                Best o;
+                o.k = __shfl_xor_sync(0xffffffffu, b.k, off);
+                o.i = __shfl_xor_sync(0xffffffffu, b.i, off);
+                o.ok = __shfl_xor_sync(0xffffffffu, b.ok, off);
+                b = pick(b, o);
+            }
+            if (!b.ok) break;
+            if (lane == 0) {
+                out_score[r] = from_order_key(b.k);
+                out_index[r] = b.i;
+            }
+            p = b;
+        }
+        if (lane == 0) ctrl->n_out = r;
+        return;
     }
+    // many candidates (degenerate, e.g. flat images): block-wide rounds
     int r = 0;
     for (; r < k; ++r) {
         Best b{0, 0ull, 0};
         for (unsigned long long c = t; c < nc; c += blockDim.x) {
-            const long long kk = staged ? skey[c] : order_key(score[c]);
-            const unsigned long long idx = staged ? sidx[c] : index_base + cand[c];
+            const long long kk = order_key(score[c]);
+            const unsigned long long idx = index_base + cand[c];
             if (r > 0 && !better_k(prev.k, prev.i, kk, idx)) continue;
             b = pick(b, Best{kk, idx, 1});
         }
