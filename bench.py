@@ -57,11 +57,14 @@ SMEM_BYTES_PER_CLK_PER_SM = 128
 ALG_BYTES_PER_EVAL = 72  # (2r+1)^2 = 9 window pixels x 8 B float2
 
 
-def make_inputs(name):
+def make_inputs(name, noise_seed=None):
     c = CONFIGS[name]
+    sigma, nseed = c["sigma"], c["nseed"]
+    if noise_seed is not None:  # another frame of the same scene
+        sigma, nseed = max(sigma, 1.0), noise_seed
     spec = ea.SceneSpec(c["W"], c["H"], "l_bracket", c["size"],
                         (c["pose"][0], c["pose"][1], D(c["pose"][2])), c["clutter"], c["seed"],
-                        c["occluder"], c["illum"], c["sigma"], c["nseed"])
+                        c["occluder"], c["illum"], sigma, nseed)
     img, tmpl, truth, occ = ea.compose_scene(spec)
     L = c["L"]
     step = float(1 << (L - 1))
@@ -257,42 +260,46 @@ def bench_ours(args, rank, world, local_rank):
     pose_pts = nx * ny * nt * n_top  # whole job, all ranks
     value = pose_pts * args.steps / (tot_ms / 1e3)
 
-    # ---- e2e: public detect call with a host image ------------------------------------------
-    pinned = torch.from_numpy(img).pin_memory()
-    host_img = pinned.numpy()
+    # ---- e2e: the public batch-detect call on host images ----------------------------------
+    # Throughput mode: each step is one image (H2D from pinned memory, device
+    # pyramid + Sobel, top-level search, refinement, D2H of the outcome); the
+    # library overlaps image i+1's H2D with image i's search.  For N > 1 the
+    # images are sharded across ranks (each rank its own batch).
+    scenes = [img] + [make_inputs(args.config, noise_seed=101 + j)[0] for j in range(3)]
+    pinned = [torch.from_numpy(scenes[j % len(scenes)]).pin_memory() for j in range(args.steps)]
+    host_imgs = [p.numpy() for p in pinned]
     k = cfg.topk
     h2d = img.size * 8
-    d2h = (48 + 16 * k) + (L - 1) * (32 * k + 4 * (k + 1))
-
-    def detect_step():
-        if world == 1:
-            return det.detect(host_img)
-        det.levels.set_image(host_img)
-        s = gather(ea.search_top_slab(det.levels, cfg, it0, it1))
-        out = ea.refine(det.levels, cfg, s) if rank == 0 else None
-        return out
-
-    for _ in range(args.warmup):
-        detect_step()
+    d2h = 472 + 48  # ea_outcome + control block per image
+    det.detect_batch(host_imgs)  # warm-up: same batch size (pinned result slots, tables)
     barrier()
-    phases = []
-    eev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-           for _ in range(args.steps)]
-    outcome = None
-    for i in range(args.steps):
-        flush.zero_()
-        eev[i][0].record(stream)
-        outcome = detect_step()
-        eev[i][1].record(stream)
-        st_d = ctx.stats()
-        phases.append((st_d["image_ms"], st_d["top_ms"], st_d["refine_ms"]))
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    outs = det.detect_batch(host_imgs)
+    e1.record(stream)
     barrier()
-    e2e_ms = sum(a.elapsed_time(b) for a, b in eev)
+    e2e_ms = e0.elapsed_time(e1)
+    e2e_launches = ctx.stats()["kernels_launched"]
     if world > 1:
         t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
-    e2e = pose_pts * args.steps / (e2e_ms / 1e3)
+    e2e = pose_pts * args.steps * world / (e2e_ms / 1e3) if world > 1 else \
+        pose_pts * args.steps / (e2e_ms / 1e3)
+    outcome = outs[0]
+
+    # ---- single-image detect latency (same public API, one image per call) -------------------
+    phases, lat = [], []
+    for i in range(min(args.steps, 20) + args.warmup):
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record(stream)
+        det.detect(host_imgs[i % len(host_imgs)])
+        a1.record(stream)
+        torch.cuda.synchronize(dev)
+        if i >= args.warmup:
+            lat.append(a0.elapsed_time(a1))
+            st_d = ctx.stats()
+            phases.append((st_d["image_ms"], st_d["top_ms"], st_d["refine_ms"]))
 
     if rank != 0:
         return
@@ -315,10 +322,13 @@ def bench_ours(args, rank, world, local_rank):
                    "pose_evals_per_step": pose_pts, "l2": "flushed (256 MiB write) between steps",
                    "parallelism": f"theta-slab x{world}" if world > 1 else "single GPU"},
         "e2e": {"value": e2e, "unit": "pose-evals/s", "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h, "detect_latency_ms": e2e_ms / args.steps,
-                "phases_ms_median": {k: statistics.median(p[i] for p in phases)
-                                     for i, k in enumerate(("h2d_pyramid_gradients",
-                                                            "top_level_search", "refinement"))}},
+                "d2h_bytes_per_step": d2h, "ms_per_image": e2e_ms / args.steps,
+                "api": "Detector.detect_batch (ea_detect_batch), pinned host images",
+                "detect_latency_ms": statistics.median(lat),
+                "latency_phases_ms_median": {
+                    k: statistics.median(p[i] for p in phases)
+                    for i, k in enumerate(("h2d_pyramid_gradients", "top_level_search",
+                                           "refinement"))}},
         "roofline": {"bound": "smem", "kernel": "screen_fast_kernel" if st["screen_path"] == 1
                      else "screen_general_kernel", "achieved": achieved,
                      "peak": smem_peak_gbs, "unit": "GB/s", "frac": achieved / smem_peak_gbs,
@@ -331,6 +341,7 @@ def bench_ours(args, rank, world, local_rank):
                      statistics.median(step_ms),
                      "peak_source": f"{n_sm} SMs x 128 B/clk x sm_max_mhz from {peak_src}"},
         "gpu_launches": int(launches),
+        "gpu_launches_e2e": int(e2e_launches),
         "clocks": clk.summary(),
         "search": {"candidates": st["candidates"], "screen_delta": st["screen_delta"],
                    "flagged_points": st["flagged_points"],

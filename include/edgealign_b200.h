@@ -321,6 +321,11 @@ ea_status ea_coarse_to_fine(ea_ctx* ctx, const double* const* tmpl_levels,
 ea_status ea_detect(ea_ctx* ctx, ea_levels* lv, const double* image, int w, int h,
                     const ea_search_config* cfg, ea_outcome* out);
 
+/* Throughput mode (BASELINE configs[3]): `count` host images of one size,
+ * image i+1's H2D overlapping image i's device pipeline; outs[count]. */
+ea_status ea_detect_batch(ea_ctx* ctx, ea_levels* lv, const double* const* images, int count,
+                          int w, int h, const ea_search_config* cfg, ea_outcome* outs);
+
 /* ---- synthetic scenes (synth.cpp:24-300), host C++ ---------------------- */
 ea_status ea_render_template(int template_id, int size, double* out);  /* synth.cpp:62-128 */
 /* compose_scene  synth.cpp:178-300.  canvas: W*H, tmpl: size*size. */

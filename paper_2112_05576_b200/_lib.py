@@ -10,7 +10,7 @@ import os
 from . import abi
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libedgealign_b200.so")
+LIB_PATH = os.environ.get("EAB_LIB_PATH") or os.path.join(HERE, "libedgealign_b200.so")
 
 _lib = None
 
@@ -95,6 +95,8 @@ _SIGS = {
                                     C.POINTER(abi.Outcome)]),
     "ea_detect": (C.c_int, [_P, _P, _dp, C.c_int, C.c_int, C.POINTER(abi.SearchConfig),
                             C.POINTER(abi.Outcome)]),
+    "ea_detect_batch": (C.c_int, [_P, _P, C.POINTER(_dp), C.c_int, C.c_int, C.c_int,
+                                  C.POINTER(abi.SearchConfig), C.POINTER(abi.Outcome)]),
     "ea_render_template": (C.c_int, [C.c_int, C.c_int, _dp]),
     "ea_compose_scene": (C.c_int, [C.POINTER(abi.SceneSpec), _dp, _dp, C.POINTER(abi.Pose),
                                    _dp]),

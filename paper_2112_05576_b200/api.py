@@ -503,6 +503,23 @@ class Detector:
         return out
 
 
+    def detect_batch(self, images):
+        """Throughput mode: one call for many same-size host images (pinned
+        buffers overlap their H2D with the previous image's search)."""
+        imgs = [i if (isinstance(i, np.ndarray) and i.dtype == np.float64 and i.flags.c_contiguous)
+                else _f64(i) for i in images]
+        if not imgs:
+            return []
+        h, w = imgs[0].shape
+        if any(i.shape != (h, w) for i in imgs):
+            raise ValueError("detect_batch needs images of one size")
+        ptrs = (_dp * len(imgs))(*[_ptr(i) for i in imgs])
+        outs = (Outcome * len(imgs))()
+        _check(lib().ea_detect_batch(self.ctx.handle, self.levels.handle, ptrs, len(imgs), w, h,
+                                     C.byref(self.config), outs))
+        return list(outs)
+
+
 # ---- synthetic scenes (synth.cpp:62-300) -----------------------------------------
 def render_template(template_id, size):
     tid = abi.TEMPLATE_IDS[template_id] if isinstance(template_id, str) else template_id

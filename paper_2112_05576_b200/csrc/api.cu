@@ -203,6 +203,33 @@ int pyramid_levels_feasible(int w, int h) {  // image.cpp:263-272
 
 // build_pyramid (image.cpp:274-291) on the device: level 0 at d_buf, each next
 // level appended.  Returns level offsets/dims.
+// build_pyramid (image.cpp:274-291) on the device.  Level 0 is read from
+// `level0` (may alias d_buf); levels >= 1 are written to d_buf at *offs.
+void device_pyramid_from(ea_ctx* ctx, const double* level0, double* d_buf, int w, int h,
+                         int levels, std::vector<const double*>* srcs, std::vector<int>* dims) {
+    if (levels < 1) fail(EA_ERR_INVALID_ARGUMENT, "num_levels must be >= 1");
+    const int feasible = pyramid_levels_feasible(w, h);
+    if (levels > feasible) {
+        fail(EA_ERR_SIZE, "pyramid of " + std::to_string(levels) +
+                              " levels would drop below 8x8; maximum feasible level count is " +
+                              std::to_string(feasible));
+    }
+    const double* src = level0;
+    double* dst = d_buf;
+    for (int l = 0; l < levels; ++l) {
+        srcs->push_back(src);
+        dims->push_back(w);
+        dims->push_back(h);
+        if (l + 1 < levels) {
+            launch_downsample(ctx, src, w, h, dst);
+            src = dst;
+            dst += (size_t)(w / 2) * (h / 2);
+        }
+        w /= 2;
+        h /= 2;
+    }
+}
+
 void device_pyramid(ea_ctx* ctx, double* d_buf, int w, int h, int levels,
                     std::vector<size_t>* offs, std::vector<int>* dims) {
     if (levels < 1) fail(EA_ERR_INVALID_ARGUMENT, "num_levels must be >= 1");
@@ -913,42 +940,70 @@ std::vector<Beam> seeds_to_beam(const std::vector<ea_scored_pose>& seeds) {
     return beam;
 }
 
-// search_levels (search.cpp:254-357) with the whole pipeline on the device:
-// top-level search -> seed beam -> refinement levels, one D2H at the end.
+void build_working(ea_ctx* ctx, ea_levels* lv, const double* d_level0, int w, int h,
+                   int levels);
+void set_working_image(ea_ctx* ctx, ea_levels* lv, const double* image, int w, int h,
+                       int levels);
+
+// Theta tables for a config, or nullptr when refinement must be host-assisted.
+const double* detect_tables(ea_ctx* ctx, const ea_search_config& cfg) {
+    const int top = cfg.num_levels - 1;
+    if (top == 0) return nullptr;
+    const int k = cfg.topk, R = cfg.refine_radius, side = 2 * R + 1;
+    if ((size_t)k * side * side * side > 4096 || k > 64) return nullptr;
+    const ea_pose_grid tg = top_grid_of(cfg);
+    return theta_tables(ctx, tg, counts_of(tg).nt, top, R);
+}
+
+// Enqueue search_levels (search.cpp:254-357) entirely on the device: top-level
+// search -> seed beam -> refinement levels; the outcome lands in `d_out` and a
+// copy of the control block (candidate count for the overflow check) in
+// `d_ctrl`.  Nothing waits on the host.
+TopLaunch enqueue_levels(ea_ctx* ctx, const ea_levels* lv, const ea_search_config& cfg,
+                         const double* tables, unsigned long long cap, ea_outcome* d_out,
+                         SearchCtrl* d_ctrl) {
+    const int top = cfg.num_levels - 1;
+    const int k = cfg.topk;
+    const ea_pose_grid tg = top_grid_of(cfg);
+    const ea_grid_counts c = counts_of(tg);
+    const TopLaunch t = top_enqueue(ctx, lv->models[top], lv->fields[top], tg, cfg.score_params, k,
+                                    0, 0, cap);
+    if (ctx->timing) EAB_CUDA(cudaEventRecord(ctx->ev[3], ctx->stream));
+    RefineState st = refine_state(ctx, k);
+    st.out = d_out;
+    EAB_CUDA(cudaMemsetAsync(st.out, 0, sizeof(ea_outcome), ctx->stream));
+    launch_seed_beam(ctx, t.top_score, t.top_index, &ctx->ctrl.as<SearchCtrl>()->n_out,
+                     seed_args(tg, c, cfg), st.beam[0], st.cnt[0], st.out);
+    if (top > 0) refine_enqueue(ctx, lv, cfg, tg, tables, st);
+    EAB_CUDA(cudaMemcpyAsync(d_ctrl, ctx->ctrl.p, sizeof(SearchCtrl), cudaMemcpyDeviceToDevice,
+                             ctx->stream));
+    return t;
+}
+
+// search_levels for one image: enqueue, one D2H of (outcome, control), sync.
 void search_levels_device(ea_ctx* ctx, const ea_levels* lv, const ea_search_config& cfg,
                           ea_outcome* out) {
     const int top = cfg.num_levels - 1;
-    const int k = cfg.topk, R = cfg.refine_radius, side = 2 * R + 1;
-    const ea_pose_grid tg = top_grid_of(cfg);
-    const ea_grid_counts c = counts_of(tg);
-    const size_t E = (size_t)k * side * side * side;
-    const double* tables = nullptr;
-    if (top > 0) {
-        if (E <= 4096 && k <= 64) tables = theta_tables(ctx, tg, c.nt, top, R);
-        if (!tables) {  // very wide beams: host-assisted refinement
-            const auto seeds = top_search(ctx, lv->models[top], lv->fields[top], tg,
-                                          cfg.score_params, k, 0, 0);
-            const ea_search_stats keep = ctx->stats;
-            refine_levels(ctx, lv, cfg, tg, seeds_to_beam(seeds), out);
-            const int launched = ctx->stats.kernels_launched;
-            ctx->stats = keep;
-            ctx->stats.kernels_launched = launched;
-            return;
-        }
+    const double* tables = detect_tables(ctx, cfg);
+    if (top > 0 && !tables) {  // very wide beams: host-assisted refinement
+        const ea_pose_grid tg = top_grid_of(cfg);
+        const auto seeds = top_search(ctx, lv->models[top], lv->fields[top], tg,
+                                      cfg.score_params, cfg.topk, 0, 0);
+        const ea_search_stats keep = ctx->stats;
+        refine_levels(ctx, lv, cfg, tg, seeds_to_beam(seeds), out);
+        const int launched = ctx->stats.kernels_launched;
+        ctx->stats = keep;
+        ctx->stats.kernels_launched = launched;
+        return;
     }
+    char* dres = (char*)ctx->rslots.ensure(sizeof(ea_outcome) + sizeof(SearchCtrl));
+    ea_outcome* d_out = (ea_outcome*)dres;
+    SearchCtrl* d_ctrl = (SearchCtrl*)(dres + sizeof(ea_outcome));
     unsigned long long cap = initial_cap(ctx);
     for (int attempt = 0; attempt < 3; ++attempt) {
-        const TopLaunch t = top_enqueue(ctx, lv->models[top], lv->fields[top], tg,
-                                        cfg.score_params, k, 0, 0, cap);
-        if (ctx->timing) EAB_CUDA(cudaEventRecord(ctx->ev[3], ctx->stream));
-        const RefineState st = refine_state(ctx, k);
-        EAB_CUDA(cudaMemsetAsync(st.out, 0, sizeof(ea_outcome), ctx->stream));
-        launch_seed_beam(ctx, t.top_score, t.top_index, &ctx->ctrl.as<SearchCtrl>()->n_out,
-                         seed_args(tg, c, cfg), st.beam[0], st.cnt[0], st.out);
-        if (top > 0) refine_enqueue(ctx, lv, cfg, tg, tables, st);
-        char* h = (char*)ctx->h_out.ensure(sizeof(SearchCtrl));
-        d2h(ctx, h, ctx->ctrl.p, sizeof(SearchCtrl));
-        d2h(ctx, out, st.out, sizeof(ea_outcome));
+        const TopLaunch t = enqueue_levels(ctx, lv, cfg, tables, cap, d_out, d_ctrl);
+        char* h = (char*)ctx->h_out.ensure(sizeof(ea_outcome) + sizeof(SearchCtrl));
+        d2h(ctx, h, dres, sizeof(ea_outcome) + sizeof(SearchCtrl));
         if (ctx->timing) EAB_CUDA(cudaEventRecord(ctx->ev[7], ctx->stream));
         sync(ctx);
         if (ctx->timing) {
@@ -961,11 +1016,75 @@ void search_levels_device(ea_ctx* ctx, const ea_levels* lv, const ea_search_conf
             ctx->stats.refine_ms = ms;
         }
         SearchCtrl hc;
-        std::memcpy(&hc, h, sizeof hc);
-        if (top_stats(ctx, t, hc)) return;
+        std::memcpy(&hc, h + sizeof(ea_outcome), sizeof hc);
+        if (top_stats(ctx, t, hc)) {
+            std::memcpy(out, h, sizeof(ea_outcome));
+            return;
+        }
         cap = hc.cand_count;  // band admitted more than the buffer: grow, redo
     }
     fail(EA_ERR_INTERNAL, "candidate buffer did not converge");
+}
+
+// Batch detect (throughput mode): image i+1's H2D on a copy stream overlaps
+// image i's device pipeline; outcomes come back asynchronously; one sync.
+void detect_batch(ea_ctx* ctx, ea_levels* lv, const double* const* images, int count, int w,
+                  int h, const ea_search_config& cfg, ea_outcome* outs) {
+    const int L = cfg.num_levels;
+    const double* tables = detect_tables(ctx, cfg);
+    if (L > 1 && !tables) {  // host-assisted refinement: no overlap, one by one
+        for (int i = 0; i < count; ++i) {
+            set_working_image(ctx, lv, images[i], w, h, L);
+            search_levels_device(ctx, lv, cfg, outs + i);
+        }
+        return;
+    }
+    if (w < 1 || h < 1) {
+        fail(EA_ERR_SIZE, "image dimensions must be at least 1x1, got " + std::to_string(w) + "x" +
+                              std::to_string(h));
+    }
+    if (!ctx->copy_stream) EAB_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream,
+                                                              cudaStreamNonBlocking));
+    for (auto& e : ctx->bev)
+        if (!e) EAB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    const size_t img_bytes = sizeof(double) * (size_t)w * h;
+    double* raw[2] = {(double*)lv->raw[0].ensure(img_bytes), (double*)lv->raw[1].ensure(img_bytes)};
+    const size_t slot = sizeof(ea_outcome) + sizeof(SearchCtrl);
+    char* dres = (char*)ctx->rslots.ensure(slot * (size_t)count);
+    char* hres = (char*)ctx->h_out.ensure(slot * (size_t)count);
+    const unsigned long long cap = std::max<unsigned long long>(initial_cap(ctx), 1ull << 20);
+    std::vector<TopLaunch> launches;
+    launches.reserve(count);
+    sync(ctx);
+    for (int i = 0; i < count; ++i) {
+        const int b = i & 1;
+        // copy stream: wait until image i-2 released buffer b, then H2D image i
+        if (i >= 2) EAB_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ctx->bev[2 + b], 0));
+        EAB_CUDA(cudaMemcpyAsync(raw[b], images[i], img_bytes, cudaMemcpyHostToDevice,
+                                 ctx->copy_stream));
+        EAB_CUDA(cudaEventRecord(ctx->bev[b], ctx->copy_stream));
+        // compute stream: pyramid + gradients, release the buffer, search
+        EAB_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->bev[b], 0));
+        build_working(ctx, lv, raw[b], w, h, L);
+        EAB_CUDA(cudaEventRecord(ctx->bev[2 + b], ctx->stream));
+        check_search_config(lv, cfg);
+        ea_outcome* d_out = (ea_outcome*)(dres + slot * i);
+        SearchCtrl* d_ctrl = (SearchCtrl*)(dres + slot * i + sizeof(ea_outcome));
+        launches.push_back(enqueue_levels(ctx, lv, cfg, tables, cap, d_out, d_ctrl));
+        d2h(ctx, hres + slot * i, dres + slot * i, slot);
+    }
+    sync(ctx);
+    EAB_CUDA(cudaStreamSynchronize(ctx->copy_stream));
+    for (int i = 0; i < count; ++i) {
+        SearchCtrl hc;
+        std::memcpy(&hc, hres + slot * i + sizeof(ea_outcome), sizeof hc);
+        if (top_stats(ctx, launches[i], hc)) {
+            std::memcpy(outs + i, hres + slot * i, sizeof(ea_outcome));
+        } else {  // overflowed the candidate buffer: redo this image alone
+            set_working_image(ctx, lv, images[i], w, h, L);
+            search_levels_device(ctx, lv, cfg, outs + i);
+        }
+    }
 }
 
 // Template side of prepare_levels (search.cpp:222-234) for one level.
@@ -1009,20 +1128,20 @@ void free_levels(ea_levels* lv) {
     delete lv;
 }
 
-void set_working_image(ea_ctx* ctx, ea_levels* lv, const double* image, int w, int h,
-                       int levels) {
+// Working side from a level-0 image already on the device: pyramid levels
+// 1.. into lv->image, Sobel field per level (gradient.cpp:12-27).
+void build_working(ea_ctx* ctx, ea_levels* lv, const double* d_level0, int w, int h,
+                   int levels) {
     if (w < 1 || h < 1) {
         fail(EA_ERR_SIZE, "image dimensions must be at least 1x1, got " + std::to_string(w) + "x" +
                               std::to_string(h));
     }
-    const size_t elems = pyramid_elems(w, h, std::max(levels, 1));
-    double* d = (double*)lv->image.ensure(sizeof(double) * elems);
-    h2d_staged(ctx, d, image, sizeof(double) * (size_t)w * h);
-    std::vector<size_t> offs;
+    const size_t elems = pyramid_elems(w / 2, h / 2, std::max(levels - 1, 1));
+    double* d = (double*)lv->image.ensure(sizeof(double) * (elems ? elems : 1));
+    std::vector<const double*> srcs;
     std::vector<int> dims;
-    device_pyramid(ctx, d, w, h, levels, &offs, &dims);
-    // reuse field objects when dims match
-    for (int l = 0; l < levels; ++l) {
+    device_pyramid_from(ctx, d_level0, d, w, h, levels, &srcs, &dims);
+    for (int l = 0; l < levels; ++l) {  // reuse field objects when dims match
         const int lw = dims[2 * l], lh = dims[2 * l + 1];
         if (l < (int)lv->fields.size() &&
             (lv->fields[l]->width != lw || lv->fields[l]->height != lh)) {
@@ -1031,12 +1150,23 @@ void set_working_image(ea_ctx* ctx, ea_levels* lv, const double* image, int w, i
         }
         if (l >= (int)lv->fields.size()) lv->fields.push_back(nullptr);
         if (!lv->fields[l]) lv->fields[l] = new_field(lw, lh);
-        sobel_into(ctx, d + offs[l], lw, lh, lv->fields[l]);
+        sobel_into(ctx, srcs[l], lw, lh, lv->fields[l]);
     }
     while ((int)lv->fields.size() > levels) {
         delete lv->fields.back();
         lv->fields.pop_back();
     }
+}
+
+void set_working_image(ea_ctx* ctx, ea_levels* lv, const double* image, int w, int h,
+                       int levels) {
+    if (w < 1 || h < 1) {
+        fail(EA_ERR_SIZE, "image dimensions must be at least 1x1, got " + std::to_string(w) + "x" +
+                              std::to_string(h));
+    }
+    double* raw = (double*)lv->raw[0].ensure(sizeof(double) * (size_t)w * h);
+    h2d_staged(ctx, raw, image, sizeof(double) * (size_t)w * h);
+    build_working(ctx, lv, raw, w, h, levels);
 }
 
 }  // namespace
@@ -1098,6 +1228,9 @@ void ea_ctx_destroy(ea_ctx* ctx) {
     ctx->h_out.release();
     for (auto& e : ctx->ev)
         if (e) cudaEventDestroy(e);
+    for (auto& e : ctx->bev)
+        if (e) cudaEventDestroy(e);
+    if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
     if (prev >= 0) cudaSetDevice(prev);
@@ -1843,6 +1976,24 @@ ea_status ea_detect(ea_ctx* ctx, ea_levels* lv, const double* image, int w, int 
             EAB_CUDA(cudaEventElapsedTime(&ms, ctx->ev[4], ctx->ev[5]));
             ctx->stats.image_ms = ms;
         }
+        ctx->stats.kernels_launched = (int)(ctx->launches - launched0);
+    });
+}
+
+ea_status ea_detect_batch(ea_ctx* ctx, ea_levels* lv, const double* const* images, int count,
+                          int w, int h, const ea_search_config* cfg, ea_outcome* outs) {
+    return guard([&] {
+        need(ctx, "ctx");
+        need(lv, "levels");
+        need(cfg, "config");
+        if (count <= 0) return;
+        need(images, "images");
+        need(outs, "outs");
+        DeviceGuard dg(ctx->device);
+        if ((int)lv->models.size() < cfg->num_levels)
+            fail(EA_ERR_INVALID_ARGUMENT, "prepared levels do not cover num_levels");
+        const uint64_t launched0 = ctx->launches;
+        detect_batch(ctx, lv, images, count, w, h, *cfg, outs);
         ctx->stats.kernels_launched = (int)(ctx->launches - launched0);
     });
 }

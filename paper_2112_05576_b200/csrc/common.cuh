@@ -93,7 +93,8 @@ struct ea_model {
 struct ea_levels {
     std::vector<ea_model*> models;  // owned
     std::vector<ea_field*> fields;  // owned; may be empty until set_image
-    eab::DevBuf image;              // working level-0 image + pyramid scratch
+    eab::DevBuf image;              // working pyramid levels >= 1
+    eab::DevBuf raw[2];             // level-0 images (double-buffered in batch mode)
 };
 
 struct ea_ctx {
@@ -116,7 +117,9 @@ struct ea_ctx {
     // glibc (theta, cos, sin) of every refinement path of every top-level theta
     std::vector<double> ttab_key;
     std::vector<size_t> ttab_off;
-    eab::DevBuf ttab, rstate;
+    eab::DevBuf ttab, rstate, rslots;
+    cudaStream_t copy_stream = nullptr;  // batch-mode H2D
+    cudaEvent_t bev[4] = {nullptr, nullptr, nullptr, nullptr};
 };
 
 namespace eab {

@@ -117,9 +117,12 @@ __device__ __forceinline__ int hist_bin(float s) {
     return b < 0 ? 0 : (b >= kHistBins ? kHistBins - 1 : b);
 }
 
-// 12 warps per SM for 8-row lane strips (<= 168 registers), 8 warps for 16.
+// CTA size of the lattice kernel (one CTA per SM).
+#ifndef EAB_SCREEN_THREADS
+#define EAB_SCREEN_THREADS 256  // 8 warps x 218 regs beat 12 x 168 (spills) on B200
+#endif
 template <int S>
-constexpr int screen_threads() { return S <= 8 ? 384 : 256; }
+constexpr int screen_threads() { return S <= 8 ? EAB_SCREEN_THREADS : 256; }
 constexpr int kTW = 8;  // poses per lane along x
 
 // One model point over a lane's 8 x S pose block: walk the S + 2R plane rows

@@ -374,3 +374,23 @@ def test_config2_detect_bit_exact(ea, oracle):
     want = oracle.coarse_to_fine(tp, wp, cfg)
     got = ea.Detector(tmpl, cfg).detect(img)
     assert got.key() == want.key()
+
+
+def test_detect_batch_matches_single(ea, oracle):
+    """Throughput-mode batch detect == per-image detect == oracle."""
+    specs = [dict(canvas_width=160, canvas_height=128, template_id="l_bracket", template_size=48,
+                  true_pose=(80 + 3 * i, 64 - 2 * i, D(20 + 35 * i)), clutter_segments=10 + i,
+                  clutter_seed=i, noise_sigma=1.0 * (i % 2), noise_seed=7 + i) for i in range(5)]
+    imgs, tmpl = [], None
+    for kw in specs:
+        img, t = scene(ea, **kw)
+        imgs.append(img)
+        tmpl = t
+    cfg = ea.SearchConfig(grid=ea.PoseGrid(0, 159, 2, 0, 127, 2, 0.0, D(355), D(5)),
+                          num_levels=2, score_params=ea.ScoreParams(3))
+    det = ea.Detector(tmpl, cfg)
+    batch = det.detect_batch(imgs)
+    tp = oracle.build_pyramid(tmpl, 2)
+    for img, got in zip(imgs, batch):
+        assert got.key() == det.detect(img).key()
+        assert got.key() == oracle.coarse_to_fine(tp, oracle.build_pyramid(img, 2), cfg).key()
