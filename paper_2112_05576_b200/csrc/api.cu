@@ -392,6 +392,12 @@ ScreenPlan screen(ea_ctx* ctx, const ea_model* m, const ea_field* f, const ea_po
     a.dy = g.dy;
     a.R = R;
     a.ignore = p.polarity == EA_POLARITY_IGNORE;
+    {   // warp tile 32x64 or 16x128: whichever pads the translation grid least
+        auto padded = [&](uint64_t cols, uint64_t rows) {
+            return ((plan.c.nx + cols - 1) / cols * cols) * ((plan.c.ny + rows - 1) / rows * rows);
+        };
+        a.xg = padded(16, 128) < padded(32, 64) ? 2 : 4;
+    }
     a.K = K;
     a.B3 = B3;
     a.scale = (float)(std::ldexp(1.0, e - 22) / (double)n);

@@ -158,6 +158,7 @@ struct ScreenArgs {
     double x0, dx, y0, dy;
     int R;
     int ignore;
+    int xg;           // lattice warp tile: xg * 8 columns x (32 / xg) * 8 rows
     float K;          // fixed-point fold constant 3*2^e
     unsigned B3;      // bits of K
     float scale;      // 2^(e-22) / n
@@ -181,8 +182,8 @@ void launch_point_vote(ea_ctx* ctx, const ea_field* f, int cx, int cy, int R, do
 // Work-item geometry of the screening map, for the compaction pass.
 struct ItemGeom {
     unsigned long long n_items;
-    int lattice;           // 1: items are (theta, wy, wx) tiles of 32 x rows poses
-    unsigned nwx, nwy, rows;
+    int lattice;           // 1: items are (theta, wy, wx) tiles of cols x rows poses
+    unsigned nwx, nwy, rows, cols;
     unsigned long long nx, ny, total;
 };
 ItemGeom screen_items(const ScreenArgs& a, bool fast);

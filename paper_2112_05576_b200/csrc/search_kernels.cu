@@ -235,7 +235,7 @@ struct TailPlan {
     unsigned* done;             // [n_tail] arrival counters
 };
 
-template <int R, int S, int SHIFT, bool IGNORE, typename PX>
+template <int R, int S, int SHIFT, bool IGNORE, typename PX, int XG>
 __global__ void __launch_bounds__(screen_threads<S>(), 1)
     screen_fast_kernel(const ScreenArgs a, const unsigned nwx, const unsigned nwy,
                        const TailPlan tp, const int vec16) {
@@ -253,7 +253,8 @@ __global__ void __launch_bounds__(screen_threads<S>(), 1)
     constexpr int NC = kTW + 2 * R;
     constexpr int NACC = S * kTW;
     const int lane = threadIdx.x & 31;
-    const int yg = lane & 7, xg = lane >> 3;
+    constexpr int YG = 32 / XG;  // lane strips along y; XG groups of 8 columns along x
+    const int yg = lane % YG, xg = lane / YG;
     const int H1 = a.geom.H + 1, PW = a.geom.PW, XL = a.geom.PW - 1;
     const int cx_lo = 1 + a.geom.PL, cx_hi = a.geom.W + a.geom.PL, Z = a.geom.zero;
     const float K = a.K;
@@ -281,9 +282,9 @@ __global__ void __launch_bounds__(screen_threads<S>(), 1)
         const unsigned long long rest = item / nwx;
         const unsigned wy = (unsigned)(rest % nwy);
         const unsigned long long itr = rest / nwy;
-        const int X0 = (int)wx * 32;
+        const int X0 = (int)wx * (8 * XG);
         const int X = X0 + xg * kTW;
-        const int Y = (int)wy * (8 * S) + yg * S;
+        const int Y = (int)wy * (YG * S) + yg * S;
         const int4* rot = a.rot_screen + (size_t)itr * a.n;
 
         int acc[S][kTW];
@@ -300,7 +301,7 @@ __global__ void __launch_bounds__(screen_threads<S>(), 1)
                 const int cb = p.x + a.ix0 + X - R + cx_lo;   // padded column of window start
                 const int rb = p.y + a.iy0 + Y - R + 1;       // padded row of window start
                 const int cw = p.x + a.ix0 + X0 - R + cx_lo;  // warp's first column (uniform)
-                if (cw >= 0 && cw + 24 + NC - 1 <= XL) {
+                if (cw >= 0 && cw + 8 * (XG - 1) + NC - 1 <= XL) {
                     point_rows<R, S, SHIFT, IGNORE, false, PX>(P, PW, XL, cx_lo, cx_hi, H1, Z,
                                                               cb, rb, dxf, dyf, K, B3, acc);
                 } else {
@@ -354,14 +355,15 @@ __global__ void __launch_bounds__(screen_threads<S>(), 1)
     }
 }
 
-template <int R, int S, int SHIFT, bool IGNORE, typename PX>
+template <int R, int S, int SHIFT, bool IGNORE, typename PX, int XG>
 static void run_fast(ea_ctx* ctx, const ScreenArgs& a) {
-    const unsigned nwx = (unsigned)((a.nx + 31) / 32);
-    const unsigned nwy = (unsigned)((a.ny + 8 * S - 1) / (8 * S));
+    constexpr int YG = 32 / XG;
+    const unsigned nwx = (unsigned)((a.nx + 8 * XG - 1) / (8 * XG));
+    const unsigned nwy = (unsigned)((a.ny + YG * S - 1) / (YG * S));
     const unsigned long long items = (unsigned long long)nwx * nwy * a.it_count;
     const size_t plane_bytes = (a.geom.bytes() + 15) & ~(size_t)15;
     const size_t smem = kHistBins * sizeof(unsigned) + plane_bytes;
-    auto kern = screen_fast_kernel<R, S, SHIFT, IGNORE, PX>;
+    auto kern = screen_fast_kernel<R, S, SHIFT, IGNORE, PX, XG>;
     EAB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     constexpr int threads = screen_threads<S>();
     unsigned long long warps_per_cta = threads / 32;
@@ -400,14 +402,20 @@ bool launch_screen_fast(ea_ctx* ctx, const ScreenArgs& a) {
     if (a.geom.shift != 3) return false;  // 8-row lane strips
     const bool ig = a.ignore != 0;
     const bool half = a.geom.elem_bytes == 4;
+#define EAB_FAST_XG(RR, XGV)                                                \
+    if (half) {                                                             \
+        if (ig) run_fast<RR, 8, 3, true, __half2, XGV>(ctx, a);             \
+        else run_fast<RR, 8, 3, false, __half2, XGV>(ctx, a);               \
+    } else {                                                                \
+        if (ig) run_fast<RR, 8, 3, true, float2, XGV>(ctx, a);              \
+        else run_fast<RR, 8, 3, false, float2, XGV>(ctx, a);                \
+    }
 #define EAB_FAST(RR)                                                        \
     if (a.R == RR) {                                                        \
-        if (half) {                                                         \
-            if (ig) run_fast<RR, 8, 3, true, __half2>(ctx, a);              \
-            else run_fast<RR, 8, 3, false, __half2>(ctx, a);                \
+        if (a.xg == 2) {                                                    \
+            EAB_FAST_XG(RR, 2)                                              \
         } else {                                                            \
-            if (ig) run_fast<RR, 8, 3, true, float2>(ctx, a);               \
-            else run_fast<RR, 8, 3, false, float2>(ctx, a);                 \
+            EAB_FAST_XG(RR, 4)                                              \
         }                                                                   \
         return true;                                                        \
     }
@@ -415,6 +423,7 @@ bool launch_screen_fast(ea_ctx* ctx, const ScreenArgs& a) {
     EAB_FAST(0)
     EAB_FAST(2)
 #undef EAB_FAST
+#undef EAB_FAST_XG
     return false;
 }
 
@@ -598,14 +607,16 @@ __global__ void __launch_bounds__(256) compact_kernel(const float* __restrict__ 
         for (int q = 0; q < 8; ++q) {
         const unsigned long long it = it0 + q * nwarps;
         if (it >= g.n_items || !(best[q] >= thr)) continue;
-        const unsigned steps = g.lattice ? g.rows : 1u;
+        // a lane covers column (lane % cols) of rows (lane / cols) + k * rstep
+        const unsigned rstep = g.lattice ? 32u / g.cols : 1u;
+        const unsigned steps = g.lattice ? g.rows / rstep : 1u;
         unsigned long long base = 0, x = 0, y0 = 0;
         if (g.lattice) {
             const unsigned long long wx = it % g.nwx, rest = it / g.nwx;
             const unsigned long long wy = rest % g.nwy, itr = rest / g.nwy;
             base = itr * plane;
-            x = wx * 32 + lane;
-            y0 = wy * g.rows;
+            x = wx * g.cols + lane % g.cols;
+            y0 = wy * g.rows + lane / g.cols;
         }
         for (unsigned r0 = 0; r0 < steps; r0 += 16) {
             // 16 rows of loads in flight before any ballot/atomic
@@ -616,7 +627,7 @@ __global__ void __launch_bounds__(256) compact_kernel(const float* __restrict__ 
             for (int qq = 0; qq < 16; ++qq) {
                 const unsigned r = r0 + qq;
                 if (g.lattice) {
-                    const unsigned long long y = y0 + r;
+                    const unsigned long long y = y0 + (unsigned long long)r * rstep;
                     okk[qq] = r < steps && x < g.nx && y < g.ny;
                     idx[qq] = base + y * g.nx + x;
                 } else {
@@ -654,9 +665,11 @@ ItemGeom screen_items(const ScreenArgs& a, bool fast) {
     g.total = a.nx * a.ny * a.it_count;
     if (fast) {
         const unsigned S = a.geom.shift == 3 ? 8u : 16u;
+        const unsigned XG = a.xg == 2 ? 2u : 4u;
         g.lattice = 1;
-        g.rows = 8 * S;
-        g.nwx = (unsigned)((a.nx + 31) / 32);
+        g.cols = 8 * XG;
+        g.rows = (32 / XG) * S;
+        g.nwx = (unsigned)((a.nx + g.cols - 1) / g.cols);
         g.nwy = (unsigned)((a.ny + g.rows - 1) / g.rows);
         g.n_items = (unsigned long long)g.nwx * g.nwy * a.it_count;
     } else {

@@ -394,3 +394,16 @@ def test_detect_batch_matches_single(ea, oracle):
     for img, got in zip(imgs, batch):
         assert got.key() == det.detect(img).key()
         assert got.key() == oracle.coarse_to_fine(tp, oracle.build_pyramid(img, 2), cfg).key()
+
+
+@pytest.mark.slow
+def test_config3_detect_bit_exact(ea, oracle):
+    """BASELINE configs[2]: 2592x1944 (5 MP), 256 px model, 0.25 deg full
+    rotation, 5 levels (the theta-sharded config)."""
+    import bench
+    img, tmpl, cfg, truth = bench.make_inputs("cfg3")
+    L = cfg.num_levels
+    tp, wp = oracle.build_pyramid(tmpl, L), oracle.build_pyramid(img, L)
+    want = oracle.coarse_to_fine(tp, wp, cfg)
+    got = ea.Detector(tmpl, cfg).detect(img)
+    assert got.key() == want.key()
