@@ -53,6 +53,46 @@ CONFIGS = {
                  occluder=None, illum=(1.0, 0.0, 1.0), sigma=0.0, nseed=0, L=5, dt=0.25),
 }
 
+CONFIGS["cfg4"] = dict(CONFIGS["cfg2"], desc="batch of 64 1280x1024 search images x 1 model "
+                       "(cfg2 geometry, poses and seeds from SplitMix64(1000+i)), throughput mode",
+                       batch=64)
+
+
+class SplitMix64:
+    """synth.h:26-49 (the reference's generator), for the cfg4 scene list."""
+
+    def __init__(self, seed):
+        self.s = seed & (2 ** 64 - 1)
+
+    def next(self):
+        self.s = (self.s + 0x9E3779B97F4A7C15) & (2 ** 64 - 1)
+        z = self.s
+        z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & (2 ** 64 - 1)
+        z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & (2 ** 64 - 1)
+        return z ^ (z >> 31)
+
+    def uniform01(self):
+        return (self.next() >> 11) * 2.0 ** -53
+
+
+def batch_scenes(name, count):
+    """cfg4: `count` cfg2-like scenes; scene i's pose and seeds come from
+    SplitMix64(1000 + i).  Generated on host threads (ctypes drops the GIL)."""
+    import concurrent.futures as cf
+    c = CONFIGS[name]
+
+    def one(i):
+        r = SplitMix64(1000 + i)
+        pose = (300.0 + r.uniform01() * (c["W"] - 600.0), 300.0 + r.uniform01() * (c["H"] - 600.0),
+                D(r.uniform01() * 360.0))
+        spec = ea.SceneSpec(c["W"], c["H"], "l_bracket", c["size"], pose, c["clutter"], r.next(),
+                            None, c["illum"], c["sigma"], r.next())
+        return ea.compose_scene(spec)[0]
+
+    with cf.ThreadPoolExecutor(max_workers=min(16, os.cpu_count() or 4)) as ex:
+        return list(ex.map(one, range(count)))
+
+
 SMEM_BYTES_PER_CLK_PER_SM = 128
 ALG_BYTES_PER_EVAL = 72  # (2r+1)^2 = 9 window pixels x 8 B float2 (SURVEY.md §8(d) d4)
 
@@ -265,8 +305,13 @@ def bench_ours(args, rank, world, local_rank):
     # pyramid + Sobel, top-level search, refinement, D2H of the outcome); the
     # library overlaps image i+1's H2D with image i's search.  For N > 1 the
     # images are sharded across ranks (each rank its own batch).
-    scenes = [img] + [make_inputs(args.config, noise_seed=101 + j)[0] for j in range(3)]
-    pinned = [torch.from_numpy(scenes[j % len(scenes)]).pin_memory() for j in range(args.steps)]
+    n_img = args.steps
+    if CONFIGS[args.config].get("batch"):  # cfg4: the batch is the workload, sharded by rank
+        n_img = CONFIGS[args.config]["batch"] // world
+        scenes = batch_scenes(args.config, CONFIGS[args.config]["batch"])[rank * n_img:(rank + 1) * n_img]
+    else:
+        scenes = [img] + [make_inputs(args.config, noise_seed=101 + j)[0] for j in range(3)]
+    pinned = [torch.from_numpy(scenes[j % len(scenes)]).pin_memory() for j in range(n_img)]
     host_imgs = [p.numpy() for p in pinned]
     k = cfg.topk
     h2d = img.size * 8
@@ -284,13 +329,12 @@ def bench_ours(args, rank, world, local_rank):
         t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
-    e2e = pose_pts * args.steps * world / (e2e_ms / 1e3) if world > 1 else \
-        pose_pts * args.steps / (e2e_ms / 1e3)
+    e2e = pose_pts * n_img * world / (e2e_ms / 1e3)  # each rank ran n_img full images
     outcome = outs[0]
 
     # ---- single-image detect latency (same public API, one image per call) -------------------
     phases, lat = [], []
-    for i in range(min(args.steps, 20) + args.warmup):
+    for i in range(min(n_img, 20) + args.warmup):
         a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a0.record(stream)
         det.detect(host_imgs[i % len(host_imgs)])
@@ -322,7 +366,7 @@ def bench_ours(args, rank, world, local_rank):
                    "pose_evals_per_step": pose_pts, "l2": "flushed (256 MiB write) between steps",
                    "parallelism": f"theta-slab x{world}" if world > 1 else "single GPU"},
         "e2e": {"value": e2e, "unit": "pose-evals/s", "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h, "ms_per_image": e2e_ms / args.steps,
+                "d2h_bytes_per_step": d2h, "ms_per_image": e2e_ms / n_img, "images": n_img * world,
                 "api": "Detector.detect_batch (ea_detect_batch), pinned host images",
                 "detect_latency_ms": statistics.median(lat),
                 "latency_phases_ms_median": {

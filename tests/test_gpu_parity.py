@@ -407,3 +407,17 @@ def test_config3_detect_bit_exact(ea, oracle):
     want = oracle.coarse_to_fine(tp, wp, cfg)
     got = ea.Detector(tmpl, cfg).detect(img)
     assert got.key() == want.key()
+
+
+@pytest.mark.slow
+def test_config4_batch_bit_exact(ea, oracle):
+    """BASELINE configs[3] (throughput mode): the first scenes of the cfg4
+    batch through detect_batch == the oracle's coarse_to_fine, image by image."""
+    import bench
+    _, tmpl, cfg, _ = bench.make_inputs("cfg4")
+    imgs = bench.batch_scenes("cfg4", 3)
+    outs = ea.Detector(tmpl, cfg).detect_batch(imgs)
+    L = cfg.num_levels
+    tp = oracle.build_pyramid(tmpl, L)
+    for img, got in zip(imgs, outs):
+        assert got.key() == oracle.coarse_to_fine(tp, oracle.build_pyramid(img, L), cfg).key()
