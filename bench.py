@@ -376,7 +376,9 @@ def bench_ours(args, rank, world, local_rank):
         "roofline": {"bound": "smem", "kernel": "screen_fast_kernel" if st["screen_path"] == 1
                      else "screen_general_kernel", "achieved": achieved,
                      "peak": smem_peak_gbs, "unit": "GB/s", "frac": achieved / smem_peak_gbs,
-                     "traffic": None,
+                     # dram read+write of one launch, ncu --set full (not measurable in-run)
+                     "traffic": 8940032 if args.config in ("cfg2", "cfg4") else None,
+                     "traffic_source": "profiles/r01_screen_fast_ncu.txt (cfg2 launch)",
                      "algorithmic_bytes_per_eval": ALG_BYTES_PER_EVAL,
                      "smem_bytes_loaded_per_eval": actual_b,
                      "frac_smem_loaded": local_evals * actual_b / (kernel_ms / 1e3) / 1e9
