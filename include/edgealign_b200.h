@@ -160,7 +160,7 @@ typedef struct {
     uint64_t candidates_needed;/* candidates the threshold admitted             */
     double screen_delta;       /* rigorous |fp32 screen - fp64 score| bound     */
     double threshold;          /* band threshold used for the exact pass        */
-    int32_t screen_path;       /* 1 = smem lattice kernel, 2 = general kernel   */
+    int32_t screen_path;       /* 1 = smem lattice, 2 = general, 3 = region lattice */
     int32_t flagged_points;    /* rounding-ambiguous (theta, point) pairs        */
     int32_t kernels_launched;  /* kernels of this library in the last search    */
     int32_t _pad;

@@ -345,11 +345,17 @@ ScreenPlan screen(ea_ctx* ctx, const ea_model* m, const ea_field* f, const ea_po
     // Zero columns beyond the ring so no lattice window needs clamping:
     // |offset| <= ceil(max |p_i|) + 1 for every rotation of the model.
     int PL = 0, PR = 0;
+    int ro_int = 0;
+    // Region mode: even the unpadded plane exceeds shared memory, so the
+    // plane stays in global memory and CTAs stage halo regions of it.
+    const bool region =
+        lattice && fast_smem_bytes(plane_geom(f->width, f->height, shift, 0, 0, 8)) > ctx->smem_optin;
     if (lattice) {
         double rmax = 0.0;
         for (const ea_edge_point& q : m->host)
             rmax = std::max(rmax, std::sqrt(q.x_rel * q.x_rel + q.y_rel * q.y_rel));
         const long ro = (long)std::ceil(rmax) + 2;
+        ro_int = (int)std::min<long>(ro, 1 << 20);
         const long ix0 = (long)g.x0, span = (long)((plan.c.nx + 31) / 32) * 32;
         PL = (int)std::max(0L, ro + R - 1 - ix0);
         PR = (int)std::max(0L, ix0 + span + ro + R - f->width - 1);
@@ -360,6 +366,7 @@ ScreenPlan screen(ea_ctx* ctx, const ea_model* m, const ea_field* f, const ea_po
         while ((PL > 0 || PR > 0) && bytes(PL, PR) > budget) {  // shrink: clamp path covers
             if (PL >= PR) --PL; else --PR;
         }
+        if (region) PL = PR = 0, elem = 8;  // halo regions are zero-filled instead
     }
     PlaneGeom geom = plane_geom(f->width, f->height, shift, PL, PR, elem);
     if (elem == 4 && fast_smem_bytes(geom) > ctx->smem_optin) {  // whole plane must fit
@@ -398,6 +405,7 @@ ScreenPlan screen(ea_ctx* ctx, const ea_model* m, const ea_field* f, const ea_po
         };
         a.xg = padded(16, 128) < padded(32, 64) ? 2 : 4;
     }
+    a.ro = ro_int;
     a.K = K;
     a.B3 = B3;
     a.scale = (float)(std::ldexp(1.0, e - 22) / (double)n);
@@ -408,11 +416,11 @@ ScreenPlan screen(ea_ctx* ctx, const ea_model* m, const ea_field* f, const ea_po
     plan.fast = false;
     if (ctx->timing) EAB_CUDA(cudaEventRecord(ctx->ev[1], ctx->stream));
     if (plan.slab_poses) {
-        if (lattice) plan.fast = launch_screen_fast(ctx, a);
+        if (lattice) plan.fast = region ? launch_screen_region(ctx, a) : launch_screen_fast(ctx, a);
         if (!plan.fast) launch_screen_general(ctx, a);
     }
     if (ctx->timing) EAB_CUDA(cudaEventRecord(ctx->ev[2], ctx->stream));
-    ctx->stats.screen_path = plan.fast ? 1 : 2;
+    ctx->stats.screen_path = plan.fast ? (region ? 3 : 1) : 2;
     if (plan.fast && geom.elem_bytes == 4)
         plan.delta += std::sqrt(2.0) * std::ldexp(1.0, -11) + std::ldexp(1.0, -24);
     plan.items = screen_items(a, plan.fast);

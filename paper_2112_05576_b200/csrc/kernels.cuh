@@ -159,6 +159,7 @@ struct ScreenArgs {
     int R;
     int ignore;
     int xg;           // lattice warp tile: xg * 8 columns x (32 / xg) * 8 rows
+    int ro;           // region kernel: bound on |lattice offset| of every rotated point
     float K;          // fixed-point fold constant 3*2^e
     unsigned B3;      // bits of K
     float scale;      // 2^(e-22) / n
@@ -172,6 +173,10 @@ struct ScreenArgs {
 size_t fast_smem_bytes(const PlaneGeom& g);
 // Returns true if the smem lattice kernel handled the launch.
 bool launch_screen_fast(ea_ctx* ctx, const ScreenArgs& a);
+// Region-tiled lattice kernel for planes larger than shared memory (float2
+// plane in global memory, one warp tile + model-radius halo per CTA stage).
+// Returns false when even one halo region does not fit.
+bool launch_screen_region(ea_ctx* ctx, const ScreenArgs& a);
 void launch_screen_general(ea_ctx* ctx, const ScreenArgs& a);
 
 // delta is widened on the device by 2*ctrl->flags/flag_n when flag_n > 0.

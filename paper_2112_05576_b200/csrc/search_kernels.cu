@@ -136,7 +136,8 @@ template <int R, int S, int SHIFT, bool IGNORE, bool CLAMP, typename PX>
 __device__ __forceinline__ void point_rows(const PX* __restrict__ P, const int PW,
                                            const int XL, const int cx_lo, const int cx_hi,
                                            const int H1, const int Z, const int cb,
-                                           const int rb, const float dxf, const float dyf,
+                                           const int rb, const int ry_lo, const int ry_hi,
+                                           const float dxf, const float dyf,
                                            const float K, const int B3, int (&acc)[S][kTW]) {
     constexpr int NC = kTW + 2 * R;  // columns per row
     constexpr int NR = S + 2 * R;    // rows per point
@@ -192,7 +193,7 @@ __device__ __forceinline__ void point_rows(const PX* __restrict__ P, const int P
                 if constexpr (IGNORE) v = v + K;
                 if constexpr (R >= 2) {
                     const int cys = rb + R + s;  // padded row of the window centre
-                    const bool in = ((cmask >> j) & 1u) && cys >= 1 && cys <= H1 - 1;
+                    const bool in = ((cmask >> j) & 1u) && cys >= ry_lo && cys <= ry_hi;
                     v = in ? v : K;
                 }
                 acc[s][j] += __float_as_int(v) - B3;
@@ -235,6 +236,34 @@ struct TailPlan {
     unsigned* done;             // [n_tail] arrival counters
 };
 
+// Lane epilogue shared by the lattice kernels: scores of the lane's 8 x S
+// block into the map and the CTA histogram, warp max into item_max[item].
+template <int S>
+__device__ __forceinline__ void emit_tile(const ScreenArgs& a, const int (&acc)[S][kTW],
+                                          const int X, const int Y, unsigned long long itr,
+                                          unsigned long long item, unsigned* hist,
+                                          const int lane) {
+    float* out = a.map + (size_t)itr * (a.nx * a.ny);
+    float best = -INFINITY;
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+        const unsigned long long iy = (unsigned long long)(Y + s);
+#pragma unroll
+        for (int j = 0; j < kTW; ++j) {
+            const unsigned long long ix = (unsigned long long)(X + j);
+            if (ix < a.nx && iy < a.ny) {
+                const float sc = (float)acc[s][j] * a.scale;
+                out[iy * a.nx + ix] = sc;
+                best = fmaxf(best, sc);
+                atomicAdd(&hist[hist_bin(sc)], 1u);
+            }
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) best = fmaxf(best, __shfl_xor_sync(0xffffffffu, best, o));
+    if (lane == 0) a.item_max[item] = best;
+}
+
 template <int R, int S, int SHIFT, bool IGNORE, typename PX, int XG>
 __global__ void __launch_bounds__(screen_threads<S>(), 1)
     screen_fast_kernel(const ScreenArgs a, const unsigned nwx, const unsigned nwy,
@@ -259,7 +288,6 @@ __global__ void __launch_bounds__(screen_threads<S>(), 1)
     const int cx_lo = 1 + a.geom.PL, cx_hi = a.geom.W + a.geom.PL, Z = a.geom.zero;
     const float K = a.K;
     const int B3 = (int)a.B3;
-    const unsigned long long plane_poses = a.nx * a.ny;
     const unsigned long long total = tp.n_main + tp.n_tail * (unsigned long long)tp.f;
 
     for (;;) {
@@ -303,10 +331,12 @@ __global__ void __launch_bounds__(screen_threads<S>(), 1)
                 const int cw = p.x + a.ix0 + X0 - R + cx_lo;  // warp's first column (uniform)
                 if (cw >= 0 && cw + 8 * (XG - 1) + NC - 1 <= XL) {
                     point_rows<R, S, SHIFT, IGNORE, false, PX>(P, PW, XL, cx_lo, cx_hi, H1, Z,
-                                                              cb, rb, dxf, dyf, K, B3, acc);
+                                                              cb, rb, 1, H1 - 1, dxf, dyf, K,
+                                                              B3, acc);
                 } else {
                     point_rows<R, S, SHIFT, IGNORE, true, PX>(P, PW, XL, cx_lo, cx_hi, H1, Z,
-                                                             cb, rb, dxf, dyf, K, B3, acc);
+                                                             cb, rb, 1, H1 - 1, dxf, dyf, K,
+                                                             B3, acc);
                 }
                 p = pn;
             }
@@ -328,25 +358,7 @@ __global__ void __launch_bounds__(screen_threads<S>(), 1)
 #pragma unroll
                 for (int j = 0; j < kTW; ++j) acc[s][j] = __ldcg(part + (s * kTW + j) * 32 + lane);
         }
-        float* out = a.map + (size_t)itr * plane_poses;
-        float best = -INFINITY;
-#pragma unroll
-        for (int s = 0; s < S; ++s) {
-            const unsigned long long iy = (unsigned long long)(Y + s);
-#pragma unroll
-            for (int j = 0; j < kTW; ++j) {
-                const unsigned long long ix = (unsigned long long)(X + j);
-                if (ix < a.nx && iy < a.ny) {
-                    const float sc = (float)acc[s][j] * a.scale;
-                    out[iy * a.nx + ix] = sc;
-                    best = fmaxf(best, sc);
-                    atomicAdd(&hist[hist_bin(sc)], 1u);
-                }
-            }
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) best = fmaxf(best, __shfl_xor_sync(0xffffffffu, best, o));
-        if (lane == 0) a.item_max[item] = best;
+        emit_tile<S>(a, acc, X, Y, itr, item, hist, lane);
     }
     __syncthreads();
     for (int b = threadIdx.x; b < kHistBins; b += blockDim.x) {
@@ -424,6 +436,167 @@ bool launch_screen_fast(ea_ctx* ctx, const ScreenArgs& a) {
     EAB_FAST(2)
 #undef EAB_FAST
 #undef EAB_FAST_XG
+    return false;
+}
+
+// Region-tiled lattice kernel: the plane lives in global memory (zero ring,
+// row skew as in PlaneGeom) and each CTA stages, in shared memory, the
+// window that one warp tile of translations can touch: the tile plus a halo
+// h = ro + R, where ro bounds |lattice offset| of every rotated model point.
+// Inside the region no window needs clamping and no row leaves it, so the
+// inner loop is the smem kernel's unclamped path.  Cells of the region off
+// the padded plane are zero (a zero plane pixel contributes the fixed-point
+// zero vote, exactly like the ring).
+//
+// Work: CTA items (warp tile m, theta group g) of kGroup thetas, one per
+// warp, ordered tile-major and split into contiguous equal runs per CTA, so a
+// CTA reloads its region only when its run crosses into the next tile.
+struct RegionPlan {
+    int RW, RH;              // region pitch (elements, even) and rows
+    int elems16;             // region size in 16 B chunks
+    unsigned long long n_items;  // warp tiles x theta groups
+    unsigned groups;         // theta groups per warp tile
+};
+constexpr int kGroup = 8;  // thetas per CTA item (= warps per CTA)
+
+template <int R, int S, int SHIFT, bool IGNORE, int XG>
+__global__ void __launch_bounds__(256, 1)
+    screen_region_kernel(const ScreenArgs a, const unsigned nwx, const unsigned nwy,
+                         const RegionPlan rp) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    unsigned* hist = reinterpret_cast<unsigned*>(smem);
+    float2* P = reinterpret_cast<float2*>(smem + kHistBins * sizeof(unsigned));
+    for (int i = threadIdx.x; i < kHistBins; i += blockDim.x) hist[i] = 0u;
+
+    constexpr int YG = 32 / XG;
+    constexpr int TWX = 8 * XG, TWY = YG * S;  // warp tile
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+    const int yg = lane % YG, xg = lane / YG;
+    const int h = a.ro + R;
+    const int PW = a.geom.PW, GH = a.geom.H + 2;
+    const float2* G = static_cast<const float2*>(a.plane);
+    const float K = a.K;
+    const int B3 = (int)a.B3;
+
+    const unsigned long long b0 = rp.n_items * blockIdx.x / gridDim.x;
+    const unsigned long long b1 = rp.n_items * (blockIdx.x + 1) / gridDim.x;
+    long long loaded = -1;
+    for (unsigned long long ci = b0; ci < b1; ++ci) {
+        const unsigned long long tile = ci / rp.groups;
+        const unsigned g = (unsigned)(ci % rp.groups);
+        const unsigned wx = (unsigned)(tile % nwx), wy = (unsigned)(tile / nwx);
+        const int TX0 = (int)wx * TWX, TY0 = (int)wy * TWY;
+        // region (0, 0) = padded plane (C0, R0)
+        const int C0 = TX0 + a.ix0 + 1 + a.geom.PL - h;
+        const int R0 = TY0 + a.iy0 + 1 - h;
+        if ((long long)tile != loaded) {
+            __syncthreads();  // previous item's readers are done
+            for (int r = warp; r < rp.RH; r += nwarp) {
+                const int gr = R0 + r;
+                float2* srow = P + r * rp.RW + (r >> SHIFT);
+                if (gr >= 0 && gr < GH) {
+                    const float2* grow = G + (size_t)gr * PW + (gr >> SHIFT);
+                    for (int c = lane; c < rp.RW; c += 32) {
+                        const int gc = C0 + c;
+                        srow[c] = (gc >= 0 && gc < PW) ? __ldg(grow + gc) : make_float2(0.f, 0.f);
+                    }
+                } else {
+                    for (int c = lane; c < rp.RW; c += 32) srow[c] = make_float2(0.f, 0.f);
+                }
+            }
+            __syncthreads();
+            loaded = (long long)tile;
+        }
+        const unsigned long long itr = (unsigned long long)g * kGroup + warp;
+        if (itr >= a.it_count) continue;  // warp-uniform; barriers above are CTA-uniform
+        const int Xr = xg * kTW, Yr = yg * S;  // lane block inside the tile
+        const int4* rot = a.rot_screen + (size_t)itr * a.n;
+        // field bounds in region coordinates (window-centre mask for R >= 2)
+        const int cx_lo = 1 + a.geom.PL - C0, cx_hi = a.geom.W + a.geom.PL - C0;
+        const int ry_lo = 1 - R0, ry_hi = a.geom.H - R0;
+
+        int acc[S][kTW];
+#pragma unroll
+        for (int s = 0; s < S; ++s)
+#pragma unroll
+            for (int j = 0; j < kTW; ++j) acc[s][j] = 0;
+        if (a.n > 0) {
+            int4 p = __ldg(rot);
+            for (int i = 0; i < a.n; ++i) {
+                const int4 pn = __ldg(rot + (i + 1 < a.n ? i + 1 : i));
+                const float dxf = __int_as_float(p.z), dyf = __int_as_float(p.w);
+                const int cb = p.x + Xr + h - R;  // region column of the window start
+                const int rb = p.y + Yr + h - R;  // region row of the window start
+                point_rows<R, S, SHIFT, IGNORE, false, float2>(P, rp.RW, rp.RW - 1, cx_lo, cx_hi,
+                                                              rp.RH - 1, 0, cb, rb, ry_lo, ry_hi,
+                                                              dxf, dyf, K, B3, acc);
+                p = pn;
+            }
+        }
+        const unsigned long long item = (itr * nwy + wy) * nwx + wx;
+        emit_tile<S>(a, acc, TX0 + Xr, TY0 + Yr, itr, item, hist, lane);
+    }
+    __syncthreads();
+    for (int b = threadIdx.x; b < kHistBins; b += blockDim.x) {
+        const unsigned v = hist[b];
+        if (v) atomicAdd(&a.hist[b], v);
+    }
+}
+
+static RegionPlan region_plan(const ScreenArgs& a, int R) {
+    constexpr int S = 8;
+    const int YG = 32 / a.xg;
+    const int h = a.ro + R;
+    RegionPlan rp{};
+    rp.RW = 8 * a.xg + 2 * h;
+    rp.RW += rp.RW & 1;  // even pitch: lane slots stay yg + 8*xg (mod 16)
+    rp.RH = YG * S + 2 * h;
+    const size_t elems = (size_t)rp.RH * rp.RW + (size_t)((rp.RH - 1) >> 3) + 1;
+    rp.elems16 = (int)((elems * sizeof(float2) + 15) / 16);
+    return rp;
+}
+
+static size_t region_smem(const RegionPlan& rp) {
+    return kHistBins * sizeof(unsigned) + (size_t)rp.elems16 * 16;
+}
+
+template <int R, bool IGNORE, int XG>
+static void run_region(ea_ctx* ctx, const ScreenArgs& a, RegionPlan rp) {
+    constexpr int S = 8, YG = 32 / XG;
+    const unsigned nwx = (unsigned)((a.nx + 8 * XG - 1) / (8 * XG));
+    const unsigned nwy = (unsigned)((a.ny + YG * S - 1) / (YG * S));
+    rp.groups = (unsigned)((a.it_count + kGroup - 1) / kGroup);
+    rp.n_items = (unsigned long long)nwx * nwy * rp.groups;
+    const size_t smem = region_smem(rp);
+    auto kern = screen_region_kernel<R, S, 3, IGNORE, XG>;
+    EAB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    unsigned long long ctas = std::min<unsigned long long>(rp.n_items, (unsigned)ctx->sm_count);
+    if (ctas == 0) ctas = 1;
+    kern<<<(unsigned)ctas, kGroup * 32, smem, ctx->stream>>>(a, nwx, nwy, rp);
+    check_launch("screen_region_kernel");
+    count_launch(ctx);
+}
+
+bool launch_screen_region(ea_ctx* ctx, const ScreenArgs& a) {
+    if (a.geom.shift != 3 || a.geom.elem_bytes != 8 || a.R > 2) return false;
+    const RegionPlan rp = region_plan(a, a.R);
+    if (region_smem(rp) > ctx->smem_optin) return false;
+    const bool ig = a.ignore != 0;
+#define EAB_REGION(RR)                                                          \
+    if (a.R == RR) {                                                            \
+        if (a.xg == 2) {                                                        \
+            if (ig) run_region<RR, true, 2>(ctx, a, rp);                        \
+            else run_region<RR, false, 2>(ctx, a, rp);                          \
+        } else {                                                                \
+            if (ig) run_region<RR, true, 4>(ctx, a, rp);                        \
+            else run_region<RR, false, 4>(ctx, a, rp);                          \
+        }                                                                       \
+        return true;                                                            \
+    }
+    EAB_REGION(1)
+    EAB_REGION(0)
+    EAB_REGION(2)
+#undef EAB_REGION
     return false;
 }
 

@@ -249,6 +249,48 @@ def test_screen_bound(ea, oracle, nb, pol, general, plane_mode):
     assert delta < (2e-6 if (general or plane_mode == "f32") else 1e-3)
 
 
+REGION_CASES = [
+    # (model, size, field w, h, grid, nb, polarity): top planes larger than
+    # shared memory -> region-tiled lattice kernel (screen_path 3)
+    ("l_bracket", 40, 400, 330, (0, 399, 1, 0, 329, 1, 0.0, D(330), D(30)), 3, 0),
+    ("rectangle", 64, 420, 300, (-12, 431, 1, -9, 310, 1, 0.1, D(200), D(20)), 3, 0),
+    ("ring", 24, 380, 380, (0, 379, 1, 0, 379, 1, 0.0, D(350), D(50)), 1, 0),
+    ("cross", 48, 400, 320, (3, 396, 1, 2, 317, 1, 0.0, D(340), D(20)), 5, 0),
+    ("l_bracket", 64, 360, 360, (0, 359, 1, 0, 359, 1, 0.0, D(300), D(60)), 3, 1),
+    # halo region of a 96 px model exceeds shared memory -> general kernel
+    ("l_bracket", 96, 360, 360, (0, 359, 1, 0, 359, 1, 0.0, D(300), D(60)), 3, 0),
+]
+
+
+@pytest.mark.parametrize("case", range(len(REGION_CASES)))
+def test_region_search_bit_exact(ea, oracle, case):
+    shape, size, w, h, g, nb, pol = REGION_CASES[case]
+    rng = np.random.default_rng(300 + case)
+    tm = oracle.prepare_model(oracle.render_template(shape, size))
+    f = oracle.compute_gradients(rand_image(rng, w, h, real=case % 2 == 1))
+    grid = ea.PoseGrid(*g)
+    params = ea.ScoreParams(nb, pol)
+    for k in (1, 9):
+        got = ea.search_topk(tm, f, grid, params, k=k)
+        assert ea.default_context().stats()["screen_path"] == (2 if size > 64 else 3)
+        want = oracle.search_topk(tm.points, f, grid, params, k)
+        assert keys(got) == keys(want)
+
+
+@pytest.mark.parametrize("nb,pol", [(3, 0), (5, 1), (1, 0)])
+def test_region_screen_bound(ea, oracle, nb, pol):
+    rng = np.random.default_rng(40 + nb)
+    tm = oracle.prepare_model(oracle.render_template("l_bracket", 56))
+    f = oracle.compute_gradients(rand_image(rng, 300, 420, real=True))
+    grid = ea.PoseGrid(-20, 310, 1, -15, 430, 1, 0.2, D(300), D(60))
+    params = ea.ScoreParams(nb, pol)
+    sf, delta = ea.screen_map(tm, f, grid, params)
+    assert ea.default_context().stats()["screen_path"] == 3
+    s = oracle.score_map(tm.points, f, grid, params, 1 << 30)
+    err = np.abs(sf.astype(np.float64) - s).max()
+    assert err <= delta, (err, delta)
+
+
 def test_theta_slabs_merge_to_full(ea, oracle):
     """Theta-sharded search + `better` merge == the full search (the
     multi-GPU exchange, search.cpp:116-139)."""
