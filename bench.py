@@ -56,6 +56,13 @@ CONFIGS = {
 CONFIGS["cfg4"] = dict(CONFIGS["cfg2"], desc="batch of 64 1280x1024 search images x 1 model "
                        "(cfg2 geometry, poses and seeds from SplitMix64(1000+i)), throughput mode",
                        batch=64)
+CONFIGS["cfg5"] = dict(desc="2592x1944 cluttered image, 8 models (rectangle/ring/l_bracket/cross "
+                            "cycling, 64-400 px), 0.5 deg over 360, 4 levels, nb 3, one detect "
+                            "per model on a shared pyramid (multi-model, multi-instance)",
+                       W=2592, H=1944, clutter=400, seed=23, occluder=None, illum=(1.0, 0.0, 1.0),
+                       sigma=0.0, nseed=0, L=4, dt=0.5, multi=True,
+                       sizes=(64, 96, 128, 160, 200, 256, 320, 400))
+SHAPES = ("rectangle", "ring", "l_bracket", "cross")
 
 
 class SplitMix64:
@@ -113,6 +120,40 @@ def make_inputs(name, noise_seed=None):
     cfg = ea.SearchConfig(grid=grid, num_levels=L, score_params=ea.ScoreParams(3), topk=5,
                           refine_radius=2, min_score=0.5)
     return img, tmpl, cfg, truth
+
+
+def multi_stamps(name):
+    """cfg5 stamps: model i (shape i mod 4, size sizes[i]) in cell i of a 4x2
+    grid, jitter and angle from SplitMix64(5000 + i)."""
+    c = CONFIGS[name]
+    cw, ch = c["W"] / 4.0, c["H"] / 2.0
+    stamps = []
+    for i, size in enumerate(c["sizes"]):
+        r = SplitMix64(5000 + i)
+        ux = cw * (i % 4 + 0.5) + (r.uniform01() - 0.5) * 40.0
+        uy = ch * (i // 4 + 0.5) + (r.uniform01() - 0.5) * 40.0
+        stamps.append((SHAPES[i % 4], size, (ux, uy, D(r.uniform01() * 360.0))))
+    return stamps
+
+
+def make_multi_inputs(name, noise_seed=None):
+    """cfg5: (image, [template images], cfg, [truth poses])."""
+    c = CONFIGS[name]
+    sigma, nseed = c["sigma"], c["nseed"]
+    if noise_seed is not None:
+        sigma, nseed = max(sigma, 1.0), noise_seed
+    stamps = multi_stamps(name)
+    spec = ea.SceneSpec(c["W"], c["H"], "rectangle", 0, (0.0, 0.0, 0.0), c["clutter"], c["seed"],
+                        c["occluder"], c["illum"], sigma, nseed)
+    img = ea.compose_multi(spec, stamps)
+    tmpls = [ea.render_template(t, s) for t, s, _ in stamps]
+    L = c["L"]
+    step = float(1 << (L - 1))
+    grid = ea.PoseGrid(0.0, c["W"] - 1.0, step, 0.0, c["H"] - 1.0, step, 0.0,
+                       D(360.0 - c["dt"]), D(c["dt"]))
+    cfg = ea.SearchConfig(grid=grid, num_levels=L, score_params=ea.ScoreParams(3), topk=5,
+                          refine_radius=2, min_score=0.5)
+    return img, tmpls, cfg, [p for _, _, p in stamps]
 
 
 def top_grid(cfg):
@@ -188,14 +229,20 @@ def reference_sample(name, target_s=12.0, threads=0):
     on a theta slice of the top level: returns (pose_evals, seconds, sample)."""
     from oracle.pyoracle import ReferenceLib
     ref = ReferenceLib()
-    img, tmpl, cfg, _ = make_inputs(name)
+    if CONFIGS[name].get("multi"):
+        img, tmpls, cfg, _ = make_multi_inputs(name)
+    else:
+        img, tmpl, cfg, _ = make_inputs(name)
+        tmpls = [tmpl]
     L = cfg.num_levels
-    tp, wp = ref.build_pyramid(tmpl, L), ref.build_pyramid(img, L)
-    models, fields = ref.prepare_levels(tp, wp, cfg)
-    m, f = models[L - 1], fields[L - 1]
+    wp = ref.build_pyramid(img, L)
+    mf = []  # (top model points, top field) per model
+    for tmpl in tmpls:
+        models, fields = ref.prepare_levels(ref.build_pyramid(tmpl, L), wp, cfg)
+        mf.append((models[L - 1].points, fields[L - 1]))
     tg = top_grid(cfg)
     nx, ny, nt = ref.grid_counts(tg)
-    n = len(m.points)
+    n = sum(len(p) for p, _ in mf)
     threads = threads or len(os.sched_getaffinity(0))
 
     def run(nth):
@@ -203,7 +250,8 @@ def reference_sample(name, target_s=12.0, threads=0):
                         tg.t0 + (nth - 1) * tg.dt, tg.dt)
         assert ref.grid_counts(g)[2] == nth
         t0 = time.perf_counter()
-        ref.search_topk(m.points, f, g, cfg.score_params, cfg.topk, threads=threads)
+        for pts, f in mf:
+            ref.search_topk(pts, f, g, cfg.score_params, cfg.topk, threads=threads)
         return time.perf_counter() - t0
 
     probe = max(1, min(nt, threads // 8 or 1))
@@ -211,8 +259,10 @@ def reference_sample(name, target_s=12.0, threads=0):
     nth = int(min(nt, max(probe, probe * target_s / max(dt, 1e-3))))
     secs = run(nth)
     evals = nx * ny * nth * n
-    sample = (f"{name} top level, theta slice {nth}/{nt} ({nx}x{ny} translations, {n} model "
-              f"points), reference search_topk Backend::Parallel")
+    what = f"{len(mf)} models, {n} top model points in all" if len(mf) > 1 else \
+        f"{n} model points"
+    sample = (f"{name} top level, theta slice {nth}/{nt} ({nx}x{ny} translations, {what}), "
+              f"reference search_topk Backend::Parallel")
     return evals, secs, sample, threads
 
 
@@ -249,13 +299,21 @@ def bench_ours(args, rank, world, local_rank):
     ctx.set_stream(stream.cuda_stream)
     ctx.set_timing(True)
 
-    img, tmpl, cfg, truth = make_inputs(args.config)
-    det = ea.Detector(tmpl, cfg, ctx)           # template side, once (untimed prep)
-    det.levels.set_image(img)                    # working pyramid resident in HBM
+    multi = bool(CONFIGS[args.config].get("multi"))
+    if multi:
+        img, tmpls, cfg, truth = make_multi_inputs(args.config)
+    else:
+        img, tmpl, cfg, truth = make_inputs(args.config)
+        tmpls = [tmpl]
+    dets = [ea.Detector(t, cfg, ctx) for t in tmpls]  # template sides, once (untimed prep)
+    det = dets[0]
+    for d in dets:
+        d.levels.set_image(img)                  # working pyramid resident in HBM
     tg = top_grid(cfg)
     nx, ny, nt = ea.grid_counts(tg)
     L = cfg.num_levels
-    n_top = len(det.levels.model(L - 1).points)
+    n_tops = [len(d.levels.model(L - 1).points) for d in dets]
+    n_top = sum(n_tops)
     it0, it1 = parallel.theta_slab(nt, rank, world)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
 
@@ -264,9 +322,15 @@ def bench_ours(args, rank, world, local_rank):
             return seeds
         return parallel.gather_topk(seeds, cfg.topk, device=dev)
 
+    step_screen = []
+
     def top_step():
-        seeds = ea.search_top_slab(det.levels, cfg, it0, it1)
-        return gather(seeds)
+        out = []
+        step_screen.clear()
+        for d in dets:  # one top-level search per model (cfg5: 8)
+            out.append(gather(ea.search_top_slab(d.levels, cfg, it0, it1)))
+            step_screen.append(ctx.stats()["screen_ms"])
+        return out
 
     def barrier():
         if world > 1:
@@ -287,7 +351,7 @@ def bench_ours(args, rank, world, local_rank):
             ev[i][0].record(stream)
             seeds = top_step()
             ev[i][1].record(stream)
-            screen_ms.append(ctx.stats()["screen_ms"])
+            screen_ms.append(sum(step_screen))
         barrier()
     launches = ctx.kernel_launches() - launches0
     st = ctx.stats()
@@ -309,18 +373,27 @@ def bench_ours(args, rank, world, local_rank):
     if CONFIGS[args.config].get("batch"):  # cfg4: the batch is the workload, sharded by rank
         n_img = CONFIGS[args.config]["batch"] // world
         scenes = batch_scenes(args.config, CONFIGS[args.config]["batch"])[rank * n_img:(rank + 1) * n_img]
+    elif multi:
+        n_img = min(n_img, 8)
+        scenes = [img] + [make_multi_inputs(args.config, noise_seed=101 + j)[0] for j in range(3)]
     else:
         scenes = [img] + [make_inputs(args.config, noise_seed=101 + j)[0] for j in range(3)]
     pinned = [torch.from_numpy(scenes[j % len(scenes)]).pin_memory() for j in range(n_img)]
     host_imgs = [p.numpy() for p in pinned]
     k = cfg.topk
     h2d = img.size * 8
-    d2h = 472 + 48  # ea_outcome + control block per image
-    det.detect_batch(host_imgs)  # warm-up: same batch size (pinned result slots, tables)
+    d2h = (472 + 48) * len(dets)  # ea_outcome + control block per image and model
+
+    def e2e_run():
+        if multi:  # one ea_detect_multi call per image: shared pyramid, 8 models
+            return [ea.detect_multi(dets, im) for im in host_imgs]
+        return det.detect_batch(host_imgs)
+
+    e2e_run()  # warm-up: same batch size (pinned result slots, tables)
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
-    outs = det.detect_batch(host_imgs)
+    outs = e2e_run()
     e1.record(stream)
     barrier()
     e2e_ms = e0.elapsed_time(e1)
@@ -337,7 +410,10 @@ def bench_ours(args, rank, world, local_rank):
     for i in range(min(n_img, 20) + args.warmup):
         a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a0.record(stream)
-        det.detect(host_imgs[i % len(host_imgs)])
+        if multi:
+            ea.detect_multi(dets, host_imgs[i % len(host_imgs)])
+        else:
+            det.detect(host_imgs[i % len(host_imgs)])
         a1.record(stream)
         torch.cuda.synchronize(dev)
         if i >= args.warmup:
@@ -362,19 +438,22 @@ def bench_ours(args, rank, world, local_rank):
         "higher_is_better": True, "scaling": "strong" if world > 1 else "none",
         "vs_baseline": None, "dtype": "f32 screen + f64 exact verify", "data": "synthetic",
         "config": {"workload": f"{args.config}: {CONFIGS[args.config]['desc']}",
-                   "top_level_grid": f"{nx}x{ny}x{nt}", "top_model_points": n_top,
+                   "top_level_grid": f"{nx}x{ny}x{nt}",
+                   "top_model_points": n_tops if multi else n_top,
                    "pose_evals_per_step": pose_pts, "l2": "flushed (256 MiB write) between steps",
                    "parallelism": f"theta-slab x{world}" if world > 1 else "single GPU"},
         "e2e": {"value": e2e, "unit": "pose-evals/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_image": e2e_ms / n_img, "images": n_img * world,
-                "api": "Detector.detect_batch (ea_detect_batch), pinned host images",
+                "api": ("detect_multi (ea_detect_multi), one call per pinned host image"
+                        if multi else "Detector.detect_batch (ea_detect_batch), pinned host images"),
                 "detect_latency_ms": statistics.median(lat),
                 "latency_phases_ms_median": {
                     k: statistics.median(p[i] for p in phases)
                     for i, k in enumerate(("h2d_pyramid_gradients", "top_level_search",
                                            "refinement"))}},
-        "roofline": {"bound": "smem", "kernel": "screen_fast_kernel" if st["screen_path"] == 1
-                     else "screen_general_kernel", "achieved": achieved,
+        "roofline": {"bound": "smem", "kernel": {1: "screen_fast_kernel",
+                                                 3: "screen_region_kernel"}.get(
+                         st["screen_path"], "screen_general_kernel"), "achieved": achieved,
                      "peak": smem_peak_gbs, "unit": "GB/s", "frac": achieved / smem_peak_gbs,
                      # dram read+write of one launch, ncu --set full (not measurable in-run)
                      "traffic": 8940032 if args.config in ("cfg2", "cfg4") else None,
@@ -391,9 +470,9 @@ def bench_ours(args, rank, world, local_rank):
         "clocks": clk.summary(),
         "search": {"candidates": st["candidates"], "screen_delta": st["screen_delta"],
                    "flagged_points": st["flagged_points"],
-                   "detected": bool(outcome.found) if outcome is not None else None,
-                   "pose": outcome.pose.astuple() if outcome is not None else None,
-                   "score": outcome.score if outcome is not None else None,
+                   "detected": [bool(o.found) for o in outcome] if multi else bool(outcome.found),
+                   "pose": [o.pose.astuple() for o in outcome] if multi else outcome.pose.astuple(),
+                   "score": [o.score for o in outcome] if multi else outcome.score,
                    "truth": truth},
     }
     if not args.no_cpu_baseline:

@@ -152,6 +152,12 @@ typedef struct {
     uint64_t noise_seed;
 } ea_scene_spec;
 
+/* One template of a multi-stamp scene. */
+typedef struct {
+    int32_t template_id, template_size;
+    ea_pose pose;
+} ea_stamp;
+
 /* Device-side accounting of the last top-level search on a context. */
 typedef struct {
     uint64_t poses;            /* grid poses screened                          */
@@ -321,6 +327,14 @@ ea_status ea_coarse_to_fine(ea_ctx* ctx, const double* const* tmpl_levels,
 ea_status ea_detect(ea_ctx* ctx, ea_levels* lv, const double* image, int w, int h,
                     const ea_search_config* cfg, ea_outcome* out);
 
+/* Multi-model detect (BASELINE configs[4]): one host image, n prepared
+ * template sides (one ea_levels per model, all prepared for cfg).  The
+ * working pyramid is built once -- into models[0]'s working side -- and
+ * every model's search_levels runs against it, back to back on the stream
+ * with one sync; outs[n].  Equals ea_detect per model. */
+ea_status ea_detect_multi(ea_ctx* ctx, ea_levels* const* models, int n, const double* image,
+                          int w, int h, const ea_search_config* cfg, ea_outcome* outs);
+
 /* Throughput mode (BASELINE configs[3]): `count` host images of one size,
  * image i+1's H2D overlapping image i's device pipeline; outs[count]. */
 ea_status ea_detect_batch(ea_ctx* ctx, ea_levels* lv, const double* const* images, int count,
@@ -331,6 +345,14 @@ ea_status ea_render_template(int template_id, int size, double* out);  /* synth.
 /* compose_scene  synth.cpp:178-300.  canvas: W*H, tmpl: size*size. */
 ea_status ea_compose_scene(const ea_scene_spec* spec, double* canvas, double* tmpl,
                            ea_pose* truth_pose, double* occluded_fraction);
+/* Multi-stamp scene (BASELINE configs[4]; not in the reference, which stamps
+ * one template per scene -- SURVEY.md H8): background + clutter as
+ * compose_scene, then each stamp in order with compose_scene's inverse-mapped
+ * paste (synth.cpp:224-244), then occluder / illumination / noise.  The
+ * spec's template_id, template_size and true_pose are ignored.  With one stamp
+ * the canvas equals ea_compose_scene's. */
+ea_status ea_compose_multi(const ea_scene_spec* spec, const ea_stamp* stamps, int n_stamps,
+                           double* canvas);
 
 #ifdef __cplusplus
 }

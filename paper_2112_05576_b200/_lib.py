@@ -97,7 +97,11 @@ _SIGS = {
                             C.POINTER(abi.Outcome)]),
     "ea_detect_batch": (C.c_int, [_P, _P, C.POINTER(_dp), C.c_int, C.c_int, C.c_int,
                                   C.POINTER(abi.SearchConfig), C.POINTER(abi.Outcome)]),
+    "ea_detect_multi": (C.c_int, [_P, C.POINTER(_P), C.c_int, _dp, C.c_int, C.c_int,
+                                  C.POINTER(abi.SearchConfig), C.POINTER(abi.Outcome)]),
     "ea_render_template": (C.c_int, [C.c_int, C.c_int, _dp]),
+    "ea_compose_multi": (C.c_int, [C.POINTER(abi.SceneSpec), C.POINTER(abi.Stamp), C.c_int,
+                                   _dp]),
     "ea_compose_scene": (C.c_int, [C.POINTER(abi.SceneSpec), _dp, _dp, C.POINTER(abi.Pose),
                                    _dp]),
 }

@@ -128,6 +128,17 @@ class SearchConfig(C.Structure):
         self.worker_count = worker_count
 
 
+class Stamp(C.Structure):
+    """ea_stamp: one template of a multi-stamp scene (ea_compose_multi)."""
+    _fields_ = [("template_id", C.c_int32), ("template_size", C.c_int32), ("pose", Pose)]
+
+    def __init__(self, template_id="rectangle", template_size=0, pose=(0.0, 0.0, 0.0)):
+        super().__init__()
+        self.template_id = TEMPLATE_IDS[template_id] if isinstance(template_id, str) else template_id
+        self.template_size = template_size
+        self.pose = Pose(*pose)
+
+
 class SceneSpec(C.Structure):
     """edgealign::SceneSpec (synth.h:67-79); theta in radians."""
     _fields_ = [("canvas_width", C.c_int32), ("canvas_height", C.c_int32),

@@ -520,12 +520,40 @@ class Detector:
         return list(outs)
 
 
+def detect_multi(detectors, image):
+    """Multi-model detect (ea_detect_multi): one image, several Detectors that
+    share a context and a config; the working pyramid is built once (into the
+    first detector's levels).  -> one Outcome per detector."""
+    if not detectors:
+        return []
+    ctx, cfg = detectors[0].ctx, detectors[0].config
+    for d in detectors:
+        if d.ctx is not ctx:
+            raise ValueError("detect_multi needs detectors on one context")
+    img = image if (isinstance(image, np.ndarray) and image.dtype == np.float64
+                    and image.flags.c_contiguous) else _f64(image)
+    hs = (C.c_void_p * len(detectors))(*[d.levels.handle for d in detectors])
+    outs = (Outcome * len(detectors))()
+    _check(lib().ea_detect_multi(ctx.handle, hs, len(detectors), _ptr(img), img.shape[1],
+                                 img.shape[0], C.byref(cfg), outs))
+    return list(outs)
+
+
 # ---- synthetic scenes (synth.cpp:62-300) -----------------------------------------
 def render_template(template_id, size):
     tid = abi.TEMPLATE_IDS[template_id] if isinstance(template_id, str) else template_id
     out = np.zeros((max(size, 1), max(size, 1)))
     _check(lib().ea_render_template(int(tid), int(size), _ptr(out)))
     return out
+
+
+def compose_multi(spec, stamps):
+    """Multi-stamp scene (ea_compose_multi): spec's canvas, clutter, occluder,
+    illumination and noise; `stamps` = [(template_id, size, (ux, uy, theta))]."""
+    arr = (abi.Stamp * max(len(stamps), 1))(*[abi.Stamp(t, s, p) for t, s, p in stamps])
+    canvas = np.zeros((max(spec.canvas_height, 1), max(spec.canvas_width, 1)))
+    _check(lib().ea_compose_multi(C.byref(spec), arr, len(stamps), _ptr(canvas)))
+    return canvas
 
 
 def compose_scene(spec):

@@ -313,7 +313,10 @@ ScreenPlan screen(ea_ctx* ctx, const ea_model* m, const ea_field* f, const ea_po
     unsigned* hist = (unsigned*)ctx->hist.ensure(sizeof(unsigned) * kHistBins);
     EAB_CUDA(cudaMemsetAsync(ctrl, 0, sizeof(SearchCtrl), ctx->stream));
     EAB_CUDA(cudaMemsetAsync(hist, 0, sizeof(unsigned) * kHistBins, ctx->stream));
-    launch_rotate(ctx, m->pts.as<double>(), n, d_cs, (int)nth, rot, scr, &ctrl->flags);
+    // per-theta ambiguous-point counts + list of flagged thetas (see ScreenArgs::amb)
+    int* amb = (int*)ctx->amb.ensure(sizeof(int) * (2 * nth + 2));
+    EAB_CUDA(cudaMemsetAsync(amb, 0, sizeof(int) * (2 * nth + 2), ctx->stream));
+    launch_rotate(ctx, m->pts.as<double>(), n, d_cs, (int)nth, rot, scr, &ctrl->flags, amb);
 
     // Fixed-point fold exponent: sums of n votes stay below 2^31.
     int e = 0;
@@ -406,6 +409,7 @@ ScreenPlan screen(ea_ctx* ctx, const ea_model* m, const ea_field* f, const ea_po
         a.xg = padded(16, 128) < padded(32, 64) ? 2 : 4;
     }
     a.ro = ro_int;
+    a.amb = amb;
     a.K = K;
     a.B3 = B3;
     a.scale = (float)(std::ldexp(1.0, e - 22) / (double)n);
@@ -417,7 +421,8 @@ ScreenPlan screen(ea_ctx* ctx, const ea_model* m, const ea_field* f, const ea_po
     if (ctx->timing) EAB_CUDA(cudaEventRecord(ctx->ev[1], ctx->stream));
     if (plan.slab_poses) {
         if (lattice) plan.fast = region ? launch_screen_region(ctx, a) : launch_screen_fast(ctx, a);
-        if (!plan.fast) launch_screen_general(ctx, a);
+        if (plan.fast) launch_screen_flagged(ctx, a);  // thetas the lattice kernel skipped
+        else launch_screen_general(ctx, a);
     }
     if (ctx->timing) EAB_CUDA(cudaEventRecord(ctx->ev[2], ctx->stream));
     ctx->stats.screen_path = plan.fast ? (region ? 3 : 1) : 2;
@@ -487,10 +492,9 @@ TopLaunch top_enqueue(ea_ctx* ctx, const ea_model* m, const ea_field* f, const e
     x.dy = g.dy;
     unsigned* cand = (unsigned*)ctx->cand.ensure(sizeof(unsigned) * cap);
     double* cs = (double*)ctx->cand_score.ensure(sizeof(double) * cap);
-    // band threshold from the histogram (delta widened on the device by the
-    // rounding-ambiguous pairs, lattice path only), then the compaction
+    // band threshold from the histogram, then the compaction
     launch_compact(ctx, ctx->map.as<float>(), ctx->item_max.as<float>(), t.plan.items, ctrl, cand,
-                   cap, ctx->hist.as<unsigned>(), k, t.plan.delta, t.plan.fast ? t.n : 0);
+                   cap, ctx->hist.as<unsigned>(), k, t.plan.delta);
     launch_rescore(ctx, x, cand, ctrl, cap, cs);
     launch_select(ctx, cand, cs, ctrl, cap, k, t.plan.it_begin * t.plan.c.nx * t.plan.c.ny,
                   t.top_score, t.top_index);
@@ -503,7 +507,7 @@ bool top_stats(ea_ctx* ctx, const TopLaunch& t, const SearchCtrl& hc) {
     ctx->stats.candidates_needed = hc.needed;
     ctx->stats.threshold = hc.thr;
     ctx->stats.flagged_points = hc.flags;
-    ctx->stats.screen_delta = t.plan.delta + (t.plan.fast ? 2.0 * hc.flags / t.n : 0.0);
+    ctx->stats.screen_delta = t.plan.delta;
     return hc.cand_count <= t.cap;
 }
 
@@ -1099,6 +1103,76 @@ void detect_batch(ea_ctx* ctx, ea_levels* lv, const double* const* images, int c
             search_levels_device(ctx, lv, cfg, outs + i);
         }
     }
+}
+
+// Multi-model detect: the working pyramid is built once (into models[0]),
+// then every model's search_levels is enqueued against it with its own
+// outcome slot; one sync.  A model whose candidate band overflowed the
+// buffer is redone alone (search_levels_device grows the buffer).
+void detect_multi(ea_ctx* ctx, ea_levels* const* models, int n, const double* image, int w,
+                  int h, const ea_search_config& cfg, ea_outcome* outs) {
+    const int L = cfg.num_levels;
+    for (int i = 0; i < n; ++i) {
+        need(models[i], "models[i]");
+        if ((int)models[i]->models.size() < L)
+            fail(EA_ERR_INVALID_ARGUMENT, "prepared levels of model " + std::to_string(i) +
+                                              " do not cover num_levels");
+    }
+    if (ctx->timing) EAB_CUDA(cudaEventRecord(ctx->ev[4], ctx->stream));
+    ea_levels* work = models[0];
+    set_working_image(ctx, work, image, w, h, L);
+    if (ctx->timing) EAB_CUDA(cudaEventRecord(ctx->ev[5], ctx->stream));
+    // a view = model i's template side + the shared working side (not owned)
+    struct View {
+        ea_levels lv;
+        ~View() {
+            lv.models.clear();
+            lv.fields.clear();
+        }
+    };
+    std::vector<View> views(n);
+    for (int i = 0; i < n; ++i) {
+        views[i].lv.models = models[i]->models;
+        views[i].lv.fields = work->fields;
+        check_search_config(&views[i].lv, cfg);
+    }
+    const double* tables = detect_tables(ctx, cfg);
+    if (L > 1 && !tables) {  // host-assisted refinement: one by one
+        for (int i = 0; i < n; ++i) search_levels_device(ctx, &views[i].lv, cfg, outs + i);
+        return;
+    }
+    const size_t slot = sizeof(ea_outcome) + sizeof(SearchCtrl);
+    char* dres = (char*)ctx->rslots.ensure(slot * (size_t)n);
+    char* hres = (char*)ctx->h_out.ensure(slot * (size_t)n);
+    const unsigned long long cap = std::max<unsigned long long>(initial_cap(ctx), 1ull << 20);
+    std::vector<TopLaunch> launches;
+    launches.reserve(n);
+    for (int i = 0; i < n; ++i) {
+        ea_outcome* d_out = (ea_outcome*)(dres + slot * i);
+        SearchCtrl* d_ctrl = (SearchCtrl*)(dres + slot * i + sizeof(ea_outcome));
+        launches.push_back(enqueue_levels(ctx, &views[i].lv, cfg, tables, cap, d_out, d_ctrl));
+        d2h(ctx, hres + slot * i, dres + slot * i, slot);
+    }
+    if (ctx->timing) EAB_CUDA(cudaEventRecord(ctx->ev[7], ctx->stream));
+    sync(ctx);
+    if (ctx->timing) {
+        float ms = 0.f;
+        EAB_CUDA(cudaEventElapsedTime(&ms, ctx->ev[4], ctx->ev[5]));
+        ctx->stats.image_ms = ms;
+        EAB_CUDA(cudaEventElapsedTime(&ms, ctx->ev[5], ctx->ev[7]));
+        ctx->stats.top_ms = ms;  // all models' search_levels
+        ctx->stats.refine_ms = 0.0;
+    }
+    std::vector<int> redo;
+    for (int i = 0; i < n; ++i) {
+        SearchCtrl hc;
+        std::memcpy(&hc, hres + slot * i + sizeof(ea_outcome), sizeof hc);
+        if (top_stats(ctx, launches[i], hc))
+            std::memcpy(outs + i, hres + slot * i, sizeof(ea_outcome));
+        else
+            redo.push_back(i);
+    }
+    for (int i : redo) search_levels_device(ctx, &views[i].lv, cfg, outs + i);
 }
 
 // Template side of prepare_levels (search.cpp:222-234) for one level.
@@ -1746,7 +1820,7 @@ ea_status ea_screen_map(ea_ctx* ctx, const ea_model* m, const ea_field* f, const
         d2h(ctx, out, ctx->map.p, sizeof(float) * total);
         sync(ctx);
         ctx->stats.flagged_points = hc.flags;
-        ctx->stats.screen_delta = plan.delta + (plan.fast ? 2.0 * hc.flags / m->n : 0.0);
+        ctx->stats.screen_delta = plan.delta;
         if (delta) *delta = ctx->stats.screen_delta;
     });
 }
@@ -2012,6 +2086,22 @@ ea_status ea_detect_batch(ea_ctx* ctx, ea_levels* lv, const double* const* image
     });
 }
 
+ea_status ea_detect_multi(ea_ctx* ctx, ea_levels* const* models, int n, const double* image,
+                          int w, int h, const ea_search_config* cfg, ea_outcome* outs) {
+    return guard([&] {
+        need(ctx, "ctx");
+        need(cfg, "config");
+        if (n <= 0) return;
+        need(models, "models");
+        need(image, "image");
+        need(outs, "outs");
+        DeviceGuard dg(ctx->device);
+        const uint64_t launched0 = ctx->launches;
+        detect_multi(ctx, models, n, image, w, h, *cfg, outs);
+        ctx->stats.kernels_launched = (int)(ctx->launches - launched0);
+    });
+}
+
 // ---- synthetic scenes ----------------------------------------------------------------------
 ea_status ea_render_template(int template_id, int size, double* out) {
     return guard([&] {
@@ -2031,6 +2121,15 @@ ea_status ea_compose_scene(const ea_scene_spec* spec, double* canvas, double* tm
         host_compose_scene(*spec, canvas, tmpl, &tp, &occ);
         if (truth_pose) *truth_pose = tp;
         if (occluded_fraction) *occluded_fraction = occ;
+    });
+}
+
+ea_status ea_compose_multi(const ea_scene_spec* spec, const ea_stamp* stamps, int n_stamps,
+                           double* canvas) {
+    return guard([&] {
+        need(spec, "spec");
+        need(canvas, "canvas");
+        host_compose_multi(*spec, stamps, n_stamps, canvas);
     });
 }
 

@@ -17,6 +17,7 @@ std::vector<ea_edge_point> host_extract_edge_model(const double* gx, const doubl
 
 // Synthetic scenes (synth.cpp:24-300), host only: libm-dependent generator.
 void host_render_template(int id, int size, double* out);
+void host_compose_multi(const ea_scene_spec& s, const ea_stamp* stamps, int n, double* canvas);
 void host_compose_scene(const ea_scene_spec& s, double* canvas, double* tmpl,
                         ea_pose* truth_pose, double* occluded_fraction);
 

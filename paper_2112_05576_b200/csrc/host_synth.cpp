@@ -132,82 +132,110 @@ void host_render_template(int id, int size, double* img) {
     }
 }
 
-void host_compose_scene(const ea_scene_spec& s, double* canvas, double* tmpl,
-                        ea_pose* truth_pose, double* occluded_fraction) {
+namespace {
+
+// One template placed at a pose: the rendered template, its edge centroid
+// (template_edge_centroid, synth.cpp:169-174) and the forward-mapped bbox,
+// which must stay on the canvas (synth.cpp:196-217).
+struct Stamp {
+    int T = 0;
+    std::vector<double> tmpl;
+    std::vector<ea_edge_point> pts;
+    double ccx = 0.0, ccy = 0.0;
+    ea_pose pose{};
+    double c = 1.0, sn = 0.0;
+    double lo_x = 0, hi_x = 0, lo_y = 0, hi_y = 0;
+};
+
+Stamp make_stamp(int template_id, int T, ea_pose pose, int W, int H) {
+    Stamp st;
+    st.T = T;
+    st.pose = pose;
+    st.tmpl.assign((size_t)std::max(T, 1) * std::max(T, 1), 0.0);
+    host_render_template(template_id, T, st.tmpl.data());
+    std::vector<double> tgx, tgy, tmag;
+    sobel_host(st.tmpl.data(), T, T, tgx, tgy, tmag);
+    st.pts = host_extract_edge_model(tgx.data(), tgy.data(), tmag.data(), T, T,
+                                     host_default_thresholds(tmag.data(), tmag.size()), &st.ccx,
+                                     &st.ccy);
+    st.c = std::cos(pose.theta);
+    st.sn = std::sin(pose.theta);
+    st.lo_x = st.lo_y = 1e300;
+    st.hi_x = st.hi_y = -1e300;
+    for (int corner = 0; corner < 4; ++corner) {
+        const double tx = (corner & 1 ? (double)(T - 1) : 0.0) - st.ccx;
+        const double ty = (corner & 2 ? (double)(T - 1) : 0.0) - st.ccy;
+        const double px = (st.c * tx - st.sn * ty) + pose.ux;
+        const double py = (st.sn * tx + st.c * ty) + pose.uy;
+        st.lo_x = std::min(st.lo_x, px);
+        st.hi_x = std::max(st.hi_x, px);
+        st.lo_y = std::min(st.lo_y, py);
+        st.hi_y = std::max(st.hi_y, py);
+    }
+    if (st.lo_x < 0.0 || st.lo_y < 0.0 || st.hi_x > W - 1.0 || st.hi_y > H - 1.0) {
+        char buf[256];
+        std::snprintf(buf, sizeof buf,
+                      "transformed template leaves the canvas (bbox [%f, %f] .. [%f, %f])",
+                      st.lo_x, st.lo_y, st.hi_x, st.hi_y);
+        fail(EA_ERR_GEOMETRY, buf);
+    }
+    return st;
+}
+
+void check_spec(const ea_scene_spec& s) {
     if (s.canvas_width < 16 || s.canvas_height < 16)
         fail(EA_ERR_INVALID_ARGUMENT, "canvas must be at least 16x16");
     if (!(s.gain > 0.0) || !(s.gamma > 0.0))
         fail(EA_ERR_INVALID_ARGUMENT, "illumination gain and gamma must be positive");
     if (s.noise_sigma < 0.0) fail(EA_ERR_INVALID_ARGUMENT, "noise_sigma must be >= 0");
-    const int W = s.canvas_width, H = s.canvas_height, T = s.template_size;
+}
 
-    host_render_template(s.template_id, T, tmpl);
-    std::vector<double> tgx, tgy, tmag;
-    sobel_host(tmpl, T, T, tgx, tgy, tmag);
-    double ccx = 0.0, ccy = 0.0;
-    const std::vector<ea_edge_point> pts = host_extract_edge_model(
-        tgx.data(), tgy.data(), tmag.data(), T, T,
-        host_default_thresholds(tmag.data(), tmag.size()), &ccx, &ccy);
-
-    const ea_pose pose = s.true_pose;
-    const double c = std::cos(pose.theta), sn = std::sin(pose.theta);
-    // Forward-mapped template corners must stay on the canvas.
-    double lo_x = 1e300, hi_x = -1e300, lo_y = 1e300, hi_y = -1e300;
-    for (int corner = 0; corner < 4; ++corner) {
-        const double tx = (corner & 1 ? (double)(T - 1) : 0.0) - ccx;
-        const double ty = (corner & 2 ? (double)(T - 1) : 0.0) - ccy;
-        const double px = (c * tx - sn * ty) + pose.ux;
-        const double py = (sn * tx + c * ty) + pose.uy;
-        lo_x = std::min(lo_x, px);
-        hi_x = std::max(hi_x, px);
-        lo_y = std::min(lo_y, py);
-        hi_y = std::max(hi_y, py);
-    }
-    if (lo_x < 0.0 || lo_y < 0.0 || hi_x > W - 1.0 || hi_y > H - 1.0) {
-        char buf[256];
-        std::snprintf(buf, sizeof buf,
-                      "transformed template leaves the canvas (bbox [%f, %f] .. [%f, %f])", lo_x,
-                      lo_y, hi_x, hi_y);
-        fail(EA_ERR_GEOMETRY, buf);
-    }
-
+// Background + clutter line segments (draw_clutter, synth.cpp:134-165).
+void draw_background(const ea_scene_spec& s, double* canvas) {
+    const int W = s.canvas_width, H = s.canvas_height;
     std::fill(canvas, canvas + (size_t)W * H, kBackground);
-    {  // clutter line segments
-        Rng rng(s.clutter_seed);
-        for (int seg = 0; seg < s.clutter_segments; ++seg) {
-            const double ax = rng.unit() * W, ay = rng.unit() * H;
-            const double bx = rng.unit() * W, by = rng.unit() * H;
-            const double value = rng.unit() * 255.0;
-            const int pen = 1 + (int)(rng.next() & 1ULL);
-            const int steps = 1 + (int)(2.0 * std::hypot(bx - ax, by - ay));
-            for (int i = 0; i <= steps; ++i) {
-                const double t = (double)i / steps;
-                const int px = nearest_up(ax + t * (bx - ax));
-                const int py = nearest_up(ay + t * (by - ay));
-                for (int dy = 0; dy < pen; ++dy)
-                    for (int dx = 0; dx < pen; ++dx) {
-                        const int X = px + dx, Y = py + dy;
-                        if (X >= 0 && X < W && Y >= 0 && Y < H) canvas[(size_t)Y * W + X] = value;
-                    }
-            }
+    Rng rng(s.clutter_seed);
+    for (int seg = 0; seg < s.clutter_segments; ++seg) {
+        const double ax = rng.unit() * W, ay = rng.unit() * H;
+        const double bx = rng.unit() * W, by = rng.unit() * H;
+        const double value = rng.unit() * 255.0;
+        const int pen = 1 + (int)(rng.next() & 1ULL);
+        const int steps = 1 + (int)(2.0 * std::hypot(bx - ax, by - ay));
+        for (int i = 0; i <= steps; ++i) {
+            const double t = (double)i / steps;
+            const int px = nearest_up(ax + t * (bx - ax));
+            const int py = nearest_up(ay + t * (by - ay));
+            for (int dy = 0; dy < pen; ++dy)
+                for (int dx = 0; dx < pen; ++dx) {
+                    const int X = px + dx, Y = py + dy;
+                    if (X >= 0 && X < W && Y >= 0 && Y < H) canvas[(size_t)Y * W + X] = value;
+                }
         }
     }
-    {  // inverse-mapped stamp, template lookup rounds half down
-        const int x_lo = std::max(0, (int)std::floor(lo_x) - 1);
-        const int y_lo = std::max(0, (int)std::floor(lo_y) - 1);
-        const int x_hi = std::min(W - 1, (int)std::ceil(hi_x) + 1);
-        const int y_hi = std::min(H - 1, (int)std::ceil(hi_y) + 1);
-        for (int y = y_lo; y <= y_hi; ++y) {
-            for (int x = x_lo; x <= x_hi; ++x) {
-                const double rx = x - pose.ux, ry = y - pose.uy;
-                const int ix = (int)std::ceil(((c * rx + sn * ry) + ccx) - 0.5);
-                const int iy = (int)std::ceil(((-sn * rx + c * ry) + ccy) - 0.5);
-                if (ix < 0 || ix >= T || iy < 0 || iy >= T) continue;
-                const double v = tmpl[(size_t)iy * T + ix];
-                if (v != kBackground) canvas[(size_t)y * W + x] = v;
-            }
+}
+
+// Inverse-mapped stamp, template lookup rounds half down (synth.cpp:224-244).
+void paste(const Stamp& st, int W, int H, double* canvas) {
+    const int x_lo = std::max(0, (int)std::floor(st.lo_x) - 1);
+    const int y_lo = std::max(0, (int)std::floor(st.lo_y) - 1);
+    const int x_hi = std::min(W - 1, (int)std::ceil(st.hi_x) + 1);
+    const int y_hi = std::min(H - 1, (int)std::ceil(st.hi_y) + 1);
+    const int T = st.T;
+    for (int y = y_lo; y <= y_hi; ++y) {
+        for (int x = x_lo; x <= x_hi; ++x) {
+            const double rx = x - st.pose.ux, ry = y - st.pose.uy;
+            const int ix = (int)std::ceil(((st.c * rx + st.sn * ry) + st.ccx) - 0.5);
+            const int iy = (int)std::ceil(((-st.sn * rx + st.c * ry) + st.ccy) - 0.5);
+            if (ix < 0 || ix >= T || iy < 0 || iy >= T) continue;
+            const double v = st.tmpl[(size_t)iy * T + ix];
+            if (v != kBackground) canvas[(size_t)y * W + x] = v;
         }
     }
+}
+
+// Occluder, gamma then gain/bias, noise (synth.cpp:246-285).
+void finish(const ea_scene_spec& s, double* canvas) {
+    const int W = s.canvas_width, H = s.canvas_height;
     if (s.has_occluder) {
         const int x_lo = std::max(0, s.occ_x), y_lo = std::max(0, s.occ_y);
         const int x_hi = std::min(W - 1, s.occ_x + s.occ_w - 1);
@@ -215,7 +243,7 @@ void host_compose_scene(const ea_scene_spec& s, double* canvas, double* tmpl,
         for (int y = y_lo; y <= y_hi; ++y)
             for (int x = x_lo; x <= x_hi; ++x) canvas[(size_t)y * W + x] = s.occ_fill;
     }
-    for (size_t i = 0; i < (size_t)W * H; ++i) {  // gamma, then gain/bias
+    for (size_t i = 0; i < (size_t)W * H; ++i) {
         const double v = canvas[i];
         const double g = (s.gamma == 1.0) ? v : 255.0 * std::pow(v / 255.0, s.gamma);
         canvas[i] = s.gain * g + s.bias;
@@ -224,18 +252,46 @@ void host_compose_scene(const ea_scene_spec& s, double* canvas, double* tmpl,
         Rng rng(s.noise_seed);
         for (size_t i = 0; i < (size_t)W * H; ++i) canvas[i] += s.noise_sigma * rng.gauss();
     }
-    *truth_pose = pose;
-    *occluded_fraction = 0.0;
-    if (s.has_occluder) {
-        int hit = 0;
-        for (const ea_edge_point& p : pts) {
-            const int ix = nearest_up((c * p.x_rel - sn * p.y_rel) + pose.ux);
-            const int iy = nearest_up((sn * p.x_rel + c * p.y_rel) + pose.uy);
-            if (ix >= s.occ_x && ix < s.occ_x + s.occ_w && iy >= s.occ_y && iy < s.occ_y + s.occ_h)
-                ++hit;
-        }
-        *occluded_fraction = (double)hit / (double)pts.size();
+}
+
+double occluded_fraction(const ea_scene_spec& s, const Stamp& st) {
+    if (!s.has_occluder) return 0.0;
+    int hit = 0;
+    for (const ea_edge_point& p : st.pts) {
+        const int ix = nearest_up((st.c * p.x_rel - st.sn * p.y_rel) + st.pose.ux);
+        const int iy = nearest_up((st.sn * p.x_rel + st.c * p.y_rel) + st.pose.uy);
+        if (ix >= s.occ_x && ix < s.occ_x + s.occ_w && iy >= s.occ_y && iy < s.occ_y + s.occ_h)
+            ++hit;
     }
+    return (double)hit / (double)st.pts.size();
+}
+
+}  // namespace
+
+void host_compose_scene(const ea_scene_spec& s, double* canvas, double* tmpl,
+                        ea_pose* truth_pose, double* occluded) {
+    check_spec(s);
+    const Stamp st = make_stamp(s.template_id, s.template_size, s.true_pose, s.canvas_width,
+                                s.canvas_height);
+    std::copy(st.tmpl.begin(), st.tmpl.end(), tmpl);
+    draw_background(s, canvas);
+    paste(st, s.canvas_width, s.canvas_height, canvas);
+    finish(s, canvas);
+    *truth_pose = st.pose;
+    *occluded = occluded_fraction(s, st);
+}
+
+void host_compose_multi(const ea_scene_spec& s, const ea_stamp* stamps, int n, double* canvas) {
+    check_spec(s);
+    if (n < 0 || (n > 0 && !stamps)) fail(EA_ERR_INVALID_ARGUMENT, "bad stamp list");
+    std::vector<Stamp> sts;
+    sts.reserve(n);
+    for (int i = 0; i < n; ++i)
+        sts.push_back(make_stamp(stamps[i].template_id, stamps[i].template_size, stamps[i].pose,
+                                 s.canvas_width, s.canvas_height));
+    draw_background(s, canvas);
+    for (const Stamp& st : sts) paste(st, s.canvas_width, s.canvas_height, canvas);
+    finish(s, canvas);
 }
 
 }  // namespace eab

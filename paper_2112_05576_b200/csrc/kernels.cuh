@@ -140,8 +140,10 @@ void launch_plane(ea_ctx* ctx, const ea_field* f, double eps, const PlaneGeom& g
 
 // rotate_model for many thetas: rot_exact = px|py|dx|dy (each nth*n doubles),
 // rot_screen = {ox, oy, dxf, dyf} per (theta, point) for the lattice kernel.
+// amb (with rot_screen): [nth] rounding-ambiguous points per theta, then the
+// count and the list of thetas that have any (AmbList); flags: their total.
 void launch_rotate(ea_ctx* ctx, const double* pts_soa, int n, const double* cs, int nth,
-                   double* rot_exact, int4* rot_screen, int* flags);
+                   double* rot_exact, int4* rot_screen, int* flags, int* amb = nullptr);
 
 struct ScreenArgs {
     const void* plane;        // float2 or __half2 elements (geom.elem_bytes)
@@ -160,6 +162,11 @@ struct ScreenArgs {
     int ignore;
     int xg;           // lattice warp tile: xg * 8 columns x (32 / xg) * 8 rows
     int ro;           // region kernel: bound on |lattice offset| of every rotated point
+    // Thetas with a rounding-ambiguous lattice offset (amb[it] > 0) are left
+    // to the general kernel (exact fp64 centres): the lattice kernels skip
+    // them (item_max = +inf so compaction scans their map), the general kernel
+    // runs over the list amb[nth + 1 ..] of amb[nth] entries.
+    const int* amb;
     float K;          // fixed-point fold constant 3*2^e
     unsigned B3;      // bits of K
     float scale;      // 2^(e-22) / n
@@ -178,10 +185,10 @@ bool launch_screen_fast(ea_ctx* ctx, const ScreenArgs& a);
 // Returns false when even one halo region does not fit.
 bool launch_screen_region(ea_ctx* ctx, const ScreenArgs& a);
 void launch_screen_general(ea_ctx* ctx, const ScreenArgs& a);
+// The general kernel over the flagged thetas of a lattice launch only.
+void launch_screen_flagged(ea_ctx* ctx, const ScreenArgs& a);
 
-// delta is widened on the device by 2*ctrl->flags/flag_n when flag_n > 0.
-void launch_threshold(ea_ctx* ctx, const unsigned* hist, int k, double delta, int flag_n,
-                      SearchCtrl* ctrl);
+void launch_threshold(ea_ctx* ctx, const unsigned* hist, int k, double delta, SearchCtrl* ctrl);
 void launch_point_vote(ea_ctx* ctx, const ea_field* f, int cx, int cy, int R, double dx,
                        double dy, double eps, bool absolute, double* out);
 // Work-item geometry of the screening map, for the compaction pass.
@@ -195,7 +202,7 @@ ItemGeom screen_items(const ScreenArgs& a, bool fast);
 // Compaction with the band threshold (see launch_threshold) computed in-kernel.
 void launch_compact(ea_ctx* ctx, const float* map, const float* item_max, const ItemGeom& g,
                     SearchCtrl* ctrl, unsigned* cand, unsigned long long cap,
-                    const unsigned* hist, int k, double delta, int flag_n);
+                    const unsigned* hist, int k, double delta);
 
 struct ExactArgs {
     const double* gx;

@@ -51,7 +51,7 @@ __device__ __forceinline__ int lattice_offset(double p, bool* amb) {
 __global__ void rotate_kernel(const double* __restrict__ pts, int n,
                               const double* __restrict__ cs, int nth,
                               double* __restrict__ rot, int4* __restrict__ scr,
-                              int* __restrict__ flags) {
+                              int* __restrict__ flags, int* __restrict__ amb_list) {
     const size_t total = (size_t)nth * n;
     const size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= total) return;
@@ -74,16 +74,22 @@ __global__ void rotate_kernel(const double* __restrict__ pts, int n,
         const int ox = lattice_offset(px, &amb);
         const int oy = lattice_offset(py, &amb);
         scr[t] = make_int4(ox, oy, __float_as_int((float)ndx), __float_as_int((float)ndy));
-        if (amb) atomicAdd(flags, 1);
+        if (amb) {
+            atomicAdd(flags, 1);
+            if (amb_list && atomicAdd(amb_list + th, 1) == 0) {  // first ambiguous point of th
+                const int pos = atomicAdd(amb_list + nth, 1);
+                amb_list[nth + 1 + pos] = th;
+            }
+        }
     }
 }
 
 void launch_rotate(ea_ctx* ctx, const double* pts_soa, int n, const double* cs, int nth,
-                   double* rot_exact, int4* rot_screen, int* flags) {
+                   double* rot_exact, int4* rot_screen, int* flags, int* amb) {
     const size_t total = (size_t)nth * n;
     if (total == 0) return;
     rotate_kernel<<<(unsigned)((total + 255) / 256), 256, 0, ctx->stream>>>(
-        pts_soa, n, cs, nth, rot_exact, rot_screen, flags);
+        pts_soa, n, cs, nth, rot_exact, rot_screen, flags, amb);
     check_launch("rotate_kernel");
     count_launch(ctx);
 }
@@ -314,6 +320,10 @@ __global__ void __launch_bounds__(screen_threads<S>(), 1)
         const int X = X0 + xg * kTW;
         const int Y = (int)wy * (YG * S) + yg * S;
         const int4* rot = a.rot_screen + (size_t)itr * a.n;
+        if (__ldg(a.amb + itr) != 0) {  // flagged theta: the general kernel scores it
+            if (lane == 0) a.item_max[item] = INFINITY;
+            continue;
+        }
 
         int acc[S][kTW];
 #pragma unroll
@@ -509,6 +519,11 @@ __global__ void __launch_bounds__(256, 1)
         }
         const unsigned long long itr = (unsigned long long)g * kGroup + warp;
         if (itr >= a.it_count) continue;  // warp-uniform; barriers above are CTA-uniform
+        const unsigned long long item = (itr * nwy + wy) * nwx + wx;
+        if (__ldg(a.amb + itr) != 0) {  // flagged theta: the general kernel scores it
+            if (lane == 0) a.item_max[item] = INFINITY;
+            continue;
+        }
         const int Xr = xg * kTW, Yr = yg * S;  // lane block inside the tile
         const int4* rot = a.rot_screen + (size_t)itr * a.n;
         // field bounds in region coordinates (window-centre mask for R >= 2)
@@ -533,7 +548,6 @@ __global__ void __launch_bounds__(256, 1)
                 p = pn;
             }
         }
-        const unsigned long long item = (itr * nwy + wy) * nwx + wx;
         emit_tile<S>(a, acc, TX0 + Xr, TY0 + Yr, itr, item, hist, lane);
     }
     __syncthreads();
@@ -606,11 +620,13 @@ bool launch_screen_region(ea_ctx* ctx, const ScreenArgs& a) {
 // fixed-point arithmetic is the same as the lattice kernel's.
 template <bool IGNORE>
 __global__ void __launch_bounds__(256)
-    screen_general_kernel(const ScreenArgs a, const unsigned long long total) {
+    screen_general_kernel(const ScreenArgs a, unsigned long long total, const int* tlist) {
     __shared__ unsigned hist[kHistBins];
     for (int i = threadIdx.x; i < kHistBins; i += blockDim.x) hist[i] = 0u;
     __syncthreads();
     const unsigned long long plane_poses = a.nx * a.ny;
+    // list mode: logical theta j -> slab theta tlist[j + 1], tlist[0] entries
+    if (tlist) total = (unsigned long long)__ldg(tlist) * plane_poses;
     const int W = a.geom.W, H = a.geom.H, PW = a.geom.PW, SH = a.geom.shift;
     const int R = a.R;
     const float K = a.K;
@@ -621,7 +637,8 @@ __global__ void __launch_bounds__(256)
         const unsigned long long t = t0 + lane;
         float sc = -INFINITY;
         if (t < total) {
-        const unsigned long long itr = t / plane_poses;
+        const unsigned long long itr = tlist ? (unsigned long long)__ldg(tlist + 1 + t / plane_poses)
+                                             : t / plane_poses;
         const unsigned long long rem = t % plane_poses;
         const unsigned long long iy = rem / a.nx, ix = rem % a.nx;
         const double ux = lattice(a.x0, ix, a.dx);
@@ -657,9 +674,10 @@ __global__ void __launch_bounds__(256)
             acc += __float_as_int(best) - B3;
         }
         sc = (float)acc * a.scale;
-        a.map[t] = sc;
+        a.map[itr * plane_poses + rem] = sc;
         atomicAdd(&hist[hist_bin(sc)], 1u);
         }
+        if (tlist) continue;  // item_max belongs to the lattice items (set to +inf)
         float best = sc;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) best = fmaxf(best, __shfl_xor_sync(0xffffffffu, best, o));
@@ -679,10 +697,27 @@ void launch_screen_general(ea_ctx* ctx, const ScreenArgs& a) {
     if (blocks > cap) blocks = cap;
     if (blocks == 0) blocks = 1;
     if (a.ignore)
-        screen_general_kernel<true><<<(unsigned)blocks, 256, 0, ctx->stream>>>(a, total);
+        screen_general_kernel<true><<<(unsigned)blocks, 256, 0, ctx->stream>>>(a, total, nullptr);
     else
-        screen_general_kernel<false><<<(unsigned)blocks, 256, 0, ctx->stream>>>(a, total);
+        screen_general_kernel<false><<<(unsigned)blocks, 256, 0, ctx->stream>>>(a, total, nullptr);
     check_launch("screen_general_kernel");
+    count_launch(ctx);
+}
+
+// Flagged thetas (a few per full rotation, e.g. 90/180/270 deg for a model
+// with half-integer coordinates): their count lives on the device, so the
+// grid is sized for the worst case and idle blocks exit at once.
+void launch_screen_flagged(ea_ctx* ctx, const ScreenArgs& a) {
+    const unsigned long long worst = a.nx * a.ny * a.it_count;
+    unsigned long long blocks = std::min<unsigned long long>((worst + 255) / 256,
+                                                             (unsigned long long)ctx->sm_count * 2);
+    if (blocks == 0) blocks = 1;
+    const int* tlist = a.amb + a.it_count;
+    if (a.ignore)
+        screen_general_kernel<true><<<(unsigned)blocks, 256, 0, ctx->stream>>>(a, 0, tlist);
+    else
+        screen_general_kernel<false><<<(unsigned)blocks, 256, 0, ctx->stream>>>(a, 0, tlist);
+    check_launch("screen_general_kernel(flagged)");
     count_launch(ctx);
 }
 
@@ -693,8 +728,8 @@ void launch_screen_general(ea_ctx* ctx, const ScreenArgs& a) {
 // of the candidate count.
 template <int BLOCK>
 __device__ __forceinline__ float block_threshold(const unsigned* __restrict__ hist, int k,
-                                                 double delta, int flag_n,
-                                                 SearchCtrl* ctrl, bool write) {
+                                                 double delta, SearchCtrl* ctrl,
+                                                 bool write) {
     using Scan = cub::BlockScan<unsigned long long, BLOCK>;
     constexpr int PER = kHistBins / BLOCK;
     __shared__ typename Scan::TempStorage tmp;
@@ -723,7 +758,6 @@ __device__ __forceinline__ float block_threshold(const unsigned* __restrict__ hi
     if (t == 0) {
         float thr = -INFINITY;
         if (kbin >= 0) {  // else fewer than k poses: every pose is a candidate
-            if (flag_n > 0) delta += 2.0 * (double)ctrl->flags / (double)flag_n;
             const double lo = (double)kbin / 2048.0 - 1.0;
             const double th = lo - 2.0 * delta - 9.5367431640625e-07;  // 2^-20
             thr = (float)th;
@@ -740,14 +774,12 @@ __device__ __forceinline__ float block_threshold(const unsigned* __restrict__ hi
 // fewer than k scores lie strictly above T_f) and sets thr = lo(b) - 2*delta -
 // 2^-20 (the slack covers fp32 rounding inside hist_bin).
 __global__ void __launch_bounds__(256) threshold_kernel(const unsigned* __restrict__ hist, int k,
-                                                        double delta, int flag_n,
-                                                        SearchCtrl* ctrl) {
-    block_threshold<256>(hist, k, delta, flag_n, ctrl, true);
+                                                        double delta, SearchCtrl* ctrl) {
+    block_threshold<256>(hist, k, delta, ctrl, true);
 }
 
-void launch_threshold(ea_ctx* ctx, const unsigned* hist, int k, double delta, int flag_n,
-                      SearchCtrl* ctrl) {
-    threshold_kernel<<<1, 256, 0, ctx->stream>>>(hist, k, delta, flag_n, ctrl);
+void launch_threshold(ea_ctx* ctx, const unsigned* hist, int k, double delta, SearchCtrl* ctrl) {
+    threshold_kernel<<<1, 256, 0, ctx->stream>>>(hist, k, delta, ctrl);
     check_launch("threshold_kernel");
     count_launch(ctx);
 }
@@ -763,8 +795,8 @@ __global__ void __launch_bounds__(256) compact_kernel(const float* __restrict__ 
                                                       unsigned* __restrict__ cand,
                                                       unsigned long long cap,
                                                       const unsigned* __restrict__ hist, int k,
-                                                      double delta, int flag_n) {
-    const float thr = block_threshold<256>(hist, k, delta, flag_n, ctrl, blockIdx.x == 0);
+                                                      double delta) {
+    const float thr = block_threshold<256>(hist, k, delta, ctrl, blockIdx.x == 0);
     const int lane = threadIdx.x & 31;
     const unsigned long long warp = ((unsigned long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const unsigned long long nwarps = ((unsigned long long)gridDim.x * blockDim.x) >> 5;
@@ -854,13 +886,13 @@ ItemGeom screen_items(const ScreenArgs& a, bool fast) {
 
 void launch_compact(ea_ctx* ctx, const float* map, const float* item_max, const ItemGeom& g,
                     SearchCtrl* ctrl, unsigned* cand, unsigned long long cap,
-                    const unsigned* hist, int k, double delta, int flag_n) {
+                    const unsigned* hist, int k, double delta) {
     unsigned long long blocks = (g.n_items * 32 + 255) / 256;
     const unsigned long long maxb = (unsigned long long)ctx->sm_count;
     if (blocks > maxb) blocks = maxb;
     if (blocks == 0) blocks = 1;
     compact_kernel<<<(unsigned)blocks, 256, 0, ctx->stream>>>(map, item_max, g, ctrl, cand, cap,
-                                                              hist, k, delta, flag_n);
+                                                              hist, k, delta);
     check_launch("compact_kernel");
     count_launch(ctx);
 }

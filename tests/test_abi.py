@@ -46,7 +46,7 @@ STRUCTS = {
     "ea_edge_point": abi.EdgePoint, "ea_scored_pose": abi.ScoredPose,
     "ea_level_trace": abi.LevelTrace, "ea_outcome": abi.Outcome,
     "ea_search_config": abi.SearchConfig, "ea_scene_spec": abi.SceneSpec,
-    "ea_search_stats": abi.SearchStats,
+    "ea_search_stats": abi.SearchStats, "ea_stamp": abi.Stamp,
 }
 
 

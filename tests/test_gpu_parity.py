@@ -291,6 +291,31 @@ def test_region_screen_bound(ea, oracle, nb, pol):
     assert err <= delta, (err, delta)
 
 
+@pytest.mark.parametrize("shape,size,w,h", [("rectangle", 32, 60, 50), ("ring", 24, 48, 48),
+                                             ("ring", 96, 400, 320)])
+def test_flagged_thetas_exact(ea, oracle, shape, size, w, h):
+    """Half-integer model coordinates at 90/180/270 deg give rounding-ambiguous
+    lattice offsets (cos 90 deg != 0 in fp64): those thetas go through the
+    general kernel, the rest through the lattice (or region) kernel, and
+    the screening bound stays two-sided, so the band stays narrow."""
+    rng = np.random.default_rng(size + w)
+    pts = np.array(oracle.prepare_model(oracle.render_template(shape, size)).points)
+    pts[:, :2] = np.floor(pts[:, :2]) + 0.5  # half-integer coordinates (as pyramid models get)
+    tm = ea.EdgeModel(pts)
+    f = oracle.compute_gradients(rand_image(rng, w, h, real=True))
+    grid = ea.PoseGrid(0, w - 1, 1, 0, h - 1, 1, 0.0, D(355), D(5))
+    params = ea.ScoreParams(3)
+    got = ea.search_topk(tm, f, grid, params, k=5)
+    st = ea.default_context().stats()
+    assert st["flagged_points"] > 0 and st["screen_path"] in (1, 3)
+    assert st["candidates"] < 2000
+    assert keys(got) == keys(oracle.search_topk(tm.points, f, grid, params, 5))
+    if w * h <= 3000:
+        sf, delta = ea.screen_map(tm, f, grid, params)
+        s = oracle.score_map(tm.points, f, grid, params, 1 << 30)
+        assert np.abs(sf.astype(np.float64) - s).max() <= delta
+
+
 def test_theta_slabs_merge_to_full(ea, oracle):
     """Theta-sharded search + `better` merge == the full search (the
     multi-GPU exchange, search.cpp:116-139)."""
@@ -463,3 +488,42 @@ def test_config4_batch_bit_exact(ea, oracle):
     tp = oracle.build_pyramid(tmpl, L)
     for img, got in zip(imgs, outs):
         assert got.key() == oracle.coarse_to_fine(tp, oracle.build_pyramid(img, L), cfg).key()
+
+
+def test_detect_multi_matches_oracle(ea, oracle):
+    """Multi-model detect on a multi-stamp scene whose top level (320x240)
+    exceeds shared memory (region-tiled screening): each model's outcome ==
+    its own Detector.detect == the oracle's coarse_to_fine."""
+    stamps = [("l_bracket", 64, (150.0, 130.0, D(40))), ("cross", 96, (460.0, 140.0, D(15))),
+              ("ring", 80, (170.0, 350.0, 0.0)), ("rectangle", 72, (470.0, 340.0, D(200)))]
+    spec = ea.SceneSpec(640, 480, "rectangle", 0, (0, 0, 0), 60, 5, None, (1.1, 4.0, 1.0), 1.5, 9)
+    img = ea.compose_multi(spec, stamps)
+    cfg = ea.SearchConfig(grid=ea.PoseGrid(0, 639, 2, 0, 479, 2, 0.0, D(350), D(10)),
+                          num_levels=2, score_params=ea.ScoreParams(3), topk=3)
+    tmpls = [ea.render_template(t, s) for t, s, _ in stamps]
+    dets = [ea.Detector(t, cfg) for t in tmpls]
+    outs = ea.detect_multi(dets, img)
+    wp = oracle.build_pyramid(img, 2)
+    for t, d, got in zip(tmpls, dets, outs):
+        want = oracle.coarse_to_fine(oracle.build_pyramid(t, 2), wp, cfg)
+        assert got.key() == want.key()
+        assert got.key() == d.detect(img).key()
+    assert ea.default_context().stats()["screen_path"] == 3
+
+
+@pytest.mark.slow
+def test_config5_multi_detect_bit_exact(ea, oracle):
+    """BASELINE configs[4]: 2592x1944 cluttered multi-stamp scene, 8 models
+    (64-400 px), 0.5 deg, 4 levels: detect_multi == oracle, model by model."""
+    import bench
+    img, tmpls, cfg, _ = bench.make_multi_inputs("cfg5")
+    L = cfg.num_levels
+    dets = [ea.Detector(t, cfg) for t in tmpls]
+    outs = ea.detect_multi(dets, img)
+    wp = oracle.build_pyramid(img, L)
+    # Parity only: under 400 clutter segments the reference's top-k beam
+    # (5 seeds, no spatial suppression) locks onto clutter for several of the
+    # small/symmetric models, and so must we.
+    for t, got in zip(tmpls, outs):
+        want = oracle.coarse_to_fine(oracle.build_pyramid(t, L), wp, cfg)
+        assert got.key() == want.key()
