@@ -277,10 +277,14 @@ struct ScreenPlan {
     double delta = 0.0;
     bool fast = false;
     ItemGeom items{};
+    const double* rot = nullptr;  // exact rotation table of the slab (model cache)
+    const int* flags = nullptr;   // device count of rounding-ambiguous pairs
 };
 
+// k: the search's top-k (enables the screen kernels' histogram floor when
+// k <= kFloorK); 0 for a plain screening map.
 ScreenPlan screen(ea_ctx* ctx, const ea_model* m, const ea_field* f, const ea_pose_grid& g,
-                  const ea_score_params& p, uint64_t it_begin, uint64_t it_end) {
+                  const ea_score_params& p, uint64_t it_begin, uint64_t it_end, int k = 0) {
     ScreenPlan plan;
     plan.c = counts_of(g);
     if (it_end == 0 || it_end > plan.c.nt) it_end = plan.c.nt;
@@ -294,29 +298,38 @@ ScreenPlan screen(ea_ctx* ctx, const ea_model* m, const ea_field* f, const ea_po
     const int n = m->n;
     const int R = (p.neighborhood - 1) / 2;
 
-    // Tables for the slab's thetas.
+    // Tables for the slab's thetas, cached on the model (see ea_model::tab_key).
     const size_t nth = plan.it_count;
-    double* d_cs = (double*)ctx->cs.ensure(sizeof(double) * 2 * (nth ? nth : 1));
-    const std::vector<double> key{g.t0, g.dt, (double)plan.c.nt, (double)it_begin, (double)nth};
-    if (key != ctx->cs_dev_key) {  // device copy of the slab's cos/sin, reused across calls
-        const std::vector<double>& cs_all = theta_cs(ctx, g.t0, g.dt, plan.c.nt);
-        ctx->cs_dev_key.clear();
-        h2d_staged(ctx, d_cs, cs_all.data() + 2 * it_begin, sizeof(double) * 2 * nth);
-        ctx->cs_dev_key = key;
-    }
-    // Slab-relative rotation tables: row (it - it_begin) of px|py|dx|dy and of
-    // the lattice table.
     const size_t slab_pairs = nth * (size_t)n;
-    double* rot = (double*)ctx->rot_exact.ensure(sizeof(double) * 4 * (slab_pairs ? slab_pairs : 1));
-    int4* scr = (int4*)ctx->rot_screen.ensure(sizeof(int4) * (slab_pairs ? slab_pairs : 1));
+    ea_model* mm = const_cast<ea_model*>(m);
+    const std::vector<double> key{g.t0, g.dt, (double)plan.c.nt, (double)it_begin, (double)nth};
+    double* rot = (double*)mm->rot.ensure(sizeof(double) * 4 * (slab_pairs ? slab_pairs : 1));
+    int4* scr = (int4*)mm->scr.ensure(sizeof(int4) * (slab_pairs ? slab_pairs : 1));
+    // per-theta ambiguous-point counts, the flagged-theta list (ScreenArgs::amb)
+    // and, in the last slot, the total of ambiguous pairs
+    int* amb = (int*)mm->amb.ensure(sizeof(int) * (2 * nth + 3));
+    int4* sched = (int4*)mm->sched.ensure(sizeof(int4) * (nth ? nth : 1) * (1 + 2 * (size_t)n));
+    if (key != mm->tab_key) {
+        mm->tab_key.clear();
+        double* d_cs = (double*)ctx->cs.ensure(sizeof(double) * 2 * (nth ? nth : 1));
+        if (key != ctx->cs_dev_key) {  // device copy of the slab's cos/sin
+            const std::vector<double>& cs_all = theta_cs(ctx, g.t0, g.dt, plan.c.nt);
+            ctx->cs_dev_key.clear();
+            h2d_staged(ctx, d_cs, cs_all.data() + 2 * it_begin, sizeof(double) * 2 * nth);
+            ctx->cs_dev_key = key;
+        }
+        EAB_CUDA(cudaMemsetAsync(amb, 0, sizeof(int) * (2 * nth + 3), ctx->stream));
+        launch_rotate(ctx, m->pts.as<double>(), n, d_cs, (int)nth, rot, scr, amb + 2 * nth + 2,
+                      amb);
+        launch_schedule(ctx, scr, n, (int)nth, sched);
+        mm->tab_key = key;
+    }
     SearchCtrl* ctrl = (SearchCtrl*)ctx->ctrl.ensure(sizeof(SearchCtrl));
     unsigned* hist = (unsigned*)ctx->hist.ensure(sizeof(unsigned) * kHistBins);
     EAB_CUDA(cudaMemsetAsync(ctrl, 0, sizeof(SearchCtrl), ctx->stream));
     EAB_CUDA(cudaMemsetAsync(hist, 0, sizeof(unsigned) * kHistBins, ctx->stream));
-    // per-theta ambiguous-point counts + list of flagged thetas (see ScreenArgs::amb)
-    int* amb = (int*)ctx->amb.ensure(sizeof(int) * (2 * nth + 2));
-    EAB_CUDA(cudaMemsetAsync(amb, 0, sizeof(int) * (2 * nth + 2), ctx->stream));
-    launch_rotate(ctx, m->pts.as<double>(), n, d_cs, (int)nth, rot, scr, &ctrl->flags, amb);
+    plan.rot = rot;
+    plan.flags = amb + 2 * nth + 2;
 
     // Fixed-point fold exponent: sums of n votes stay below 2^31.
     int e = 0;
@@ -327,8 +340,6 @@ ScreenPlan screen(ea_ctx* ctx, const ea_model* m, const ea_field* f, const ea_po
     std::memcpy(&B3, &K, sizeof B3);
     // |S_f - S| <= 2^(e-20) (candidate + fold rounding) + 2^-23 (final fp32 store)
     plan.delta = std::ldexp(1.0, e - 20) + std::ldexp(1.0, -23);
-    // fp16 plane (lattice path): |n_h - n| <= 2^-11 |n| per component, so a
-    // candidate moves by at most sqrt(2) * 2^-11 (+ subnormal slack 2^-24).
 
     // Path choice.
     // Integer origin + unit steps: every translation is an exact integer,
@@ -337,14 +348,10 @@ ScreenPlan screen(ea_ctx* ctx, const ea_model* m, const ea_field* f, const ea_po
     const bool lattice = is_int(g.x0) && is_int(g.y0) && std::fabs(g.x1) <= 1048576.0 &&
                          std::fabs(g.y1) <= 1048576.0 && g.dx == 1.0 && g.dy == 1.0 && R <= 2 &&
                          f->ring_max < p.eps_mag;
-    // Lane strips of 8 rows (64 accumulators, 12 warps/SM) measured faster
-    // than 16 rows (128 accumulators, 8 warps/SM, spills) on B200.
+    // Lane strips of 8 rows (64 accumulators, 8 warps/SM) measured faster
+    // than 16 rows (128 accumulators: spills) on B200.
     const int shift = 3;
-    int elem = 8;  // float2 plane
-    if (lattice) {
-        const char* pe = std::getenv("EAB_PLANE");
-        elem = (pe && std::strcmp(pe, "f16") == 0) ? 4 : 8;  // fp32 plane unless asked
-    }
+    const int elem = 8;  // float2 plane (an fp16 plane measured no faster: issue-bound)
     // Zero columns beyond the ring so no lattice window needs clamping:
     // |offset| <= ceil(max |p_i|) + 1 for every rotation of the model.
     int PL = 0, PR = 0;
@@ -352,7 +359,9 @@ ScreenPlan screen(ea_ctx* ctx, const ea_model* m, const ea_field* f, const ea_po
     // Region mode: even the unpadded plane exceeds shared memory, so the
     // plane stays in global memory and CTAs stage halo regions of it.
     const bool region =
-        lattice && fast_smem_bytes(plane_geom(f->width, f->height, shift, 0, 0, 8)) > ctx->smem_optin;
+        lattice && (fast_smem_bytes(plane_geom(f->width, f->height, shift, 0, 0, 8)) >
+                        ctx->smem_optin ||
+                    std::getenv("EAB_FORCE_REGION") != nullptr);
     if (lattice) {
         double rmax = 0.0;
         for (const ea_edge_point& q : m->host)
@@ -369,13 +378,9 @@ ScreenPlan screen(ea_ctx* ctx, const ea_model* m, const ea_field* f, const ea_po
         while ((PL > 0 || PR > 0) && bytes(PL, PR) > budget) {  // shrink: clamp path covers
             if (PL >= PR) --PL; else --PR;
         }
-        if (region) PL = PR = 0, elem = 8;  // halo regions are zero-filled instead
+        if (region) PL = PR = 0;  // halo regions are zero-filled instead
     }
-    PlaneGeom geom = plane_geom(f->width, f->height, shift, PL, PR, elem);
-    if (elem == 4 && fast_smem_bytes(geom) > ctx->smem_optin) {  // whole plane must fit
-        elem = 8;
-        geom = plane_geom(f->width, f->height, shift, PL, PR, elem);
-    }
+    const PlaneGeom geom = plane_geom(f->width, f->height, shift, PL, PR, elem);
     void* plane = ctx->plane.ensure(geom.bytes());
     EAB_CUDA(cudaMemsetAsync(plane, 0, geom.bytes(), ctx->stream));
     launch_plane(ctx, f, p.eps_mag, geom, plane, &ctrl->ring_bad);
@@ -408,8 +413,10 @@ ScreenPlan screen(ea_ctx* ctx, const ea_model* m, const ea_field* f, const ea_po
         };
         a.xg = padded(16, 128) < padded(32, 64) ? 2 : 4;
     }
+    a.sched = sched;
     a.ro = ro_int;
     a.amb = amb;
+    a.kf = (k >= 1 && k <= 8) ? k : 0;
     a.K = K;
     a.B3 = B3;
     a.scale = (float)(std::ldexp(1.0, e - 22) / (double)n);
@@ -426,8 +433,6 @@ ScreenPlan screen(ea_ctx* ctx, const ea_model* m, const ea_field* f, const ea_po
     }
     if (ctx->timing) EAB_CUDA(cudaEventRecord(ctx->ev[2], ctx->stream));
     ctx->stats.screen_path = plan.fast ? (region ? 3 : 1) : 2;
-    if (plan.fast && geom.elem_bytes == 4)
-        plan.delta += std::sqrt(2.0) * std::ldexp(1.0, -11) + std::ldexp(1.0, -24);
     plan.items = screen_items(a, plan.fast);
     return plan;
 }
@@ -469,7 +474,7 @@ TopLaunch top_enqueue(ea_ctx* ctx, const ea_model* m, const ea_field* f, const e
     ctx->stats = ea_search_stats{};
     if (ctx->timing) EAB_CUDA(cudaEventRecord(ctx->ev[0], ctx->stream));
     TopLaunch t;
-    t.plan = screen(ctx, m, f, g, p, it_begin, it_end);
+    t.plan = screen(ctx, m, f, g, p, it_begin, it_end, k);
     t.k = k;
     t.n = m->n;
     t.cap = cap;
@@ -482,7 +487,7 @@ TopLaunch top_enqueue(ea_ctx* ctx, const ea_model* m, const ea_field* f, const e
     if (t.plan.slab_poses == 0) return t;
 
     const size_t slab_pairs = t.plan.it_count * (size_t)t.n;
-    ExactArgs x = exact_args(f, p, ctx->rot_exact.as<double>(), slab_pairs, t.n);
+    ExactArgs x = exact_args(f, p, t.plan.rot, slab_pairs, t.n);
     x.nx = t.plan.c.nx;
     x.ny = t.plan.c.ny;
     x.it_begin = t.plan.it_begin;
@@ -494,7 +499,7 @@ TopLaunch top_enqueue(ea_ctx* ctx, const ea_model* m, const ea_field* f, const e
     double* cs = (double*)ctx->cand_score.ensure(sizeof(double) * cap);
     // band threshold from the histogram, then the compaction
     launch_compact(ctx, ctx->map.as<float>(), ctx->item_max.as<float>(), t.plan.items, ctrl, cand,
-                   cap, ctx->hist.as<unsigned>(), k, t.plan.delta);
+                   cap, ctx->hist.as<unsigned>(), k, t.plan.delta, t.plan.flags);
     launch_rescore(ctx, x, cand, ctrl, cap, cs);
     launch_select(ctx, cand, cs, ctrl, cap, k, t.plan.it_begin * t.plan.c.nx * t.plan.c.ny,
                   t.top_score, t.top_index);
@@ -1310,7 +1315,7 @@ void ea_ctx_destroy(ea_ctx* ctx) {
                       &ctx->item_max, &ctx->tail,
                       &ctx->hist, &ctx->ctrl, &ctx->cand, &ctx->cand_score, &ctx->topk,
                       &ctx->refine_poses, &ctx->refine_scores, &ctx->beam, &ctx->accum64,
-                      &ctx->work})
+                      &ctx->work, &ctx->ttab, &ctx->rstate, &ctx->rslots})
         b->release();
     ctx->h_stage.release();
     ctx->h_out.release();
@@ -1815,11 +1820,11 @@ ea_status ea_screen_map(ea_ctx* ctx, const ea_model* m, const ea_field* f, const
         DeviceGuard dg(ctx->device);
         ctx->stats = ea_search_stats{};
         const ScreenPlan plan = screen(ctx, m, f, *g, *p, 0, 0);
-        SearchCtrl hc;
-        d2h(ctx, &hc, ctx->ctrl.p, sizeof hc);
+        int flags = 0;
+        d2h(ctx, &flags, plan.flags, sizeof flags);
         d2h(ctx, out, ctx->map.p, sizeof(float) * total);
         sync(ctx);
-        ctx->stats.flagged_points = hc.flags;
+        ctx->stats.flagged_points = flags;
         ctx->stats.screen_delta = plan.delta;
         if (delta) *delta = ctx->stats.screen_delta;
     });

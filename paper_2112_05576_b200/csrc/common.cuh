@@ -26,6 +26,10 @@ inline void cuda_check(cudaError_t e, const char* what) {
 struct DevBuf {
     void* p = nullptr;
     size_t cap = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() { release(); }
     void* ensure(size_t bytes) {
         if (bytes > cap) {
             if (p) cudaFree(p);
@@ -50,6 +54,10 @@ struct DevBuf {
 struct HostBuf {
     void* p = nullptr;
     size_t cap = 0;
+    HostBuf() = default;
+    HostBuf(const HostBuf&) = delete;
+    HostBuf& operator=(const HostBuf&) = delete;
+    ~HostBuf() { release(); }
     void* ensure(size_t bytes) {
         if (bytes > cap) {
             if (p) cudaFreeHost(p);
@@ -88,6 +96,12 @@ struct ea_model {
     int source_level = 0;
     std::vector<ea_edge_point> host;  // AoS copy (template side stays on host too)
     eab::DevBuf pts;                  // device SoA: x_rel | y_rel | dx | dy
+    // Rotation tables, ambiguity list and lattice schedule of the theta slab
+    // searched last: the model is immutable, so they depend only on the grid's
+    // theta axis and are reused by every later search of that slab (one
+    // detect per image).  Written on the owning context's stream.
+    std::vector<double> tab_key;
+    eab::DevBuf rot, scr, amb, sched;
 };
 
 struct ea_levels {
@@ -109,7 +123,7 @@ struct ea_ctx {
     cudaEvent_t ev[8] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
     // scratch
     eab::DevBuf cs, rot_exact, rot_screen, plane, map, item_max, tail, hist, ctrl, cand, cand_score, topk,
-        refine_poses, refine_scores, beam, accum64, work, amb;
+        refine_poses, refine_scores, beam, accum64, work;
     eab::HostBuf h_stage, h_out;
     // glibc cos/sin tables of theta grids, cached per (t0, dt, nt)
     std::map<std::vector<double>, std::vector<double>> cs_cache;

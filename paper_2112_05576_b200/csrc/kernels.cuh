@@ -144,11 +144,15 @@ void launch_plane(ea_ctx* ctx, const ea_field* f, double eps, const PlaneGeom& g
 // count and the list of thetas that have any (AmbList); flags: their total.
 void launch_rotate(ea_ctx* ctx, const double* pts_soa, int n, const double* cs, int nth,
                    double* rot_exact, int4* rot_screen, int* flags, int* amb = nullptr);
+// Lattice point schedule per theta: points sorted by (oy, ox), same-row
+// neighbours paired (see search_kernels.cu).  sched: nth x (1 + 2n) int4.
+void launch_schedule(ea_ctx* ctx, const int4* rot_screen, int n, int nth, int4* sched);
 
 struct ScreenArgs {
     const void* plane;        // float2 or __half2 elements (geom.elem_bytes)
     PlaneGeom geom;
     const int4* rot_screen;     // [theta - it_begin][point]
+    const int4* sched;          // lattice point schedule per theta (schedule_kernel)
     const double* rot_exact;    // px | py | dx | dy, rows theta - it_begin
     size_t rot_stride;          // it_count * n (offset of py inside rot_exact)
     int n;                      // model points
@@ -167,6 +171,7 @@ struct ScreenArgs {
     // them (item_max = +inf so compaction scans their map), the general kernel
     // runs over the list amb[nth + 1 ..] of amb[nth] entries.
     const int* amb;
+    int kf;           // histogram floor rank (the search's k if <= 8, else 0 = off)
     float K;          // fixed-point fold constant 3*2^e
     unsigned B3;      // bits of K
     float scale;      // 2^(e-22) / n
@@ -202,7 +207,7 @@ ItemGeom screen_items(const ScreenArgs& a, bool fast);
 // Compaction with the band threshold (see launch_threshold) computed in-kernel.
 void launch_compact(ea_ctx* ctx, const float* map, const float* item_max, const ItemGeom& g,
                     SearchCtrl* ctrl, unsigned* cand, unsigned long long cap,
-                    const unsigned* hist, int k, double delta);
+                    const unsigned* hist, int k, double delta, const int* flags);
 
 struct ExactArgs {
     const double* gx;

@@ -131,89 +131,272 @@ template <int S>
 constexpr int screen_threads() { return S <= 8 ? EAB_SCREEN_THREADS : 256; }
 constexpr int kTW = 8;  // poses per lane along x
 
-// One model point over a lane's 8 x S pose block: walk the S + 2R plane rows
-// its windows touch.  CLAMP=false is the warp-uniform interior case (every
-// column of the warp's windows lies inside the padded plane): loads address
-// [row + immediate].  CLAMP=true clamps each column into the zero ring.
-__device__ __forceinline__ float2 px_f32(float2 v) { return v; }
-__device__ __forceinline__ float2 px_f32(__half2 v) { return __half22float2(v); }
-
-template <int R, int S, int SHIFT, bool IGNORE, bool CLAMP, typename PX>
-__device__ __forceinline__ void point_rows(const PX* __restrict__ P, const int PW,
+// One model point (NP = 1) or a pair of points on the same lattice row whose
+// windows start DXP columns apart (NP = 2) over a lane's 8 x S pose block:
+// walk the S + 2R plane rows the windows touch.  A pair loads the union of
+// its two windows once (8 + 2R + DXP pixels per row instead of 2 x (8 + 2R)).
+// (Packed FFMA2 scoring of a pixel against both points was tried: at this
+// register pressure the pair-alignment MOVs cost more than it saved.)  CLAMP=false is the
+// warp-uniform interior case (every column of the warp's windows lies inside
+// the padded plane): loads address [row + immediate]; CLAMP=true clamps each
+// column into the zero ring.  STRIP=false (region kernel): every row is
+// inside the staged region.  Votes are accumulated as raw bit patterns
+// bits(K + vote); the caller subtracts (points processed) x bits(K) once.
+template <int R, int S, int SHIFT, bool IGNORE, bool CLAMP, bool STRIP, int NP, int DXP>
+__device__ __forceinline__ void point_rows(const float2* __restrict__ P, const int PW,
                                            const int XL, const int cx_lo, const int cx_hi,
                                            const int H1, const int Z, const int cb,
                                            const int rb, const int ry_lo, const int ry_hi,
-                                           const float dxf, const float dyf,
-                                           const float K, const int B3, int (&acc)[S][kTW]) {
-    constexpr int NC = kTW + 2 * R;  // columns per row
-    constexpr int NR = S + 2 * R;    // rows per point
-    int col[CLAMP ? NC : 1];
+                                           const float dx1, const float dy1, const float dx2,
+                                           const float dy2, const float K,
+                                           unsigned (&acc)[S][kTW]) {
+    constexpr int NC = kTW + 2 * R;                     // columns per point window
+    constexpr int NCU = NC + (NP == 2 ? DXP : 0);       // columns of the union
+    constexpr int NR = S + 2 * R;                       // rows per point
+    constexpr int HP = 2 * R > 0 ? 2 * R : 1;
+    int col[CLAMP ? NCU : 1];
     if constexpr (CLAMP) {
 #pragma unroll
-        for (int m = 0; m < NC; ++m) col[m] = min(max(cb + m, 0), XL);
+        for (int m = 0; m < NCU; ++m) col[m] = min(max(cb + m, 0), XL);
     }
     // For R <= 1 the zero ring makes an off-field centre vote exactly 0; a
     // 5-wide window can reach real pixels, so R >= 2 masks those centres.
-    unsigned cmask = 0xffu;
+    unsigned cmask1 = 0xffu, cmask2 = 0xffu;
     if constexpr (R >= 2) {
-        cmask = 0u;
+        cmask1 = cmask2 = 0u;
 #pragma unroll
         for (int j = 0; j < kTW; ++j) {
-            const int cxj = cb + R + j;  // padded column of the window centre
-            cmask |= (cxj >= cx_lo && cxj <= cx_hi) ? (1u << j) : 0u;
+            const int c1 = cb + R + j, c2 = c1 + DXP;  // padded columns of the centres
+            cmask1 |= (c1 >= cx_lo && c1 <= cx_hi) ? (1u << j) : 0u;
+            cmask2 |= (c2 >= cx_lo && c2 <= cx_hi) ? (1u << j) : 0u;
         }
     }
-    float hprev[2 * R > 0 ? 2 * R : 1][kTW];
+    float hprev1[HP][kTW], hprev2[NP == 2 ? HP : 1][kTW];
 #pragma unroll
     for (int r = 0; r < NR; ++r) {
         // Rows off the plane read the zero strip at an offset congruent (mod
         // one wavefront of elements) to where the row would be, so the lanes'
         // bank spacing survives at the top/bottom edges.
-        constexpr int kBankMask = 128 / (int)sizeof(PX) - 1;
+        constexpr int kBankMask = 128 / (int)sizeof(float2) - 1;
         const int yv = rb + r;
         const int va = yv * PW + (yv >> SHIFT);
-        const PX* row = P + (((unsigned)yv <= (unsigned)H1) ? va : Z + (va & kBankMask));
+        const float2* row = P + (!STRIP || (unsigned)yv <= (unsigned)H1 ? va : Z + (va & kBankMask));
         if constexpr (!CLAMP) row += cb;
-        float c[NC];
+        float c1[NCU], c2[NP == 2 ? NCU : 1];
 #pragma unroll
-        for (int m = 0; m < NC; ++m) {
-            const float2 v = px_f32(CLAMP ? row[col[m]] : row[m]);
-            if constexpr (IGNORE) {
-                c[m] = fabsf(fmaf(dyf, v.y, dxf * v.x));
+        for (int m = 0; m < NCU; ++m) {
+            const float2 v = CLAMP ? row[col[m]] : row[m];
+            if constexpr (NP == 2) {
+                if constexpr (IGNORE) {
+                    c1[m] = fabsf(fmaf(dy1, v.y, dx1 * v.x));
+                    c2[m] = fabsf(fmaf(dy2, v.y, dx2 * v.x));
+                } else {
+                    c1[m] = fmaf(dy1, v.y, fmaf(dx1, v.x, K));
+                    c2[m] = fmaf(dy2, v.y, fmaf(dx2, v.x, K));
+                }
+            } else if constexpr (IGNORE) {
+                c1[m] = fabsf(fmaf(dy1, v.y, dx1 * v.x));
             } else {
-                c[m] = fmaf(dyf, v.y, fmaf(dxf, v.x, K));
+                c1[m] = fmaf(dy1, v.y, fmaf(dx1, v.x, K));
             }
         }
-        float h[kTW];
+        float h1[kTW], h2[NP == 2 ? kTW : 1];
 #pragma unroll
-        for (int j = 0; j < kTW; ++j) h[j] = max_run<2 * R + 1>(c + j);
+        for (int j = 0; j < kTW; ++j) h1[j] = max_run<2 * R + 1>(c1 + j);
+        if constexpr (NP == 2) {
+#pragma unroll
+            for (int j = 0; j < kTW; ++j) h2[j] = max_run<2 * R + 1>(c2 + DXP + j);
+        }
         if (r >= 2 * R) {
             const int s = r - 2 * R;
+            const int cys = rb + R + s;  // padded row of the window centres
+            const bool row_in = R < 2 || (cys >= ry_lo && cys <= ry_hi);
 #pragma unroll
             for (int j = 0; j < kTW; ++j) {
-                float col_v[2 * R + 1];
+                float cv[2 * R + 1];
 #pragma unroll
-                for (int q = 0; q < 2 * R; ++q) col_v[q] = hprev[q][j];
-                col_v[2 * R] = h[j];
-                float v = max_run<2 * R + 1>(col_v);
-                if constexpr (IGNORE) v = v + K;
-                if constexpr (R >= 2) {
-                    const int cys = rb + R + s;  // padded row of the window centre
-                    const bool in = ((cmask >> j) & 1u) && cys >= ry_lo && cys <= ry_hi;
-                    v = in ? v : K;
+                for (int q = 0; q < 2 * R; ++q) cv[q] = hprev1[q][j];
+                cv[2 * R] = h1[j];
+                float v1 = max_run<2 * R + 1>(cv);
+                if constexpr (IGNORE) v1 = v1 + K;
+                if constexpr (R >= 2) v1 = (row_in && ((cmask1 >> j) & 1u)) ? v1 : K;
+                if constexpr (NP == 2) {
+#pragma unroll
+                    for (int q = 0; q < 2 * R; ++q) cv[q] = hprev2[q][j];
+                    cv[2 * R] = h2[j];
+                    float v2 = max_run<2 * R + 1>(cv);
+                    if constexpr (IGNORE) v2 = v2 + K;
+                    if constexpr (R >= 2) v2 = (row_in && ((cmask2 >> j) & 1u)) ? v2 : K;
+                    acc[s][j] += __float_as_uint(v1) + __float_as_uint(v2);
+                } else {
+                    acc[s][j] += __float_as_uint(v1);
                 }
-                acc[s][j] += __float_as_int(v) - B3;
             }
         }
         if constexpr (R > 0) {
 #pragma unroll
             for (int q = 0; q + 1 < 2 * R; ++q)
 #pragma unroll
-                for (int j = 0; j < kTW; ++j) hprev[q][j] = hprev[q + 1][j];
+                for (int j = 0; j < kTW; ++j) {
+                    hprev1[q][j] = hprev1[q + 1][j];
+                    if constexpr (NP == 2) hprev2[q][j] = hprev2[q + 1][j];
+                }
 #pragma unroll
-            for (int j = 0; j < kTW; ++j) hprev[2 * R - 1][j] = h[j];
+            for (int j = 0; j < kTW; ++j) {
+                hprev1[2 * R - 1][j] = h1[j];
+                if constexpr (NP == 2) hprev2[2 * R - 1][j] = h2[j];
+            }
         }
     }
+}
+
+// ---- point schedule ------------------------------------------------------------
+// Per theta, the lattice kernels walk a schedule instead of the raw point
+// list: points sorted by (oy, ox) and paired greedily when they share a
+// lattice row and their windows start at most kMaxPairDx columns apart.
+// Layout per theta (stride 1 + 2n int4): header {singles, pairs dx=0, pairs
+// dx=1, 0}, then 2 int4 per entry {ox, oy, dxf, dyf} x {second point or
+// unused}, singles first, then pairs by dx.  The sum over points is integer and
+// order-free, so the schedule does not change a score.
+constexpr int kMaxPairDx = 1;  // dx = 2 pairs: a fourth unrolled body, net loss (icache)
+constexpr int kPairMaxN = 1024;  // larger models: singles only
+
+__global__ void __launch_bounds__(256) schedule_kernel(const int4* __restrict__ scr, int n,
+                                                       int4* __restrict__ sched, int dmin,
+                                                       int dmax) {
+    const int th = blockIdx.x;
+    const int4* pts = scr + (size_t)th * n;
+    int4* out = sched + (size_t)th * (1 + 2 * (size_t)n);
+    __shared__ int4 sp[kPairMaxN];       // the theta's points
+    __shared__ short order[kPairMaxN];   // sorted position -> point
+    __shared__ short slot[kPairMaxN];    // sorted position -> output entry (-1: second of a pair)
+    if (n > kPairMaxN) {
+        if (threadIdx.x == 0) out[0] = make_int4(n, 0, 0, 0);
+        for (int i = threadIdx.x; i < n; i += blockDim.x) out[1 + 2 * i] = __ldg(pts + i);
+        return;
+    }
+    for (int i = threadIdx.x; i < n; i += blockDim.x) sp[i] = __ldg(pts + i);
+    __syncthreads();
+    // rank by (oy, ox, index): n^2 / 256 smem comparisons per thread
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const int4 p = sp[i];
+        int rank = 0;
+        for (int k = 0; k < n; ++k) {
+            const int4 q = sp[k];
+            rank += (q.y < p.y) || (q.y == p.y && (q.x < p.x || (q.x == p.x && k < i)));
+        }
+        order[rank] = (short)i;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {  // greedy pairing along the sorted list, then output slots
+        int c[3] = {0, 0, 0};
+        for (int i = 0; i < n;) {
+            const int4 a = sp[order[i]];
+            int kind = 0;
+            if (i + 1 < n) {
+                const int4 b = sp[order[i + 1]];
+                const int d = b.x - a.x;
+                if (b.y == a.y && d >= dmin && d <= dmax) kind = 1 + d;
+            }
+            slot[i] = (short)(kind << 12);  // type now, entry index below
+            if (kind) slot[i + 1] = -1;
+            ++c[kind];
+            i += kind ? 2 : 1;
+        }
+        int cur[3] = {0, c[0], c[0] + c[1]};
+        for (int i = 0; i < n; ++i) {
+            if (slot[i] < 0) continue;
+            const int kind = slot[i] >> 12;
+            slot[i] = (short)(cur[kind]++ | (kind ? 0x4000 : 0));
+        }
+        out[0] = make_int4(c[0], c[1], c[2], 0);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {  // scatter the entries
+        const int sl = slot[i];
+        if (sl < 0) continue;
+        const int e = sl & 0x3fff;
+        out[1 + 2 * e] = sp[order[i]];
+        if (sl & 0x4000) out[2 + 2 * e] = sp[order[i + 1]];
+    }
+}
+
+void launch_schedule(ea_ctx* ctx, const int4* scr, int n, int nth, int4* sched) {
+    if (nth == 0 || n == 0) return;
+    // EAB_NO_PAIRS=1: singles only (A/B measurements)
+    static const int dmax = std::getenv("EAB_NO_PAIRS") ? -1 : kMaxPairDx;
+    schedule_kernel<<<nth, 256, 0, ctx->stream>>>(scr, n, sched, 0, dmax);
+    check_launch("schedule_kernel");
+    count_launch(ctx);
+}
+
+// Geometry a lane needs to walk schedule entries (see run_entries).
+struct LaneGeom {
+    const float2* P;
+    int PW, XL, cx_lo, cx_hi, H1, Z;
+    int cbase, rbase;  // window start = (ox + cbase, oy + rbase) in padded/region coordinates
+    int ry_lo, ry_hi;  // field rows (window-centre mask for R >= 2)
+    int cwbase, wspan; // EDGE: warp's first column = ox + cwbase; lanes span wspan more columns
+};
+
+template <int R, int S, int SHIFT, bool IGNORE, bool EDGE, bool STRIP, int NP, int DXP>
+__device__ __forceinline__ void one_entry(const LaneGeom& g, const int4 p, const float dx2,
+                                          const float dy2, const float K,
+                                          unsigned (&acc)[S][kTW]) {
+    const float dx1 = __int_as_float(p.z), dy1 = __int_as_float(p.w);
+    const int cb = p.x + g.cbase, rb = p.y + g.rbase;
+    constexpr int NCU = kTW + 2 * R + (NP == 2 ? DXP : 0);
+    if constexpr (EDGE) {
+        const int cw = p.x + g.cwbase;  // warp-uniform
+        if (!(cw >= 0 && cw + g.wspan + NCU - 1 <= g.XL)) {
+            point_rows<R, S, SHIFT, IGNORE, true, STRIP, NP, DXP>(
+                g.P, g.PW, g.XL, g.cx_lo, g.cx_hi, g.H1, g.Z, cb, rb, g.ry_lo, g.ry_hi, dx1, dy1,
+                dx2, dy2, K, acc);
+            return;
+        }
+    }
+    point_rows<R, S, SHIFT, IGNORE, false, STRIP, NP, DXP>(g.P, g.PW, g.XL, g.cx_lo, g.cx_hi,
+                                                           g.H1, g.Z, cb, rb, g.ry_lo, g.ry_hi,
+                                                           dx1, dy1, dx2, dy2, K, acc);
+}
+
+// One lane block over schedule entries [e0, e1): singles, then pairs by dx.
+// Returns the number of model points processed (for the bits(K) correction).
+template <int R, int S, int SHIFT, bool IGNORE, bool EDGE, bool STRIP>
+__device__ __forceinline__ int run_entries(const int4* __restrict__ ent, const int4 hdr, int e0,
+                                           int e1, const LaneGeom& g, const float K,
+                                           unsigned (&acc)[S][kTW]) {
+    int done = 0;
+    int lo = 0;
+    const int bounds[3] = {hdr.x, hdr.y, hdr.z};
+#pragma unroll
+    for (int t = 0; t < 3; ++t) {
+        const int hi = lo + bounds[t];
+        const int b = max(lo, e0), e = min(hi, e1);
+        if (b < e) {
+            int4 p = __ldg(ent + 2 * b), q = __ldg(ent + 2 * b + 1);
+            for (int i = b; i < e; ++i) {
+                // prefetch the next entry: its loads overlap this entry's rows
+                const int in = i + 1 < e ? i + 1 : i;
+                const int4 pn = __ldg(ent + 2 * in);
+                const int4 qn = t == 0 ? q : __ldg(ent + 2 * in + 1);
+                if (t == 0) {
+                    one_entry<R, S, SHIFT, IGNORE, EDGE, STRIP, 1, 0>(g, p, 0.f, 0.f, K, acc);
+                } else {
+                    const float dx2 = __int_as_float(q.z), dy2 = __int_as_float(q.w);
+                    if (t == 1)
+                        one_entry<R, S, SHIFT, IGNORE, EDGE, STRIP, 2, 0>(g, p, dx2, dy2, K, acc);
+                    else
+                        one_entry<R, S, SHIFT, IGNORE, EDGE, STRIP, 2, 1>(g, p, dx2, dy2, K, acc);
+                }
+                p = pn;
+                q = qn;
+            }
+        }
+        if (e > b) done += (e - b) * (t == 0 ? 1 : 2);
+        lo = hi;
+    }
+    return done;
 }
 
 // The smem lattice kernel (integer top-level lattice with unit steps).
@@ -244,11 +427,33 @@ struct TailPlan {
 
 // Lane epilogue shared by the lattice kernels: scores of the lane's 8 x S
 // block into the map and the CTA histogram, warp max into item_max[item].
+//
+// Histogram floor: a pose whose score is below `floor` (the kf-th largest
+// maximum among the warp's finished items, kf = k) is not counted -- there
+// are kf distinct poses at or above the floor, so floor <= T_f (the k-th
+// largest score), every bin above bin(T_f) keeps its exact count and bin
+// (T_f) still reaches k: the threshold bin is unchanged.
+constexpr int kFloorK = 8;  // k <= 8 uses the floor
+__device__ __forceinline__ float warp_floor(const float* wtop, int kf) {
+    return kf > 0 ? wtop[kf - 1] : -INFINITY;
+}
+__device__ __forceinline__ void floor_insert(float* wtop, float best, int lane) {
+    if (lane == 0 && best > wtop[kFloorK - 1]) {
+        int i = kFloorK - 1;
+        while (i > 0 && wtop[i - 1] < best) {
+            wtop[i] = wtop[i - 1];
+            --i;
+        }
+        wtop[i] = best;
+    }
+    __syncwarp();
+}
+
 template <int S>
-__device__ __forceinline__ void emit_tile(const ScreenArgs& a, const int (&acc)[S][kTW],
-                                          const int X, const int Y, unsigned long long itr,
-                                          unsigned long long item, unsigned* hist,
-                                          const int lane) {
+__device__ __forceinline__ float emit_tile(const ScreenArgs& a, const int (&acc)[S][kTW],
+                                           const int X, const int Y, unsigned long long itr,
+                                           unsigned long long item, unsigned* hist,
+                                           const int lane, const float floor) {
     float* out = a.map + (size_t)itr * (a.nx * a.ny);
     float best = -INFINITY;
 #pragma unroll
@@ -261,22 +466,26 @@ __device__ __forceinline__ void emit_tile(const ScreenArgs& a, const int (&acc)[
                 const float sc = (float)acc[s][j] * a.scale;
                 out[iy * a.nx + ix] = sc;
                 best = fmaxf(best, sc);
-                atomicAdd(&hist[hist_bin(sc)], 1u);
+                if (sc >= floor) atomicAdd(&hist[hist_bin(sc)], 1u);
             }
         }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) best = fmaxf(best, __shfl_xor_sync(0xffffffffu, best, o));
     if (lane == 0) a.item_max[item] = best;
+    return best;
 }
 
-template <int R, int S, int SHIFT, bool IGNORE, typename PX, int XG>
+template <int R, int S, int SHIFT, bool IGNORE, int XG>
 __global__ void __launch_bounds__(screen_threads<S>(), 1)
     screen_fast_kernel(const ScreenArgs a, const unsigned nwx, const unsigned nwy,
                        const TailPlan tp, const int vec16) {
     extern __shared__ __align__(16) unsigned char smem[];
     unsigned* hist = reinterpret_cast<unsigned*>(smem);
-    PX* P = reinterpret_cast<PX*>(smem + kHistBins * sizeof(unsigned));
+    float2* P = reinterpret_cast<float2*>(smem + kHistBins * sizeof(unsigned));
+    __shared__ float wtop_all[16][kFloorK];
+    float* wtop = wtop_all[threadIdx.x >> 5];
+    if ((threadIdx.x & 31) < kFloorK) wtop[threadIdx.x & 31] = -INFINITY;
     {
         const int4* src = reinterpret_cast<const int4*>(a.plane);
         int4* dst = reinterpret_cast<int4*>(P);
@@ -285,16 +494,25 @@ __global__ void __launch_bounds__(screen_threads<S>(), 1)
     }
     __syncthreads();
 
-    constexpr int NC = kTW + 2 * R;
     constexpr int NACC = S * kTW;
     const int lane = threadIdx.x & 31;
     constexpr int YG = 32 / XG;  // lane strips along y; XG groups of 8 columns along x
     const int yg = lane % YG, xg = lane / YG;
-    const int H1 = a.geom.H + 1, PW = a.geom.PW, XL = a.geom.PW - 1;
-    const int cx_lo = 1 + a.geom.PL, cx_hi = a.geom.W + a.geom.PL, Z = a.geom.zero;
     const float K = a.K;
-    const int B3 = (int)a.B3;
     const unsigned long long total = tp.n_main + tp.n_tail * (unsigned long long)tp.f;
+    const size_t sstride = 1 + 2 * (size_t)a.n;
+
+    LaneGeom g;
+    g.P = P;
+    g.PW = a.geom.PW;
+    g.XL = a.geom.PW - 1;
+    g.cx_lo = 1 + a.geom.PL;
+    g.cx_hi = a.geom.W + a.geom.PL;
+    g.H1 = a.geom.H + 1;
+    g.Z = a.geom.zero;
+    g.ry_lo = 1;
+    g.ry_hi = a.geom.H;
+    g.wspan = 8 * (XG - 1);
 
     for (;;) {
         unsigned long long work = 0;
@@ -303,14 +521,12 @@ __global__ void __launch_bounds__(screen_threads<S>(), 1)
         if (work >= total) break;
         unsigned long long item = work;
         long long tslot = -1;
-        int p0 = 0, p1 = a.n;
+        int ch = 0;
         if (work >= tp.n_main) {
             const unsigned long long m = work - tp.n_main;
             tslot = (long long)(m / (unsigned)tp.f);
-            const int ch = (int)(m % (unsigned)tp.f);
+            ch = (int)(m % (unsigned)tp.f);
             item = tp.n_main + (unsigned long long)tslot;
-            p0 = (int)((long long)ch * a.n / tp.f);
-            p1 = (int)((long long)(ch + 1) * a.n / tp.f);
         }
         const unsigned wx = (unsigned)(item % nwx);
         const unsigned long long rest = item / nwx;
@@ -319,44 +535,40 @@ __global__ void __launch_bounds__(screen_threads<S>(), 1)
         const int X0 = (int)wx * (8 * XG);
         const int X = X0 + xg * kTW;
         const int Y = (int)wy * (YG * S) + yg * S;
-        const int4* rot = a.rot_screen + (size_t)itr * a.n;
         if (__ldg(a.amb + itr) != 0) {  // flagged theta: the general kernel scores it
             if (lane == 0) a.item_max[item] = INFINITY;
             continue;
         }
+        const int4* sch = a.sched + itr * sstride;
+        const int4 hdr = __ldg(sch);
+        const int n_ent = hdr.x + hdr.y + hdr.z + hdr.w;
+        int e0 = 0, e1 = n_ent;
+        if (tslot >= 0) {
+            e0 = (int)((long long)ch * n_ent / tp.f);
+            e1 = (int)((long long)(ch + 1) * n_ent / tp.f);
+        }
+        g.cbase = a.ix0 + X - R + g.cx_lo;   // padded column of the window start - ox
+        g.rbase = a.iy0 + Y - R + 1;         // padded row of the window start - oy
+        g.cwbase = a.ix0 + X0 - R + g.cx_lo; // warp's first column - ox
 
-        int acc[S][kTW];
+        unsigned acc[S][kTW];
 #pragma unroll
         for (int s = 0; s < S; ++s)
 #pragma unroll
-            for (int j = 0; j < kTW; ++j) acc[s][j] = 0;
-
-        if (p0 < p1) {
-            int4 p = __ldg(rot + p0);
-            for (int i = p0; i < p1; ++i) {
-                const int4 pn = __ldg(rot + (i + 1 < p1 ? i + 1 : i));
-                const float dxf = __int_as_float(p.z), dyf = __int_as_float(p.w);
-                const int cb = p.x + a.ix0 + X - R + cx_lo;   // padded column of window start
-                const int rb = p.y + a.iy0 + Y - R + 1;       // padded row of window start
-                const int cw = p.x + a.ix0 + X0 - R + cx_lo;  // warp's first column (uniform)
-                if (cw >= 0 && cw + 8 * (XG - 1) + NC - 1 <= XL) {
-                    point_rows<R, S, SHIFT, IGNORE, false, PX>(P, PW, XL, cx_lo, cx_hi, H1, Z,
-                                                              cb, rb, 1, H1 - 1, dxf, dyf, K,
-                                                              B3, acc);
-                } else {
-                    point_rows<R, S, SHIFT, IGNORE, true, PX>(P, PW, XL, cx_lo, cx_hi, H1, Z,
-                                                             cb, rb, 1, H1 - 1, dxf, dyf, K,
-                                                             B3, acc);
-                }
-                p = pn;
-            }
-        }
+            for (int j = 0; j < kTW; ++j) acc[s][j] = 0u;
+        const int done = run_entries<R, S, SHIFT, IGNORE, true, true>(sch + 1, hdr, e0, e1, g, K, acc);
+        int sc[S][kTW];
+        const unsigned corr = (unsigned)done * a.B3;
+#pragma unroll
+        for (int s = 0; s < S; ++s)
+#pragma unroll
+            for (int j = 0; j < kTW; ++j) sc[s][j] = (int)(acc[s][j] - corr);
         if (tslot >= 0) {  // micro-item: merge, last arrival finalises
             int* part = tp.part + (size_t)tslot * NACC * 32;
 #pragma unroll
             for (int s = 0; s < S; ++s)
 #pragma unroll
-                for (int j = 0; j < kTW; ++j) atomicAdd(part + (s * kTW + j) * 32 + lane, acc[s][j]);
+                for (int j = 0; j < kTW; ++j) atomicAdd(part + (s * kTW + j) * 32 + lane, sc[s][j]);
             __threadfence();
             unsigned old = 0;
             if (lane == 0) old = atomicAdd(tp.done + tslot, 1u);
@@ -366,9 +578,11 @@ __global__ void __launch_bounds__(screen_threads<S>(), 1)
 #pragma unroll
             for (int s = 0; s < S; ++s)
 #pragma unroll
-                for (int j = 0; j < kTW; ++j) acc[s][j] = __ldcg(part + (s * kTW + j) * 32 + lane);
+                for (int j = 0; j < kTW; ++j) sc[s][j] = __ldcg(part + (s * kTW + j) * 32 + lane);
         }
-        emit_tile<S>(a, acc, X, Y, itr, item, hist, lane);
+        const float best = emit_tile<S>(a, sc, X, Y, itr, item, hist, lane,
+                                        warp_floor(wtop, a.kf));
+        floor_insert(wtop, best, lane);
     }
     __syncthreads();
     for (int b = threadIdx.x; b < kHistBins; b += blockDim.x) {
@@ -377,7 +591,7 @@ __global__ void __launch_bounds__(screen_threads<S>(), 1)
     }
 }
 
-template <int R, int S, int SHIFT, bool IGNORE, typename PX, int XG>
+template <int R, int S, int SHIFT, bool IGNORE, int XG>
 static void run_fast(ea_ctx* ctx, const ScreenArgs& a) {
     constexpr int YG = 32 / XG;
     const unsigned nwx = (unsigned)((a.nx + 8 * XG - 1) / (8 * XG));
@@ -385,7 +599,7 @@ static void run_fast(ea_ctx* ctx, const ScreenArgs& a) {
     const unsigned long long items = (unsigned long long)nwx * nwy * a.it_count;
     const size_t plane_bytes = (a.geom.bytes() + 15) & ~(size_t)15;
     const size_t smem = kHistBins * sizeof(unsigned) + plane_bytes;
-    auto kern = screen_fast_kernel<R, S, SHIFT, IGNORE, PX, XG>;
+    auto kern = screen_fast_kernel<R, S, SHIFT, IGNORE, XG>;
     EAB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     constexpr int threads = screen_threads<S>();
     unsigned long long warps_per_cta = threads / 32;
@@ -422,16 +636,11 @@ size_t fast_smem_bytes(const PlaneGeom& g) {
 bool launch_screen_fast(ea_ctx* ctx, const ScreenArgs& a) {
     if (fast_smem_bytes(a.geom) > ctx->smem_optin) return false;
     if (a.geom.shift != 3) return false;  // 8-row lane strips
+    if (a.geom.elem_bytes != 8) return false;
     const bool ig = a.ignore != 0;
-    const bool half = a.geom.elem_bytes == 4;
 #define EAB_FAST_XG(RR, XGV)                                                \
-    if (half) {                                                             \
-        if (ig) run_fast<RR, 8, 3, true, __half2, XGV>(ctx, a);             \
-        else run_fast<RR, 8, 3, false, __half2, XGV>(ctx, a);               \
-    } else {                                                                \
-        if (ig) run_fast<RR, 8, 3, true, float2, XGV>(ctx, a);              \
-        else run_fast<RR, 8, 3, false, float2, XGV>(ctx, a);                \
-    }
+    if (ig) run_fast<RR, 8, 3, true, XGV>(ctx, a);                          \
+    else run_fast<RR, 8, 3, false, XGV>(ctx, a);
 #define EAB_FAST(RR)                                                        \
     if (a.R == RR) {                                                        \
         if (a.xg == 2) {                                                    \
@@ -477,6 +686,9 @@ __global__ void __launch_bounds__(256, 1)
     unsigned* hist = reinterpret_cast<unsigned*>(smem);
     float2* P = reinterpret_cast<float2*>(smem + kHistBins * sizeof(unsigned));
     for (int i = threadIdx.x; i < kHistBins; i += blockDim.x) hist[i] = 0u;
+    __shared__ float wtop_all[kGroup][kFloorK];
+    float* wtop = wtop_all[threadIdx.x >> 5];
+    if ((threadIdx.x & 31) < kFloorK) wtop[threadIdx.x & 31] = -INFINITY;
 
     constexpr int YG = 32 / XG;
     constexpr int TWX = 8 * XG, TWY = YG * S;  // warp tile
@@ -486,7 +698,6 @@ __global__ void __launch_bounds__(256, 1)
     const int PW = a.geom.PW, GH = a.geom.H + 2;
     const float2* G = static_cast<const float2*>(a.plane);
     const float K = a.K;
-    const int B3 = (int)a.B3;
 
     const unsigned long long b0 = rp.n_items * blockIdx.x / gridDim.x;
     const unsigned long long b1 = rp.n_items * (blockIdx.x + 1) / gridDim.x;
@@ -525,30 +736,38 @@ __global__ void __launch_bounds__(256, 1)
             continue;
         }
         const int Xr = xg * kTW, Yr = yg * S;  // lane block inside the tile
-        const int4* rot = a.rot_screen + (size_t)itr * a.n;
-        // field bounds in region coordinates (window-centre mask for R >= 2)
-        const int cx_lo = 1 + a.geom.PL - C0, cx_hi = a.geom.W + a.geom.PL - C0;
-        const int ry_lo = 1 - R0, ry_hi = a.geom.H - R0;
+        LaneGeom lg;
+        lg.P = P;
+        lg.PW = rp.RW;
+        lg.XL = rp.RW - 1;
+        lg.cx_lo = 1 + a.geom.PL - C0;  // field bounds in region coordinates
+        lg.cx_hi = a.geom.W + a.geom.PL - C0;
+        lg.H1 = rp.RH - 1;
+        lg.Z = 0;
+        lg.cbase = Xr + h - R;  // region column of the window start - ox
+        lg.rbase = Yr + h - R;  // region row of the window start - oy
+        lg.ry_lo = 1 - R0;
+        lg.ry_hi = a.geom.H - R0;
+        lg.cwbase = lg.wspan = 0;
+        const int4* sch = a.sched + itr * (1 + 2 * (size_t)a.n);
+        const int4 hdr = __ldg(sch);
 
-        int acc[S][kTW];
+        unsigned uacc[S][kTW];
 #pragma unroll
         for (int s = 0; s < S; ++s)
 #pragma unroll
-            for (int j = 0; j < kTW; ++j) acc[s][j] = 0;
-        if (a.n > 0) {
-            int4 p = __ldg(rot);
-            for (int i = 0; i < a.n; ++i) {
-                const int4 pn = __ldg(rot + (i + 1 < a.n ? i + 1 : i));
-                const float dxf = __int_as_float(p.z), dyf = __int_as_float(p.w);
-                const int cb = p.x + Xr + h - R;  // region column of the window start
-                const int rb = p.y + Yr + h - R;  // region row of the window start
-                point_rows<R, S, SHIFT, IGNORE, false, float2>(P, rp.RW, rp.RW - 1, cx_lo, cx_hi,
-                                                              rp.RH - 1, 0, cb, rb, ry_lo, ry_hi,
-                                                              dxf, dyf, K, B3, acc);
-                p = pn;
-            }
-        }
-        emit_tile<S>(a, acc, TX0 + Xr, TY0 + Yr, itr, item, hist, lane);
+            for (int j = 0; j < kTW; ++j) uacc[s][j] = 0u;
+        const int done = run_entries<R, S, SHIFT, IGNORE, false, false>(
+            sch + 1, hdr, 0, hdr.x + hdr.y + hdr.z + hdr.w, lg, K, uacc);
+        int acc[S][kTW];
+        const unsigned corr = (unsigned)done * a.B3;
+#pragma unroll
+        for (int s = 0; s < S; ++s)
+#pragma unroll
+            for (int j = 0; j < kTW; ++j) acc[s][j] = (int)(uacc[s][j] - corr);
+        const float best = emit_tile<S>(a, acc, TX0 + Xr, TY0 + Yr, itr, item, hist, lane,
+                                        warp_floor(wtop, a.kf));
+        floor_insert(wtop, best, lane);
     }
     __syncthreads();
     for (int b = threadIdx.x; b < kHistBins; b += blockDim.x) {
@@ -795,7 +1014,8 @@ __global__ void __launch_bounds__(256) compact_kernel(const float* __restrict__ 
                                                       unsigned* __restrict__ cand,
                                                       unsigned long long cap,
                                                       const unsigned* __restrict__ hist, int k,
-                                                      double delta) {
+                                                      double delta, const int* flags) {
+    if (blockIdx.x == 0 && threadIdx.x == 0 && flags) ctrl->flags = *flags;  // for the stats
     const float thr = block_threshold<256>(hist, k, delta, ctrl, blockIdx.x == 0);
     const int lane = threadIdx.x & 31;
     const unsigned long long warp = ((unsigned long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -886,13 +1106,13 @@ ItemGeom screen_items(const ScreenArgs& a, bool fast) {
 
 void launch_compact(ea_ctx* ctx, const float* map, const float* item_max, const ItemGeom& g,
                     SearchCtrl* ctrl, unsigned* cand, unsigned long long cap,
-                    const unsigned* hist, int k, double delta) {
+                    const unsigned* hist, int k, double delta, const int* flags) {
     unsigned long long blocks = (g.n_items * 32 + 255) / 256;
     const unsigned long long maxb = (unsigned long long)ctx->sm_count;
     if (blocks > maxb) blocks = maxb;
     if (blocks == 0) blocks = 1;
     compact_kernel<<<(unsigned)blocks, 256, 0, ctx->stream>>>(map, item_max, g, ctrl, cand, cap,
-                                                              hist, k, delta);
+                                                              hist, k, delta, flags);
     check_launch("compact_kernel");
     count_launch(ctx);
 }

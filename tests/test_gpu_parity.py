@@ -144,7 +144,7 @@ SEARCH_CASES = [
 
 
 @pytest.mark.parametrize("case", range(len(SEARCH_CASES)))
-def test_search_topk_bit_exact(ea, oracle, case, plane_mode):
+def test_search_topk_bit_exact(ea, oracle, case):
     size, w, h, g, nb, pol = SEARCH_CASES[case]
     rng = np.random.default_rng(100 + case)
     m = rand_model(oracle, rng, size)
@@ -223,16 +223,9 @@ def test_score_map_bit_exact(ea, oracle):
         assert np.array_equal(got, want)
 
 
-@pytest.fixture(params=["f16", "f32"])
-def plane_mode(request, monkeypatch):
-    """Screening plane storage of the lattice kernel (EAB_PLANE)."""
-    monkeypatch.setenv("EAB_PLANE", request.param)
-    return request.param
-
-
 @pytest.mark.parametrize("nb,pol,general", [(3, 0, False), (1, 0, False), (5, 0, False),
                                             (3, 1, False), (3, 0, True), (7, 1, True)])
-def test_screen_bound(ea, oracle, nb, pol, general, plane_mode):
+def test_screen_bound(ea, oracle, nb, pol, general):
     """|S_f - S| <= delta for every pose (the premise of exactness)."""
     rng = np.random.default_rng(nb * 10 + pol)
     tm = oracle.prepare_model(oracle.render_template("l_bracket", 48))
@@ -246,7 +239,7 @@ def test_screen_bound(ea, oracle, nb, pol, general, plane_mode):
     s = oracle.score_map(tm.points, f, grid, params, 1 << 30)
     err = np.abs(sf.astype(np.float64) - s).max()
     assert err <= delta, (err, delta)
-    assert delta < (2e-6 if (general or plane_mode == "f32") else 1e-3)
+    assert delta < 2e-6
 
 
 REGION_CASES = [
