@@ -156,6 +156,39 @@ def make_multi_inputs(name, noise_seed=None):
     return img, tmpls, cfg, [p for _, _, p in stamps]
 
 
+def lattice_bytes_per_eval(models, tg, it0, it1, R=1, S=8):
+    """Shared-memory bytes the lattice kernel loads per pose-evaluation, from
+    its point schedule (search_kernels.cu schedule_kernel, restated): per
+    theta, points sorted by (oy, ox) and same-row neighbours with dx <= 1
+    paired; a single loads (8+2R)(S+2R) float2 per 8xS poses, a pair
+    (8+2R+dx)(S+2R) for two points.  Host cos/sin differ from glibc's in the
+    last bit at most, which can move a rounding tie: a model, not a count."""
+    import math
+    px_total = evals = 0
+    for pts in models:
+        pts = np.asarray(pts)
+        for it in range(it0, it1):
+            t = tg.t0 + it * tg.dt
+            c, s_ = math.cos(t), math.sin(t)
+            ox = np.floor(c * pts[:, 0] - s_ * pts[:, 1] + 0.5).astype(np.int64)
+            oy = np.floor(s_ * pts[:, 0] + c * pts[:, 1] + 0.5).astype(np.int64)
+            order = np.lexsort((np.arange(len(pts)), ox, oy))
+            i, n = 0, len(order)
+            while i < n:
+                a = order[i]
+                if i + 1 < n:
+                    b = order[i + 1]
+                    d = ox[b] - ox[a]
+                    if oy[b] == oy[a] and 0 <= d <= 1:
+                        px_total += (8 + 2 * R + d) * (S + 2 * R)
+                        i += 2
+                        continue
+                px_total += (8 + 2 * R) * (S + 2 * R)
+                i += 1
+            evals += n * 8 * S
+    return px_total * 8.0 / max(evals, 1)
+
+
 def top_grid(cfg):
     s = float(1 << (cfg.num_levels - 1))
     g = cfg.grid
@@ -430,8 +463,7 @@ def bench_ours(args, rank, world, local_rank):
     kernel_ms = statistics.median(screen_ms)
     local_evals = nx * ny * (it1 - it0) * n_top
     achieved = local_evals * ALG_BYTES_PER_EVAL / (kernel_ms / 1e3) / 1e9
-    S = 16 if os.environ.get("EAB_SCREEN_ROWS") == "16" else 8
-    actual_b = (S + 2) / S * (10 / 8) * 8  # smem bytes the lattice kernel really loads / eval
+    actual_b = lattice_bytes_per_eval([d.levels.model(L - 1).points for d in dets], tg, it0, it1)
     line = {
         "metric": "pose-evals/sec", "value": value, "unit": "pose-evals/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot_ms / args.steps,

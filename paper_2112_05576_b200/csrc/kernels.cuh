@@ -64,33 +64,80 @@ struct SearchCtrl {
 
 // ---- exact fp64 primitives (reference op order) ------------------------------
 
-// vote_at + vote_span  similarity.cpp:30-52, kernels_scalar.cpp:39-56
+// a1/m1 > a2/m2 for m1, m2 > 0, decided exactly from the products a1*m2 and
+// a2*m1 as (rounded, fma error) pairs: rounding is monotone, so the rounded
+// parts order the exact products except when they tie, where the error terms
+// decide.  (A false answer on an exact tie of the quotients is harmless: equal
+// quotients round to the same vote.)
+__device__ __forceinline__ bool frac_greater(double a1, double m1, double a2, double m2) {
+    const double h1 = __dmul_rn(a1, m2), h2 = __dmul_rn(a2, m1);
+    if (h1 != h2) return h1 > h2;
+    return __fma_rn(a1, m2, -h1) > __fma_rn(a2, m1, -h2);
+}
+
+// vote_at + vote_span  similarity.cpp:30-52, kernels_scalar.cpp:39-56.
+// The window max of the rounded quotients (dx*gx + dy*gy) / mag equals the
+// rounded quotient of the exact argmax (correct rounding is monotone), so the
+// window is scanned with exact fraction comparisons (first maximum kept, as
+// the reference's strict `>`) and only the winner is divided: one DDIV per
+// vote instead of one per pixel.
 __device__ __forceinline__ double vote_exact(const double* __restrict__ gx,
                                              const double* __restrict__ gy,
                                              const double* __restrict__ mag, int W, int H,
                                              int cx, int cy, int R, double dx, double dy,
                                              double eps, bool absolute) {
+    double ba = 0.0, bm = 1.0;  // best candidate as a fraction
+    bool have = false;
+    if (R == 1 && cx >= 1 && cx + 1 < W && cy >= 1 && cy + 1 < H) {
+        // interior 3x3 window: issue all 27 loads before any compare, so the
+        // vote costs one memory latency instead of nine
+        double m[9], gxv[9], gyv[9];
+#pragma unroll
+        for (int q = 0; q < 9; ++q) {
+            const size_t o = (size_t)(cy - 1 + q / 3) * W + (cx - 1 + q % 3);
+            m[q] = __ldg(mag + o);
+            gxv[q] = __ldg(gx + o);
+            gyv[q] = __ldg(gy + o);
+        }
+#pragma unroll
+        for (int q = 0; q < 9; ++q) {  // row-major: the reference's scan order
+            double a = 0.0, d = 1.0;
+            if (m[q] >= eps) {
+                a = __dadd_rn(__dmul_rn(dx, gxv[q]), __dmul_rn(dy, gyv[q]));
+                d = m[q];
+            }
+            if (absolute) a = fabs(a);
+            if (!have || frac_greater(a, d, ba, bm)) {
+                ba = a;
+                bm = d;
+                have = true;
+            }
+        }
+        return bm == 1.0 ? ba : __ddiv_rn(ba, bm);
+    }
     const int x0 = cx - R < 0 ? 0 : cx - R;
     const int x1 = cx + R >= W ? W - 1 : cx + R;
     const int y0 = cy - R < 0 ? 0 : cy - R;
     const int y1 = cy + R >= H ? H - 1 : cy + R;
     if (x0 > x1 || y0 > y1) return 0.0;
-    double best = -INFINITY;
     for (int y = y0; y <= y1; ++y) {
         const size_t row = (size_t)y * W;
         for (int x = x0; x <= x1; ++x) {
             const double m = __ldg(mag + row + x);
-            double cand = 0.0;
+            double a = 0.0, d = 1.0;  // below eps: candidate 0 (= 0 / 1)
             if (m >= eps) {
-                cand = __ddiv_rn(__dadd_rn(__dmul_rn(dx, __ldg(gx + row + x)),
-                                           __dmul_rn(dy, __ldg(gy + row + x))),
-                                 m);
+                a = __dadd_rn(__dmul_rn(dx, __ldg(gx + row + x)), __dmul_rn(dy, __ldg(gy + row + x)));
+                d = m;
             }
-            if (absolute) cand = fabs(cand);
-            if (cand > best) best = cand;
+            if (absolute) a = fabs(a);
+            if (!have || frac_greater(a, d, ba, bm)) {
+                ba = a;
+                bm = d;
+                have = true;
+            }
         }
     }
-    return best;
+    return bm == 1.0 ? ba : __ddiv_rn(ba, bm);
 }
 
 // One model point of score_rotated (similarity.cpp:102-116): projection,

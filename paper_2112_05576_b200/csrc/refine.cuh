@@ -30,12 +30,18 @@ struct RefineArgs {
     const int* beam_count;
     BeamDev* beam_out;
     int* beam_count_out;
-    double* votes;        // [entry][point], pose-major
+    double* votes;        // [entry][point] vote rows when they do not fit shared memory
+    double* rot;          // [parent * side + kt][px | py | dx | dy][point]
+    int votes_in_smem;    // set by launch_refine_level
     double* entries;      // [entry] score, ux, uy, theta
+    double* poses;        // ux[E] | uy[E] | theta[E] (refine_rotate_kernel)
+    long long* keys;      // order_key(score), LLONG_MIN for duplicates
     int* dup;             // [entry] an earlier entry has the same pose
     ea_outcome* outcome;  // device copy of the result
 };
 
+constexpr int kRefineThreads = 128;               // threads per pose (refine_entry_kernel)
+constexpr size_t kRefineSmemMax = 96 * 1024;      // vote rows in smem up to this size
 void launch_refine_level(ea_ctx* ctx, const RefineArgs& a);
 
 // Top-level grid + search params the seed kernel needs.

@@ -6,15 +6,15 @@
 // host evaluates glibc cos/sin for all paths of the k seeds once (k * sum
 // side^d values) and the levels run without host round trips:
 //
-//   refine_votes_kernel   one CTA per (parent, kt, point chunk): rotates the
-//                         chunk exactly (similarity.cpp:79-86), then every
-//                         thread computes exact fp64 votes of (pose, point)
-//                         pairs for the side^2 lattice poses.  votes[i][e].
-//   refine_sum_kernel     one warp per pose: ordered fp64 sum (model-point
+//   refine_rotate_kernel  exact rotation of the model for each (parent, kt)
+//                         (similarity.cpp:79-86), shared by its side^2 poses.
+//   refine_entry_kernel   one CTA per pose: exact votes of all points into a
+//                         shared-memory row, ordered fp64 sum (model-point
 //                         order, then /n) + "an earlier entry has this pose".
 //   refine_rank_kernel    one warp per pose: rank among first occurrences in
 //                         the stable-sort order -> new beam slot, trace,
 //                         final outcome.
+#include <algorithm>
 #include <climits>
 
 #include "kernels.cuh"
@@ -22,103 +22,101 @@
 
 namespace eab {
 
-__global__ void __launch_bounds__(256) refine_votes_kernel(const RefineArgs a) {
-    extern __shared__ double rot[];  // px | py | dx | dy of this chunk
-    const int side = a.side, R = a.R;
-    const int pk = blockIdx.x;         // parent * side + (kt + R)
-    const int p = pk / side;
-    if (p >= *a.beam_count) return;
-    const int i0 = blockIdx.y * a.chunk;
-    const int cn = min(a.chunk, a.n - i0);
-    if (cn <= 0) return;
-    const BeamDev parent = a.beam[p];
+// Exact rotation (similarity.cpp:79-86) of every model point for each
+// (parent, kt): shared by the side^2 lattice poses of that pair.
+__global__ void __launch_bounds__(128) refine_rotate_kernel(const RefineArgs a) {
+    const int side = a.side;
+    const int pk = blockIdx.x;  // parent * side + (kt + R)
+    if (pk / side >= *a.beam_count) return;
+    const BeamDev parent = a.beam[pk / side];
     const int path = parent.path * side + (pk % side);
     const double c = a.table[3 * path + 1], s = a.table[3 * path + 2];
-    for (int t = threadIdx.x; t < cn; t += blockDim.x) {
-        const int i = i0 + t;
+    if (blockIdx.y == 0) {  // the pair's side^2 lattice poses (search.cpp:305-312)
+        const int ss = side * side, E = a.max_parents * side * ss;
+        const double cx = __dmul_rn(parent.ux, 2.0), cy = __dmul_rn(parent.uy, 2.0);
+        const double th = a.table[3 * path];
+        for (int j = threadIdx.x; j < ss; j += blockDim.x) {
+            const int ky = j / side - a.R, kx = j % side - a.R;
+            const int e = pk * ss + j;
+            a.poses[e] = __dadd_rn(cx, __dmul_rn((double)kx, a.step_x));
+            a.poses[E + e] = __dadd_rn(cy, __dmul_rn((double)ky, a.step_y));
+            a.poses[2 * E + e] = th;
+        }
+    }
+    double* out = a.rot + (size_t)pk * 4 * a.n;
+    for (int i = blockIdx.y * blockDim.x + threadIdx.x; i < a.n; i += gridDim.y * blockDim.x) {
         const double x = a.pts[i], y = a.pts[a.n + i];
         const double dx = a.pts[2 * a.n + i], dy = a.pts[3 * a.n + i];
         const double rx = __dsub_rn(__dmul_rn(c, dx), __dmul_rn(s, dy));
         const double ry = __dadd_rn(__dmul_rn(s, dx), __dmul_rn(c, dy));
         const double norm = __dsqrt_rn(__dadd_rn(__dmul_rn(rx, rx), __dmul_rn(ry, ry)));
-        rot[t] = __dsub_rn(__dmul_rn(c, x), __dmul_rn(s, y));
-        rot[a.chunk + t] = __dadd_rn(__dmul_rn(s, x), __dmul_rn(c, y));
-        rot[2 * a.chunk + t] = __ddiv_rn(rx, norm);
-        rot[3 * a.chunk + t] = __ddiv_rn(ry, norm);
+        out[i] = __dsub_rn(__dmul_rn(c, x), __dmul_rn(s, y));
+        out[a.n + i] = __dadd_rn(__dmul_rn(s, x), __dmul_rn(c, y));
+        out[2 * a.n + i] = __ddiv_rn(rx, norm);
+        out[3 * a.n + i] = __ddiv_rn(ry, norm);
+    }
+}
+
+// Score of each lattice pose (score_rotated, similarity.cpp:102-118): one
+// CTA per pose.  Threads compute the exact votes of the model points
+// (strided) into a vote row (shared memory, or global for very large models);
+// then thread 0 adds them in model-point order -- the reference's sequential
+// fp64 sum, bit for bit -- and divides by n, while warp 1 checks whether an
+// earlier entry in generation order has the identical pose: identical poses
+// score identically, so after the stable sort the first occurrence is the one
+// kept (search.cpp:330-345).
+__global__ void __launch_bounds__(kRefineThreads) refine_entry_kernel(const RefineArgs a) {
+    extern __shared__ double sv[];
+    __shared__ int dup_s;
+    const int side = a.side, ss = side * side;
+    const int E = *a.beam_count * side * ss;
+    const int e = blockIdx.x;
+    if (e >= E) return;  // whole CTA
+    const int EM = a.max_parents * side * ss;  // pose array stride
+    const double px = a.poses[e], py = a.poses[EM + e], pt = a.poses[2 * EM + e];
+    const int n = a.n;
+    const double* rot = a.rot + (size_t)(e / ss) * 4 * n;
+    double* vb = a.votes_in_smem ? sv : a.votes + (size_t)e * n;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        int inb;
+        vb[i] = point_term_exact(rot[i], rot[n + i], rot[2 * n + i], rot[3 * n + i], px, py,
+                                 a.gx, a.gy, a.mag, a.W, a.H, a.vote_R, a.eps, a.ignore != 0,
+                                 &inb);
     }
     __syncthreads();
-    const double cx = __dmul_rn(parent.ux, 2.0), cy = __dmul_rn(parent.uy, 2.0);
-    const int ss = side * side;
-    for (int t = threadIdx.x; t < ss * cn; t += blockDim.x) {
-        const int j = t / cn, ii = t % cn;
-        const int ky = j / side - R, kx = j % side - R;
-        const double ux = __dadd_rn(cx, __dmul_rn((double)kx, a.step_x));
-        const double uy = __dadd_rn(cy, __dmul_rn((double)ky, a.step_y));
-        int inb;
-        const double v = point_term_exact(rot[ii], rot[a.chunk + ii], rot[2 * a.chunk + ii],
-                                          rot[3 * a.chunk + ii], ux, uy, a.gx, a.gy, a.mag, a.W,
-                                          a.H, a.vote_R, a.eps, a.ignore != 0, &inb);
-        a.votes[((size_t)pk * ss + j) * a.n + i0 + ii] = v;  // pose-major
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (warp == 1) {
+        int dup = 0;
+        for (int q = lane; q < e; q += 32)
+            dup |= (a.poses[q] == px && a.poses[EM + q] == py && a.poses[2 * EM + q] == pt) ? 1
+                                                                                              : 0;
+        dup = __any_sync(0xffffffffu, dup);
+        if (lane == 0) dup_s = dup;
     }
-}
-
-__device__ __forceinline__ void entry_pose(const RefineArgs& a, int e, double* ux, double* uy,
-                                           double* th) {
-    const int side = a.side, ss = side * side;
-    const int pk = e / ss, j = e % ss;
-    const BeamDev& parent = a.beam[pk / side];
-    const int ky = j / side - a.R, kx = j % side - a.R;
-    *ux = __dadd_rn(__dmul_rn(parent.ux, 2.0), __dmul_rn((double)kx, a.step_x));
-    *uy = __dadd_rn(__dmul_rn(parent.uy, 2.0), __dmul_rn((double)ky, a.step_y));
-    *th = a.table[3 * (parent.path * side + (pk % side))];
-}
-
-// Ordered fp64 sum of each lattice pose's votes (model-point order, then /n,
-// similarity.cpp:109-118): one warp per pose; lanes load 32 consecutive votes,
-// every lane walks them in order through shuffles (the chain is the
-// reference's sequential sum).  Also emits the pose (search.cpp:308-312).
-__global__ void __launch_bounds__(256) refine_sum_kernel(const RefineArgs a) {
-    const int side = a.side, R = a.R, ss = side * side;
-    const int E = *a.beam_count * side * ss;
-    const int lane = threadIdx.x & 31;
-    const int e = (int)(((unsigned)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
-    if (e >= E) return;
-    const double* row = a.votes + (size_t)e * a.n;
-    double sum = 0.0;
-    for (int q = 0; q < a.n; q += 32) {
-        const double v = q + lane < a.n ? __ldg(row + q + lane) : 0.0;
-        const int lim = a.n - q < 32 ? a.n - q : 32;
-        double t[32];
-#pragma unroll
-        for (int l = 0; l < 32; ++l) t[l] = __shfl_sync(0xffffffffu, v, l);
-#pragma unroll
-        for (int l = 0; l < 32; ++l)
-            if (l < lim) sum = __dadd_rn(sum, t[l]);
-    }
-    // The pose of entry e (search.cpp:305-312) and whether an earlier entry in
-    // generation order has the identical pose: identical poses score
-    // identically, so after the stable sort the first occurrence is the one
-    // kept (search.cpp:330-345).
-    double px, py, pt;
-    entry_pose(a, e, &px, &py, &pt);
-    int dup = 0;
-    for (int q0 = 0; q0 < e; q0 += 32) {  // warp-uniform trip count
-        const int q = q0 + lane;
-        if (q < e) {
-            double qx, qy, qt;
-            entry_pose(a, q, &qx, &qy, &qt);
-            dup |= (qx == px && qy == py && qt == pt) ? 1 : 0;
+    double score = 0.0;
+    if (threadIdx.x == 0) {
+        double sum = 0.0;
+        int i = 0;
+        for (; i + 4 <= n; i += 4) {  // independent loads, one dependent add chain
+            const double v0 = vb[i], v1 = vb[i + 1], v2 = vb[i + 2], v3 = vb[i + 3];
+            sum = __dadd_rn(sum, v0);
+            sum = __dadd_rn(sum, v1);
+            sum = __dadd_rn(sum, v2);
+            sum = __dadd_rn(sum, v3);
         }
-        if (__any_sync(0xffffffffu, dup)) break;
+        for (; i < n; ++i) sum = __dadd_rn(sum, vb[i]);
+        score = __ddiv_rn(sum, (double)n);
     }
-    dup = __any_sync(0xffffffffu, dup);
-    if (lane == 0) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const int dup = dup_s;
         double* out = a.entries + 4 * (size_t)e;
-        out[0] = __ddiv_rn(sum, (double)a.n);
+        out[0] = score;
         out[1] = px;
         out[2] = py;
         out[3] = pt;
         a.dup[e] = dup;
+        a.keys[e] = dup ? LLONG_MIN : order_key(score);
     }
 }
 
@@ -139,14 +137,14 @@ __global__ void __launch_bounds__(256) refine_rank_kernel(const RefineArgs a) {
     const int lane = threadIdx.x & 31;
     const int e = (int)(((unsigned)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
     if (e >= E) return;
-    const long long ke = order_key(a.entries[4 * (size_t)e]);
-    const bool mine = a.dup[e] == 0;
+    const long long ke = a.keys[e];
+    const bool mine = ke != LLONG_MIN;  // first occurrence of its pose
     int rank = 0, distinct = 0;
+#pragma unroll 4
     for (int q = lane; q < E; q += 32) {
-        if (a.dup[q]) continue;
-        ++distinct;
-        const long long kq = order_key(a.entries[4 * (size_t)q]);
-        rank += (kq > ke) || (kq == ke && q < e);
+        const long long kq = a.keys[q];
+        distinct += kq != LLONG_MIN;
+        rank += (kq > ke) || (kq == ke && q < e);  // duplicates never outrank
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -231,15 +229,24 @@ void launch_seed_beam(ea_ctx* ctx, const double* top_score, const unsigned long 
     count_launch(ctx);
 }
 
-void launch_refine_level(ea_ctx* ctx, const RefineArgs& a) {
-    const int grid_x = a.max_parents * a.side;
-    const int grid_y = (a.n + a.chunk - 1) / a.chunk;
-    refine_votes_kernel<<<dim3(grid_x, grid_y), 256, 4 * sizeof(double) * a.chunk,
-                          ctx->stream>>>(a);
-    check_launch("refine_votes_kernel");
+void launch_refine_level(ea_ctx* ctx, const RefineArgs& a_in) {
+    RefineArgs a = a_in;
+    const int pairs = a.max_parents * a.side;
+    const int gy = std::max(1, std::min((a.n + 127) / 128, 8));
+    refine_rotate_kernel<<<dim3(pairs, gy), 128, 0, ctx->stream>>>(a);
+    check_launch("refine_rotate_kernel");
     const int e_max = a.max_parents * a.side * a.side * a.side;
-    refine_sum_kernel<<<(e_max * 32 + 255) / 256, 256, 0, ctx->stream>>>(a);
-    check_launch("refine_sum_kernel");
+    const size_t smem = sizeof(double) * (size_t)a.n;
+    a.votes_in_smem = smem <= kRefineSmemMax ? 1 : 0;
+    static bool attr_set = false;
+    if (!attr_set) {
+        EAB_CUDA(cudaFuncSetAttribute(refine_entry_kernel,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)kRefineSmemMax));
+        attr_set = true;
+    }
+    refine_entry_kernel<<<e_max, kRefineThreads, a.votes_in_smem ? smem : 0, ctx->stream>>>(a);
+    check_launch("refine_entry_kernel");
     refine_rank_kernel<<<(e_max * 32 + 255) / 256, 256, 0, ctx->stream>>>(a);
     check_launch("refine_rank_kernel");
     count_launch(ctx, 3);

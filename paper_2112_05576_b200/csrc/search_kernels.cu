@@ -676,10 +676,13 @@ struct RegionPlan {
     unsigned long long n_items;  // warp tiles x theta groups
     unsigned groups;         // theta groups per warp tile
 };
-constexpr int kGroup = 8;  // thetas per CTA item (= warps per CTA)
+#ifndef EAB_REGION_WARPS
+#define EAB_REGION_WARPS 8
+#endif
+constexpr int kGroup = EAB_REGION_WARPS;  // thetas per CTA item (= warps per CTA)
 
 template <int R, int S, int SHIFT, bool IGNORE, int XG>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(kGroup * 32, 1)
     screen_region_kernel(const ScreenArgs a, const unsigned nwx, const unsigned nwy,
                          const RegionPlan rp) {
     extern __shared__ __align__(16) unsigned char smem[];

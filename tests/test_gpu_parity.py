@@ -520,3 +520,25 @@ def test_config5_multi_detect_bit_exact(ea, oracle):
     for t, got in zip(tmpls, outs):
         want = oracle.coarse_to_fine(oracle.build_pyramid(t, L), wp, cfg)
         assert got.key() == want.key()
+
+
+@pytest.mark.parametrize("G", [1, 3, 8])
+def test_sharded_detect_flow(ea, oracle, G):
+    """The multi-GPU detect on one device: theta-slab top-level searches
+    (search_top_slab, one per rank), the `better` merge (what gather_topk
+    does over NCCL), then refine from the merged seeds == detect == oracle."""
+    img, tmpl = scene(ea, canvas_width=200, canvas_height=160, template_id="l_bracket",
+                      template_size=56, true_pose=(96, 84, D(63)), clutter_segments=25,
+                      clutter_seed=4, noise_sigma=1.0, noise_seed=2)
+    cfg = ea.SearchConfig(grid=ea.PoseGrid(0, 199, 4, 0, 159, 4, 0.0, D(357), D(3)),
+                          num_levels=3, score_params=ea.ScoreParams(3), topk=4)
+    det = ea.Detector(tmpl, cfg)
+    want = det.detect(img)
+    nt = ea.grid_counts(ea.PoseGrid(0, 49.75, 1, 0, 39.75, 1, 0.0, D(357), D(3)))[2]
+    seeds = []
+    for g in range(G):
+        seeds += ea.search_top_slab(det.levels, cfg, nt * g // G, nt * (g + 1) // G)
+    got = ea.refine(det.levels, cfg, ea.merge_topk(seeds, cfg.topk))
+    assert got.key() == want.key()
+    tp, wp = oracle.build_pyramid(tmpl, 3), oracle.build_pyramid(img, 3)
+    assert got.key() == oracle.coarse_to_fine(tp, wp, cfg).key()
