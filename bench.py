@@ -100,6 +100,14 @@ def batch_scenes(name, count):
         return list(ex.map(one, range(count)))
 
 
+# DRAM read + write of one screen-kernel launch, from `ncu --set full` captures
+# (not measurable inside the timed run); per config.
+TRAFFIC = {
+    "cfg2": (6630656, "profiles/r01_screen_fast_ncu.txt (cfg2 launch)"),
+    "cfg4": (6630656, "profiles/r01_screen_fast_ncu.txt (cfg2 geometry)"),
+    "cfg5": (388506368, "profiles/r01_screen_region_ncu.txt (cfg5 model 5 launch; "
+                        "the 227 MB fp32 map is written through to DRAM)"),
+}
 SMEM_BYTES_PER_CLK_PER_SM = 128
 ALG_BYTES_PER_EVAL = 72  # (2r+1)^2 = 9 window pixels x 8 B float2
 
@@ -488,8 +496,8 @@ def bench_ours(args, rank, world, local_rank):
                          st["screen_path"], "screen_general_kernel"), "achieved": achieved,
                      "peak": smem_peak_gbs, "unit": "GB/s", "frac": achieved / smem_peak_gbs,
                      # dram read+write of one launch, ncu --set full (not measurable in-run)
-                     "traffic": 8940032 if args.config in ("cfg2", "cfg4") else None,
-                     "traffic_source": "profiles/r01_screen_fast_ncu.txt (cfg2 launch)",
+                     "traffic": TRAFFIC.get(args.config, (None, None))[0],
+                     "traffic_source": TRAFFIC.get(args.config, (None, "not captured"))[1],
                      "algorithmic_bytes_per_eval": ALG_BYTES_PER_EVAL,
                      "smem_bytes_loaded_per_eval": actual_b,
                      "frac_smem_loaded": local_evals * actual_b / (kernel_ms / 1e3) / 1e9
