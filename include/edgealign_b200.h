@@ -238,6 +238,15 @@ ea_status ea_extract_edge_model(const double* gx, const double* gy, const double
                                 double* centroid_x, double* centroid_y);
 
 /* Device edge models (edgealign::EdgeModel, edge_model.h:40-45). */
+/* extract_edge_model on a device field (edge_model.cpp:53-149): peak, NMS,
+ * hysteresis and emission on the device; th == NULL uses default_thresholds
+ * (edge_model.cpp:17-24).  Same points, order and centroid as the host
+ * ea_extract_edge_model. */
+ea_status ea_field_extract_model(ea_ctx* ctx, const ea_field* field, const ea_edge_thresholds* th,
+                                 int level, ea_model** out);
+/* Points (AoS, model order) and centroid of a model. */
+ea_status ea_model_points(const ea_model* m, ea_edge_point* points, int cap, int* n_out,
+                          double* centroid_x, double* centroid_y);
 ea_status ea_model_create(ea_ctx* ctx, const ea_edge_point* points, int n,
                           double centroid_x, double centroid_y, int source_level,
                           ea_model** out);

@@ -51,6 +51,9 @@ _SIGS = {
     "ea_model_create": (C.c_int, [_P, C.POINTER(abi.EdgePoint), C.c_int, C.c_double,
                                   C.c_double, C.c_int, C.POINTER(_P)]),
     "ea_model_size": (C.c_int, [_P]),
+    "ea_field_extract_model": (C.c_int, [_P, _P, C.POINTER(abi.EdgeThresholds), C.c_int,
+                                         C.POINTER(_P)]),
+    "ea_model_points": (C.c_int, [_P, C.POINTER(abi.EdgePoint), C.c_int, _ip, _dp, _dp]),
     "ea_model_free": (None, [_P]),
     "ea_validate_params": (C.c_int, [C.POINTER(abi.ScoreParams)]),
     "ea_point_vote": (C.c_int, [_P, C.c_double, C.c_double, _P, C.c_int, C.c_int,

@@ -177,6 +177,27 @@ class DeviceModel:
             self.handle = None
 
 
+def extract_edge_model_device(field, thresholds=None, level=0, ctx=None):
+    """extract_edge_model (edge_model.cpp:53-149) on the device
+    (ea_field_extract_model); thresholds None = default_thresholds.
+    -> EdgeModel with the points read back."""
+    ctx = ctx or default_context()
+    f = _field(field, ctx)
+    h = C.c_void_p()
+    th = None if thresholds is None else C.byref(
+        thresholds if isinstance(thresholds, abi.EdgeThresholds) else abi.EdgeThresholds(*thresholds))
+    _check(lib().ea_field_extract_model(ctx.handle, f.handle, th, int(level), C.byref(h)))
+    try:
+        n, cx, cy = C.c_int(), C.c_double(), C.c_double()
+        _check(lib().ea_model_points(h, None, 0, C.byref(n), C.byref(cx), C.byref(cy)))
+        pts = np.zeros((max(n.value, 1), 5))
+        _check(lib().ea_model_points(h, pts.ctypes.data_as(C.POINTER(EdgePoint)), n.value,
+                                     C.byref(n), C.byref(cx), C.byref(cy)))
+    finally:
+        lib().ea_model_free(h)
+    return EdgeModel(pts[: n.value], cx.value, cy.value, int(level))
+
+
 def _field(f, ctx):
     return f if isinstance(f, DeviceField) else DeviceField.upload(f, ctx)
 

@@ -15,9 +15,10 @@ CSRC = os.path.join(HERE, "csrc")
 OBJ = os.path.join(HERE, "_build")
 LIB = os.path.join(HERE, "libedgealign_b200.so")
 
-CU_SOURCES = ["api.cu", "field_kernels.cu", "search_kernels.cu", "refine_kernels.cu"]
+CU_SOURCES = ["api.cu", "field_kernels.cu", "search_kernels.cu", "refine_kernels.cu",
+              "model_kernels.cu"]
 CPP_SOURCES = ["host_model.cpp", "host_synth.cpp"]
-HEADERS = ["common.cuh", "kernels.cuh", "refine.cuh", "failure.h", "host_model.h"]
+HEADERS = ["common.cuh", "kernels.cuh", "refine.cuh", "model.cuh", "failure.h", "host_model.h"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 HOST_FLAGS = "-fPIC,-ffp-contract=off,-O2,-Wall"

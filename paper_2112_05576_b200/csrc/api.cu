@@ -15,6 +15,7 @@
 
 #include "host_model.h"
 #include "kernels.cuh"
+#include "model.cuh"
 #include "refine.cuh"
 
 using namespace eab;
@@ -1197,28 +1198,87 @@ void detect_multi(ea_ctx* ctx, ea_levels* const* models, int n, const double* im
 }
 
 // Template side of prepare_levels (search.cpp:222-234) for one level.
+// extract_edge_model (edge_model.cpp:53-149) on a device field: peak, NMS,
+// hysteresis and emission on the device (model_kernels.cu); pixels whose
+// orientation bin needs glibc's atan2 are decided here with the reference's
+// formula.  th == nullptr: default_thresholds (edge_model.cpp:17-24).
+ea_model* extract_model_device(ea_ctx* ctx, const ea_field* f, const ea_edge_thresholds* th,
+                               int level) {
+    if (th && (th->low < 0.0 || th->low > th->high))
+        fail(EA_ERR_INVALID_ARGUMENT, "edge thresholds need 0 <= low <= high");
+    const int w = f->width, h = f->height;
+    const size_t total = (size_t)w * h;
+    const size_t head = 128;
+    char* buf = (char*)ctx->mscratch.ensure(head + total * (sizeof(ea_edge_point) + 6));
+    ModelScratch* ms = (ModelScratch*)buf;
+    ea_edge_point* pts = (ea_edge_point*)(buf + head);
+    int* amb = (int*)(buf + head + total * sizeof(ea_edge_point));
+    unsigned char* state = (unsigned char*)(amb + total);
+    unsigned char* kept = state + total;
+    ModelScratch* hs = (ModelScratch*)ctx->h_out.ensure(sizeof(ModelScratch));
+    std::memset(hs, 0, sizeof *hs);
+    hs->use_default = th ? 0 : 1;
+    if (th) {
+        hs->low = th->low;
+        hs->high = th->high;
+    }
+    h2d(ctx, ms, hs, sizeof *hs);
+    launch_magmax(ctx, f->mag(), total, ms);
+    launch_nms(ctx, f->gx(), f->gy(), f->mag(), w, h, ms, state, kept, amb);
+    d2h(ctx, hs, ms, sizeof *hs);
+    sync(ctx);
+    if (hs->n_amb > 0) {  // bins on the host, with the reference's atan2 formula
+        const int na = hs->n_amb;
+        std::vector<double> g(3 * total);
+        std::vector<int> list(na);
+        std::vector<unsigned char> st(total), kp(total);
+        d2h(ctx, g.data(), f->g.p, g.size() * sizeof(double));
+        d2h(ctx, list.data(), amb, sizeof(int) * (size_t)na);
+        d2h(ctx, st.data(), state, total);
+        d2h(ctx, kp.data(), kept, total);
+        sync(ctx);
+        const double* gx = g.data();
+        const double* gy = gx + total;
+        const double* mag = gy + total;
+        for (const int o : list) {
+            const unsigned char v = host_nms_state(gx, gy, mag, w, o % w, o / w, hs->low, hs->high);
+            st[o] = v;
+            kp[o] = v == 2;
+        }
+        h2d_staged(ctx, state, st.data(), total);
+        h2d_staged(ctx, kept, kp.data(), total);
+    }
+    launch_hysteresis_emit(ctx, f->gx(), f->gy(), f->mag(), state, kept, w, h, ms, pts);
+    d2h(ctx, hs, ms, sizeof *hs);
+    sync(ctx);
+    const int n = hs->n_kept;
+    if (n == 0) {
+        double peak;
+        std::memcpy(&peak, &hs->peak_bits, sizeof peak);
+        char msg[128];
+        std::snprintf(msg, sizeof msg,
+                      "edge extraction produced an empty model (max gradient magnitude %f)", peak);
+        fail(EA_ERR_EMPTY_MODEL, msg, peak);
+    }
+    std::vector<ea_edge_point> host(n);
+    const double cx = hs->cx, cy = hs->cy;
+    d2h(ctx, host.data(), pts, sizeof(ea_edge_point) * (size_t)n);
+    sync(ctx);
+    return new_model(ctx, host.data(), n, cx, cy, level);
+}
+
+// Template side of prepare_levels (search.cpp:222-234) for one level.
 ea_model* template_model(ea_ctx* ctx, const double* d_img, int w, int h,
                          const ea_search_config& cfg, int level) {
     ea_field* tf = new_field(w, h);
-    std::vector<double> g(3 * (size_t)w * h);
     try {
         sobel_into(ctx, d_img, w, h, tf);
-        d2h(ctx, g.data(), tf->g.p, g.size() * sizeof(double));
-        sync(ctx);
-    } catch (...) {
+        ea_model* m = extract_model_device(ctx, tf, cfg.has_thresholds ? &cfg.thresholds : nullptr,
+                                           level);
         delete tf;
-        throw;
-    }
-    delete tf;
-    const size_t np = (size_t)w * h;
-    const ea_edge_thresholds th =
-        cfg.has_thresholds ? cfg.thresholds : host_default_thresholds(g.data() + 2 * np, np);
-    double cx = 0, cy = 0;
-    std::vector<ea_edge_point> pts;
-    try {
-        pts = host_extract_edge_model(g.data(), g.data() + np, g.data() + 2 * np, w, h, th, &cx,
-                                      &cy);
+        return m;
     } catch (const Failure& e) {
+        delete tf;
         if (e.code == EA_ERR_EMPTY_MODEL) {
             fail(EA_ERR_EMPTY_MODEL,
                  "edge model extraction failed at pyramid level " + std::to_string(level) + ": " +
@@ -1226,8 +1286,10 @@ ea_model* template_model(ea_ctx* ctx, const double* d_img, int w, int h,
                  e.value);
         }
         throw;
+    } catch (...) {
+        delete tf;
+        throw;
     }
-    return new_model(ctx, pts.data(), (int)pts.size(), cx, cy, level);
 }
 
 void free_levels(ea_levels* lv) {
@@ -1331,7 +1393,7 @@ void ea_ctx_destroy(ea_ctx* ctx) {
                       &ctx->item_max, &ctx->tail,
                       &ctx->hist, &ctx->ctrl, &ctx->cand, &ctx->cand_score, &ctx->topk,
                       &ctx->refine_poses, &ctx->refine_scores, &ctx->beam, &ctx->accum64,
-                      &ctx->work, &ctx->ttab, &ctx->rstate, &ctx->rslots})
+                      &ctx->work, &ctx->ttab, &ctx->rstate, &ctx->rslots, &ctx->mscratch})
         b->release();
     ctx->h_stage.release();
     ctx->h_out.release();
@@ -1614,6 +1676,30 @@ ea_status ea_extract_edge_model(const double* gx, const double* gy, const double
         if (points) {
             for (int i = 0; i < (int)pts.size() && i < cap; ++i) points[i] = pts[i];
         }
+    });
+}
+
+ea_status ea_field_extract_model(ea_ctx* ctx, const ea_field* field, const ea_edge_thresholds* th,
+                                 int level, ea_model** out) {
+    return guard([&] {
+        need(ctx, "ctx");
+        need(field, "field");
+        need(out, "out");
+        DeviceGuard dg(ctx->device);
+        *out = extract_model_device(ctx, field, th, level);
+    });
+}
+
+ea_status ea_model_points(const ea_model* m, ea_edge_point* points, int cap, int* n_out,
+                          double* cx, double* cy) {
+    return guard([&] {
+        need(m, "model");
+        need(n_out, "n_out");
+        *n_out = m->n;
+        if (cx) *cx = m->centroid_x;
+        if (cy) *cy = m->centroid_y;
+        if (points)
+            for (int i = 0; i < m->n && i < cap; ++i) points[i] = m->host[i];
     });
 }
 

@@ -123,7 +123,7 @@ struct ea_ctx {
     cudaEvent_t ev[8] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
     // scratch
     eab::DevBuf cs, rot_exact, rot_screen, plane, map, item_max, tail, hist, ctrl, cand, cand_score, topk,
-        refine_poses, refine_scores, beam, accum64, work;
+        refine_poses, refine_scores, beam, accum64, work, mscratch;
     eab::HostBuf h_stage, h_out;
     // glibc cos/sin tables of theta grids, cached per (t0, dt, nt)
     std::map<std::vector<double>, std::vector<double>> cs_cache;

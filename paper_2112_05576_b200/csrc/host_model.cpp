@@ -1,15 +1,14 @@
-// host_model.cpp -- template-side model preparation on the host.
+// host_model.cpp -- template-side helpers on the host.
 //
-// The reference prepares the template once per search (prepare_levels,
-// search.cpp:208-238, "the untimed preparation stage", search.h:92-93).  Its
-// gradient field is computed on the device by the same Sobel kernel as the
-// search image; the sparse extraction below (direction-binned non-maximum
-// suppression + 8-connected hysteresis + centroid, edge_model.cpp:17-149)
-// runs on the host because it is a once-per-model, branchy flood fill.
-// Moving it to the GPU is SURVEY.md §8(f)-1.
+// The template side (prepare_levels, search.cpp:208-238) runs on the device:
+// Sobel, peak, NMS, hysteresis and emission (model_kernels.cu, SURVEY.md
+// §8(f)-1).  This file keeps (a) the reference's orientation bin with the
+// host libm's atan2 -- the same library the reference links -- for the few
+// pixels whose bin the device cannot decide exactly (host_nms_state), and (b)
+// a whole host extraction behind ea_extract_edge_model, the host-array entry
+// point of the C-ABI (edge_model.cpp:17-149).
 //
-// Compiled with -ffp-contract=off; atan2 is the host libm's, the same one the
-// reference links, so orientation bins agree at the bin boundaries.
+// Compiled with -ffp-contract=off.
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
@@ -37,6 +36,20 @@ int direction_bin(double gx, double gy) {
     return 0;
 }
 }  // namespace
+
+unsigned char host_nms_state(const double* gx, const double* gy, const double* mag, int w, int x,
+                             int y, double low, double high) {
+    static const int step_x[4] = {1, 1, 0, -1};
+    static const int step_y[4] = {0, 1, 1, 1};
+    const size_t o = (size_t)y * w + x;
+    const double m = mag[o];
+    if (m <= 0.0 || m < low) return 0;
+    const int b = direction_bin(gx[o], gy[o]);
+    const double ahead = mag[(size_t)(y + step_y[b]) * w + (x + step_x[b])];
+    const double behind = mag[(size_t)(y - step_y[b]) * w + (x - step_x[b])];
+    if (m > ahead && m >= behind) return m >= high ? 2 : 1;
+    return 0;
+}
 
 ea_edge_thresholds host_default_thresholds(const double* mag, size_t count) {
     double peak = 0.0;

@@ -15,6 +15,12 @@ std::vector<ea_edge_point> host_extract_edge_model(const double* gx, const doubl
                                                    const ea_edge_thresholds& th,
                                                    double* centroid_x, double* centroid_y);
 
+// NMS state (0 out, 1 weak, 2 strong) of interior pixel (x, y) with the
+// reference's atan2 bins (edge_model.cpp:34-45, 77-90); the device extraction
+// asks for the pixels whose bin it cannot decide without glibc.
+unsigned char host_nms_state(const double* gx, const double* gy, const double* mag, int w, int x,
+                             int y, double low, double high);
+
 // Synthetic scenes (synth.cpp:24-300), host only: libm-dependent generator.
 void host_render_template(int id, int size, double* out);
 void host_compose_multi(const ea_scene_spec& s, const ea_stamp* stamps, int n, double* canvas);

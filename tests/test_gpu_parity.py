@@ -542,3 +542,61 @@ def test_sharded_detect_flow(ea, oracle, G):
     assert got.key() == want.key()
     tp, wp = oracle.build_pyramid(tmpl, 3), oracle.build_pyramid(img, 3)
     assert got.key() == oracle.coarse_to_fine(tp, wp, cfg).key()
+
+
+# ---- template side on the device ----------------------------------------
+def model_key(m):
+    return (np.asarray(m.points).tobytes(), m.centroid_x, m.centroid_y)
+
+
+@pytest.mark.parametrize("shape", ["rectangle", "ring", "l_bracket", "cross"])
+@pytest.mark.parametrize("size", [16, 33, 64, 200, 400])
+def test_device_edge_model_templates(ea, oracle, shape, size):
+    img = oracle.render_template(shape, size)
+    f = oracle.compute_gradients(img)
+    got = ea.extract_edge_model_device(f)
+    want = oracle.extract_edge_model(f, oracle.default_thresholds(f), 0)
+    assert model_key(got) == model_key(want)
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_device_edge_model_random_fields(ea, oracle, seed):
+    rng = np.random.default_rng(500 + seed)
+    f = oracle.compute_gradients(rand_image(rng, 57 + seed, 43, real=seed % 2 == 1))
+    for th in (None, (0.0, 0.0), (10.0, 10.0), (5.0, 300.0)):
+        want_th = oracle.default_thresholds(f) if th is None else th
+        got = ea.extract_edge_model_device(f, th)
+        want = oracle.extract_edge_model(f, want_th, 0)
+        assert model_key(got) == model_key(want)
+
+
+def test_device_edge_model_boundary_bins(ea, oracle):
+    """Gradients exactly on the 22.5/67.5/112.5/157.5 degree bin boundaries
+    (in fp64) go to the host's atan2 and must bin like the reference."""
+    rng = np.random.default_rng(9)
+    h, w = 24, 30
+    gx = rng.normal(size=(h, w)) * 20
+    gy = rng.normal(size=(h, w)) * 20
+    t = 0.41421356237309503
+    dirs = [(1.0, t), (t, 1.0), (-t, 1.0), (-1.0, t), (1.0, -t), (-t, -1.0), (t, -1.0)]
+    for k in range(200):
+        y, x = 1 + rng.integers(0, h - 2), 1 + rng.integers(0, w - 2)
+        s = float(rng.integers(1, 50))
+        gx[y, x], gy[y, x] = dirs[k % len(dirs)][0] * s, dirs[k % len(dirs)][1] * s
+    gx[0, :] = gx[-1, :] = gx[:, 0] = gx[:, -1] = 0.0
+    gy[0, :] = gy[-1, :] = gy[:, 0] = gy[:, -1] = 0.0
+    mag = np.sqrt(gx * gx + gy * gy)
+    f = (gx, gy, mag)
+    for th in (None, (1.0, 30.0)):
+        want_th = oracle.default_thresholds(f) if th is None else th
+        assert model_key(ea.extract_edge_model_device(f, th)) == \
+            model_key(oracle.extract_edge_model(f, want_th, 0))
+
+
+def test_device_edge_model_errors(ea):
+    z = np.zeros((9, 9))
+    with pytest.raises(ea.EmptyModelError, match="empty model"):
+        ea.extract_edge_model_device((z, z, z))
+    f = ea.compute_gradients(np.arange(100.0).reshape(10, 10) ** 2)
+    with pytest.raises(ea.InvalidArgument, match="0 <= low <= high"):
+        ea.extract_edge_model_device(f, (5.0, 1.0))
