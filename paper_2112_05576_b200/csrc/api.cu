@@ -357,6 +357,14 @@ ScreenPlan screen(ea_ctx* ctx, const ea_model* m, const ea_field* f, const ea_po
     // |offset| <= ceil(max |p_i|) + 1 for every rotation of the model.
     int PL = 0, PR = 0;
     int ro_int = 0;
+    bool edge = false;
+    int xg = 4;
+    {   // warp tile 32x64 or 16x128: whichever pads the translation grid least
+        auto padded = [&](uint64_t cols, uint64_t rows) {
+            return ((plan.c.nx + cols - 1) / cols * cols) * ((plan.c.ny + rows - 1) / rows * rows);
+        };
+        xg = padded(16, 128) < padded(32, 64) ? 2 : 4;
+    }
     // Region mode: even the unpadded plane exceeds shared memory, so the
     // plane stays in global memory and CTAs stage halo regions of it.
     const bool region =
@@ -369,16 +377,19 @@ ScreenPlan screen(ea_ctx* ctx, const ea_model* m, const ea_field* f, const ea_po
             rmax = std::max(rmax, std::sqrt(q.x_rel * q.x_rel + q.y_rel * q.y_rel));
         const long ro = (long)std::ceil(rmax) + 2;
         ro_int = (int)std::min<long>(ro, 1 << 20);
-        const long ix0 = (long)g.x0, span = (long)((plan.c.nx + 31) / 32) * 32;
+        const long tw = 8L * xg;  // warp tile width: the lanes' last window column
+        const long ix0 = (long)g.x0, span = (long)((plan.c.nx + tw - 1) / tw) * tw;
         PL = (int)std::max(0L, ro + R - 1 - ix0);
         PR = (int)std::max(0L, ix0 + span + ro + R - f->width - 1);
         const size_t budget = ctx->smem_optin;  // hist + plane must fit one CTA
         auto bytes = [&](int l, int r) {
             return fast_smem_bytes(plane_geom(f->width, f->height, shift, l, r, elem));
         };
+        const int PL0 = PL, PR0 = PR;
         while ((PL > 0 || PR > 0) && bytes(PL, PR) > budget) {  // shrink: clamp path covers
             if (PL >= PR) --PL; else --PR;
         }
+        edge = PL < PL0 || PR < PR0;
         if (region) PL = PR = 0;  // halo regions are zero-filled instead
     }
     const PlaneGeom geom = plane_geom(f->width, f->height, shift, PL, PR, elem);
@@ -408,14 +419,10 @@ ScreenPlan screen(ea_ctx* ctx, const ea_model* m, const ea_field* f, const ea_po
     a.dy = g.dy;
     a.R = R;
     a.ignore = p.polarity == EA_POLARITY_IGNORE;
-    {   // warp tile 32x64 or 16x128: whichever pads the translation grid least
-        auto padded = [&](uint64_t cols, uint64_t rows) {
-            return ((plan.c.nx + cols - 1) / cols * cols) * ((plan.c.ny + rows - 1) / rows * rows);
-        };
-        a.xg = padded(16, 128) < padded(32, 64) ? 2 : 4;
-    }
+    a.xg = xg;
     a.sched = sched;
     a.ro = ro_int;
+    a.edge = edge ? 1 : 0;
     a.amb = amb;
     a.kf = (k >= 1 && k <= 8) ? k : 0;
     a.K = K;
@@ -1372,7 +1379,9 @@ ea_status ea_ctx_create(int device, ea_ctx** out) {
         auto* c = new ea_ctx;
         c->device = device;
         c->sm_count = prop.multiProcessorCount;
-        c->smem_optin = prop.sharedMemPerBlockOptin;
+        // dynamic shared memory budget: the opt-in limit minus 1 KB for the
+        // screen kernels' static arrays (per-warp histogram floors)
+        c->smem_optin = prop.sharedMemPerBlockOptin - 1024;
         cudaError_t se = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
         if (se != cudaSuccess) {
             delete c;

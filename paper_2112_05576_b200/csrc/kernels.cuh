@@ -213,6 +213,7 @@ struct ScreenArgs {
     int ignore;
     int xg;           // lattice warp tile: xg * 8 columns x (32 / xg) * 8 rows
     int ro;           // region kernel: bound on |lattice offset| of every rotated point
+    int edge;         // smem kernel: zero columns shrunk to fit, windows may need clamping
     // Thetas with a rounding-ambiguous lattice offset (amb[it] > 0) are left
     // to the general kernel (exact fp64 centres): the lattice kernels skip
     // them (item_max = +inf so compaction scans their map), the general kernel

@@ -250,6 +250,8 @@ REGION_CASES = [
     ("ring", 24, 380, 380, (0, 379, 1, 0, 379, 1, 0.0, D(350), D(50)), 1, 0),
     ("cross", 48, 400, 320, (3, 396, 1, 2, 317, 1, 0.0, D(340), D(20)), 5, 0),
     ("l_bracket", 64, 360, 360, (0, 359, 1, 0, 359, 1, 0.0, D(300), D(60)), 3, 1),
+    # plane fits shared memory only with shrunk zero columns -> clamping variant
+    ("l_bracket", 72, 300, 85, (0, 299, 1, 0, 84, 1, 0.0, D(330), D(30)), 3, 0),
     # halo region of a 96 px model exceeds shared memory -> general kernel
     ("l_bracket", 96, 360, 360, (0, 359, 1, 0, 359, 1, 0.0, D(300), D(60)), 3, 0),
 ]
@@ -265,7 +267,7 @@ def test_region_search_bit_exact(ea, oracle, case):
     params = ea.ScoreParams(nb, pol)
     for k in (1, 9):
         got = ea.search_topk(tm, f, grid, params, k=k)
-        assert ea.default_context().stats()["screen_path"] == (2 if size > 64 else 3)
+        assert ea.default_context().stats()["screen_path"] == (2 if size > 90 else 1 if h < 100 else 3)
         want = oracle.search_topk(tm.points, f, grid, params, k)
         assert keys(got) == keys(want)
 
