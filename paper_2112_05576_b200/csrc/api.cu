@@ -867,9 +867,12 @@ struct RefineState {
     int* cnt[2];
 };
 
-RefineState refine_state(ea_ctx* ctx, int k) {
+// slot 0/1: two independent states (batch mode refines image i on the refine
+// stream while image i+1's top level seeds the other one).
+RefineState refine_state(ea_ctx* ctx, int k, int slot = 0) {
     const size_t beam_bytes = sizeof(BeamDev) * (size_t)k;
-    char* b = (char*)ctx->rstate.ensure(sizeof(ea_outcome) + 2 * beam_bytes + 4 * sizeof(int));
+    const size_t one = (sizeof(ea_outcome) + 2 * beam_bytes + 4 * sizeof(int) + 255) & ~(size_t)255;
+    char* b = (char*)ctx->rstate.ensure(2 * one) + one * slot;
     RefineState r;
     r.out = (ea_outcome*)b;
     r.beam[0] = (BeamDev*)(b + sizeof(ea_outcome));
@@ -989,6 +992,8 @@ std::vector<Beam> seeds_to_beam(const std::vector<ea_scored_pose>& seeds) {
 
 void build_working(ea_ctx* ctx, ea_levels* lv, const double* d_level0, int w, int h,
                    int levels);
+void build_working_into(ea_ctx* ctx, std::vector<ea_field*>& fields, DevBuf& image,
+                        const double* d_level0, int w, int h, int levels);
 void set_working_image(ea_ctx* ctx, ea_levels* lv, const double* image, int w, int h,
                        int levels);
 
@@ -1100,9 +1105,23 @@ void detect_batch(ea_ctx* ctx, ea_levels* lv, const double* const* images, int c
     char* dres = (char*)ctx->rslots.ensure(slot * (size_t)count);
     char* hres = (char*)ctx->h_out.ensure(slot * (size_t)count);
     const unsigned long long cap = std::max<unsigned long long>(initial_cap(ctx), 1ull << 20);
+    if (!ctx->refine_stream) EAB_CUDA(cudaStreamCreateWithFlags(&ctx->refine_stream,
+                                                                cudaStreamNonBlocking));
+    for (auto& e : ctx->rev)
+        if (!e) EAB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    // Two working sets (pyramid + fields) and two refinement states: image i
+    // refines on the refine stream from set/state i&1 while image i+1 builds
+    // its pyramid and searches its top level on the compute stream (the
+    // latency-bound refinement kernels fill the SMs the screen kernel leaves).
+    std::vector<ea_field*>* sets[2] = {&lv->fields, &lv->fields2};
+    DevBuf* images_b[2] = {&lv->image, &lv->image2};
+    const int top = L - 1;
+    const ea_pose_grid tg = top_grid_of(cfg);
+    const ea_grid_counts gc = counts_of(tg);
     std::vector<TopLaunch> launches;
     launches.reserve(count);
     sync(ctx);
+    cudaStream_t main_stream = ctx->stream;
     for (int i = 0; i < count; ++i) {
         const int b = i & 1;
         // copy stream: wait until image i-2 released buffer b, then H2D image i
@@ -1110,18 +1129,57 @@ void detect_batch(ea_ctx* ctx, ea_levels* lv, const double* const* images, int c
         EAB_CUDA(cudaMemcpyAsync(raw[b], images[i], img_bytes, cudaMemcpyHostToDevice,
                                  ctx->copy_stream));
         EAB_CUDA(cudaEventRecord(ctx->bev[b], ctx->copy_stream));
-        // compute stream: pyramid + gradients, release the buffer, search
-        EAB_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->bev[b], 0));
-        build_working(ctx, lv, raw[b], w, h, L);
-        EAB_CUDA(cudaEventRecord(ctx->bev[2 + b], ctx->stream));
-        check_search_config(lv, cfg);
+        // compute stream: set b is free once image i-2's refinement is done
+        EAB_CUDA(cudaStreamWaitEvent(main_stream, ctx->bev[b], 0));
+        if (i >= 2) EAB_CUDA(cudaStreamWaitEvent(main_stream, ctx->rev[2 + b], 0));
+        build_working_into(ctx, *sets[b], *images_b[b], raw[b], w, h, L);
+        EAB_CUDA(cudaEventRecord(ctx->bev[2 + b], main_stream));
+        ea_levels view;  // template side + working set b (not owned)
+        view.models = lv->models;
+        view.fields = *sets[b];
+        struct Release {
+            ea_levels& v;
+            ~Release() {
+                v.models.clear();
+                v.fields.clear();
+            }
+        } release{view};
+        check_search_config(&view, cfg);
         ea_outcome* d_out = (ea_outcome*)(dres + slot * i);
         SearchCtrl* d_ctrl = (SearchCtrl*)(dres + slot * i + sizeof(ea_outcome));
-        launches.push_back(enqueue_levels(ctx, lv, cfg, tables, cap, d_out, d_ctrl));
-        d2h(ctx, hres + slot * i, dres + slot * i, slot);
+        // top level + seeds on the compute stream
+        const TopLaunch t = top_enqueue(ctx, view.models[top], view.fields[top], tg,
+                                        cfg.score_params, cfg.topk, 0, 0, cap);
+        RefineState st = refine_state(ctx, cfg.topk, b);
+        st.out = d_out;
+        EAB_CUDA(cudaMemsetAsync(st.out, 0, sizeof(ea_outcome), main_stream));
+        launch_seed_beam(ctx, t.top_score, t.top_index, &ctx->ctrl.as<SearchCtrl>()->n_out,
+                         seed_args(tg, gc, cfg), st.beam[0], st.cnt[0], st.out);
+        EAB_CUDA(cudaMemcpyAsync(d_ctrl, ctx->ctrl.p, sizeof(SearchCtrl),
+                                 cudaMemcpyDeviceToDevice, main_stream));
+        EAB_CUDA(cudaEventRecord(ctx->rev[b], main_stream));
+        launches.push_back(t);
+        // refinement levels + D2H of the outcome on the refine stream
+        EAB_CUDA(cudaStreamWaitEvent(ctx->refine_stream, ctx->rev[b], 0));
+        ctx->stream = ctx->refine_stream;
+        try {
+            if (top > 0) refine_enqueue(ctx, &view, cfg, tg, tables, st);
+            d2h(ctx, hres + slot * i, dres + slot * i, slot);
+        } catch (...) {
+            ctx->stream = main_stream;
+            throw;
+        }
+        ctx->stream = main_stream;
+        EAB_CUDA(cudaEventRecord(ctx->rev[2 + b], ctx->refine_stream));
     }
     sync(ctx);
+    EAB_CUDA(cudaStreamSynchronize(ctx->refine_stream));
     EAB_CUDA(cudaStreamSynchronize(ctx->copy_stream));
+    if ((count - 1) & 1) {  // keep "the working side is the last image's"
+        std::swap(lv->fields, lv->fields2);
+        std::swap(lv->image.p, lv->image2.p);
+        std::swap(lv->image.cap, lv->image2.cap);
+    }
     for (int i = 0; i < count; ++i) {
         SearchCtrl hc;
         std::memcpy(&hc, hres + slot * i + sizeof(ea_outcome), sizeof hc);
@@ -1303,37 +1361,42 @@ void free_levels(ea_levels* lv) {
     if (!lv) return;
     for (auto* m : lv->models) delete m;
     for (auto* f : lv->fields) delete f;
+    for (auto* f : lv->fields2) delete f;
     delete lv;
 }
 
 // Working side from a level-0 image already on the device: pyramid levels
 // 1.. into lv->image, Sobel field per level (gradient.cpp:12-27).
-void build_working(ea_ctx* ctx, ea_levels* lv, const double* d_level0, int w, int h,
-                   int levels) {
+void build_working_into(ea_ctx* ctx, std::vector<ea_field*>& fields, DevBuf& image,
+                        const double* d_level0, int w, int h, int levels) {
     if (w < 1 || h < 1) {
         fail(EA_ERR_SIZE, "image dimensions must be at least 1x1, got " + std::to_string(w) + "x" +
                               std::to_string(h));
     }
     const size_t elems = pyramid_elems(w / 2, h / 2, std::max(levels - 1, 1));
-    double* d = (double*)lv->image.ensure(sizeof(double) * (elems ? elems : 1));
+    double* d = (double*)image.ensure(sizeof(double) * (elems ? elems : 1));
     std::vector<const double*> srcs;
     std::vector<int> dims;
     device_pyramid_from(ctx, d_level0, d, w, h, levels, &srcs, &dims);
     for (int l = 0; l < levels; ++l) {  // reuse field objects when dims match
         const int lw = dims[2 * l], lh = dims[2 * l + 1];
-        if (l < (int)lv->fields.size() &&
-            (lv->fields[l]->width != lw || lv->fields[l]->height != lh)) {
-            delete lv->fields[l];
-            lv->fields[l] = nullptr;
+        if (l < (int)fields.size() && (fields[l]->width != lw || fields[l]->height != lh)) {
+            delete fields[l];
+            fields[l] = nullptr;
         }
-        if (l >= (int)lv->fields.size()) lv->fields.push_back(nullptr);
-        if (!lv->fields[l]) lv->fields[l] = new_field(lw, lh);
-        sobel_into(ctx, srcs[l], lw, lh, lv->fields[l]);
+        if (l >= (int)fields.size()) fields.push_back(nullptr);
+        if (!fields[l]) fields[l] = new_field(lw, lh);
+        sobel_into(ctx, srcs[l], lw, lh, fields[l]);
     }
-    while ((int)lv->fields.size() > levels) {
-        delete lv->fields.back();
-        lv->fields.pop_back();
+    while ((int)fields.size() > levels) {
+        delete fields.back();
+        fields.pop_back();
     }
+}
+
+void build_working(ea_ctx* ctx, ea_levels* lv, const double* d_level0, int w, int h,
+                   int levels) {
+    build_working_into(ctx, lv->fields, lv->image, d_level0, w, h, levels);
 }
 
 void set_working_image(ea_ctx* ctx, ea_levels* lv, const double* image, int w, int h,
@@ -1410,7 +1473,10 @@ void ea_ctx_destroy(ea_ctx* ctx) {
         if (e) cudaEventDestroy(e);
     for (auto& e : ctx->bev)
         if (e) cudaEventDestroy(e);
+    for (auto& e : ctx->rev)
+        if (e) cudaEventDestroy(e);
     if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
+    if (ctx->refine_stream) cudaStreamDestroy(ctx->refine_stream);
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
     if (prev >= 0) cudaSetDevice(prev);

@@ -109,6 +109,8 @@ struct ea_levels {
     std::vector<ea_field*> fields;  // owned; may be empty until set_image
     eab::DevBuf image;              // working pyramid levels >= 1
     eab::DevBuf raw[2];             // level-0 images (double-buffered in batch mode)
+    std::vector<ea_field*> fields2; // batch mode: second working set (owned)
+    eab::DevBuf image2;
 };
 
 struct ea_ctx {
@@ -132,8 +134,10 @@ struct ea_ctx {
     std::vector<double> ttab_key;
     std::vector<size_t> ttab_off;
     eab::DevBuf ttab, rstate, rslots;
-    cudaStream_t copy_stream = nullptr;  // batch-mode H2D
+    cudaStream_t copy_stream = nullptr;    // batch-mode H2D
+    cudaStream_t refine_stream = nullptr;  // batch-mode refinement
     cudaEvent_t bev[4] = {nullptr, nullptr, nullptr, nullptr};
+    cudaEvent_t rev[4] = {nullptr, nullptr, nullptr, nullptr};  // seeds ready / refine done
 };
 
 namespace eab {
