@@ -96,6 +96,42 @@ void launch_rotate(ea_ctx* ctx, const double* pts_soa, int n, const double* cs, 
 
 // ---- 2. screening ------------------------------------------------------------
 
+// 1D bulk copy global -> shared through the TMA engine, completing on an
+// mbarrier (cp.async.bulk + mbarrier expect_tx; sizes multiple of 16 B).
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_copy_to_smem(void* dst, const void* src, unsigned bytes,
+                                                  unsigned long long* bar) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+    constexpr unsigned kChunk = 32768;
+    for (unsigned off = 0; off < bytes; off += kChunk) {
+        const unsigned len = bytes - off < kChunk ? bytes - off : kChunk;
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, "
+            "[%3];" ::"r"(smem_u32(static_cast<char*>(dst) + off)),
+            "l"(static_cast<const char*>(src) + off), "r"(len), "r"(smem_u32(bar))
+            : "memory");
+    }
+}
+__device__ __forceinline__ void mbar_wait_parity(unsigned long long* bar, unsigned parity) {
+    unsigned done = 0;
+    while (!done) {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+            " selp.u32 %0, 1, 0, p;\n}"
+            : "=r"(done)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+    }
+}
+
 __device__ __forceinline__ float fmax3(float a, float b, float c) {
     float r;
     asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
@@ -483,15 +519,18 @@ __global__ void __launch_bounds__(THREADS, 1)
     unsigned* hist = reinterpret_cast<unsigned*>(smem);
     float2* P = reinterpret_cast<float2*>(smem + kHistBins * sizeof(unsigned));
     __shared__ float wtop_all[16][kFloorK];
+    __shared__ __align__(8) unsigned long long plane_bar;
     float* wtop = wtop_all[threadIdx.x >> 5];
     if ((threadIdx.x & 31) < kFloorK) wtop[threadIdx.x & 31] = -INFINITY;
-    {
-        const int4* src = reinterpret_cast<const int4*>(a.plane);
-        int4* dst = reinterpret_cast<int4*>(P);
-        for (int i = threadIdx.x; i < vec16; i += blockDim.x) dst[i] = __ldg(src + i);
-        for (int i = threadIdx.x; i < kHistBins; i += blockDim.x) hist[i] = 0u;
+    // The plane arrives by bulk copy (TMA engine, one thread issues it) while
+    // the threads clear the histogram.
+    if (threadIdx.x == 0) {
+        mbar_init(&plane_bar, 1);
+        bulk_copy_to_smem(P, a.plane, (unsigned)vec16 * 16u, &plane_bar);
     }
+    for (int i = threadIdx.x; i < kHistBins; i += blockDim.x) hist[i] = 0u;
     __syncthreads();
+    mbar_wait_parity(&plane_bar, 0);
 
     constexpr int NACC = S * kTW;
     const int lane = threadIdx.x & 31;
