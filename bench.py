@@ -6,9 +6,10 @@ Metric (BASELINE.json): pose-evals/s = top-level poses x top-level model points
 per second of top-level search, plus detect latency per image.  One JSON line
 on rank 0.  See DESIGN.md "Measurement" for every field.
 
-  value   top-level search with the working pyramid resident in HBM (search
-          call of the product C-ABI: screen + band select + exact fp64 verify
-          + top-k [+ NCCL all-gather of per-GPU top-k for N > 1]), L2 flushed
+  value   top-level search with the working pyramid resident in HBM and the
+          results left in HBM (ea_search_top_slab_async: screen + band select +
+          exact fp64 verify + top-k rows [+ NCCL all-gather of per-GPU rows and
+          device merge for N > 1]), steps enqueued back to back, L2 flushed
           between steps, CUDA events on the library's stream, max over ranks.
   e2e     the same metric through the public detect call with a HOST image:
           H2D of the level-0 image from pinned memory, device pyramid + Sobel,
@@ -335,7 +336,10 @@ def bench_ours(args, rank, world, local_rank):
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    stream = torch.cuda.current_stream(dev)
+    # One non-default stream shared by torch (L2 flush, events, NCCL) and the
+    # library, so device-resident steps are ordered without host syncs.
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
     ctx = ea.Context(local_rank)
     ctx.set_stream(stream.cuda_stream)
     ctx.set_timing(True)
@@ -358,19 +362,16 @@ def bench_ours(args, rank, world, local_rank):
     it0, it1 = parallel.theta_slab(nt, rank, world)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
 
-    def gather(seeds):
-        if world == 1:
-            return seeds
-        return parallel.gather_topk(seeds, cfg.topk, device=dev)
-
-    step_screen = []
+    k = cfg.topk
+    rows = [torch.empty((k, 5), dtype=torch.float64, device=dev) for _ in dets]
 
     def top_step():
+        """One top-level search per model (cfg5: 8), device-resident: slab
+        search -> k rows in HBM -> (N > 1) NCCL all-gather + device merge."""
         out = []
-        step_screen.clear()
-        for d in dets:  # one top-level search per model (cfg5: 8)
-            out.append(gather(ea.search_top_slab(d.levels, cfg, it0, it1)))
-            step_screen.append(ctx.stats()["screen_ms"])
+        for d, r in zip(dets, rows):
+            ea.search_top_slab_async(d.levels, cfg, it0, it1, r.data_ptr())
+            out.append(parallel.gather_rows_device(r, k, ctx) if world > 1 else r)
         return out
 
     def barrier():
@@ -379,23 +380,29 @@ def bench_ours(args, rank, world, local_rank):
         torch.cuda.synchronize(dev)
 
     # ---- value: device-resident top-level search --------------------------------------
+    # Steps are enqueued back to back (no host round trip inside the timed
+    # region: results stay in HBM, as in the multi-GPU data path); the L2
+    # flush sits between one step's end event and the next step's start.
     for _ in range(args.warmup):
         top_step()
     barrier()
+    ea.async_status(ctx)  # reset the overflow flag and the kernel-time ring
     launches0 = ctx.kernel_launches()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]
-    screen_ms, seeds = [], None
     with ClockSampler(local_rank) as clk:
         for i in range(args.steps):
             flush.zero_()
             ev[i][0].record(stream)
-            seeds = top_step()
+            top_step()
             ev[i][1].record(stream)
-            screen_ms.append(sum(step_screen))
         barrier()
     launches = ctx.kernel_launches() - launches0
-    st = ctx.stats()
+    overflowed, times = ea.async_status(ctx)
+    if overflowed:
+        raise RuntimeError("candidate buffer overflow in the device-resident search")
+    per_step = len(dets)
+    screen_ms = [sum(times[i:i + per_step]) for i in range(0, len(times) - per_step + 1, per_step)]
     step_ms = [a.elapsed_time(b) for a, b in ev]
     tot_ms = sum(step_ms)
     if world > 1:
@@ -462,6 +469,7 @@ def bench_ours(args, rank, world, local_rank):
             st_d = ctx.stats()
             phases.append((st_d["image_ms"], st_d["top_ms"], st_d["refine_ms"]))
 
+    st = ctx.stats()  # the last detect's top-level search
     if rank != 0:
         return
     peaks, peak_src = measured_peaks()

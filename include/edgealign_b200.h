@@ -324,6 +324,23 @@ ea_status ea_search_levels(ea_ctx* ctx, const ea_levels* lv, const ea_search_con
 ea_status ea_search_top_slab(ea_ctx* ctx, const ea_levels* lv,
                              const ea_search_config* cfg, uint64_t it_begin,
                              uint64_t it_end, ea_scored_pose* seeds, int* n_seeds);
+/* Device-resident form of ea_search_top_slab (the multi-GPU data path):
+ * enqueued on the context's stream, no host sync.  Writes k rows of five
+ * doubles {score, grid_index, ux, uy, theta} to device memory d_rows (rows
+ * past the count have a NaN score) -- the layout all-gathered over NCCL. */
+ea_status ea_search_top_slab_async(ea_ctx* ctx, const ea_levels* lv,
+                                   const ea_search_config* cfg, uint64_t it_begin,
+                                   uint64_t it_end, double* d_rows);
+/* The `better` merge (search.cpp:130-139) of n_rows device rows into k
+ * device rows, enqueued on the context's stream. */
+ea_status ea_merge_rows_async(ea_ctx* ctx, const double* d_rows, int n_rows, int k,
+                              double* d_out);
+/* Synchronises the context; *overflowed = 1 if an async search since the
+ * last call admitted more candidates than its buffer (its rows are then
+ * unreliable: rerun with ea_search_top_slab); screen_ms[0..*n_times) = the
+ * screening-kernel times of the timed searches since the last call. */
+ea_status ea_ctx_async_status(ea_ctx* ctx, int* overflowed, float* screen_ms, int cap,
+                              int* n_times);
 ea_status ea_refine(ea_ctx* ctx, const ea_levels* lv, const ea_search_config* cfg,
                     const ea_scored_pose* seeds, int n_seeds, ea_outcome* out);
 /* coarse_to_fine  search.cpp:359-364 */

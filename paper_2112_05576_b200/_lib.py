@@ -91,6 +91,10 @@ _SIGS = {
     "ea_search_levels": (C.c_int, [_P, _P, C.POINTER(abi.SearchConfig), C.POINTER(abi.Outcome)]),
     "ea_search_top_slab": (C.c_int, [_P, _P, C.POINTER(abi.SearchConfig), C.c_uint64,
                                      C.c_uint64, C.POINTER(abi.ScoredPose), _ip]),
+    "ea_search_top_slab_async": (C.c_int, [_P, _P, C.POINTER(abi.SearchConfig), C.c_uint64,
+                                           C.c_uint64, C.c_void_p]),
+    "ea_merge_rows_async": (C.c_int, [_P, C.c_void_p, C.c_int, C.c_int, C.c_void_p]),
+    "ea_ctx_async_status": (C.c_int, [_P, _ip, C.POINTER(C.c_float), C.c_int, _ip]),
     "ea_refine": (C.c_int, [_P, _P, C.POINTER(abi.SearchConfig), C.POINTER(abi.ScoredPose),
                             C.c_int, C.POINTER(abi.Outcome)]),
     "ea_coarse_to_fine": (C.c_int, [_P, C.POINTER(_dp), _ip, C.c_int, C.POINTER(_dp), _ip,

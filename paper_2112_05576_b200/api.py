@@ -487,6 +487,29 @@ def search_top_slab(levels, config, it_begin, it_end):
     return list(out[: n.value])
 
 
+def search_top_slab_async(levels, config, it_begin, it_end, d_rows):
+    """Device-resident slab search: k rows {score, index, ux, uy, theta}
+    (float64) written to the device address `d_rows` on the context's stream;
+    no host sync (ea_search_top_slab_async)."""
+    _check(lib().ea_search_top_slab_async(levels.ctx.handle, levels.handle, C.byref(config),
+                                          C.c_uint64(it_begin), C.c_uint64(it_end),
+                                          C.c_void_p(int(d_rows))))
+
+
+def merge_rows_async(ctx, d_rows, n_rows, k, d_out):
+    """`better` merge of n_rows device rows into k device rows (no sync)."""
+    _check(lib().ea_merge_rows_async(ctx.handle, C.c_void_p(int(d_rows)), int(n_rows), int(k),
+                                     C.c_void_p(int(d_out))))
+
+
+def async_status(ctx, cap=4096):
+    """Sync; -> (overflowed, [screen-kernel ms of the timed searches since the last call])."""
+    of, n = C.c_int(), C.c_int()
+    times = (C.c_float * cap)()
+    _check(lib().ea_ctx_async_status(ctx.handle, C.byref(of), times, cap, C.byref(n)))
+    return bool(of.value), [times[i] for i in range(n.value)]
+
+
 def refine(levels, config, seeds):
     arr = (ScoredPose * max(len(seeds), 1))(*seeds)
     out = Outcome()

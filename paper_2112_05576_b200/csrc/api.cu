@@ -323,12 +323,16 @@ ScreenPlan screen(ea_ctx* ctx, const ea_model* m, const ea_field* f, const ea_po
         launch_rotate(ctx, m->pts.as<double>(), n, d_cs, (int)nth, rot, scr, amb + 2 * nth + 2,
                       amb);
         launch_schedule(ctx, scr, n, (int)nth, sched);
+        // once per model and slab: does any theta need the general kernel?
+        int n_flagged = 0;
+        d2h(ctx, &n_flagged, amb + nth, sizeof n_flagged);
+        sync(ctx);
+        mm->n_flagged = n_flagged;
         mm->tab_key = key;
     }
     SearchCtrl* ctrl = (SearchCtrl*)ctx->ctrl.ensure(sizeof(SearchCtrl));
     unsigned* hist = (unsigned*)ctx->hist.ensure(sizeof(unsigned) * kHistBins);
-    EAB_CUDA(cudaMemsetAsync(ctrl, 0, sizeof(SearchCtrl), ctx->stream));
-    EAB_CUDA(cudaMemsetAsync(hist, 0, sizeof(unsigned) * kHistBins, ctx->stream));
+    // (both cleared by the plane kernel below)
     plan.rot = rot;
     plan.flags = amb + 2 * nth + 2;
 
@@ -394,8 +398,8 @@ ScreenPlan screen(ea_ctx* ctx, const ea_model* m, const ea_field* f, const ea_po
     }
     const PlaneGeom geom = plane_geom(f->width, f->height, shift, PL, PR, elem);
     void* plane = ctx->plane.ensure(geom.bytes());
-    EAB_CUDA(cudaMemsetAsync(plane, 0, geom.bytes(), ctx->stream));
-    launch_plane(ctx, f, p.eps_mag, geom, plane, &ctrl->ring_bad);
+    launch_plane(ctx, f, p.eps_mag, geom, plane, hist, kHistBins,
+                 reinterpret_cast<unsigned*>(ctrl), (int)(sizeof(SearchCtrl) / sizeof(unsigned)));
     float* map = (float*)ctx->map.ensure(sizeof(float) * (plan.slab_poses ? plan.slab_poses : 1));
     float* item_max =
         (float*)ctx->item_max.ensure(sizeof(float) * (plan.slab_poses / 32 + plan.it_count * 64 + 64));
@@ -433,13 +437,21 @@ ScreenPlan screen(ea_ctx* ctx, const ea_model* m, const ea_field* f, const ea_po
     a.hist = hist;
     a.ctrl = ctrl;
     plan.fast = false;
-    if (ctx->timing) EAB_CUDA(cudaEventRecord(ctx->ev[1], ctx->stream));
+    if (ctx->timing) {
+        EAB_CUDA(cudaEventRecord(ctx->ev[1], ctx->stream));
+        EAB_CUDA(cudaEventRecord(ctx->tev[2 * ctx->tev_next], ctx->stream));
+    }
     if (plan.slab_poses) {
         if (lattice) plan.fast = region ? launch_screen_region(ctx, a) : launch_screen_fast(ctx, a);
-        if (plan.fast) launch_screen_flagged(ctx, a);  // thetas the lattice kernel skipped
-        else launch_screen_general(ctx, a);
+        if (!plan.fast) launch_screen_general(ctx, a);
+        else if (mm->n_flagged > 0) launch_screen_flagged(ctx, a);  // thetas the lattice kernel skipped
     }
-    if (ctx->timing) EAB_CUDA(cudaEventRecord(ctx->ev[2], ctx->stream));
+    if (ctx->timing) {
+        EAB_CUDA(cudaEventRecord(ctx->ev[2], ctx->stream));
+        EAB_CUDA(cudaEventRecord(ctx->tev[2 * ctx->tev_next + 1], ctx->stream));
+        ctx->tev_next = (ctx->tev_next + 1) % ea_ctx::kTimeRing;
+        ctx->tev_pending = std::min(ctx->tev_pending + 1, ea_ctx::kTimeRing);
+    }
     ctx->stats.screen_path = plan.fast ? (region ? 3 : 1) : 2;
     plan.items = screen_items(a, plan.fast);
     return plan;
@@ -1475,6 +1487,8 @@ void ea_ctx_destroy(ea_ctx* ctx) {
         if (e) cudaEventDestroy(e);
     for (auto& e : ctx->rev)
         if (e) cudaEventDestroy(e);
+    for (auto& e : ctx->tev)
+        if (e) cudaEventDestroy(e);
     if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
     if (ctx->refine_stream) cudaStreamDestroy(ctx->refine_stream);
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
@@ -1524,6 +1538,7 @@ ea_status ea_ctx_set_timing(ea_ctx* ctx, int on) {
         DeviceGuard dg(ctx->device);
         if (on && !ctx->ev[0]) {
             for (auto& e : ctx->ev) EAB_CUDA(cudaEventCreate(&e));
+            for (auto& e : ctx->tev) EAB_CUDA(cudaEventCreate(&e));
         }
         ctx->timing = on != 0;
     });
@@ -2152,6 +2167,76 @@ ea_status ea_search_top_slab(ea_ctx* ctx, const ea_levels* lv, const ea_search_c
                                   cfg->score_params, cfg->topk, it_begin, it_end);
         for (size_t i = 0; i < r.size(); ++i) seeds[i] = r[i];
         *n_seeds = (int)r.size();
+    });
+}
+
+ea_status ea_search_top_slab_async(ea_ctx* ctx, const ea_levels* lv,
+                                   const ea_search_config* cfg, uint64_t it_begin,
+                                   uint64_t it_end, double* d_rows) {
+    return guard([&] {
+        need(ctx, "ctx");
+        need(lv, "levels");
+        need(cfg, "config");
+        need(d_rows, "d_rows");
+        check_search_config(lv, *cfg);
+        DeviceGuard dg(ctx->device);
+        const int top = cfg->num_levels - 1;
+        if (it_end == 0) it_end = 1;
+        const ea_pose_grid tg = top_grid_of(*cfg);
+        const ea_grid_counts c = counts_of(tg);
+        if (!ctx->async_flag.p) {
+            ctx->async_flag.ensure(sizeof(int));
+            EAB_CUDA(cudaMemsetAsync(ctx->async_flag.p, 0, sizeof(int), ctx->stream));
+        }
+        // a generous candidate buffer: the band is checked on the device and
+        // reported by ea_ctx_async_status
+        const unsigned long long cap = std::max<unsigned long long>(initial_cap(ctx), 1ull << 20);
+        const TopLaunch t = top_enqueue(ctx, lv->models[top], lv->fields[top], tg,
+                                        cfg->score_params, cfg->topk, it_begin, it_end, cap);
+        RowGrid g{tg.x0, tg.dx, tg.y0, tg.dy, tg.t0, tg.dt, c.nx, c.ny};
+        launch_topk_rows(ctx, t.top_score, t.top_index, ctx->ctrl.as<SearchCtrl>(), cap,
+                         cfg->topk, g, d_rows, ctx->async_flag.as<int>());
+    });
+}
+
+ea_status ea_merge_rows_async(ea_ctx* ctx, const double* d_rows, int n_rows, int k,
+                              double* d_out) {
+    return guard([&] {
+        need(ctx, "ctx");
+        need(d_rows, "d_rows");
+        need(d_out, "d_out");
+        if (k < 1) fail(EA_ERR_INVALID_ARGUMENT, "topk must be >= 1");
+        if (n_rows < 0 || n_rows > 8192) fail(EA_ERR_INVALID_ARGUMENT, "0 <= n_rows <= 8192");
+        DeviceGuard dg(ctx->device);
+        launch_merge_rows(ctx, d_rows, n_rows, k, d_out);
+    });
+}
+
+ea_status ea_ctx_async_status(ea_ctx* ctx, int* overflowed, float* screen_ms, int cap,
+                              int* n_times) {
+    return guard([&] {
+        need(ctx, "ctx");
+        DeviceGuard dg(ctx->device);
+        sync(ctx);
+        int of = 0;
+        if (ctx->async_flag.p) {
+            EAB_CUDA(cudaMemcpy(&of, ctx->async_flag.p, sizeof of, cudaMemcpyDeviceToHost));
+            EAB_CUDA(cudaMemset(ctx->async_flag.p, 0, sizeof(int)));
+        }
+        if (overflowed) *overflowed = of;
+        int n = 0;
+        if (ctx->timing) {
+            const int pend = ctx->tev_pending;
+            for (int q = 0; q < pend && n < cap; ++q) {
+                const int slot = (ctx->tev_next - pend + q + ea_ctx::kTimeRing) % ea_ctx::kTimeRing;
+                float ms = 0.f;
+                EAB_CUDA(cudaEventElapsedTime(&ms, ctx->tev[2 * slot], ctx->tev[2 * slot + 1]));
+                if (screen_ms) screen_ms[n] = ms;
+                ++n;
+            }
+            ctx->tev_pending = 0;
+        }
+        if (n_times) *n_times = n;
     });
 }
 

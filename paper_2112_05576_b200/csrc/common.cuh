@@ -102,6 +102,7 @@ struct ea_model {
     // detect per image).  Written on the owning context's stream.
     std::vector<double> tab_key;
     eab::DevBuf rot, scr, amb, sched;
+    int n_flagged = 0;  // flagged thetas of the cached slab
 };
 
 struct ea_levels {
@@ -138,6 +139,12 @@ struct ea_ctx {
     cudaStream_t refine_stream = nullptr;  // batch-mode refinement
     cudaEvent_t bev[4] = {nullptr, nullptr, nullptr, nullptr};
     cudaEvent_t rev[4] = {nullptr, nullptr, nullptr, nullptr};  // seeds ready / refine done
+    // async (device-resident) searches: overflow flag and a ring of screen
+    // kernel event pairs read back by ea_ctx_async_status
+    eab::DevBuf async_flag;
+    static constexpr int kTimeRing = 64;
+    cudaEvent_t tev[2 * kTimeRing] = {};
+    int tev_next = 0, tev_pending = 0;
 };
 
 namespace eab {

@@ -58,29 +58,27 @@ __global__ void sobel_kernel(const double* __restrict__ img, int w, int h,
 // (yp >> shift) for conflict-free lane strides (see search_kernels.cu).
 // n = (gx/mag, gy/mag) rounded to fp32 when mag >= eps, else (0, 0) -- the
 // latter gives exactly the reference's neutral 0 vote (kernels_scalar.cpp:44-47).
-// Also records whether the field's own outer ring votes 0 everywhere, which
-// is what makes the zero ring equivalent to the reference's window clipping.
-// The fp16 variant rounds g/|g| from fp64 directly to half (one rounding,
-// |error| <= 2^-11 |n| per component; the screening bound accounts for it).
-template <typename PX>
-__device__ __forceinline__ PX make_px(double nx, double ny);
-template <>
-__device__ __forceinline__ float2 make_px<float2>(double nx, double ny) {
-    return make_float2((float)nx, (float)ny);
-}
-template <>
-__device__ __forceinline__ __half2 make_px<__half2>(double nx, double ny) {
-    return __halves2half2(__double2half(nx), __double2half(ny));
-}
-
-template <typename PX>
+// One launch writes every element a screening kernel reads: field pixels,
+// the zero ring and zero columns, and the zero strip that stands in for
+// off-plane rows (so the buffer needs no memset); block (0, 0) also clears
+// the search's histogram and control block (`clear`, `clear2`).
 __global__ void plane_kernel(const double* __restrict__ gx, const double* __restrict__ gy,
-                             const double* __restrict__ mag, int W, int H, double eps,
-                             int PW, int PL, int shift, PX* __restrict__ plane,
-                             int* __restrict__ ring_bad) {
+                             const double* __restrict__ mag, int W, int H, double eps, int PW,
+                             int PL, int shift, int zero, int zero_len,
+                             float2* __restrict__ plane, unsigned* __restrict__ clear,
+                             int clear_words, unsigned* __restrict__ clear2, int clear2_words) {
     const int xp = blockIdx.x * blockDim.x + threadIdx.x;
     const int yp = blockIdx.y;
-    if (xp >= PW || yp >= H + 2) return;
+    if (blockIdx.x == 0 && blockIdx.y == 0) {
+        for (int i = threadIdx.x; i < clear_words; i += blockDim.x) clear[i] = 0u;
+        for (int i = threadIdx.x; i < clear2_words; i += blockDim.x) clear2[i] = 0u;
+    }
+    if (yp == H + 2) {  // the zero strip
+        for (int i = xp; i < zero_len; i += gridDim.x * blockDim.x)
+            plane[zero + i] = make_float2(0.f, 0.f);
+        return;
+    }
+    if (xp >= PW) return;
     double nx = 0.0, ny = 0.0;
     const int x = xp - 1 - PL, y = yp - 1;
     if (x >= 0 && x < W && y >= 0 && y < H) {
@@ -89,10 +87,9 @@ __global__ void plane_kernel(const double* __restrict__ gx, const double* __rest
         if (m >= eps) {
             nx = __ddiv_rn(gx[o], m);
             ny = __ddiv_rn(gy[o], m);
-            if (x == 0 || y == 0 || x == W - 1 || y == H - 1) atomicOr(ring_bad, 1);
         }
     }
-    plane[(size_t)yp * PW + (yp >> shift) + xp] = make_px<PX>(nx, ny);
+    plane[(size_t)yp * PW + (yp >> shift) + xp] = make_float2((float)nx, (float)ny);
 }
 
 void launch_downsample(ea_ctx* ctx, const double* in, int w, int h, double* out) {
@@ -113,17 +110,14 @@ void launch_sobel(ea_ctx* ctx, const double* img, int w, int h, double* gx, doub
 }
 
 void launch_plane(ea_ctx* ctx, const ea_field* f, double eps, const PlaneGeom& g,
-                  void* plane, int* ring_bad) {
-    dim3 grid((g.PW + 127) / 128, g.H + 2);
-    if (g.elem_bytes == 4) {
-        plane_kernel<__half2><<<grid, 128, 0, ctx->stream>>>(
-            f->gx(), f->gy(), f->mag(), g.W, g.H, eps, g.PW, g.PL, g.shift,
-            static_cast<__half2*>(plane), ring_bad);
-    } else {
-        plane_kernel<float2><<<grid, 128, 0, ctx->stream>>>(
-            f->gx(), f->gy(), f->mag(), g.W, g.H, eps, g.PW, g.PL, g.shift,
-            static_cast<float2*>(plane), ring_bad);
-    }
+                  void* plane, unsigned* clear, int clear_words, unsigned* clear2,
+                  int clear2_words) {
+    dim3 grid((g.PW + 127) / 128, g.H + 3);  // + one row of blocks for the zero strip
+    plane_kernel<<<grid, 128, 0, ctx->stream>>>(f->gx(), f->gy(), f->mag(), g.W, g.H, eps,
+                                                 g.PW, g.PL, g.shift, g.zero,
+                                                 (int)(g.elems - (size_t)g.zero),
+                                                 static_cast<float2*>(plane), clear,
+                                                 clear_words, clear2, clear2_words);
     check_launch("plane_kernel");
     count_launch(ctx);
 }

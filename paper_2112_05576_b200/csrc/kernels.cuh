@@ -56,7 +56,7 @@ struct SearchCtrl {
     unsigned long long work_counter;  // dynamic work distribution of the screen kernel
     unsigned long long cand_count;    // poses admitted by the band threshold
     unsigned long long needed;        // histogram upper bound of cand_count
-    int ring_bad;                     // field border ring has mag >= eps somewhere
+    int _unused;
     int flags;                        // rounding-ambiguous (theta, point) pairs
     float thr;                        // band threshold on the fp32 screen score
     int n_out;                        // entries written to the top-k output
@@ -182,8 +182,12 @@ __device__ __forceinline__ double lattice(double base, unsigned long long i, dou
 void launch_downsample(ea_ctx* ctx, const double* in, int w, int h, double* out);
 void launch_sobel(ea_ctx* ctx, const double* img, int w, int h, double* gx, double* gy,
                   double* mag);
+// Screening plane (float2 g/|g|, zero ring/columns/strip) + clears
+// clear[0 .. clear_words) and clear2[0 .. clear2_words) (the search's
+// histogram and control block).
 void launch_plane(ea_ctx* ctx, const ea_field* f, double eps, const PlaneGeom& g,
-                  void* plane, int* ring_bad);
+                  void* plane, unsigned* clear, int clear_words, unsigned* clear2,
+                  int clear2_words);
 
 // rotate_model for many thetas: rot_exact = px|py|dx|dy (each nth*n doubles),
 // rot_screen = {ox, oy, dxf, dyf} per (theta, point) for the lattice kernel.
@@ -278,6 +282,17 @@ void launch_select(ea_ctx* ctx, const unsigned* cand, const double* score,
                    SearchCtrl* ctrl, unsigned long long cap, int k,
                    unsigned long long index_base, double* out_score,
                    unsigned long long* out_index);
+// Device-resident top-k rows {score, index, ux, uy, theta} (f64 x 5) of a
+// search (pose_at on the device) + overflow flag; and the `better` merge of
+// n such rows into k.
+struct RowGrid {
+    double x0, dx, y0, dy, t0, dt;
+    unsigned long long nx, ny;
+};
+void launch_topk_rows(ea_ctx* ctx, const double* score, const unsigned long long* index,
+                      const SearchCtrl* ctrl, unsigned long long cap, int k, const RowGrid& g,
+                      double* rows, int* overflow);
+void launch_merge_rows(ea_ctx* ctx, const double* in, int n, int k, double* out);
 // Dense exact map (score_map search.cpp:169-202).
 void launch_exact_map(ea_ctx* ctx, const ExactArgs& a, unsigned long long total, double* out);
 

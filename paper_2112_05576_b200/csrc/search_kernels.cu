@@ -1391,6 +1391,78 @@ void launch_select(ea_ctx* ctx, const unsigned* cand, const double* score, Searc
     count_launch(ctx);
 }
 
+// ---- device-resident top-k rows (multi-GPU data path) ------------------------
+// Row = {score, grid_index, ux, uy, theta} as five doubles (grid indices are
+// < 2^53, so exact); rows past the count carry a NaN score.  The same layout
+// is all-gathered over NCCL and merged on the device.
+__global__ void topk_rows_kernel(const double* __restrict__ score,
+                                 const unsigned long long* __restrict__ index,
+                                 const SearchCtrl* __restrict__ ctrl, unsigned long long cap,
+                                 int k, RowGrid g, double* __restrict__ rows, int* overflow) {
+    const int n = ctrl->n_out;
+    if (threadIdx.x == 0 && ctrl->cand_count > cap) atomicOr(overflow, 1);
+    const unsigned long long plane = g.nx * g.ny;
+    for (int r = threadIdx.x; r < k; r += blockDim.x) {
+        double* o = rows + 5 * (size_t)r;
+        if (r < n) {
+            const unsigned long long idx = index[r];
+            const unsigned long long it = idx / plane, rem = idx % plane;
+            o[0] = score[r];
+            o[1] = (double)idx;
+            o[2] = lattice(g.x0, rem % g.nx, g.dx);  // pose_at, pose.h:84-91
+            o[3] = lattice(g.y0, rem / g.nx, g.dy);
+            o[4] = lattice(g.t0, it, g.dt);
+        } else {
+            o[0] = __longlong_as_double(0x7ff8000000000000LL);  // NaN: empty row
+            o[1] = o[2] = o[3] = o[4] = 0.0;
+        }
+    }
+}
+
+// The `better` merge of several slabs' rows (search.cpp:130-139): rank of
+// each valid row among all valid rows by (score desc, index asc); rows with
+// rank < k land at their rank, the rest of the output is NaN rows.
+__global__ void __launch_bounds__(256) merge_rows_kernel(const double* __restrict__ in, int n,
+                                                         int k, double* __restrict__ out) {
+    extern __shared__ long long mk[];  // order key | index per input row
+    long long* key = mk;
+    unsigned long long* idx = reinterpret_cast<unsigned long long*>(mk + n);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const double sc = in[5 * (size_t)i];
+        key[i] = sc != sc ? LLONG_MIN : order_key(sc);
+        idx[i] = (unsigned long long)in[5 * (size_t)i + 1];
+    }
+    for (int r = threadIdx.x; r < k; r += blockDim.x) {
+        double* o = out + 5 * (size_t)r;
+        o[0] = __longlong_as_double(0x7ff8000000000000LL);
+        o[1] = o[2] = o[3] = o[4] = 0.0;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        if (key[i] == LLONG_MIN) continue;
+        int rank = 0;
+        for (int j = 0; j < n; ++j)
+            rank += key[j] > key[i] || (key[j] == key[i] && key[j] != LLONG_MIN &&
+                                        (idx[j] < idx[i] || (idx[j] == idx[i] && j < i)));
+        if (rank < k)
+            for (int c = 0; c < 5; ++c) out[5 * (size_t)rank + c] = in[5 * (size_t)i + c];
+    }
+}
+
+void launch_topk_rows(ea_ctx* ctx, const double* score, const unsigned long long* index,
+                      const SearchCtrl* ctrl, unsigned long long cap, int k, const RowGrid& g,
+                      double* rows, int* overflow) {
+    topk_rows_kernel<<<1, 64, 0, ctx->stream>>>(score, index, ctrl, cap, k, g, rows, overflow);
+    check_launch("topk_rows_kernel");
+    count_launch(ctx);
+}
+
+void launch_merge_rows(ea_ctx* ctx, const double* in, int n, int k, double* out) {
+    merge_rows_kernel<<<1, 256, (size_t)n * 16, ctx->stream>>>(in, n, k, out);
+    check_launch("merge_rows_kernel");
+    count_launch(ctx);
+}
+
 // ---- dense exact map (score_map) -------------------------------------------------
 __global__ void __launch_bounds__(256) exact_map_kernel(const ExactArgs a,
                                                         unsigned long long total,

@@ -52,3 +52,21 @@ def gather_topk(seeds, k, device=None, group=None):
     out = torch.empty((world * k, ROW), dtype=torch.float64, device=local.device)
     dist.all_gather_into_tensor(out, local, group=group)
     return merge(unpack(out.cpu().numpy()), k)
+
+
+def gather_rows_device(local_rows, k, ctx, group=None):
+    """Device-resident exchange: all-gather every rank's k x 5 float64 rows
+    (a CUDA tensor written by search_top_slab_async) over NCCL and merge them
+    on the device (merge_rows_async).  Returns the merged k x 5 CUDA tensor;
+    nothing touches the host."""
+    import torch
+    import torch.distributed as dist
+
+    from . import api
+
+    world = dist.get_world_size(group)
+    gathered = torch.empty((world * k, ROW), dtype=torch.float64, device=local_rows.device)
+    dist.all_gather_into_tensor(gathered, local_rows, group=group)
+    merged = torch.empty((k, ROW), dtype=torch.float64, device=local_rows.device)
+    api.merge_rows_async(ctx, gathered.data_ptr(), world * k, k, merged.data_ptr())
+    return merged

@@ -602,3 +602,39 @@ def test_device_edge_model_errors(ea):
     f = ea.compute_gradients(np.arange(100.0).reshape(10, 10) ** 2)
     with pytest.raises(ea.InvalidArgument, match="0 <= low <= high"):
         ea.extract_edge_model_device(f, (5.0, 1.0))
+
+
+def test_async_slab_rows_and_device_merge(ea, oracle):
+    """Device-resident slab search rows == ea_search_top_slab; the device
+    merge of all slabs' rows == merge_topk == the full search."""
+    import torch
+    img, tmpl = scene(ea, canvas_width=200, canvas_height=160, template_id="l_bracket",
+                      template_size=56, true_pose=(96, 84, D(63)), clutter_segments=25,
+                      clutter_seed=4)
+    cfg = ea.SearchConfig(grid=ea.PoseGrid(0, 199, 4, 0, 159, 4, 0.0, D(357), D(3)),
+                          num_levels=3, score_params=ea.ScoreParams(3), topk=6)
+    det = ea.Detector(tmpl, cfg)
+    det.levels.set_image(img)
+    ctx = det.ctx
+    nt = 120
+    G, k = 5, cfg.topk
+    rows = torch.empty((G * k, 5), dtype=torch.float64, device="cuda")
+    seeds = []
+    for g in range(G):
+        a, b = nt * g // G, nt * (g + 1) // G
+        ea.search_top_slab_async(det.levels, cfg, a, b, rows[g * k:(g + 1) * k].data_ptr())
+        seeds.append(ea.search_top_slab(det.levels, cfg, a, b))
+    merged = torch.empty((k, 5), dtype=torch.float64, device="cuda")
+    ea.merge_rows_async(ctx, rows.data_ptr(), G * k, k, merged.data_ptr())
+    overflowed, _ = ea.async_status(ctx)
+    assert not overflowed
+    from paper_2112_05576_b200 import parallel
+    got = rows.cpu().numpy()
+    for g in range(G):
+        assert parallel.unpack(got[g * k:(g + 1) * k]) == [s for s in seeds[g]] or \
+            [(s.score, s.grid_index, s.pose.astuple()) for s in parallel.unpack(got[g * k:(g + 1) * k])] == \
+            [(s.score, s.grid_index, s.pose.astuple()) for s in seeds[g]]
+    want = ea.merge_topk([s for part in seeds for s in part], k)
+    full = ea.search_top_slab(det.levels, cfg, 0, nt)
+    key = lambda lst: [(s.score, int(s.grid_index), s.pose.astuple()) for s in lst]
+    assert key(parallel.unpack(merged.cpu().numpy())) == key(want) == key(full)
