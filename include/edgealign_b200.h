@@ -366,6 +366,26 @@ ea_status ea_detect_multi(ea_ctx* ctx, ea_levels* const* models, int n, const do
 ea_status ea_detect_batch(ea_ctx* ctx, ea_levels* lv, const double* const* images, int count,
                           int w, int h, const ea_search_config* cfg, ea_outcome* outs);
 
+/* ---- Netpbm codecs (image.cpp:26-219), host C++, bytes in / bytes out ---- */
+/* luminance_to_byte  image.cpp:26-34: clamp to [0, 255], round half up. */
+uint8_t ea_luminance_to_byte(double v);
+/* load_pgm  image.cpp:90-147 (P2 / P5, maxval <= 255).  out == NULL: only the
+ * dimensions.  Parse errors: EA_ERR_PARSE, ea_last_error_value() = offset. */
+ea_status ea_load_pgm(const uint8_t* bytes, size_t size, double* out, size_t cap, int* width,
+                      int* height);
+/* save_pgm  image.cpp:189-197 (P5).  out == NULL: *n_out = bytes needed. */
+ea_status ea_save_pgm(const double* image, int width, int height, uint8_t* out, size_t cap,
+                      size_t* n_out);
+/* save_ppm  image.cpp:203-227 (P6, gray + overlay points in one colour;
+ * out-of-bounds points skipped).  overlay_xy: n_overlay (x, y) pairs. */
+ea_status ea_save_ppm(const double* image, int width, int height, const int* overlay_xy,
+                      int n_overlay, uint8_t r, uint8_t g, uint8_t b, uint8_t* out, size_t cap,
+                      size_t* n_out);
+/* Pixels of model points projected at a pose, as the scorer projects them
+ * (similarity.cpp:79-80, 104-108): the overlay of a detection. */
+ea_status ea_overlay_points(const ea_edge_point* points, int n, const ea_pose* pose,
+                            int* out_xy);
+
 /* ---- synthetic scenes (synth.cpp:24-300), host C++ ---------------------- */
 ea_status ea_render_template(int template_id, int size, double* out);  /* synth.cpp:62-128 */
 /* compose_scene  synth.cpp:178-300.  canvas: W*H, tmpl: size*size. */

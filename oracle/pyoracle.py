@@ -293,6 +293,40 @@ class ReferenceLib(_Base):
     def set_isa(self, isa):
         self._check(self.lib.eref_set_isa(isa))
 
+    # ---- Netpbm codecs (image.cpp:26-219) ---------------------------------
+    def luminance_to_byte(self, v):
+        self.lib.eref_luminance_to_byte.argtypes = [C.c_double]
+        return int(self.lib.eref_luminance_to_byte(float(v)))
+
+    def load_pgm(self, data):
+        data = bytes(data)
+        w, h = C.c_int(), C.c_int()
+        self.lib.eref_load_pgm.argtypes = [C.c_char_p, C.c_size_t, C.c_void_p, C.c_size_t,
+                                           C.POINTER(C.c_int), C.POINTER(C.c_int)]
+        self._check(self.lib.eref_load_pgm(data, len(data), None, 0, C.byref(w), C.byref(h)))
+        out = np.zeros((h.value, w.value))
+        self._check(self.lib.eref_load_pgm(data, len(data), out.ctypes.data, out.size,
+                                           C.byref(w), C.byref(h)))
+        return out
+
+    def _save(self, name, img, extra):
+        img = _f64(img)
+        h, w = img.shape
+        n = C.c_size_t()
+        fn = getattr(self.lib, name)
+        self._check(fn(_ptr(img), w, h, *extra, None, 0, C.byref(n)))
+        out = (C.c_ubyte * n.value)()
+        self._check(fn(_ptr(img), w, h, *extra, out, n.value, C.byref(n)))
+        return bytes(out)
+
+    def save_pgm(self, img):
+        return self._save("eref_save_pgm", img, ())
+
+    def save_ppm(self, img, overlay, color):
+        xy = np.ascontiguousarray(np.asarray(overlay, dtype=np.int32).reshape(-1, 2))
+        return self._save("eref_save_ppm", img,
+                          (xy.ctypes.data_as(C.POINTER(C.c_int)), len(xy), *color))
+
     def default_thresholds(self, field):
         gx, gy, mag = (_f64(a) for a in field)
         h, w = mag.shape

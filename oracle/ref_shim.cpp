@@ -435,6 +435,40 @@ int eref_compose_scene(const ea_scene_spec* s, double* canvas, double* tmpl,
     });
 }
 
+// Netpbm codecs  image.cpp:26-219 (bytes in, bytes out)
+int eref_luminance_to_byte(double v) { return luminance_to_byte(v); }
+int eref_load_pgm(const unsigned char* bytes, size_t size, double* out, size_t cap, int* w,
+                  int* h) {
+    return guard([&] {
+        const Image img = load_pgm(bytes, size);
+        *w = img.width;
+        *h = img.height;
+        if (out && cap >= img.data.size())
+            std::memcpy(out, img.data.data(), sizeof(double) * img.data.size());
+    });
+}
+int eref_save_pgm(const double* img, int w, int h, unsigned char* out, size_t cap, size_t* n) {
+    return guard([&] {
+        Image im(w, h);
+        std::memcpy(im.data.data(), img, sizeof(double) * im.data.size());
+        const auto b = save_pgm(im);
+        *n = b.size();
+        if (out && cap >= b.size()) std::memcpy(out, b.data(), b.size());
+    });
+}
+int eref_save_ppm(const double* img, int w, int h, const int* xy, int n_xy, int r, int g, int b,
+                  unsigned char* out, size_t cap, size_t* n) {
+    return guard([&] {
+        Image im(w, h);
+        std::memcpy(im.data.data(), img, sizeof(double) * im.data.size());
+        std::vector<std::pair<int, int>> ov;
+        for (int i = 0; i < n_xy; ++i) ov.emplace_back(xy[2 * i], xy[2 * i + 1]);
+        const auto bytes = save_ppm(im, ov, Rgb{(std::uint8_t)r, (std::uint8_t)g, (std::uint8_t)b});
+        *n = bytes.size();
+        if (out && cap >= bytes.size()) std::memcpy(out, bytes.data(), bytes.size());
+    });
+}
+
 // resolved_workers  search.cpp:15-24
 int eref_resolved_workers(int kind, int workers) {
     return resolved_workers(make_backend(kind, workers));

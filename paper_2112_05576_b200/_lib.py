@@ -107,6 +107,14 @@ _SIGS = {
     "ea_detect_multi": (C.c_int, [_P, C.POINTER(_P), C.c_int, _dp, C.c_int, C.c_int,
                                   C.POINTER(abi.SearchConfig), C.POINTER(abi.Outcome)]),
     "ea_render_template": (C.c_int, [C.c_int, C.c_int, _dp]),
+    "ea_luminance_to_byte": (C.c_uint8, [C.c_double]),
+    "ea_load_pgm": (C.c_int, [C.c_char_p, C.c_size_t, C.c_void_p, C.c_size_t, _ip, _ip]),
+    "ea_save_pgm": (C.c_int, [_dp, C.c_int, C.c_int, C.c_void_p, C.c_size_t,
+                              C.POINTER(C.c_size_t)]),
+    "ea_save_ppm": (C.c_int, [_dp, C.c_int, C.c_int, _ip, C.c_int, C.c_uint8, C.c_uint8,
+                              C.c_uint8, C.c_void_p, C.c_size_t, C.POINTER(C.c_size_t)]),
+    "ea_overlay_points": (C.c_int, [C.POINTER(abi.EdgePoint), C.c_int, C.POINTER(abi.Pose),
+                                    _ip]),
     "ea_compose_multi": (C.c_int, [C.POINTER(abi.SceneSpec), C.POINTER(abi.Stamp), C.c_int,
                                    _dp]),
     "ea_compose_scene": (C.c_int, [C.POINTER(abi.SceneSpec), _dp, _dp, C.POINTER(abi.Pose),

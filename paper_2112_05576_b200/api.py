@@ -583,6 +583,84 @@ def detect_multi(detectors, image):
     return list(outs)
 
 
+# ---- Netpbm codecs (image.cpp:26-219) -------------------------------------------------
+def luminance_to_byte(v):
+    return int(lib().ea_luminance_to_byte(float(v)))
+
+
+def load_pgm(data):
+    """PGM bytes (P2 / P5) -> float64 image (H, W)."""
+    data = bytes(data)
+    w, h = C.c_int(), C.c_int()
+    _check(lib().ea_load_pgm(data, len(data), None, 0, C.byref(w), C.byref(h)))
+    out = np.zeros((h.value, w.value))
+    _check(lib().ea_load_pgm(data, len(data), out.ctypes.data, out.size, C.byref(w),
+                             C.byref(h)))
+    return out
+
+
+def _netpbm(fn, img, *extra):
+    img = _f64(img)
+    h, w = img.shape
+    n = C.c_size_t()
+    _check(fn(_ptr(img), w, h, *extra, None, 0, C.byref(n)))
+    out = (C.c_ubyte * n.value)()
+    _check(fn(_ptr(img), w, h, *extra, out, n.value, C.byref(n)))
+    return bytes(out)
+
+
+def save_pgm(img):
+    """float64 image -> P5 bytes (clamped, rounded half up)."""
+    return _netpbm(lib().ea_save_pgm, img)
+
+
+def save_ppm(img, overlay=(), color=(255, 0, 0)):
+    """float64 image -> P6 bytes, gray with `overlay` (x, y) pixels in `color`."""
+    xy = np.ascontiguousarray(np.asarray(overlay, dtype=np.int32).reshape(-1, 2))
+    return _netpbm(lib().ea_save_ppm, img, xy.ctypes.data_as(C.POINTER(C.c_int)), len(xy),
+                   *[int(c) for c in color])
+
+
+def overlay_points(model, pose):
+    """Pixels (n, 2) of the model's points projected at `pose` (x, y, theta)."""
+    pts = np.ascontiguousarray(getattr(model, "points", model), dtype=np.float64).reshape(-1, 5)
+    out = np.zeros((max(len(pts), 1), 2), dtype=np.int32)
+    p = pose if isinstance(pose, Pose) else Pose(*pose)
+    _check(lib().ea_overlay_points(pts.ctypes.data_as(C.POINTER(EdgePoint)), len(pts),
+                                   C.byref(p), out.ctypes.data_as(C.POINTER(C.c_int))))
+    return out[: len(pts)]
+
+
+def detect_result_json(outcome, n_model_points, elapsed_ms, backend="cuda"):
+    """DetectResult (SPEC.md cli-bench: pose (x px, y px, theta degrees),
+    score, n_model_points, elapsed_ms, backend, level_trace) as a JSON text
+    with exactly those keys; theta reported in degrees."""
+    import json
+    p = outcome.pose
+    trace = [{"level": int(t.level), "x": t.pose.ux, "y": t.pose.uy,
+              "theta_deg": rad_to_deg(t.pose.theta), "score": t.score}
+             for t in outcome.trace[: outcome.n_trace]]
+    return json.dumps({"pose": {"x": p.ux, "y": p.uy, "theta_deg": rad_to_deg(p.theta)},
+                       "score": outcome.score, "n_model_points": int(n_model_points),
+                       "elapsed_ms": float(elapsed_ms), "backend": backend,
+                       "level_trace": trace})
+
+
+def load_pgm_file(path):
+    with open(path, "rb") as f:
+        return load_pgm(f.read())
+
+
+def save_pgm_file(img, path):
+    with open(path, "wb") as f:
+        f.write(save_pgm(img))
+
+
+def save_ppm_file(img, path, overlay=(), color=(255, 0, 0)):
+    with open(path, "wb") as f:
+        f.write(save_ppm(img, overlay, color))
+
+
 # ---- synthetic scenes (synth.cpp:62-300) -----------------------------------------
 def render_template(template_id, size):
     tid = abi.TEMPLATE_IDS[template_id] if isinstance(template_id, str) else template_id

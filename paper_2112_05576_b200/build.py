@@ -17,7 +17,7 @@ LIB = os.path.join(HERE, "libedgealign_b200.so")
 
 CU_SOURCES = ["api.cu", "field_kernels.cu", "search_kernels.cu", "refine_kernels.cu",
               "model_kernels.cu"]
-CPP_SOURCES = ["host_model.cpp", "host_synth.cpp"]
+CPP_SOURCES = ["host_model.cpp", "host_synth.cpp", "host_io.cpp"]
 HEADERS = ["common.cuh", "kernels.cuh", "refine.cuh", "model.cuh", "failure.h", "host_model.h"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -2369,6 +2369,68 @@ ea_status ea_detect_multi(ea_ctx* ctx, ea_levels* const* models, int n, const do
     });
 }
 
+// ---- Netpbm codecs ---------------------------------------------------------------------------
+uint8_t ea_luminance_to_byte(double v) { return host_luminance_to_byte(v); }
+
+ea_status ea_load_pgm(const uint8_t* bytes, size_t size, double* out, size_t cap, int* w,
+                      int* h) {
+    return guard([&] {
+        need(bytes, "bytes");
+        need(w, "width");
+        need(h, "height");
+        std::vector<double> img;
+        host_load_pgm(bytes, size, out ? &img : nullptr, w, h);
+        if (out) {
+            if (cap < img.size())
+                fail(EA_ERR_INVALID_ARGUMENT, "output capacity " + std::to_string(cap) +
+                                                  " < " + std::to_string(img.size()) + " pixels");
+            std::memcpy(out, img.data(), sizeof(double) * img.size());
+        }
+    });
+}
+
+ea_status ea_save_pgm(const double* image, int w, int h, uint8_t* out, size_t cap,
+                      size_t* n_out) {
+    return guard([&] {
+        need(image, "image");
+        need(n_out, "n_out");
+        const auto b = host_save_pgm(image, w, h);
+        *n_out = b.size();
+        if (out) {
+            if (cap < b.size()) fail(EA_ERR_INVALID_ARGUMENT, "output capacity too small");
+            std::memcpy(out, b.data(), b.size());
+        }
+    });
+}
+
+ea_status ea_save_ppm(const double* image, int w, int h, const int* xy, int n_xy, uint8_t r,
+                      uint8_t g, uint8_t b, uint8_t* out, size_t cap, size_t* n_out) {
+    return guard([&] {
+        need(image, "image");
+        need(n_out, "n_out");
+        if (n_xy > 0) need(xy, "overlay");
+        const auto bytes = host_save_ppm(image, w, h, xy, std::max(n_xy, 0), r, g, b);
+        *n_out = bytes.size();
+        if (out) {
+            if (cap < bytes.size()) fail(EA_ERR_INVALID_ARGUMENT, "output capacity too small");
+            std::memcpy(out, bytes.data(), bytes.size());
+        }
+    });
+}
+
+ea_status ea_overlay_points(const ea_edge_point* points, int n, const ea_pose* pose,
+                            int* out_xy) {
+    return guard([&] {
+        need(pose, "pose");
+        if (n < 0) fail(EA_ERR_INVALID_ARGUMENT, "point count must be >= 0");
+        if (n > 0) {
+            need(points, "points");
+            need(out_xy, "out");
+        }
+        host_overlay_points(points, n, *pose, out_xy);
+    });
+}
+
 // ---- synthetic scenes ----------------------------------------------------------------------
 ea_status ea_render_template(int template_id, int size, double* out) {
     return guard([&] {

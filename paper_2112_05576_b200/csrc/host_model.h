@@ -2,6 +2,7 @@
 // the synthetic scene generator).
 #pragma once
 
+#include <cstdint>
 #include <vector>
 
 #include "failure.h"
@@ -26,5 +27,13 @@ void host_render_template(int id, int size, double* out);
 void host_compose_multi(const ea_scene_spec& s, const ea_stamp* stamps, int n, double* canvas);
 void host_compose_scene(const ea_scene_spec& s, double* canvas, double* tmpl,
                         ea_pose* truth_pose, double* occluded_fraction);
+
+// Netpbm codecs and the model overlay (host_io.cpp, image.cpp:26-219).
+uint8_t host_luminance_to_byte(double v);
+void host_load_pgm(const uint8_t* bytes, size_t size, std::vector<double>* out, int* w, int* h);
+std::vector<uint8_t> host_save_pgm(const double* img, int w, int h);
+std::vector<uint8_t> host_save_ppm(const double* img, int w, int h, const int* xy, int n_xy,
+                                   uint8_t r, uint8_t g, uint8_t b);
+void host_overlay_points(const ea_edge_point* pts, int n, const ea_pose& pose, int* xy);
 
 }  // namespace eab
