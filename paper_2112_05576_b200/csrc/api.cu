@@ -1117,8 +1117,12 @@ void detect_batch(ea_ctx* ctx, ea_levels* lv, const double* const* images, int c
     char* dres = (char*)ctx->rslots.ensure(slot * (size_t)count);
     char* hres = (char*)ctx->h_out.ensure(slot * (size_t)count);
     const unsigned long long cap = std::max<unsigned long long>(initial_cap(ctx), 1ull << 20);
-    if (!ctx->refine_stream) EAB_CUDA(cudaStreamCreateWithFlags(&ctx->refine_stream,
-                                                                cudaStreamNonBlocking));
+    if (!ctx->refine_stream) {  // lowest priority: the next image's top level goes first
+        int lo = 0, hi = 0;
+        EAB_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        const int prio = std::getenv("EAB_REFINE_SAME_PRIO") ? 0 : lo;
+        EAB_CUDA(cudaStreamCreateWithPriority(&ctx->refine_stream, cudaStreamNonBlocking, prio));
+    }
     for (auto& e : ctx->rev)
         if (!e) EAB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     // Two working sets (pyramid + fields) and two refinement states: image i

@@ -638,3 +638,42 @@ def test_async_slab_rows_and_device_merge(ea, oracle):
     full = ea.search_top_slab(det.levels, cfg, 0, nt)
     key = lambda lst: [(s.score, int(s.grid_index), s.pose.astuple()) for s in lst]
     assert key(parallel.unpack(merged.cpu().numpy())) == key(want) == key(full)
+
+
+def test_gather_rows_device_nccl_single_rank(ea, oracle):
+    """The bench's N-GPU exchange on one rank: NCCL all-gather of the device
+    rows + device merge == the local rows (world size 1)."""
+    import os
+    import socket
+
+    import torch
+    import torch.distributed as dist
+    from paper_2112_05576_b200 import parallel
+
+    img, tmpl = scene(ea, canvas_width=160, canvas_height=128, template_id="l_bracket",
+                      template_size=48, true_pose=(80, 64, D(20)), clutter_segments=10,
+                      clutter_seed=3)
+    cfg = ea.SearchConfig(grid=ea.PoseGrid(0, 159, 2, 0, 127, 2, 0.0, D(355), D(5)),
+                          num_levels=2, score_params=ea.ScoreParams(3), topk=5)
+    det = ea.Detector(tmpl, cfg)
+    det.levels.set_image(img)
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        stream = torch.cuda.Stream()
+        with torch.cuda.stream(stream):
+            det.ctx.set_stream(stream.cuda_stream)
+            rows = torch.empty((5, 5), dtype=torch.float64, device="cuda")
+            ea.search_top_slab_async(det.levels, cfg, 0, 72, rows.data_ptr())
+            merged = parallel.gather_rows_device(rows, 5, det.ctx)
+            stream.synchronize()
+        want = ea.search_top_slab(det.levels, cfg, 0, 72)
+        key = lambda lst: [(s.score, int(s.grid_index), s.pose.astuple()) for s in lst]
+        assert key(parallel.unpack(merged.cpu().numpy())) == key(want)
+    finally:
+        dist.destroy_process_group()
+        det.ctx.set_stream(None)
