@@ -485,9 +485,12 @@ struct TopLaunch {
     unsigned long long* top_index = nullptr;
 };
 
+// d_rows: also write the k device rows {score, index, ux, uy, theta} (the
+// multi-GPU data path) and raise *overflow if the band overflowed `cap`.
 TopLaunch top_enqueue(ea_ctx* ctx, const ea_model* m, const ea_field* f, const ea_pose_grid& g,
                       const ea_score_params& p, int k, uint64_t it_begin, uint64_t it_end,
-                      unsigned long long cap) {
+                      unsigned long long cap, double* d_rows = nullptr,
+                      int* overflow = nullptr) {
     validate_params(p);
     if (m->n == 0) fail(EA_ERR_INVALID_ARGUMENT, "search needs a nonempty model");
     if (k < 1) fail(EA_ERR_INVALID_ARGUMENT, "topk must be >= 1");
@@ -517,12 +520,38 @@ TopLaunch top_enqueue(ea_ctx* ctx, const ea_model* m, const ea_field* f, const e
     x.dy = g.dy;
     unsigned* cand = (unsigned*)ctx->cand.ensure(sizeof(unsigned) * cap);
     double* cs = (double*)ctx->cand_score.ensure(sizeof(double) * cap);
+    const unsigned long long index_base = t.plan.it_begin * t.plan.c.nx * t.plan.c.ny;
+    const RowGrid rg{g.x0, g.dx, g.y0, g.dy, g.t0, g.dt, t.plan.c.nx, t.plan.c.ny};
+    if (ctx->fused_finish) {
+        // band threshold, compaction, exact rescore, select (+ rows): one launch
+        FinishArgs fa{};
+        fa.map = ctx->map.as<float>();
+        fa.item_max = ctx->item_max.as<float>();
+        fa.items = t.plan.items;
+        fa.ctrl = ctrl;
+        fa.cand = cand;
+        fa.cap = cap;
+        fa.hist = ctx->hist.as<unsigned>();
+        fa.k = k;
+        fa.delta = t.plan.delta;
+        fa.flags = t.plan.flags;
+        fa.x = x;
+        fa.cand_score = cs;
+        fa.index_base = index_base;
+        fa.out_score = t.top_score;
+        fa.out_index = t.top_index;
+        fa.rg = rg;
+        fa.rows = d_rows;
+        fa.overflow = overflow;
+        launch_finish(ctx, fa);
+        return t;
+    }
     // band threshold from the histogram, then the compaction
     launch_compact(ctx, ctx->map.as<float>(), ctx->item_max.as<float>(), t.plan.items, ctrl, cand,
                    cap, ctx->hist.as<unsigned>(), k, t.plan.delta, t.plan.flags);
     launch_rescore(ctx, x, cand, ctrl, cap, cs);
-    launch_select(ctx, cand, cs, ctrl, cap, k, t.plan.it_begin * t.plan.c.nx * t.plan.c.ny,
-                  t.top_score, t.top_index);
+    launch_select(ctx, cand, cs, ctrl, cap, k, index_base, t.top_score, t.top_index);
+    if (d_rows) launch_topk_rows(ctx, t.top_score, t.top_index, ctrl, cap, k, rg, d_rows, overflow);
     return t;
 }
 
@@ -2196,10 +2225,13 @@ ea_status ea_search_top_slab_async(ea_ctx* ctx, const ea_levels* lv,
         // reported by ea_ctx_async_status
         const unsigned long long cap = std::max<unsigned long long>(initial_cap(ctx), 1ull << 20);
         const TopLaunch t = top_enqueue(ctx, lv->models[top], lv->fields[top], tg,
-                                        cfg->score_params, cfg->topk, it_begin, it_end, cap);
-        RowGrid g{tg.x0, tg.dx, tg.y0, tg.dy, tg.t0, tg.dt, c.nx, c.ny};
-        launch_topk_rows(ctx, t.top_score, t.top_index, ctx->ctrl.as<SearchCtrl>(), cap,
-                         cfg->topk, g, d_rows, ctx->async_flag.as<int>());
+                                        cfg->score_params, cfg->topk, it_begin, it_end, cap,
+                                        d_rows, ctx->async_flag.as<int>());
+        if (t.plan.slab_poses == 0) {  // empty slab: k empty rows
+            RowGrid g{tg.x0, tg.dx, tg.y0, tg.dy, tg.t0, tg.dt, c.nx, c.ny};
+            launch_topk_rows(ctx, t.top_score, t.top_index, ctx->ctrl.as<SearchCtrl>(), cap,
+                             cfg->topk, g, d_rows, ctx->async_flag.as<int>());
+        }
     });
 }
 
@@ -2228,6 +2260,21 @@ ea_status ea_ctx_async_status(ea_ctx* ctx, int* overflowed, float* screen_ms, in
             EAB_CUDA(cudaMemset(ctx->async_flag.p, 0, sizeof(int)));
         }
         if (overflowed) *overflowed = of;
+        if (ctx->trace_on && !ctx->trace.empty()) {  // per-launch end-to-end deltas
+            std::map<std::string, std::pair<double, int>> agg;
+            for (size_t i = 1; i < ctx->trace.size(); ++i) {
+                float ms = 0.f;
+                cudaEventElapsedTime(&ms, ctx->trace[i - 1].second, ctx->trace[i].second);
+                auto& a = agg[ctx->trace[i].first];
+                a.first += ms;
+                a.second += 1;
+            }
+            for (auto& kv : agg)
+                std::fprintf(stderr, "[trace] %-28s n=%5d avg_us=%8.2f\n", kv.first.c_str(),
+                             kv.second.second, 1e3 * kv.second.first / kv.second.second);
+            for (auto& t : ctx->trace) cudaEventDestroy(t.second);
+            ctx->trace.clear();
+        }
         int n = 0;
         if (ctx->timing) {
             const int pend = ctx->tev_pending;

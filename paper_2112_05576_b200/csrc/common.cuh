@@ -1,6 +1,7 @@
 // common.cuh -- shared host/device infrastructure of libedgealign_b200.
 #pragma once
 
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -9,6 +10,7 @@
 #include <map>
 #include <stdexcept>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "failure.h"
@@ -123,6 +125,11 @@ struct ea_ctx {
     uint64_t launches = 0;
     ea_search_stats stats{};
     bool timing = false;
+    bool trace_on = std::getenv("EAB_TRACE") != nullptr;
+    std::vector<std::pair<const char*, cudaEvent_t>> trace;
+    // one cooperative finish launch after the screen (EAB_NO_FUSED_FINISH=1:
+    // the separate compact/rescore/select/rows launches, for A/B measurements)
+    bool fused_finish = std::getenv("EAB_NO_FUSED_FINISH") == nullptr;
     cudaEvent_t ev[8] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
     // scratch
     eab::DevBuf cs, rot_exact, rot_screen, plane, map, item_max, tail, hist, ctrl, cand, cand_score, topk,
@@ -150,12 +157,25 @@ struct ea_ctx {
 namespace eab {
 
 // Launch bookkeeping (the bench's gpu_launches claim comes from here).
+inline const char*& last_launch_name() {
+    static thread_local const char* name = "";
+    return name;
+}
+
 inline void count_launch(ea_ctx* ctx, int n = 1) {
     ctx->launches += (uint64_t)n;
     ctx->stats.kernels_launched += n;
+    if (ctx->trace_on) {  // EAB_TRACE: an event after every launch (diagnostics)
+        cudaEvent_t e;
+        if (cudaEventCreate(&e) == cudaSuccess) {
+            cudaEventRecord(e, ctx->stream);
+            ctx->trace.emplace_back(last_launch_name(), e);
+        }
+    }
 }
 
 inline void check_launch(const char* what) {
+    last_launch_name() = what;
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) {
         fail(EA_ERR_CUDA, std::string("kernel launch ") + what + ": " + cudaGetErrorString(e));

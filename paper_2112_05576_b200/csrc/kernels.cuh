@@ -293,6 +293,30 @@ void launch_topk_rows(ea_ctx* ctx, const double* score, const unsigned long long
                       const SearchCtrl* ctrl, unsigned long long cap, int k, const RowGrid& g,
                       double* rows, int* overflow);
 void launch_merge_rows(ea_ctx* ctx, const double* in, int n, int k, double* out);
+// compaction + rescore + select (+ rows when rows != nullptr) in one
+// cooperative launch; same results as launch_compact/rescore/select/topk_rows.
+struct FinishArgs {
+    const float* map;
+    const float* item_max;
+    ItemGeom items;
+    SearchCtrl* ctrl;
+    unsigned* cand;
+    unsigned long long cap;
+    const unsigned* hist;
+    int k;
+    double delta;
+    const int* flags;
+    ExactArgs x;
+    double* cand_score;
+    unsigned long long index_base;
+    double* out_score;
+    unsigned long long* out_index;
+    RowGrid rg;
+    double* rows;
+    int* overflow;
+    unsigned long long* prof;  // optional phase timestamps (EAB_FINISH_PROF)
+};
+void launch_finish(ea_ctx* ctx, const FinishArgs& f);
 // Dense exact map (score_map search.cpp:169-202).
 void launch_exact_map(ea_ctx* ctx, const ExactArgs& a, unsigned long long total, double* out);
 

@@ -22,11 +22,16 @@
 // selecting by `better` over exact scores reproduces search_topk bit for bit.
 #include <algorithm>
 #include <climits>
+#include <cstdio>
 #include <cstdlib>
+#include <cstring>
 
+#include <cooperative_groups.h>
 #include <cub/block/block_scan.cuh>
 
 #include "kernels.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace eab {
 
@@ -157,6 +162,66 @@ __device__ __forceinline__ float max_run(const float* v) {
 __device__ __forceinline__ int hist_bin(float s) {
     int b = __float2int_rd((s + 1.0f) * 2048.0f);
     return b < 0 ? 0 : (b >= kHistBins ? kHistBins - 1 : b);
+}
+
+// Adds a CTA's shared histogram into the global one (after a __syncthreads).
+// With kf > 0 only the bins at or above the CTA's own kf-th largest score
+// are added: that score is at most the global kf-th largest T_f, so every bin
+// from bin(T_f) up keeps its exact global count and the threshold bin found
+// by block_threshold is unchanged -- while a CTA adds a handful of bins
+// instead of hundreds (global atomics were ~12% of a theta-slab launch).
+__device__ __forceinline__ void merge_hist(const unsigned* __restrict__ hist,
+                                           unsigned* __restrict__ ghist, int kf) {
+    constexpr int kChunks = 256, kPer = kHistBins / kChunks;  // chunk c: bins from the top
+    __shared__ unsigned csum[kChunks];
+    __shared__ int kbin;
+    int lo = 0;
+    if (kf > 0) {
+        for (int c = threadIdx.x; c < kChunks; c += blockDim.x) {
+            unsigned v = 0;
+#pragma unroll
+            for (int j = 0; j < kPer; ++j) v += hist[kHistBins - 1 - (c * kPer + j)];
+            csum[c] = v;
+        }
+        if (threadIdx.x == 0) kbin = 0;
+        __syncthreads();
+        if (threadIdx.x < 32) {
+            const int lane = threadIdx.x;
+            constexpr int kLane = kChunks / 32;
+            unsigned mine = 0;
+#pragma unroll
+            for (int j = 0; j < kLane; ++j) mine += csum[lane * kLane + j];
+            unsigned incl = mine;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const unsigned u = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += u;
+            }
+            unsigned run = incl - mine;  // poses in higher lanes' chunks
+            if (run < (unsigned)kf && incl >= (unsigned)kf) {
+                for (int c = lane * kLane; c < (lane + 1) * kLane; ++c) {
+                    if (run + csum[c] >= (unsigned)kf) {
+                        for (int j = 0; j < kPer; ++j) {
+                            const int b = kHistBins - 1 - (c * kPer + j);
+                            run += hist[b];
+                            if (run >= (unsigned)kf) {
+                                kbin = b;
+                                break;
+                            }
+                        }
+                        break;
+                    }
+                    run += csum[c];
+                }
+            }
+        }
+        __syncthreads();
+        lo = kbin;
+    }
+    for (int b = lo + (int)threadIdx.x; b < kHistBins; b += blockDim.x) {
+        const unsigned v = hist[b];
+        if (v) atomicAdd(&ghist[b], v);
+    }
 }
 
 // CTA size of the lattice kernel (one CTA per SM).
@@ -613,20 +678,23 @@ __global__ void __launch_bounds__(THREADS, 1)
             old = __shfl_sync(0xffffffffu, old, 0);
             if (old != (unsigned)tp.f - 1u) continue;
             __threadfence();
+            // read the merged sums and leave the slot zeroed for the next
+            // launch (no per-launch memset of the partial buffer)
 #pragma unroll
             for (int s = 0; s < S; ++s)
 #pragma unroll
-                for (int j = 0; j < kTW; ++j) sc[s][j] = __ldcg(part + (s * kTW + j) * 32 + lane);
+                for (int j = 0; j < kTW; ++j) {
+                    sc[s][j] = __ldcg(part + (s * kTW + j) * 32 + lane);
+                    __stcg(part + (s * kTW + j) * 32 + lane, 0);
+                }
+            if (lane == 0) tp.done[tslot] = 0u;
         }
         const float best = emit_tile<S>(a, sc, X, Y, itr, item, hist, lane,
                                         warp_floor(wtop, a.kf));
         floor_insert(wtop, best, lane);
     }
     __syncthreads();
-    for (int b = threadIdx.x; b < kHistBins; b += blockDim.x) {
-        const unsigned v = hist[b];
-        if (v) atomicAdd(&a.hist[b], v);
-    }
+    merge_hist(hist, a.hist, a.kf);
 }
 
 template <int R, int S, int SHIFT, bool IGNORE, int XG, bool EDGE, int THREADS>
@@ -640,26 +708,50 @@ static void run_fast(ea_ctx* ctx, const ScreenArgs& a) {
     auto kern = screen_fast_kernel<R, S, SHIFT, IGNORE, XG, EDGE, THREADS>;
     EAB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     constexpr int threads = THREADS;
-    unsigned long long warps_per_cta = threads / 32;
-    unsigned long long ctas = (items + warps_per_cta - 1) / warps_per_cta;
+    const unsigned long long warps_per_cta = threads / 32;
+    const bool split = std::getenv("EAB_NO_TAIL_SPLIT") == nullptr;
+    // Full grid (one CTA per SM) whenever the items can be split into enough
+    // point-chunks to occupy it: a theta slab of a sharded search (or any
+    // small grid) has fewer warp tiles than the P resident warps.
+    const int fmax = split && a.n >= 8 ? std::min(a.n / 4, 64) : 1;
+    unsigned long long ctas = (items * (unsigned long long)fmax + warps_per_cta - 1) / warps_per_cta;
     if (ctas > (unsigned long long)ctx->sm_count) ctas = ctx->sm_count;
     if (ctas == 0) ctas = 1;
-    // tail split (see TailPlan)
+    // tail split (see TailPlan): the last partial round of `rem` items is cut
+    // into f chunks, f minimising the makespan ceil(rem*f/P) * (1/f + c) in
+    // item units (c ~ 2%: a chunk's partial-sum merge and finalise).
     TailPlan tp{items, 0, 1, nullptr, nullptr};
     const unsigned long long P = ctas * warps_per_cta;
     const unsigned long long rem = items % P;
-    const bool split = std::getenv("EAB_NO_TAIL_SPLIT") == nullptr;
-    if (split && rem > 0 && a.n >= 8) {
-        int f = (int)std::min<unsigned long long>(P / rem, (unsigned long long)(a.n / 4));
+    if (rem > 0 && fmax >= 2) {
+        int f = 1;
+        double best = 1.02;
+        for (int ff = 2; ff <= fmax; ++ff) {
+            const double rounds = (double)((rem * (unsigned long long)ff + P - 1) / P);
+            const double cost = rounds * (1.0 / ff + 0.02);
+            if (cost < best - 1e-9) {
+                best = cost;
+                f = ff;
+            }
+        }
         if (f >= 2) {
             tp.n_main = items - rem;
             tp.n_tail = rem;
             tp.f = f;
+            // Partial sums and arrival counters are zero between launches:
+            // cleared once at allocation, then by each slot's finaliser.
             const size_t part_bytes = rem * (size_t)S * kTW * 32 * sizeof(int);
-            char* buf = (char*)ctx->tail.ensure(part_bytes + rem * sizeof(unsigned));
+            const size_t bytes = part_bytes + rem * sizeof(unsigned);
+            const void* before = ctx->tail.p;
+            const size_t cap_before = ctx->tail.cap;
+            char* buf = (char*)ctx->tail.ensure(bytes);
+            if (buf != before || ctx->tail.cap != cap_before)
+                EAB_CUDA(cudaMemsetAsync(buf, 0, ctx->tail.cap, ctx->stream));
+            // layout: partials of slot i at [i], counters after the largest
+            // partial block the buffer can hold, so a slot's counter never
+            // aliases another launch's partials
             tp.part = (int*)buf;
-            tp.done = (unsigned*)(buf + part_bytes);
-            EAB_CUDA(cudaMemsetAsync(buf, 0, part_bytes + rem * sizeof(unsigned), ctx->stream));
+            tp.done = (unsigned*)(buf + ctx->tail.cap - rem * sizeof(unsigned));
         }
     }
     kern<<<(unsigned)ctas, threads, smem, ctx->stream>>>(a, nwx, nwy, tp, (int)(plane_bytes / 16));
@@ -820,10 +912,7 @@ __global__ void __launch_bounds__(kGroup * 32, 1)
         floor_insert(wtop, best, lane);
     }
     __syncthreads();
-    for (int b = threadIdx.x; b < kHistBins; b += blockDim.x) {
-        const unsigned v = hist[b];
-        if (v) atomicAdd(&a.hist[b], v);
-    }
+    merge_hist(hist, a.hist, a.kf);
 }
 
 static RegionPlan region_plan(const ScreenArgs& a, int R) {
@@ -953,10 +1042,7 @@ __global__ void __launch_bounds__(256)
         if (lane == 0) a.item_max[t0 >> 5] = best;
     }
     __syncthreads();
-    for (int b = threadIdx.x; b < kHistBins; b += blockDim.x) {
-        const unsigned v = hist[b];
-        if (v) atomicAdd(&a.hist[b], v);
-    }
+    merge_hist(hist, a.hist, a.kf);
 }
 
 void launch_screen_general(ea_ctx* ctx, const ScreenArgs& a) {
@@ -1058,15 +1144,11 @@ void launch_threshold(ea_ctx* ctx, const unsigned* hist, int k, double delta, Se
 // threshold are skipped without touching the map (typically all but the few
 // tiles around the peaks).  Every block derives the band threshold from the
 // histogram itself (block 0 publishes it), so no separate threshold launch.
-__global__ void __launch_bounds__(256) compact_kernel(const float* __restrict__ map,
-                                                      const float* __restrict__ item_max,
-                                                      const ItemGeom g, SearchCtrl* ctrl,
-                                                      unsigned* __restrict__ cand,
-                                                      unsigned long long cap,
-                                                      const unsigned* __restrict__ hist, int k,
-                                                      double delta, const int* flags) {
-    if (blockIdx.x == 0 && threadIdx.x == 0 && flags) ctrl->flags = *flags;  // for the stats
-    const float thr = block_threshold<256>(hist, k, delta, ctrl, blockIdx.x == 0);
+__device__ __forceinline__ void compact_body(const float* __restrict__ map,
+                                             const float* __restrict__ item_max,
+                                             const ItemGeom& g, SearchCtrl* ctrl,
+                                             unsigned* __restrict__ cand, unsigned long long cap,
+                                             const float thr) {
     const int lane = threadIdx.x & 31;
     const unsigned long long warp = ((unsigned long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const unsigned long long nwarps = ((unsigned long long)gridDim.x * blockDim.x) >> 5;
@@ -1131,6 +1213,18 @@ __global__ void __launch_bounds__(256) compact_kernel(const float* __restrict__ 
         }
         }
     }
+}
+
+__global__ void __launch_bounds__(256) compact_kernel(const float* __restrict__ map,
+                                                      const float* __restrict__ item_max,
+                                                      const ItemGeom g, SearchCtrl* ctrl,
+                                                      unsigned* __restrict__ cand,
+                                                      unsigned long long cap,
+                                                      const unsigned* __restrict__ hist, int k,
+                                                      double delta, const int* flags) {
+    if (blockIdx.x == 0 && threadIdx.x == 0 && flags) ctrl->flags = *flags;  // for the stats
+    const float thr = block_threshold<256>(hist, k, delta, ctrl, blockIdx.x == 0);
+    compact_body(map, item_max, g, ctrl, cand, cap, thr);
 }
 
 ItemGeom screen_items(const ScreenArgs& a, bool fast) {
@@ -1201,11 +1295,10 @@ __device__ __forceinline__ double warp_pose_score(const ExactArgs& a, size_t bas
 // (similarity.cpp:109-118) -- the reference's fp64 score to the last bit.
 constexpr int kRescoreChunk = 256;
 
-__global__ void __launch_bounds__(256) rescore_kernel(const ExactArgs a,
-                                                      const unsigned* __restrict__ cand,
-                                                      const SearchCtrl* ctrl,
-                                                      unsigned long long cap,
-                                                      double* __restrict__ score) {
+__device__ __forceinline__ void rescore_body(const ExactArgs& a,
+                                             const unsigned* __restrict__ cand,
+                                             const SearchCtrl* ctrl, unsigned long long cap,
+                                             double* __restrict__ score) {
     __shared__ long long vmax[kRescoreChunk];
     __shared__ int2 centre[kRescoreChunk];
     unsigned long long nc = ctrl->cand_count;
@@ -1267,6 +1360,14 @@ __global__ void __launch_bounds__(256) rescore_kernel(const ExactArgs a,
     }
 }
 
+__global__ void __launch_bounds__(256) rescore_kernel(const ExactArgs a,
+                                                      const unsigned* __restrict__ cand,
+                                                      const SearchCtrl* ctrl,
+                                                      unsigned long long cap,
+                                                      double* __restrict__ score) {
+    rescore_body(a, cand, ctrl, cap, score);
+}
+
 void launch_rescore(ea_ctx* ctx, const ExactArgs& a, const unsigned* cand,
                     const SearchCtrl* ctrl, unsigned long long cap, double* score) {
     unsigned long long blocks = cap;
@@ -1298,12 +1399,11 @@ __device__ __forceinline__ Best pick(Best x, Best y) {
     return better_k(x.k, x.i, y.k, y.i) ? x : y;
 }
 
-__global__ void __launch_bounds__(256) select_kernel(const unsigned* __restrict__ cand,
-                                                     const double* __restrict__ score,
-                                                     SearchCtrl* ctrl, unsigned long long cap,
-                                                     int k, unsigned long long index_base,
-                                                     double* out_score,
-                                                     unsigned long long* out_index) {
+__device__ __forceinline__ void select_body(const unsigned* __restrict__ cand,
+                                            const double* __restrict__ score, SearchCtrl* ctrl,
+                                            unsigned long long cap, int k,
+                                            unsigned long long index_base, double* out_score,
+                                            unsigned long long* out_index) {
     constexpr int kStage = 2048;  // candidates staged in shared memory
     __shared__ long long skey[kStage];
     __shared__ unsigned long long sidx[kStage];
@@ -1382,6 +1482,15 @@ __global__ void __launch_bounds__(256) select_kernel(const unsigned* __restrict_
     if (t == 0) ctrl->n_out = r;
 }
 
+__global__ void __launch_bounds__(256) select_kernel(const unsigned* __restrict__ cand,
+                                                     const double* __restrict__ score,
+                                                     SearchCtrl* ctrl, unsigned long long cap,
+                                                     int k, unsigned long long index_base,
+                                                     double* out_score,
+                                                     unsigned long long* out_index) {
+    select_body(cand, score, ctrl, cap, k, index_base, out_score, out_index);
+}
+
 void launch_select(ea_ctx* ctx, const unsigned* cand, const double* score, SearchCtrl* ctrl,
                    unsigned long long cap, int k, unsigned long long index_base,
                    double* out_score, unsigned long long* out_index) {
@@ -1395,10 +1504,11 @@ void launch_select(ea_ctx* ctx, const unsigned* cand, const double* score, Searc
 // Row = {score, grid_index, ux, uy, theta} as five doubles (grid indices are
 // < 2^53, so exact); rows past the count carry a NaN score.  The same layout
 // is all-gathered over NCCL and merged on the device.
-__global__ void topk_rows_kernel(const double* __restrict__ score,
-                                 const unsigned long long* __restrict__ index,
-                                 const SearchCtrl* __restrict__ ctrl, unsigned long long cap,
-                                 int k, RowGrid g, double* __restrict__ rows, int* overflow) {
+__device__ __forceinline__ void topk_rows_body(const double* __restrict__ score,
+                                               const unsigned long long* __restrict__ index,
+                                               const SearchCtrl* __restrict__ ctrl,
+                                               unsigned long long cap, int k, const RowGrid& g,
+                                               double* __restrict__ rows, int* overflow) {
     const int n = ctrl->n_out;
     if (threadIdx.x == 0 && ctrl->cand_count > cap) atomicOr(overflow, 1);
     const unsigned long long plane = g.nx * g.ny;
@@ -1417,6 +1527,328 @@ __global__ void topk_rows_kernel(const double* __restrict__ score,
             o[1] = o[2] = o[3] = o[4] = 0.0;
         }
     }
+}
+
+__global__ void topk_rows_kernel(const double* __restrict__ score,
+                                 const unsigned long long* __restrict__ index,
+                                 const SearchCtrl* __restrict__ ctrl, unsigned long long cap,
+                                 int k, RowGrid g, double* __restrict__ rows, int* overflow) {
+    topk_rows_body(score, index, ctrl, cap, k, g, rows, overflow);
+}
+
+// ---- fused finish: band threshold -> compaction -> exact rescore -> top k
+// (-> rows) in ONE cooperative launch.  The separate kernels are latency
+// chains (a few dependent memory round trips and barriers each, ~50 us for
+// the four); here every phase is written for the shortest dependent chain:
+//  A  threshold   every CTA scans the 4096-bin histogram (16 bins/thread,
+//                 one load round trip, shuffle scans);
+//  B  compaction  a warp tests 32 item maxima per load and gathers a
+//                 qualifying tile with all 64 loads per lane in flight, one
+//                 atomic slot reservation per tile;
+//     grid barrier (the candidate count is final);
+//  C  rescore     one CTA per candidate, one thread per model point: the
+//                 window argmax by exact fraction compare and one division
+//                 (vote_exact), votes added in point order by one thread;
+//  D  select      the last CTA to finish C ranks the candidates by `better`
+//                 (rank = how many candidates beat it: one pass, no rounds)
+//                 and writes the top k (and the device rows).
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
+// A: band threshold (block_threshold's result) with one load round trip.
+__device__ __forceinline__ float finish_threshold(const unsigned* __restrict__ hist, int k,
+                                                  double delta) {
+    constexpr int PER = kHistBins / 256;  // blockDim.x == 256
+    __shared__ unsigned wsum[8];
+    __shared__ int kbin;
+    __shared__ float thr_s;
+    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+    unsigned v[PER], sum = 0;
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {  // chunk t: bins counted from the top
+        v[j] = __ldcg(hist + kHistBins - 1 - (PER * t + j));
+        sum += v[j];
+    }
+    unsigned incl = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned u = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += u;
+    }
+    if (lane == 31) wsum[w] = incl;
+    if (t == 0) kbin = -1;
+    __syncthreads();
+    unsigned run = incl - sum;
+    for (int q = 0; q < w; ++q) run += wsum[q];
+    if (run < (unsigned)k && run + sum >= (unsigned)k) {
+#pragma unroll 1
+        for (int j = 0; j < PER; ++j) {
+            run += v[j];
+            if (run >= (unsigned)k) {
+                kbin = kHistBins - 1 - (PER * t + j);
+                break;
+            }
+        }
+    }
+    __syncthreads();
+    if (t == 0) {
+        float thr = -INFINITY;
+        if (kbin >= 0) {  // else fewer than k poses: every pose is a candidate
+            const double lo = (double)kbin / 2048.0 - 1.0;
+            const double th = lo - 2.0 * delta - 9.5367431640625e-07;  // 2^-20
+            thr = (float)th;
+            if ((double)thr > th) thr = nextafterf(thr, -INFINITY);
+        }
+        thr_s = thr;
+    }
+    __syncthreads();
+    return thr_s;
+}
+
+// B: one warp, one qualifying work item: every pose with S_f >= thr.  Lane
+// addresses are one pointer + a 32-bit row stride, so the 64 loads issue back
+// to back (64-bit index math per load made this a 4 us instruction chain).
+__device__ __forceinline__ void finish_tile(const FinishArgs& f, unsigned long long it,
+                                            float thr, int lane) {
+    const ItemGeom& g = f.items;
+    constexpr int kMaxSteps = 64;  // 32 lanes x 64 = one 2048-pose lattice tile
+    const float kNaN = __int_as_float(0x7fffffff);  // never >= thr, even thr = -inf
+    const float* p;
+    unsigned stride = 0;
+    int nrows;  // rows of this lane inside the grid
+    unsigned long long first;  // slab-relative pose index of the lane's row 0
+    if (g.lattice) {
+        const unsigned rstep = 32u / g.cols;
+        const unsigned long long wx = it % g.nwx, rest = it / g.nwx;
+        const unsigned long long wy = rest % g.nwy, itr = rest / g.nwy;
+        const unsigned long long x = wx * g.cols + lane % g.cols;
+        const unsigned long long y0 = wy * g.rows + lane / g.cols;
+        const unsigned steps = g.rows / rstep;
+        nrows = 0;
+        if (x < g.nx && y0 < g.ny) {
+            const unsigned long long left = (g.ny - y0 + rstep - 1) / rstep;
+            nrows = (int)(left < steps ? left : steps);
+        }
+        stride = rstep * (unsigned)g.nx;
+        first = itr * (g.nx * g.ny) + y0 * g.nx + x;
+    } else {
+        first = it * 32 + lane;
+        nrows = first < g.total ? 1 : 0;
+    }
+    p = f.map + first;
+    float v[kMaxSteps];
+#pragma unroll
+    for (int r = 0; r < kMaxSteps; ++r) v[r] = r < nrows ? __ldcg(p + r * stride) : kNaN;
+    unsigned cnt = 0;
+#pragma unroll
+    for (int r = 0; r < kMaxSteps; ++r) cnt += v[r] >= thr ? 1u : 0u;
+    unsigned incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned u = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += u;
+    }
+    const unsigned total = __shfl_sync(0xffffffffu, incl, 31);
+    if (total == 0) return;
+    unsigned long long slot0 = 0;
+    if (lane == 31) slot0 = atomicAdd(&f.ctrl->cand_count, (unsigned long long)total);
+    unsigned long long slot = __shfl_sync(0xffffffffu, slot0, 31) + (incl - cnt);
+    if (cnt == 0) return;
+#pragma unroll
+    for (int r = 0; r < kMaxSteps; ++r) {  // unrolled: v stays in registers
+        if (v[r] >= thr) {
+            if (slot < f.cap) f.cand[slot] = (unsigned)(first + (unsigned long long)r * stride);
+            ++slot;
+        }
+    }
+}
+
+// C: exact fp64 score of candidate c with the whole CTA (reference order).
+__device__ __forceinline__ void finish_rescore(const ExactArgs& a, unsigned rel_idx,
+                                               double* out) {
+    __shared__ double votes[256];
+    const unsigned long long plane = a.nx * a.ny;
+    const unsigned long long itl = rel_idx / plane, rem = rel_idx % plane;
+    const double ux = lattice(a.x0, rem % a.nx, a.dx);
+    const double uy = lattice(a.y0, rem / a.nx, a.dy);
+    const size_t S = a.rot_stride, base = (size_t)itl * a.n;
+    const int t = threadIdx.x;
+    double sum = 0.0;
+    for (int p0 = 0; p0 < a.n; p0 += 256) {
+        const int i = p0 + t;
+        double v = 0.0;  // off-field centre / guarded coordinate: vote 0 (x + 0.0 == x)
+        if (i < a.n) {
+            const double px = __dadd_rn(__ldg(a.rot_exact + base + i), ux);
+            const double py = __dadd_rn(__ldg(a.rot_exact + S + base + i), uy);
+            if (px > -kCoordGuard && px < kCoordGuard && py > -kCoordGuard && py < kCoordGuard) {
+                const int cx = (int)floor(__dadd_rn(px, 0.5));
+                const int cy = (int)floor(__dadd_rn(py, 0.5));
+                if (cx >= 0 && cx < a.W && cy >= 0 && cy < a.H)
+                    v = vote_exact(a.gx, a.gy, a.mag, a.W, a.H, cx, cy, a.R,
+                                   __ldg(a.rot_exact + 2 * S + base + i),
+                                   __ldg(a.rot_exact + 3 * S + base + i), a.eps, a.ignore != 0);
+            }
+        }
+        votes[t] = v;
+        __syncthreads();
+        if (t == 0) {
+            const int cn = min(256, a.n - p0);
+            int j = 0;
+            for (; j + 8 <= cn; j += 8) {  // 8 loads in flight, then the ordered adds
+                double b[8];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) b[q] = votes[j + q];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) sum = __dadd_rn(sum, b[q]);
+            }
+            for (; j < cn; ++j) sum = __dadd_rn(sum, votes[j]);
+        }
+        __syncthreads();
+    }
+    if (t == 0) *out = __ddiv_rn(sum, (double)a.n);
+}
+
+// D: top k by `better` (score desc, index asc) as ranks; n_out = min(k, nc).
+constexpr int kRankMax = 512;  // candidates ranked in one pass; more: select_body rounds
+__device__ __forceinline__ void finish_select(const FinishArgs& f, unsigned long long nc) {
+    __shared__ long long skey[kRankMax];
+    __shared__ unsigned long long sidx[kRankMax];
+    const int t = threadIdx.x;
+    for (unsigned long long c = t; c < nc; c += blockDim.x) {
+        skey[c] = order_key(__ldcg(f.cand_score + c));
+        sidx[c] = f.index_base + __ldcg(f.cand + c);
+    }
+    __syncthreads();
+    for (unsigned long long c = t; c < nc; c += blockDim.x) {
+        const long long kc = skey[c];
+        const unsigned long long ic = sidx[c];
+        int r = 0;
+        for (unsigned long long j = 0; j < nc && r < f.k; ++j)
+            r += better_k(skey[j], sidx[j], kc, ic) ? 1 : 0;
+        if (r < f.k) {
+            f.out_score[r] = from_order_key(kc);
+            f.out_index[r] = ic;
+        }
+    }
+    if (t == 0) f.ctrl->n_out = (int)(nc < (unsigned long long)f.k ? nc : (unsigned long long)f.k);
+}
+
+#define EAB_PROF(slot)                                                                    \
+    if (f.prof) {                                                                         \
+        __syncthreads();                                                                  \
+        if (threadIdx.x == 0) atomicMax(f.prof + (slot), gtimer() - f.prof[15]);          \
+    }
+
+__global__ void __launch_bounds__(256) finish_kernel(const FinishArgs f) {
+    cg::grid_group grid = cg::this_grid();
+    if (f.prof && blockIdx.x == 0 && threadIdx.x == 0) {
+        f.prof[15] = gtimer();
+        __threadfence();
+    }
+    if (f.prof) grid.sync();
+    const int lane = threadIdx.x & 31;
+    if (blockIdx.x == 0 && threadIdx.x == 0 && f.flags) f.ctrl->flags = *f.flags;
+    const float thr = finish_threshold(f.hist, f.k, f.delta);
+    if (blockIdx.x == 0 && threadIdx.x == 0) f.ctrl->thr = thr;
+    EAB_PROF(0)
+    {   // B: warps take 32 consecutive items per item_max load
+        const unsigned long long warp = ((unsigned long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+        const unsigned long long nwarps = ((unsigned long long)gridDim.x * blockDim.x) >> 5;
+        // Lane l of warp w tests item w + l*nwarps (+ 32*nwarps per round):
+        // the qualifying tiles cluster around the peaks (same translation
+        // tile, adjacent thetas) and this spreads them over warps.
+        unsigned long long tb0 = f.prof ? gtimer() : 0;
+        unsigned ntiles = 0;
+        for (unsigned long long b0 = warp; b0 < f.items.n_items; b0 += nwarps * 32) {
+            const unsigned long long it = b0 + (unsigned long long)lane * nwarps;
+            const float m = it < f.items.n_items ? __ldcg(f.item_max + it)
+                                                 : __int_as_float(0x7fffffff);  // NaN: skip
+            unsigned mask = __ballot_sync(0xffffffffu, m >= thr);
+            while (mask) {
+                const int j = __ffs(mask) - 1;
+                mask &= mask - 1;
+                finish_tile(f, b0 + (unsigned long long)j * nwarps, thr, lane);
+                ++ntiles;
+            }
+        }
+        if (f.prof && lane == 0) {
+            atomicMax(f.prof + 8, (unsigned long long)ntiles);
+            atomicMax(f.prof + 10, gtimer() - tb0);
+        }
+    }
+    EAB_PROF(1)
+    grid.sync();
+    EAB_PROF(2)
+    unsigned long long nc = __ldcg(&f.ctrl->cand_count);
+    if (nc > f.cap) nc = f.cap;  // overflow: reported, the caller retries with a larger cap
+    for (unsigned long long c = blockIdx.x; c < nc; c += gridDim.x)
+        finish_rescore(f.x, __ldcg(f.cand + c), f.cand_score + c);
+    EAB_PROF(3)
+    // D on the CTA that finishes C last
+    __shared__ int last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        last = atomicAdd(reinterpret_cast<unsigned*>(&f.ctrl->_unused), 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    if (nc <= (unsigned long long)kRankMax)
+        finish_select(f, nc);
+    else
+        select_body(f.cand, f.cand_score, f.ctrl, f.cap, f.k, f.index_base, f.out_score,
+                    f.out_index);
+    if (threadIdx.x == 0) f.ctrl->_unused = 0;
+    EAB_PROF(4)
+    __syncthreads();
+    if (f.rows) topk_rows_body(f.out_score, f.out_index, f.ctrl, f.cap, f.k, f.rg, f.rows,
+                               f.overflow);
+    EAB_PROF(5)
+}
+#undef EAB_PROF
+
+void launch_finish(ea_ctx* ctx, const FinishArgs& f) {
+    static int per_sm = -1;  // co-resident CTAs per SM (same binary for every device)
+    if (per_sm < 0) {
+        EAB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, finish_kernel, 256, 0));
+        if (per_sm < 1) fail(EA_ERR_CUDA, "finish_kernel cannot be resident");
+    }
+    // One CTA per SM: rescoring is one CTA per candidate; more CTAs only make
+    // the grid barrier dearer for the common case of a handful of candidates.
+    static const int per_sm_use = std::getenv("EAB_FINISH_PER_SM")
+                                      ? std::atoi(std::getenv("EAB_FINISH_PER_SM")) : 1;
+    const unsigned blocks = (unsigned)ctx->sm_count * (unsigned)std::max(1, std::min(per_sm, per_sm_use));
+    FinishArgs fa = f;
+    static unsigned long long* prof = nullptr;  // EAB_FINISH_PROF: phase timestamps
+    static int nprof = 0;
+    if (std::getenv("EAB_FINISH_PROF")) {
+        unsigned long long h[16];
+        if (!prof) {
+            EAB_CUDA(cudaMalloc(&prof, 16 * sizeof(unsigned long long)));
+        } else if (nprof > 0) {
+            EAB_CUDA(cudaStreamSynchronize(ctx->stream));
+            EAB_CUDA(cudaMemcpy(h, prof, sizeof h, cudaMemcpyDeviceToHost));
+            std::fprintf(stderr, "[finish] ns thr/compact/barrier/rescore/select/rows:");
+            for (int i = 0; i < 6; ++i) std::fprintf(stderr, " %llu", h[i]);
+            std::fprintf(stderr, " | tile_load %llu atomic %llu max_tiles/warp %llu tiles %llu warp_B %llu",
+                         h[6], h[7], h[8], h[9], h[10]);
+            std::fprintf(stderr, "\n");
+        }
+        std::memset(h, 0, sizeof h);
+        h[8] = ~0ull;
+        EAB_CUDA(cudaMemcpy(prof, h, sizeof h, cudaMemcpyHostToDevice));
+        ++nprof;
+        fa.prof = prof;
+    }
+    void* args[] = {&fa};
+    EAB_CUDA(cudaLaunchCooperativeKernel((const void*)finish_kernel, dim3(blocks), dim3(256), args,
+                                         0, ctx->stream));
+    check_launch("finish_kernel");
+    count_launch(ctx);
 }
 
 // The `better` merge of several slabs' rows (search.cpp:130-139): rank of
