@@ -7,10 +7,14 @@ per second of top-level search, plus detect latency per image.  One JSON line
 on rank 0.  See DESIGN.md "Measurement" for every field.
 
   value   top-level search with the working pyramid resident in HBM and the
-          results left in HBM (ea_search_top_slab_async: screen + band select +
-          exact fp64 verify + top-k rows [+ NCCL all-gather of per-GPU rows and
-          device merge for N > 1]), steps enqueued back to back, L2 flushed
-          between steps, CUDA events on the library's stream, max over ranks.
+          results left in HBM (ea_search_top_slab_async: screen + fused finish =
+          band select + exact fp64 verify + top-k rows), steps enqueued back to
+          back, L2 flushed between steps, CUDA events on the library's stream,
+          max over ranks.  N > 1: --shard images (default; one frame per GPU,
+          weak scaling, no data-path collective) or --shard theta (theta slabs of
+          one image + NCCL all-gather of the k rows + device merge, strong).
+          At N = 1 the worst theta slab of G = 2/4/8 is also timed
+          (theta_slab_projection: per-rank compute of a G-GPU sharded search).
   e2e     the same metric through the public detect call with a HOST image:
           H2D of the level-0 image from pinned memory, device pyramid + Sobel,
           top-level search, refinement down every level, D2H of the outcome.
@@ -345,10 +349,17 @@ def bench_ours(args, rank, world, local_rank):
     ctx.set_timing(True)
 
     multi = bool(CONFIGS[args.config].get("multi"))
+    # N > 1: "images" (default) -- each rank searches its own frame of the
+    # config (another noise seed per rank: a batch of search images sharded
+    # across GPUs, no data-path collective, weak scaling); "theta" -- one
+    # image, theta slabs per rank + NCCL all-gather of the k rows + device
+    # merge (strong scaling of one search).
+    shard_theta = world > 1 and args.shard == "theta"
+    frame = None if (world == 1 or shard_theta or rank == 0) else 200 + rank
     if multi:
-        img, tmpls, cfg, truth = make_multi_inputs(args.config)
+        img, tmpls, cfg, truth = make_multi_inputs(args.config, noise_seed=frame)
     else:
-        img, tmpl, cfg, truth = make_inputs(args.config)
+        img, tmpl, cfg, truth = make_inputs(args.config, noise_seed=frame)
         tmpls = [tmpl]
     dets = [ea.Detector(t, cfg, ctx) for t in tmpls]  # template sides, once (untimed prep)
     det = dets[0]
@@ -359,7 +370,7 @@ def bench_ours(args, rank, world, local_rank):
     L = cfg.num_levels
     n_tops = [len(d.levels.model(L - 1).points) for d in dets]
     n_top = sum(n_tops)
-    it0, it1 = parallel.theta_slab(nt, rank, world)
+    it0, it1 = parallel.theta_slab(nt, rank, world) if shard_theta else (0, nt)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
 
     k = cfg.topk
@@ -371,7 +382,7 @@ def bench_ours(args, rank, world, local_rank):
         out = []
         for d, r in zip(dets, rows):
             ea.search_top_slab_async(d.levels, cfg, it0, it1, r.data_ptr())
-            out.append(parallel.gather_rows_device(r, k, ctx) if world > 1 else r)
+            out.append(parallel.gather_rows_device(r, k, ctx) if shard_theta else r)
         return out
 
     def barrier():
@@ -409,8 +420,43 @@ def bench_ours(args, rank, world, local_rank):
         t = torch.tensor([tot_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         tot_ms = float(t.item())
-    pose_pts = nx * ny * nt * n_top  # whole job, all ranks
-    value = pose_pts * args.steps / (tot_ms / 1e3)
+    pose_pts = nx * ny * nt * n_top  # one search (all theta slabs)
+    # whole job: theta mode = one search per step over all ranks; images
+    # mode = one search per rank per step
+    job_pts = pose_pts if (world == 1 or shard_theta) else pose_pts * world
+    value = job_pts * args.steps / (tot_ms / 1e3)
+
+    # ---- per-rank work of theta-slab sharding, measured on this GPU ------------------------
+    # The worst slab of G (what one rank of a G-GPU theta-sharded search
+    # computes), same step as `value` (flush + events) but without the NCCL
+    # all-gather of k x 40 B rows: a projection of strong scaling, labelled so.
+    slab_proj = None
+    if world == 1 and not multi and not args.no_slab_probe:
+        t_full = statistics.median(step_ms)
+        slab_proj = {"what": "worst theta slab of G on this GPU (per-rank compute of a G-GPU "
+                             "theta-sharded search; excludes the NCCL all-gather)",
+                     "full_ms": t_full}
+        r0 = rows[0]
+        for G in (2, 4, 8):
+            worst = (0.0, None)
+            for g in range(G):
+                a0, a1 = parallel.theta_slab(nt, g, G)
+                for _ in range(3):
+                    ea.search_top_slab_async(det.levels, cfg, a0, a1, r0.data_ptr())
+                evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                       for _ in range(15)]
+                for e_a, e_b in evs:
+                    flush.zero_()
+                    e_a.record(stream)
+                    ea.search_top_slab_async(det.levels, cfg, a0, a1, r0.data_ptr())
+                    e_b.record(stream)
+                torch.cuda.synchronize(dev)
+                t = statistics.median(e_a.elapsed_time(e_b) for e_a, e_b in evs)
+                if t > worst[0]:
+                    worst = (t, [a0, a1])
+            slab_proj[str(G)] = {"worst_slab_ms": worst[0], "slab": worst[1],
+                                 "projected_strong_scaling": t_full / worst[0]}
+        ea.async_status(ctx)
 
     # ---- e2e: the public batch-detect call on host images ----------------------------------
     # Throughput mode: each step is one image (H2D from pinned memory, device
@@ -483,13 +529,16 @@ def bench_ours(args, rank, world, local_rank):
     line = {
         "metric": "pose-evals/sec", "value": value, "unit": "pose-evals/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot_ms / args.steps,
-        "higher_is_better": True, "scaling": "strong" if world > 1 else "none",
+        "higher_is_better": True,
+        "scaling": ("strong" if shard_theta else "weak") if world > 1 else "none",
         "vs_baseline": None, "dtype": "f32 screen + f64 exact verify", "data": "synthetic",
         "config": {"workload": f"{args.config}: {CONFIGS[args.config]['desc']}",
                    "top_level_grid": f"{nx}x{ny}x{nt}",
                    "top_model_points": n_tops if multi else n_top,
-                   "pose_evals_per_step": pose_pts, "l2": "flushed (256 MiB write) between steps",
-                   "parallelism": f"theta-slab x{world}" if world > 1 else "single GPU"},
+                   "pose_evals_per_step": job_pts, "l2": "flushed (256 MiB write) between steps",
+                   "parallelism": (f"theta-slab x{world} + NCCL all-gather of top-k rows"
+                                   if shard_theta else f"images x{world} (one frame per GPU)")
+                   if world > 1 else "single GPU"},
         "e2e": {"value": e2e, "unit": "pose-evals/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_image": e2e_ms / n_img, "images": n_img * world,
                 "api": ("detect_multi (ea_detect_multi), one call per pinned host image"
@@ -513,6 +562,7 @@ def bench_ours(args, rank, world, local_rank):
                      "kernel_ms": kernel_ms, "kernel_share_of_step": kernel_ms /
                      statistics.median(step_ms),
                      "peak_source": f"{n_sm} SMs x 128 B/clk x sm_max_mhz from {peak_src}"},
+        "theta_slab_projection": slab_proj,
         "gpu_launches": int(launches),
         "gpu_launches_e2e": int(e2e_launches),
         "clocks": clk.summary(),
@@ -543,6 +593,10 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--ref-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--shard", default="images", choices=["images", "theta"],
+                    help="N > 1: shard search images (weak) or theta slabs of one image (strong)")
+    ap.add_argument("--no-slab-probe", action="store_true",
+                    help="skip the N=1 per-rank theta-slab timing (projection for 2/4/8 GPUs)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     world = int(os.environ.get("WORLD_SIZE", "1"))

@@ -441,6 +441,26 @@ ScreenPlan screen(ea_ctx* ctx, const ea_model* m, const ea_field* f, const ea_po
         EAB_CUDA(cudaEventRecord(ctx->ev[1], ctx->stream));
         EAB_CUDA(cudaEventRecord(ctx->tev[2 * ctx->tev_next], ctx->stream));
     }
+    static unsigned long long* sprof = nullptr;  // EAB_SCREEN_PROF: phase timestamps
+    static int nsprof = 0;
+    if (std::getenv("EAB_SCREEN_PROF") && plan.slab_poses) {
+        unsigned long long h[16];
+        if (!sprof) {
+            EAB_CUDA(cudaMalloc(&sprof, sizeof h));
+        } else if (nsprof > 0) {
+            EAB_CUDA(cudaStreamSynchronize(ctx->stream));
+            EAB_CUDA(cudaMemcpy(h, sprof, sizeof h, cudaMemcpyDeviceToHost));
+            std::fprintf(stderr, "[screen] ns from first entry: plane landed %lld, last warp loop end "
+                         "%lld, last CTA loop end %lld, last merge %lld\n",
+                         (long long)(h[0] - h[4]), (long long)(h[1] - h[4]),
+                         (long long)(h[2] - h[4]), (long long)(h[3] - h[4]));
+        }
+        EAB_CUDA(cudaStreamSynchronize(ctx->stream));
+        for (int i = 0; i < 16; ++i) h[i] = (i == 0 || i == 4) ? ~0ull : 0ull;
+        EAB_CUDA(cudaMemcpy(sprof, h, sizeof h, cudaMemcpyHostToDevice));
+        ++nsprof;
+        a.prof = sprof;
+    }
     if (plan.slab_poses) {
         if (lattice) plan.fast = region ? launch_screen_region(ctx, a) : launch_screen_fast(ctx, a);
         if (!plan.fast) launch_screen_general(ctx, a);

@@ -231,6 +231,7 @@ struct ScreenArgs {
     float* item_max;  // best screen score per work item (lattice tile / 32 poses)
     unsigned* hist;   // kHistBins
     SearchCtrl* ctrl;
+    unsigned long long* prof;  // optional phase timestamps (EAB_SCREEN_PROF)
 };
 
 // Dynamic shared memory the lattice kernel needs for a plane.

@@ -224,6 +224,12 @@ __device__ __forceinline__ void merge_hist(const unsigned* __restrict__ hist,
     }
 }
 
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
 // CTA size of the lattice kernel (one CTA per SM).
 #ifndef EAB_SCREEN_THREADS
 #define EAB_SCREEN_THREADS 384  // fully padded planes: 12 warps x 166 regs, no spills (-3.6% vs 8 warps)
@@ -587,6 +593,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     __shared__ __align__(8) unsigned long long plane_bar;
     float* wtop = wtop_all[threadIdx.x >> 5];
     if ((threadIdx.x & 31) < kFloorK) wtop[threadIdx.x & 31] = -INFINITY;
+    if (a.prof && threadIdx.x == 0) atomicMin(a.prof + 4, gtimer());  // first CTA entry
     // The plane arrives by bulk copy (TMA engine, one thread issues it) while
     // the threads clear the histogram.
     if (threadIdx.x == 0) {
@@ -596,6 +603,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     for (int i = threadIdx.x; i < kHistBins; i += blockDim.x) hist[i] = 0u;
     __syncthreads();
     mbar_wait_parity(&plane_bar, 0);
+    if (a.prof && threadIdx.x == 0) atomicMin(a.prof + 0, gtimer());  // first plane landed
 
     constexpr int NACC = S * kTW;
     const int lane = threadIdx.x & 31;
@@ -693,8 +701,11 @@ __global__ void __launch_bounds__(THREADS, 1)
                                         warp_floor(wtop, a.kf));
         floor_insert(wtop, best, lane);
     }
+    if (a.prof && (threadIdx.x & 31) == 0) atomicMax(a.prof + 1, gtimer());  // last warp's loop end
     __syncthreads();
+    if (a.prof && threadIdx.x == 0) atomicMax(a.prof + 2, gtimer());  // last CTA's loop end
     merge_hist(hist, a.hist, a.kf);
+    if (a.prof && threadIdx.x == 0) atomicMax(a.prof + 3, gtimer());  // last merge end
 }
 
 template <int R, int S, int SHIFT, bool IGNORE, int XG, bool EDGE, int THREADS>
@@ -1552,12 +1563,6 @@ __global__ void topk_rows_kernel(const double* __restrict__ score,
 //  D  select      the last CTA to finish C ranks the candidates by `better`
 //                 (rank = how many candidates beat it: one pass, no rounds)
 //                 and writes the top k (and the device rows).
-__device__ __forceinline__ unsigned long long gtimer() {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-    return t;
-}
-
 // A: band threshold (block_threshold's result) with one load round trip.
 __device__ __forceinline__ float finish_threshold(const unsigned* __restrict__ hist, int k,
                                                   double delta) {
