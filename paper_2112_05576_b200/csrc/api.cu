@@ -146,6 +146,7 @@ ea_field* new_field(int w, int h) {
     auto* f = new ea_field;
     f->width = w;
     f->height = h;
+    f->version = next_field_version();
     try {
         f->g.ensure(sizeof(double) * 3 * (size_t)w * h);
     } catch (...) {
@@ -161,6 +162,7 @@ void sobel_into(ea_ctx* ctx, const double* d_img, int w, int h, ea_field* f) {
                               std::to_string(h));
     }
     launch_sobel(ctx, d_img, w, h, f->gx(), f->gy(), f->mag());
+    f->version = next_field_version();
     f->ring_max = 0.0;  // Sobel leaves the border ring at exactly 0
 }
 
@@ -398,8 +400,23 @@ ScreenPlan screen(ea_ctx* ctx, const ea_model* m, const ea_field* f, const ea_po
     }
     const PlaneGeom geom = plane_geom(f->width, f->height, shift, PL, PR, elem);
     void* plane = ctx->plane.ensure(geom.bytes());
-    launch_plane(ctx, f, p.eps_mag, geom, plane, hist, kHistBins,
-                 reinterpret_cast<unsigned*>(ctrl), (int)(sizeof(SearchCtrl) / sizeof(unsigned)));
+    // The plane is a function of the image (field), eps and the geometry:
+    // rebuilt only when one of them changed.  Its kernel also clears the
+    // histogram and control block, which otherwise the previous search's
+    // finish left clear (hist_clean).
+    const std::vector<double> pkey{(double)reinterpret_cast<uintptr_t>(f), (double)f->version,
+                                   p.eps_mag, (double)geom.W, (double)geom.H, (double)geom.PL,
+                                   (double)geom.PR, (double)geom.shift, (double)geom.elem_bytes,
+                                   (double)reinterpret_cast<uintptr_t>(plane)};
+    const bool fused = k >= 1 && ctx->fused_finish;
+    if (pkey != ctx->plane_key || !ctx->hist_clean || !fused) {
+        ctx->plane_key.clear();
+        launch_plane(ctx, f, p.eps_mag, geom, plane, hist, kHistBins,
+                     reinterpret_cast<unsigned*>(ctrl), (int)(sizeof(SearchCtrl) / sizeof(unsigned)));
+        ctx->plane_key = pkey;
+    }
+    // only the fused finish restores the between-searches state
+    ctx->hist_clean = fused;
     float* map = (float*)ctx->map.ensure(sizeof(float) * (plan.slab_poses ? plan.slab_poses : 1));
     float* item_max =
         (float*)ctx->item_max.ensure(sizeof(float) * (plan.slab_poses / 32 + plan.it_count * 64 + 64));
@@ -552,6 +569,7 @@ TopLaunch top_enqueue(ea_ctx* ctx, const ea_model* m, const ea_field* f, const e
         fa.cand = cand;
         fa.cap = cap;
         fa.hist = ctx->hist.as<unsigned>();
+        fa.hist_rw = ctx->hist.as<unsigned>();
         fa.k = k;
         fa.delta = t.plan.delta;
         fa.flags = t.plan.flags;

@@ -1,6 +1,7 @@
 // common.cuh -- shared host/device infrastructure of libedgealign_b200.
 #pragma once
 
+#include <atomic>
 #include <cstdlib>
 #include <cuda_runtime.h>
 
@@ -83,8 +84,16 @@ struct HostBuf {
 }  // namespace eab
 
 // ---- opaque handles of the C-ABI ------------------------------------------
+// Content version of gradient fields: every write (Sobel, upload) takes a
+// new number, so a cache keyed on (field, version) can never go stale.
+inline uint64_t next_field_version() {
+    static std::atomic<uint64_t> v{0};
+    return ++v;
+}
+
 struct ea_field {
     int width = 0, height = 0;
+    uint64_t version = 0;
     double ring_max = INFINITY;  // largest |g| on the outer pixel ring
     eab::DevBuf g;  // gx | gy | mag, each width*height doubles
     double* gx() const { return g.as<double>(); }
@@ -126,6 +135,13 @@ struct ea_ctx {
     ea_search_stats stats{};
     bool timing = false;
     bool trace_on = std::getenv("EAB_TRACE") != nullptr;
+    // Screening plane cache: the float2 plane in `plane` was built from this
+    // (field, version, eps, geometry); a search on the same image skips the
+    // plane kernel.  hist_clean: the histogram / control block are in their
+    // between-searches state (zero hist and work counter), which the fused
+    // finish restores; a screen without a finish (screen_map) clears it.
+    std::vector<double> plane_key;
+    bool hist_clean = false;
     std::vector<std::pair<const char*, cudaEvent_t>> trace;
     // one cooperative finish launch after the screen (EAB_NO_FUSED_FINISH=1:
     // the separate compact/rescore/select/rows launches, for A/B measurements)

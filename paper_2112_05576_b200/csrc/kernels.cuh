@@ -304,6 +304,7 @@ struct FinishArgs {
     unsigned* cand;
     unsigned long long cap;
     const unsigned* hist;
+    unsigned* hist_rw;  // the same histogram, cleared after the threshold
     int k;
     double delta;
     const int* flags;

@@ -594,6 +594,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     float* wtop = wtop_all[threadIdx.x >> 5];
     if ((threadIdx.x & 31) < kFloorK) wtop[threadIdx.x & 31] = -INFINITY;
     if (a.prof && threadIdx.x == 0) atomicMin(a.prof + 4, gtimer());  // first CTA entry
+    if (blockIdx.x == 0 && threadIdx.x == 0) a.ctrl->cand_count = 0ull;  // for the finish
     // The plane arrives by bulk copy (TMA engine, one thread issues it) while
     // the threads clear the histogram.
     if (threadIdx.x == 0) {
@@ -839,6 +840,7 @@ __global__ void __launch_bounds__(kGroup * 32, 1)
     unsigned* hist = reinterpret_cast<unsigned*>(smem);
     float2* P = reinterpret_cast<float2*>(smem + kHistBins * sizeof(unsigned));
     for (int i = threadIdx.x; i < kHistBins; i += blockDim.x) hist[i] = 0u;
+    if (blockIdx.x == 0 && threadIdx.x == 0) a.ctrl->cand_count = 0ull;  // for the finish
     __shared__ float wtop_all[kGroup][kFloorK];
     float* wtop = wtop_all[threadIdx.x >> 5];
     if ((threadIdx.x & 31) < kFloorK) wtop[threadIdx.x & 31] = -INFINITY;
@@ -992,6 +994,7 @@ __global__ void __launch_bounds__(256)
     screen_general_kernel(const ScreenArgs a, unsigned long long total, const int* tlist) {
     __shared__ unsigned hist[kHistBins];
     for (int i = threadIdx.x; i < kHistBins; i += blockDim.x) hist[i] = 0u;
+    if (blockIdx.x == 0 && threadIdx.x == 0) a.ctrl->cand_count = 0ull;  // for the finish
     __syncthreads();
     const unsigned long long plane_poses = a.nx * a.ny;
     // list mode: logical theta j -> slab theta tlist[j + 1], tlist[0] entries
@@ -1787,6 +1790,12 @@ __global__ void __launch_bounds__(256) finish_kernel(const FinishArgs f) {
     EAB_PROF(1)
     grid.sync();
     EAB_PROF(2)
+    // Every CTA has read the histogram: leave it zero, and the screen's work
+    // counter at 0, for the next search (which may skip the plane kernel that
+    // would otherwise clear them).
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < kHistBins; i += gridDim.x * blockDim.x)
+        f.hist_rw[i] = 0u;
+    if (blockIdx.x == 0 && threadIdx.x == 0) f.ctrl->work_counter = 0ull;
     unsigned long long nc = __ldcg(&f.ctrl->cand_count);
     if (nc > f.cap) nc = f.cap;  // overflow: reported, the caller retries with a larger cap
     for (unsigned long long c = blockIdx.x; c < nc; c += gridDim.x)

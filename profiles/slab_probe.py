@@ -58,6 +58,7 @@ def main():
     for G, slabs in plans:
         G = int(G)
         worst = None
+        allrec = []
         for it0, it1 in slabs:
             for _ in range(args.warmup):
                 ea.search_top_slab_async(det.levels, cfg, it0, it1, rows.data_ptr())
@@ -81,8 +82,10 @@ def main():
             scr = statistics.median(times) if times else None
             rec = {"slab": [it0, it1], "step_ms": step, "screen_ms": scr, "host_enqueue_ms": host_ms,
                    "other_ms": step - scr if scr is not None else None}
+            allrec.append((round(step, 4), round(scr, 4) if scr else None))
             if worst is None or step > worst["step_ms"]:
                 worst = rec
+        worst["all_step_screen_ms"] = allrec
         out["slabs"][G] = worst
     t1 = out["slabs"][1]["step_ms"] if 1 in out["slabs"] and not args.sizes else None
     for G, rec in out["slabs"].items():

@@ -677,3 +677,36 @@ def test_gather_rows_device_nccl_single_rank(ea, oracle):
     finally:
         dist.destroy_process_group()
         det.ctx.set_stream(None)
+
+
+def test_plane_cache_follows_field_and_params(ea, oracle):
+    """The screening plane is cached per (field, version, eps, geometry): a
+    search must see a new image after set_image (same field objects), another
+    field, another eps, and a screen_map (which leaves the histogram dirty)
+    between searches -- each result equal to the oracle's."""
+    rng = np.random.default_rng(2024)
+    m = rand_model(oracle, rng, 14)
+    imgs = [rand_image(rng, 48, 40) for _ in range(3)]
+    fields = [oracle.compute_gradients(im) for im in imgs]
+    dfields = [ea.DeviceField.upload(f) for f in fields]
+    grid = ea.PoseGrid(0, 47, 1, 0, 39, 1, 0.0, D(350), D(10))
+    dm = ea.DeviceModel(m)
+    seq = [(0, 1e-9), (1, 1e-9), (0, 1e-9), (0, 5.0), (2, 1e-9), ("map", 1e-9), (2, 1e-9),
+           (1, 5.0), (1, 5.0)]
+    for which, eps in seq:
+        params = ea.ScoreParams(3, 0, eps)
+        if which == "map":
+            ea.screen_map(dm, dfields[2], grid, params)
+            continue
+        got = ea.search_topk(dm, dfields[which], grid, params, k=5)
+        want = oracle.search_topk(m.points, fields[which], grid, params, 5)
+        assert keys(got) == keys(want), (which, eps)
+    # same levels object, new images (the fields are rewritten in place)
+    tmpl = imgs[0][4:36, 8:40]
+    cfg = ea.SearchConfig(grid=ea.PoseGrid(0, 47, 2, 0, 39, 2, 0.0, D(350), D(10)),
+                          num_levels=2, score_params=ea.ScoreParams(3))
+    det = ea.Detector(tmpl, cfg)
+    tp = oracle.build_pyramid(tmpl, 2)
+    for im in imgs + imgs[:1]:
+        got = det.detect(im)
+        assert got.key() == oracle.coarse_to_fine(tp, oracle.build_pyramid(im, 2), cfg).key()
