@@ -40,7 +40,7 @@ struct RefineArgs {
     ea_outcome* outcome;  // device copy of the result
 };
 
-constexpr int kRefineThreads = 128;               // threads per pose (refine_entry_kernel)
+constexpr int kRefineThreads = 256;               // threads per pose (refine_entry_kernel)
 constexpr size_t kRefineSmemMax = 96 * 1024;      // vote rows in smem up to this size
 void launch_refine_level(ea_ctx* ctx, const RefineArgs& a);
 

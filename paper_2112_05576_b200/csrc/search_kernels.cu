@@ -475,10 +475,12 @@ __device__ __forceinline__ int run_entries(const int4* __restrict__ ent, const i
     int done = 0;
     int lo = 0;
     const int bounds[3] = {hdr.x, hdr.y, hdr.z};
+    const int lane = threadIdx.x & 31;
 #pragma unroll
     for (int t = 0; t < 3; ++t) {
         const int hi = lo + bounds[t];
         const int b = max(lo, e0), e = min(hi, e1);
+#ifdef EAB_ENTRY_PREFETCH
         if (b < e) {
             int4 p = __ldg(ent + 2 * b), q = __ldg(ent + 2 * b + 1);
             for (int i = b; i < e; ++i) {
@@ -499,6 +501,38 @@ __device__ __forceinline__ int run_entries(const int4* __restrict__ ent, const i
                 q = qn;
             }
         }
+#else
+        // Entries arrive 32 at a time, one per lane, and are broadcast by
+        // shuffles: no global load sits inside the row loop (a per-entry
+        // prefetch shared a scoreboard with the shared-memory loads and
+        // stalled the FMAs on L2 latency).
+        for (int base = b; base < e; base += 32) {
+            const int mine = base + lane;
+            int4 pl = make_int4(0, 0, 0, 0), ql = make_int4(0, 0, 0, 0);
+            if (mine < e) {
+                pl = __ldg(ent + 2 * mine);
+                if (t != 0) ql = __ldg(ent + 2 * mine + 1);
+            }
+            const int cnt = min(32, e - base);
+            for (int j = 0; j < cnt; ++j) {
+                int4 p;
+                p.x = __shfl_sync(0xffffffffu, pl.x, j);
+                p.y = __shfl_sync(0xffffffffu, pl.y, j);
+                p.z = __shfl_sync(0xffffffffu, pl.z, j);
+                p.w = __shfl_sync(0xffffffffu, pl.w, j);
+                if (t == 0) {
+                    one_entry<R, S, SHIFT, IGNORE, EDGE, STRIP, 1, 0>(g, p, 0.f, 0.f, K, acc);
+                } else {
+                    const float dx2 = __int_as_float(__shfl_sync(0xffffffffu, ql.z, j));
+                    const float dy2 = __int_as_float(__shfl_sync(0xffffffffu, ql.w, j));
+                    if (t == 1)
+                        one_entry<R, S, SHIFT, IGNORE, EDGE, STRIP, 2, 0>(g, p, dx2, dy2, K, acc);
+                    else
+                        one_entry<R, S, SHIFT, IGNORE, EDGE, STRIP, 2, 1>(g, p, dx2, dy2, K, acc);
+                }
+            }
+        }
+#endif
         if (e > b) done += (e - b) * (t == 0 ? 1 : 2);
         lo = hi;
     }
