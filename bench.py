@@ -108,8 +108,8 @@ def batch_scenes(name, count):
 # DRAM read + write of one screen-kernel launch, from `ncu --set full` captures
 # (not measurable inside the timed run); per config.
 TRAFFIC = {
-    "cfg2": (6613760, "profiles/r01_screen_fast_ncu.txt (cfg2 launch)"),
-    "cfg4": (6613760, "profiles/r01_screen_fast_ncu.txt (cfg2 geometry)"),
+    "cfg2": (7497728, "profiles/r01_screen_fast_ncu.txt (cfg2 launch)"),
+    "cfg4": (7497728, "profiles/r01_screen_fast_ncu.txt (cfg2 geometry)"),
     "cfg5": (390487040, "profiles/r01_screen_region_ncu.txt (cfg5 model 5 launch; "
                         "the 227 MB fp32 map is written through to DRAM)"),
 }
