@@ -710,3 +710,25 @@ def test_plane_cache_follows_field_and_params(ea, oracle):
     for im in imgs + imgs[:1]:
         got = det.detect(im)
         assert got.key() == oracle.coarse_to_fine(tp, oracle.build_pyramid(im, 2), cfg).key()
+
+
+@pytest.mark.parametrize("case", [0, 3, len(SEARCH_CASES) - 1])
+def test_unfused_finish_path_matches(ea, oracle, monkeypatch, case):
+    """EAB_NO_FUSED_FINISH=1 (read at context creation) runs the separate
+    compact / rescore / select kernels instead of the cooperative finish
+    kernel: both must give the oracle's top k, on contexts used back to back."""
+    size, w, h, g, nb, pol = SEARCH_CASES[case]
+    rng = np.random.default_rng(300 + case)
+    m = rand_model(oracle, rng, size)
+    f = oracle.compute_gradients(rand_image(rng, w, h))
+    grid = ea.PoseGrid(*g)
+    params = ea.ScoreParams(nb, pol)
+    want = keys(oracle.search_topk(m.points, f, grid, params, 7))
+    monkeypatch.setenv("EAB_NO_FUSED_FINISH", "1")
+    ctx_sep = ea.Context(0)
+    monkeypatch.delenv("EAB_NO_FUSED_FINISH")
+    ctx_fused = ea.Context(0)
+    for ctx in (ctx_sep, ctx_fused, ctx_sep):
+        assert keys(ea.search_topk(m, f, grid, params, k=7, ctx=ctx)) == want
+    ctx_sep.close()
+    ctx_fused.close()
