@@ -1458,6 +1458,46 @@ void build_working_into(ea_ctx* ctx, std::vector<ea_field*>& fields, DevBuf& ima
     }
     const size_t elems = pyramid_elems(w / 2, h / 2, std::max(levels - 1, 1));
     double* d = (double*)image.ensure(sizeof(double) * (elems ? elems : 1));
+    if (levels >= 1 && levels <= kMaxFusedLevels && w >= 3 && h >= 3 &&
+        levels <= pyramid_levels_feasible(w, h)) {
+        // one launch for the whole pyramid + every level's gradient field
+        PyramidFieldsArgs pa{};
+        pa.img0 = d_level0;
+        pa.levels = levels;
+        double* dst = d;
+        int lw = w, lh = h;
+        for (int l = 0; l < levels; ++l) {
+            if (l > 0) {
+                pa.img[l] = dst;
+                dst += (size_t)lw * lh;
+            }
+            pa.w[l] = lw;
+            pa.h[l] = lh;
+            if (l < (int)fields.size() && (fields[l]->width != lw || fields[l]->height != lh)) {
+                delete fields[l];
+                fields[l] = nullptr;
+            }
+            if (l >= (int)fields.size()) fields.push_back(nullptr);
+            if (!fields[l]) fields[l] = new_field(lw, lh);
+            pa.gx[l] = fields[l]->gx();
+            pa.gy[l] = fields[l]->gy();
+            pa.mag[l] = fields[l]->mag();
+            lw /= 2;
+            lh /= 2;
+        }
+        const bool small = pa.w[levels - 1] < 3 || pa.h[levels - 1] < 3;
+        if (!small && launch_pyramid_fields(ctx, pa)) {
+            for (int l = 0; l < levels; ++l) {
+                fields[l]->version = next_field_version();
+                fields[l]->ring_max = 0.0;  // Sobel leaves the border ring at exactly 0
+            }
+            while ((int)fields.size() > levels) {
+                delete fields.back();
+                fields.pop_back();
+            }
+            return;
+        }
+    }
     std::vector<const double*> srcs;
     std::vector<int> dims;
     device_pyramid_from(ctx, d_level0, d, w, h, levels, &srcs, &dims);

@@ -5,6 +5,8 @@
 // multiply-add is contracted (the reference builds with -ffp-contract=off,
 // proj/CMakeLists.txt:12-14) and every value is bit-identical to the
 // reference's scalar kernels (proj/src/simd/kernels_scalar.cpp:14-37).
+#include <cstdlib>
+
 #include "kernels.cuh"
 
 namespace eab {
@@ -90,6 +92,133 @@ __global__ void plane_kernel(const double* __restrict__ gx, const double* __rest
         }
     }
     plane[(size_t)yp * PW + (yp >> shift) + xp] = make_float2((float)nx, (float)ny);
+}
+
+// The whole working pyramid of one image in ONE launch: a CTA owns a TT x TT
+// tile of the top level, i.e. a (TT << (L-1-l))-square tile of level l, and
+// keeps in shared memory each level's tile plus the halo its Sobel and the
+// levels above need (h_l = 2^(L-1-l) pixels: 1 at the top, doubling down).
+// It loads the level-0 region once, builds levels 1..L-1 by the 2x2 box
+// (downsample_kernel's arithmetic), and writes every level's image (l >= 1)
+// and gradient field (sobel_kernel's arithmetic, zero ring) for its tile.
+// Pixels of a region outside the level are never a source of an in-range
+// pixel (floor halving) and only feed border pixels, whose output is 0.
+// Replaces 2L - 1 dependent launches (and L reads of the level images).
+__global__ void __launch_bounds__(256) pyramid_fields_kernel(const PyramidFieldsArgs a) {
+    extern __shared__ double ps[];
+    const int L = a.levels, TT = a.tile;
+    // level l's region starts after the regions of levels 0..l-1
+    auto reg = [&](int l) {
+        int off = 0;
+        for (int j = 0; j < l; ++j) {
+            const int R = (TT + 2) << (L - 1 - j);
+            off += R * R;
+        }
+        return ps + off;
+    };
+    // level 0 region: [X0 - h0, X0 + T0 + h0) x same in y
+    {
+        const int h0 = 1 << (L - 1), T0 = TT << (L - 1), R = T0 + 2 * h0;
+        const int x0 = blockIdx.x * T0 - h0, y0 = blockIdx.y * T0 - h0;
+        const int W = a.w[0], H = a.h[0];
+        double* r0 = reg(0);
+        for (int i = threadIdx.x; i < R * R; i += blockDim.x) {
+            const int ry = i / R, rx = i - ry * R;
+            const int x = x0 + rx, y = y0 + ry;
+            r0[i] = (x >= 0 && x < W && y >= 0 && y < H) ? __ldg(a.img0 + (size_t)y * W + x) : 0.0;
+        }
+    }
+    __syncthreads();
+    for (int l = 1; l < L; ++l) {  // level l region from level l-1 region (2x2 box)
+        const int hl = 1 << (L - 1 - l), Tl = TT << (L - 1 - l), R = Tl + 2 * hl;
+        const int Rp = 2 * R;  // level l-1 region side
+        const int x0 = blockIdx.x * Tl - hl, y0 = blockIdx.y * Tl - hl;
+        const int W = a.w[l], H = a.h[l];
+        double* out = a.img[l];
+        const double* prev = reg(l - 1);
+        double* cur = reg(l);
+        for (int i = threadIdx.x; i < R * R; i += blockDim.x) {
+            const int ry = i / R, rx = i - ry * R;
+            const double* top = prev + (size_t)(2 * ry) * Rp + 2 * rx;
+            const double t = __dadd_rn(top[0], top[1]);
+            const double u = __dadd_rn(top[Rp], top[Rp + 1]);
+            const double v = __dmul_rn(__dadd_rn(t, u), 0.25);
+            cur[i] = v;
+            const int x = x0 + rx, y = y0 + ry;
+            if (rx >= hl && rx < hl + Tl && ry >= hl && ry < hl + Tl && x < W && y < H)
+                out[(size_t)y * W + x] = v;  // the tile's own pixels of the level image
+        }
+        __syncthreads();
+    }
+    for (int l = 0; l < L; ++l) {  // Sobel of each level's tile
+        const int hl = 1 << (L - 1 - l), Tl = TT << (L - 1 - l), R = Tl + 2 * hl;
+        const int W = a.w[l], H = a.h[l];
+        const int x0 = blockIdx.x * Tl, y0 = blockIdx.y * Tl;
+        double* gx = a.gx[l];
+        double* gy = a.gy[l];
+        double* mg = a.mag[l];
+        const double* rl = reg(l);
+        for (int i = threadIdx.x; i < Tl * Tl; i += blockDim.x) {
+            const int ty = i / Tl, tx = i - ty * Tl;
+            const int x = x0 + tx, y = y0 + ty;
+            if (x >= W || y >= H) continue;
+            const size_t o = (size_t)y * W + x;
+            if (x == 0 || y == 0 || x == W - 1 || y == H - 1) {
+                gx[o] = 0.0;
+                gy[o] = 0.0;
+                mg[o] = 0.0;
+                continue;
+            }
+            const double* mid = rl + (size_t)(ty + hl) * R + (tx + hl);
+            const double* above = mid - R;
+            const double* below = mid + R;
+            const double aa = above[-1], b = above[0], c = above[1];
+            const double d = mid[-1], f = mid[1];
+            const double g = below[-1], hh = below[0], ii = below[1];
+            const double ew = __dsub_rn(f, d);
+            const double ns = __dsub_rn(hh, b);
+            const double sx =
+                __dadd_rn(__dadd_rn(__dsub_rn(c, aa), __dadd_rn(ew, ew)), __dsub_rn(ii, g));
+            const double sy =
+                __dadd_rn(__dadd_rn(__dsub_rn(g, aa), __dadd_rn(ns, ns)), __dsub_rn(ii, c));
+            gx[o] = sx;
+            gy[o] = sy;
+            mg[o] = __dsqrt_rn(__dadd_rn(__dmul_rn(sx, sx), __dmul_rn(sy, sy)));
+        }
+    }
+}
+
+size_t pyramid_fields_smem(int levels, int tile) {
+    size_t n = 0;
+    for (int l = 0; l < levels; ++l) {
+        const size_t R = (size_t)(tile + 2) << (levels - 1 - l);
+        n += R * R;
+    }
+    return n * sizeof(double);
+}
+
+bool launch_pyramid_fields(ea_ctx* ctx, const PyramidFieldsArgs& a_in) {
+    if (a_in.levels < 1 || a_in.levels > kMaxFusedLevels) return false;
+    if (std::getenv("EAB_NO_FUSED_PYRAMID")) return false;
+    PyramidFieldsArgs a = a_in;
+    // largest power-of-two top tile (<= 16) whose regions fit in 100 KB
+    int tile = 16;
+    while (tile > 2 && pyramid_fields_smem(a.levels, tile) > 100 * 1024) tile /= 2;
+    const size_t smem = pyramid_fields_smem(a.levels, tile);
+    if (smem > 100 * 1024) return false;
+    a.tile = tile;
+    static bool attr_set = false;
+    if (!attr_set) {
+        EAB_CUDA(cudaFuncSetAttribute(pyramid_fields_kernel,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
+        attr_set = true;
+    }
+    const int T0 = tile << (a.levels - 1);
+    dim3 grid((a.w[0] + T0 - 1) / T0, (a.h[0] + T0 - 1) / T0);
+    pyramid_fields_kernel<<<grid, 256, smem, ctx->stream>>>(a);
+    check_launch("pyramid_fields_kernel");
+    count_launch(ctx);
+    return true;
 }
 
 void launch_downsample(ea_ctx* ctx, const double* in, int w, int h, double* out) {

@@ -180,6 +180,21 @@ __device__ __forceinline__ double lattice(double base, unsigned long long i, dou
 
 // ---- launchers ---------------------------------------------------------------
 void launch_downsample(ea_ctx* ctx, const double* in, int w, int h, double* out);
+// Pyramid levels 1..L-1 and the gradient fields of levels 0..L-1 of one
+// image in one launch (pyramid_fields_kernel); false = not launched (too many
+// levels for the shared-memory tiles, or EAB_NO_FUSED_PYRAMID): use
+// launch_downsample + launch_sobel.
+constexpr int kMaxFusedLevels = 6;
+struct PyramidFieldsArgs {
+    const double* img0;
+    int levels, tile;
+    int w[kMaxFusedLevels], h[kMaxFusedLevels];
+    double* img[kMaxFusedLevels];  // level images (index 0 unused)
+    double* gx[kMaxFusedLevels];
+    double* gy[kMaxFusedLevels];
+    double* mag[kMaxFusedLevels];
+};
+bool launch_pyramid_fields(ea_ctx* ctx, const PyramidFieldsArgs& a);
 void launch_sobel(ea_ctx* ctx, const double* img, int w, int h, double* gx, double* gy,
                   double* mag);
 // Screening plane (float2 g/|g|, zero ring/columns/strip) + clears

@@ -732,3 +732,28 @@ def test_unfused_finish_path_matches(ea, oracle, monkeypatch, case):
         assert keys(ea.search_topk(m, f, grid, params, k=7, ctx=ctx)) == want
     ctx_sep.close()
     ctx_fused.close()
+
+
+@pytest.mark.parametrize("w,h,L", [(160, 160, 1), (333, 257, 4), (162, 121, 2), (648, 486, 5),
+                                   (517, 389, 6), (97, 64, 3)])
+def test_fused_pyramid_fields_bit_exact(ea, oracle, monkeypatch, w, h, L):
+    """set_image builds every level's image and gradient field in one kernel
+    (pyramid_fields_kernel, odd sizes, 1-6 levels); EAB_NO_FUSED_PYRAMID=1
+    runs the per-level downsample + Sobel kernels.  Both equal the oracle."""
+    rng = np.random.default_rng(w * 7 + h * 3 + L)
+    tmpl = rand_image(rng, 8 << (L - 1), 8 << (L - 1), real=True)
+    img = rand_image(rng, w, h, real=True)
+    cfg = ea.SearchConfig(grid=ea.PoseGrid(0, w - 1, 1 << (L - 1), 0, h - 1, 1 << (L - 1),
+                                           0.0, D(90), D(45)), num_levels=L)
+    tp = oracle.build_pyramid(tmpl, L)
+    wp = oracle.build_pyramid(img, L)
+    want = [oracle.compute_gradients(level) for level in wp]
+    lv = ea.prepare_levels(tp, wp, cfg)
+    for fused in (True, False):
+        if not fused:
+            monkeypatch.setenv("EAB_NO_FUSED_PYRAMID", "1")
+        lv.set_image(img)
+        for l in range(L):
+            for a, b in zip(lv.field(l), want[l]):
+                assert np.array_equal(a, b), (fused, l)
+    monkeypatch.delenv("EAB_NO_FUSED_PYRAMID", raising=False)
