@@ -122,10 +122,24 @@ __global__ void __launch_bounds__(256) pyramid_fields_kernel(const PyramidFields
         const int x0 = blockIdx.x * T0 - h0, y0 = blockIdx.y * T0 - h0;
         const int W = a.w[0], H = a.h[0];
         double* r0 = reg(0);
-        for (int i = threadIdx.x; i < R * R; i += blockDim.x) {
-            const int ry = i / R, rx = i - ry * R;
-            const int x = x0 + rx, y = y0 + ry;
-            r0[i] = (x >= 0 && x < W && y >= 0 && y < H) ? __ldg(a.img0 + (size_t)y * W + x) : 0.0;
+        // 32 x 8 threads: coalesced rows, four row-loads in flight per thread
+        const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+        for (int ry0 = 0; ry0 < R; ry0 += 32) {
+            for (int rx = tx; rx < R; rx += 32) {
+                const int x = x0 + rx;
+                double v[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int ry = ry0 + ty + 8 * q, y = y0 + ry;
+                    v[q] = (ry < R && x >= 0 && x < W && y >= 0 && y < H)
+                               ? __ldg(a.img0 + (size_t)y * W + x) : 0.0;
+                }
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int ry = ry0 + ty + 8 * q;
+                    if (ry < R) r0[ry * R + rx] = v[q];
+                }
+            }
         }
     }
     __syncthreads();
@@ -137,8 +151,10 @@ __global__ void __launch_bounds__(256) pyramid_fields_kernel(const PyramidFields
         double* out = a.img[l];
         const double* prev = reg(l - 1);
         double* cur = reg(l);
-        for (int i = threadIdx.x; i < R * R; i += blockDim.x) {
-            const int ry = i / R, rx = i - ry * R;
+        const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+        for (int ry = ty; ry < R; ry += 8)
+        for (int rx = tx; rx < R; rx += 32) {
+            const int i = ry * R + rx;
             const double* top = prev + (size_t)(2 * ry) * Rp + 2 * rx;
             const double t = __dadd_rn(top[0], top[1]);
             const double u = __dadd_rn(top[Rp], top[Rp + 1]);
@@ -158,8 +174,9 @@ __global__ void __launch_bounds__(256) pyramid_fields_kernel(const PyramidFields
         double* gy = a.gy[l];
         double* mg = a.mag[l];
         const double* rl = reg(l);
-        for (int i = threadIdx.x; i < Tl * Tl; i += blockDim.x) {
-            const int ty = i / Tl, tx = i - ty * Tl;
+        const int lx = threadIdx.x & 31, ly = threadIdx.x >> 5;
+        for (int ty = ly; ty < Tl; ty += 8)
+        for (int tx = lx; tx < Tl; tx += 32) {
             const int x = x0 + tx, y = y0 + ty;
             if (x >= W || y >= H) continue;
             const size_t o = (size_t)y * W + x;
@@ -202,8 +219,10 @@ bool launch_pyramid_fields(ea_ctx* ctx, const PyramidFieldsArgs& a_in) {
     if (std::getenv("EAB_NO_FUSED_PYRAMID")) return false;
     PyramidFieldsArgs a = a_in;
     // largest power-of-two top tile (<= 16) whose regions fit in 100 KB
+    // (a tile below 8 reads the level-0 halo >= 2.25x over: slower than the
+    // per-level kernels -- measured on cfg3, 5 levels)
     int tile = 16;
-    while (tile > 2 && pyramid_fields_smem(a.levels, tile) > 100 * 1024) tile /= 2;
+    while (tile > 8 && pyramid_fields_smem(a.levels, tile) > 100 * 1024) tile /= 2;
     const size_t smem = pyramid_fields_smem(a.levels, tile);
     if (smem > 100 * 1024) return false;
     a.tile = tile;
