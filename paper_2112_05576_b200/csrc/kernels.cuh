@@ -56,7 +56,7 @@ struct SearchCtrl {
     unsigned long long work_counter;  // dynamic work distribution of the screen kernel
     unsigned long long cand_count;    // poses admitted by the band threshold
     unsigned long long needed;        // histogram upper bound of cand_count
-    int _unused;
+    unsigned finish_ticket;           // CTAs of the fused finish done with the rescore phase
     int flags;                        // rounding-ambiguous (theta, point) pairs
     float thr;                        // band threshold on the fp32 screen score
     int n_out;                        // entries written to the top-k output

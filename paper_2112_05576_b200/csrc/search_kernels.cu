@@ -1840,7 +1840,7 @@ __global__ void __launch_bounds__(256) finish_kernel(const FinishArgs f) {
     __syncthreads();
     if (threadIdx.x == 0) {
         __threadfence();
-        last = atomicAdd(reinterpret_cast<unsigned*>(&f.ctrl->_unused), 1u) == gridDim.x - 1;
+        last = atomicAdd(&f.ctrl->finish_ticket, 1u) == gridDim.x - 1;
     }
     __syncthreads();
     if (!last) return;
@@ -1850,7 +1850,7 @@ __global__ void __launch_bounds__(256) finish_kernel(const FinishArgs f) {
     else
         select_body(f.cand, f.cand_score, f.ctrl, f.cap, f.k, f.index_base, f.out_score,
                     f.out_index);
-    if (threadIdx.x == 0) f.ctrl->_unused = 0;
+    if (threadIdx.x == 0) f.ctrl->finish_ticket = 0u;
     EAB_PROF(4)
     __syncthreads();
     if (f.rows) topk_rows_body(f.out_score, f.out_index, f.ctrl, f.cap, f.k, f.rg, f.rows,
