@@ -946,12 +946,13 @@ struct RefineState {
     int* cnt[2];
 };
 
-// slot 0/1: two independent states (batch mode refines image i on the refine
-// stream while image i+1's top level seeds the other one).
+// slot 0..2: independent states (batch mode refines image i on the refine
+// stream while later images' top levels seed the other ones).
+constexpr int kBatchSets = 3;
 RefineState refine_state(ea_ctx* ctx, int k, int slot = 0) {
     const size_t beam_bytes = sizeof(BeamDev) * (size_t)k;
     const size_t one = (sizeof(ea_outcome) + 2 * beam_bytes + 4 * sizeof(int) + 255) & ~(size_t)255;
-    char* b = (char*)ctx->rstate.ensure(2 * one) + one * slot;
+    char* b = (char*)ctx->rstate.ensure(kBatchSets * one) + one * slot;
     RefineState r;
     r.out = (ea_outcome*)b;
     r.beam[0] = (BeamDev*)(b + sizeof(ea_outcome));
@@ -1192,12 +1193,13 @@ void detect_batch(ea_ctx* ctx, ea_levels* lv, const double* const* images, int c
     }
     for (auto& e : ctx->rev)
         if (!e) EAB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    // Two working sets (pyramid + fields) and two refinement states: image i
-    // refines on the refine stream from set/state i&1 while image i+1 builds
-    // its pyramid and searches its top level on the compute stream (the
-    // latency-bound refinement kernels fill the SMs the screen kernel leaves).
-    std::vector<ea_field*>* sets[2] = {&lv->fields, &lv->fields2};
-    DevBuf* images_b[2] = {&lv->image, &lv->image2};
+    // Three working sets (pyramid + fields) and refinement states: image i
+    // refines on the refine stream from set/state i%3 while images i+1, i+2
+    // build their pyramids and search their top levels on the compute stream.
+    // (With two sets image i+1 had to wait for image i-1's refinement, which
+    // the screen kernel -- holding every SM -- pushes behind itself.)
+    std::vector<ea_field*>* sets[kBatchSets] = {&lv->fields, &lv->fields2, &lv->fields3};
+    DevBuf* images_b[kBatchSets] = {&lv->image, &lv->image2, &lv->image3};
     const int top = L - 1;
     const ea_pose_grid tg = top_grid_of(cfg);
     const ea_grid_counts gc = counts_of(tg);
@@ -1206,17 +1208,18 @@ void detect_batch(ea_ctx* ctx, ea_levels* lv, const double* const* images, int c
     sync(ctx);
     cudaStream_t main_stream = ctx->stream;
     for (int i = 0; i < count; ++i) {
-        const int b = i & 1;
-        // copy stream: wait until image i-2 released buffer b, then H2D image i
-        if (i >= 2) EAB_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ctx->bev[2 + b], 0));
-        EAB_CUDA(cudaMemcpyAsync(raw[b], images[i], img_bytes, cudaMemcpyHostToDevice,
+        const int b = i % kBatchSets;  // working set + refinement state
+        const int rb = i & 1;          // level-0 upload buffer
+        // copy stream: wait until image i-2 released buffer rb, then H2D image i
+        if (i >= 2) EAB_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ctx->bev[2 + rb], 0));
+        EAB_CUDA(cudaMemcpyAsync(raw[rb], images[i], img_bytes, cudaMemcpyHostToDevice,
                                  ctx->copy_stream));
-        EAB_CUDA(cudaEventRecord(ctx->bev[b], ctx->copy_stream));
-        // compute stream: set b is free once image i-2's refinement is done
-        EAB_CUDA(cudaStreamWaitEvent(main_stream, ctx->bev[b], 0));
-        if (i >= 2) EAB_CUDA(cudaStreamWaitEvent(main_stream, ctx->rev[2 + b], 0));
-        build_working_into(ctx, *sets[b], *images_b[b], raw[b], w, h, L);
-        EAB_CUDA(cudaEventRecord(ctx->bev[2 + b], main_stream));
+        EAB_CUDA(cudaEventRecord(ctx->bev[rb], ctx->copy_stream));
+        // compute stream: set b is free once image i-3's refinement is done
+        EAB_CUDA(cudaStreamWaitEvent(main_stream, ctx->bev[rb], 0));
+        if (i >= kBatchSets) EAB_CUDA(cudaStreamWaitEvent(main_stream, ctx->rev[kBatchSets + b], 0));
+        build_working_into(ctx, *sets[b], *images_b[b], raw[rb], w, h, L);
+        EAB_CUDA(cudaEventRecord(ctx->bev[2 + rb], main_stream));
         ea_levels view;  // template side + working set b (not owned)
         view.models = lv->models;
         view.fields = *sets[b];
@@ -1253,15 +1256,16 @@ void detect_batch(ea_ctx* ctx, ea_levels* lv, const double* const* images, int c
             throw;
         }
         ctx->stream = main_stream;
-        EAB_CUDA(cudaEventRecord(ctx->rev[2 + b], ctx->refine_stream));
+        EAB_CUDA(cudaEventRecord(ctx->rev[kBatchSets + b], ctx->refine_stream));
     }
     sync(ctx);
     EAB_CUDA(cudaStreamSynchronize(ctx->refine_stream));
     EAB_CUDA(cudaStreamSynchronize(ctx->copy_stream));
-    if ((count - 1) & 1) {  // keep "the working side is the last image's"
-        std::swap(lv->fields, lv->fields2);
-        std::swap(lv->image.p, lv->image2.p);
-        std::swap(lv->image.cap, lv->image2.cap);
+    const int last = (count - 1) % kBatchSets;  // keep "the working side is the last image's"
+    if (last > 0) {
+        std::swap(lv->fields, *sets[last]);
+        std::swap(lv->image.p, images_b[last]->p);
+        std::swap(lv->image.cap, images_b[last]->cap);
     }
     for (int i = 0; i < count; ++i) {
         SearchCtrl hc;
@@ -1445,6 +1449,7 @@ void free_levels(ea_levels* lv) {
     for (auto* m : lv->models) delete m;
     for (auto* f : lv->fields) delete f;
     for (auto* f : lv->fields2) delete f;
+    for (auto* f : lv->fields3) delete f;
     delete lv;
 }
 

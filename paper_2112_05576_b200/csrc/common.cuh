@@ -121,8 +121,10 @@ struct ea_levels {
     std::vector<ea_field*> fields;  // owned; may be empty until set_image
     eab::DevBuf image;              // working pyramid levels >= 1
     eab::DevBuf raw[2];             // level-0 images (double-buffered in batch mode)
-    std::vector<ea_field*> fields2; // batch mode: second working set (owned)
+    std::vector<ea_field*> fields2; // batch mode: second and third working sets (owned)
     eab::DevBuf image2;
+    std::vector<ea_field*> fields3;
+    eab::DevBuf image3;
 };
 
 struct ea_ctx {
@@ -161,7 +163,7 @@ struct ea_ctx {
     cudaStream_t copy_stream = nullptr;    // batch-mode H2D
     cudaStream_t refine_stream = nullptr;  // batch-mode refinement
     cudaEvent_t bev[4] = {nullptr, nullptr, nullptr, nullptr};
-    cudaEvent_t rev[4] = {nullptr, nullptr, nullptr, nullptr};  // seeds ready / refine done
+    cudaEvent_t rev[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};  // seeds ready / refine done, per working set
     // async (device-resident) searches: overflow flag and a ring of screen
     // kernel event pairs read back by ea_ctx_async_status
     eab::DevBuf async_flag;
