@@ -415,8 +415,9 @@ ScreenPlan screen(ea_ctx* ctx, const ea_model* m, const ea_field* f, const ea_po
                      reinterpret_cast<unsigned*>(ctrl), (int)(sizeof(SearchCtrl) / sizeof(unsigned)));
         ctx->plane_key = pkey;
     }
-    // only the fused finish restores the between-searches state
-    ctx->hist_clean = fused;
+    // dirty until the fused finish (which restores the between-searches
+    // state) has been enqueued -- see top_enqueue
+    ctx->hist_clean = false;
     float* map = (float*)ctx->map.ensure(sizeof(float) * (plan.slab_poses ? plan.slab_poses : 1));
     float* item_max =
         (float*)ctx->item_max.ensure(sizeof(float) * (plan.slab_poses / 32 + plan.it_count * 64 + 64));
@@ -582,6 +583,7 @@ TopLaunch top_enqueue(ea_ctx* ctx, const ea_model* m, const ea_field* f, const e
         fa.rows = d_rows;
         fa.overflow = overflow;
         launch_finish(ctx, fa);
+        ctx->hist_clean = true;
         return t;
     }
     // band threshold from the histogram, then the compaction
