@@ -1465,8 +1465,11 @@ void build_working_into(ea_ctx* ctx, std::vector<ea_field*>& fields, DevBuf& ima
     }
     const size_t elems = pyramid_elems(w / 2, h / 2, std::max(levels - 1, 1));
     double* d = (double*)image.ensure(sizeof(double) * (elems ? elems : 1));
+    // Fused when the image is small enough that its ~1/2 wave of tiles is
+    // latency- rather than bandwidth-bound (cfg2 1.3 MP: 24 vs ~30 us); a 5 MP
+    // image streams better through the per-level kernels (70 vs ~35 us).
     if (levels >= 1 && levels <= kMaxFusedLevels && w >= 3 && h >= 3 &&
-        levels <= pyramid_levels_feasible(w, h)) {
+        (size_t)w * h <= ((size_t)1 << 21) && levels <= pyramid_levels_feasible(w, h)) {
         // one launch for the whole pyramid + every level's gradient field
         PyramidFieldsArgs pa{};
         pa.img0 = d_level0;
