@@ -764,21 +764,37 @@ static void run_fast(ea_ctx* ctx, const ScreenArgs& a) {
     if (ctas > (unsigned long long)ctx->sm_count) ctas = ctx->sm_count;
     if (ctas == 0) ctas = 1;
     // tail split (see TailPlan): the last partial round of `rem` items is cut
-    // into f chunks, f minimising the makespan ceil(rem*f/P) * (1/f + c) in
-    // item units (c ~ 2%: a chunk's partial-sum merge and finalise).
+    // into f chunks, f minimising the tail's makespan in item units
+    //   max(rem * (1 + c*f) / P, 1/f + c)
+    // -- warps pull micro-items dynamically, so the tail ends when either its
+    // total work (spread over P warps) or one chunk's latency is done; c ~ 6%
+    // of an item is a chunk's fixed cost (prologue, partial-sum merge,
+    // finalise).  Fitted on the B200 (profiles/r01.md, EAB_TAIL_F sweep): a
+    // 1/8 theta slab of cfg2 (900 items on 1776 warps) is fastest at f = 2
+    // (0.095 ms screen vs 0.118 at the f = 7 the older ceil-rounds model
+    // chose), cfg3's slab at f = 6-9; a tail of nearly a full round (full
+    // cfg3: 1632 items on 1776 warps) stays unsplit -- f = 2 measured +4%.
     TailPlan tp{items, 0, 1, nullptr, nullptr};
     const unsigned long long P = ctas * warps_per_cta;
     const unsigned long long rem = items % P;
     if (rem > 0 && fmax >= 2) {
+        constexpr double c = 0.06;
+        auto makespan = [&](int ff) {  // an unsplit item pays no chunk cost
+            const double cf = ff > 1 ? c : 0.0;
+            return std::max((double)rem * (1.0 + cf * ff) / (double)P, 1.0 / ff + cf);
+        };
         int f = 1;
-        double best = 1.02;
+        double best = makespan(1);
         for (int ff = 2; ff <= fmax; ++ff) {
-            const double rounds = (double)((rem * (unsigned long long)ff + P - 1) / P);
-            const double cost = rounds * (1.0 / ff + 0.02);
+            const double cost = makespan(ff);
             if (cost < best - 1e-9) {
                 best = cost;
                 f = ff;
             }
+        }
+        if (const char* ef = std::getenv("EAB_TAIL_F")) {  // diagnostic A/B of the split factor
+            const int v = std::atoi(ef);
+            if (v >= 1 && v <= fmax) f = v;
         }
         if (f >= 2) {
             tp.n_main = items - rem;
