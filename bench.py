@@ -117,7 +117,12 @@ SMEM_BYTES_PER_CLK_PER_SM = 128
 ALG_BYTES_PER_EVAL = 72  # (2r+1)^2 = 9 window pixels x 8 B float2
 
 
-def make_inputs(name, noise_seed=None):
+def make_inputs(name, noise_seed=None, compose=None):
+    """(image, template, cfg, truth) of a single-model config.  `compose`:
+    the scene composer (default: this library's ea_compose_scene; the
+    reference arm passes the reference's own compose_scene, synth.cpp:178-300,
+    so that process never loads libedgealign_b200.so -- the bytes are equal,
+    tests/test_golden.py)."""
     c = CONFIGS[name]
     sigma, nseed = c["sigma"], c["nseed"]
     if noise_seed is not None:  # another frame of the same scene
@@ -125,7 +130,7 @@ def make_inputs(name, noise_seed=None):
     spec = ea.SceneSpec(c["W"], c["H"], "l_bracket", c["size"],
                         (c["pose"][0], c["pose"][1], D(c["pose"][2])), c["clutter"], c["seed"],
                         c["occluder"], c["illum"], sigma, nseed)
-    img, tmpl, truth, occ = ea.compose_scene(spec)
+    img, tmpl, truth, occ = (compose or ea.compose_scene)(spec)
     L = c["L"]
     step = float(1 << (L - 1))
     grid = ea.PoseGrid(0.0, c["W"] - 1.0, step, 0.0, c["H"] - 1.0, step, 0.0,
@@ -169,15 +174,20 @@ def make_multi_inputs(name, noise_seed=None):
     return img, tmpls, cfg, [p for _, _, p in stamps]
 
 
-def lattice_bytes_per_eval(models, tg, it0, it1, R=1, S=8):
-    """Shared-memory bytes the lattice kernel loads per pose-evaluation, from
-    its point schedule (search_kernels.cu schedule_kernel, restated): per
-    theta, points sorted by (oy, ox) and same-row neighbours with dx <= 1
-    paired; a single loads (8+2R)(S+2R) float2 per 8xS poses, a pair
-    (8+2R+dx)(S+2R) for two points.  Host cos/sin differ from glibc's in the
-    last bit at most, which can move a rounding tie: a model, not a count."""
+def lattice_work_per_eval(models, tg, it0, it1, R=1, S=8):
+    """Per pose-evaluation, from the lattice kernel's point schedule
+    (search_kernels.cu schedule_kernel, restated): (shared-memory bytes
+    loaded, minimal thread instructions).  Per theta the points are sorted by
+    (oy, ox) and same-row neighbours with dx <= 1 paired; per lane block of
+    8 x S poses a single loads (8+2R)(S+2R) float2 and issues per window row
+    8+2R LDS, 2(8+2R) FFMA, 8 FMNMX3 (horizontal) and per pose row 8 FMNMX3
+    (vertical) + 8 accumulates; a pair loads its (8+2R+dx)(S+2R) union once,
+    doubles the FFMA and FMNMX3 and adds both votes with one IADD3.  Host
+    cos/sin may differ from glibc's in the last bit, which can move a rounding
+    tie: a model, not a count."""
     import math
-    px_total = evals = 0
+    px_total = evals = inst = 0
+    NR, NC = S + 2 * R, 8 + 2 * R
     for pts in models:
         pts = np.asarray(pts)
         for it in range(it0, it1):
@@ -193,13 +203,16 @@ def lattice_bytes_per_eval(models, tg, it0, it1, R=1, S=8):
                     b = order[i + 1]
                     d = ox[b] - ox[a]
                     if oy[b] == oy[a] and 0 <= d <= 1:
-                        px_total += (8 + 2 * R + d) * (S + 2 * R)
+                        px_total += (NC + d) * NR
+                        inst += NR * ((NC + d) + 4 * NC + 16) + S * (16 + 8)
                         i += 2
                         continue
-                px_total += (8 + 2 * R) * (S + 2 * R)
+                px_total += NC * NR
+                inst += NR * (NC + 2 * NC + 8) + S * (8 + 8)
                 i += 1
             evals += n * 8 * S
-    return px_total * 8.0 / max(evals, 1)
+    evals = max(evals, 1)
+    return px_total * 8.0 / evals, inst / evals
 
 
 def top_grid(cfg):
@@ -270,78 +283,174 @@ def measured_peaks():
 
 
 # ---- reference CPU arm -----------------------------------------------------------------
-def reference_sample(name, target_s=12.0, threads=0):
-    """The reference's own search_topk (Backend Parallel, all host threads)
-    on a theta slice of the top level: returns (pose_evals, seconds, sample)."""
-    from oracle.pyoracle import ReferenceLib
-    ref = ReferenceLib()
-    if CONFIGS[name].get("multi"):
-        img, tmpls, cfg, _ = make_multi_inputs(name)
-    else:
-        img, tmpl, cfg, _ = make_inputs(name)
-        tmpls = [tmpl]
-    L = cfg.num_levels
-    wp = ref.build_pyramid(img, L)
-    mf = []  # (top model points, top field) per model
-    for tmpl in tmpls:
-        models, fields = ref.prepare_levels(ref.build_pyramid(tmpl, L), wp, cfg)
-        mf.append((models[L - 1].points, fields[L - 1]))
-    tg = top_grid(cfg)
-    nx, ny, nt = ref.grid_counts(tg)
-    n = sum(len(p) for p, _ in mf)
-    threads = threads or len(os.sched_getaffinity(0))
+REF_FLAGS = ("g++ -std=c++20 -O3 -DNDEBUG -ffp-contract=off (proj/CMakeLists.txt:12-14 Release), "
+             "-mavx2 on simd/kernels_avx2.cpp, EDGEALIGN_HAVE_AVX2=1 (oracle/Makefile `ref`)")
 
-    def run(nth):
+
+def host_info():
+    """CPU model, host threads and compiler of the box."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    try:
+        cxx = subprocess.run(["g++", "--version"], capture_output=True, text=True,
+                             timeout=10).stdout.splitlines()[0]
+    except Exception:
+        cxx = None
+    return {"cpu_model": model, "host_threads": len(os.sched_getaffinity(0)),
+            "compiler": cxx, "flags": REF_FLAGS}
+
+
+class ReferenceWorkload:
+    """The reference itself (oracle/_ref: the reference compiled from its own
+    sources, no repo code) prepared on a config: inputs from the reference's
+    own compose_scene (synth.cpp:178-300) for single-model configs, so a
+    reference-arm process never loads libedgealign_b200.so; cfg5's
+    multi-stamp scene has no reference composer and comes from
+    ea_compose_multi."""
+
+    def __init__(self, name):
+        from oracle.pyoracle import ReferenceLib
+        self.ref = ref = ReferenceLib()
+        self.name = name
+        if CONFIGS[name].get("multi"):
+            self.img, self.tmpls, self.cfg, _ = make_multi_inputs(name)
+        else:
+            self.img, tmpl, self.cfg, _ = make_inputs(name, compose=ref.compose_scene)
+            self.tmpls = [tmpl]
+        L = self.cfg.num_levels
+        self.wp = ref.build_pyramid(self.img, L)
+        self.tps = [ref.build_pyramid(t, L) for t in self.tmpls]
+        self.mf = []  # (top model points, top field) per model
+        for tp in self.tps:
+            models, fields = ref.prepare_levels(tp, self.wp, self.cfg)
+            self.mf.append((models[L - 1].points, fields[L - 1]))
+        self.tg = top_grid(self.cfg)
+        self.nx, self.ny, self.nt = ref.grid_counts(self.tg)
+        self.n = sum(len(p) for p, _ in self.mf)
+
+    def run(self, nth, threads, backend):
+        tg = self.tg
         g = ea.PoseGrid(tg.x0, tg.x1, tg.dx, tg.y0, tg.y1, tg.dy, tg.t0,
                         tg.t0 + (nth - 1) * tg.dt, tg.dt)
-        assert ref.grid_counts(g)[2] == nth
+        assert self.ref.grid_counts(g)[2] == nth
         t0 = time.perf_counter()
-        for pts, f in mf:
-            ref.search_topk(pts, f, g, cfg.score_params, cfg.topk, threads=threads)
+        for pts, f in self.mf:
+            self.ref.search_topk(pts, f, g, self.cfg.score_params, self.cfg.topk,
+                                 threads=threads, backend=backend)
         return time.perf_counter() - t0
 
-    probe = max(1, min(nt, threads // 8 or 1))
-    dt = run(probe)
-    nth = int(min(nt, max(probe, probe * target_s / max(dt, 1e-3))))
-    secs = run(nth)
-    evals = nx * ny * nth * n
-    what = f"{len(mf)} models, {n} top model points in all" if len(mf) > 1 else \
-        f"{n} model points"
-    sample = (f"{name} top level, theta slice {nth}/{nt} ({nx}x{ny} translations, {what}), "
-              f"reference search_topk Backend::Parallel")
-    return evals, secs, sample, threads
+    def sample(self, target_s, threads, backend=abi.BACKEND_PARALLEL):
+        """search_topk on a theta slice of the top level sized for ~target_s:
+        -> (pose_evals, seconds, description)."""
+        probe = max(1, min(self.nt, threads // 8 or 1))
+        dt = self.run(probe, threads, backend)
+        nth = int(min(self.nt, max(probe, probe * target_s / max(dt, 1e-3))))
+        secs = self.run(nth, threads, backend)
+        evals = self.nx * self.ny * nth * self.n
+        what = (f"{len(self.mf)} models, {self.n} top model points in all" if len(self.mf) > 1
+                else f"{self.n} model points")
+        kind = "Parallel" if backend == abi.BACKEND_PARALLEL else "Serial"
+        desc = (f"{self.name} top level, theta slice {nth}/{self.nt} ({self.nx}x{self.ny} "
+                f"translations, {what}), reference search_topk Backend::{kind}"
+                f"{f' x {threads} threads' if kind == 'Parallel' else ''}")
+        return evals, secs, desc
+
+    def coarse_to_fine_ms(self, threads):
+        """The reference's whole detect (coarse_to_fine search.cpp:359-364:
+        prepare_levels + search_levels, Backend Parallel) on the config's
+        host pyramids, wall clock; single-model configs only (cfg5 would be
+        ~50 s of CPU)."""
+        if len(self.tps) != 1:
+            return None
+        cfg = abi.SearchConfig(grid=self.cfg.grid, num_levels=self.cfg.num_levels,
+                               score_params=self.cfg.score_params, topk=self.cfg.topk,
+                               refine_radius=self.cfg.refine_radius,
+                               min_score=self.cfg.min_score,
+                               backend_kind=abi.BACKEND_PARALLEL, worker_count=threads)
+        t0 = time.perf_counter()
+        out = self.ref.coarse_to_fine(self.tps[0], self.wp, cfg)
+        ms = (time.perf_counter() - t0) * 1e3
+        return ms, out
+
+
+def reference_baseline(name, target_s=10.0, serial_s=4.0, threads=0, work=None):
+    """cpu_baseline per BASELINE.md §3: the reference's search_topk on all host
+    threads (Parallel) and on one (Serial), its coarse_to_fine detect latency,
+    CPU model, compiler and flags."""
+    work = work or ReferenceWorkload(name)
+    threads = threads or len(os.sched_getaffinity(0))
+    evals, secs, desc = work.sample(target_s, threads)
+    s_evals, s_secs, s_desc = work.sample(serial_s, 1, abi.BACKEND_SERIAL)
+    out = {"value": evals / secs, "unit": "pose-evals/s", "cores": threads, "kind": "reference",
+           "sample": desc,
+           "serial": {"value": s_evals / s_secs, "unit": "pose-evals/s", "cores": 1,
+                      "sample": s_desc}}
+    c2f = work.coarse_to_fine_ms(threads)
+    if c2f is not None:
+        out["coarse_to_fine_ms"] = c2f[0]
+        out["coarse_to_fine"] = (f"{name}: reference coarse_to_fine (prepare_levels + "
+                                 f"search_levels), Backend::Parallel x {threads}, wall clock, "
+                                 f"found={bool(c2f[1].found)}")
+    else:
+        out["coarse_to_fine_ms"] = None
+    out.update(host_info())
+    return out
 
 
 def bench_reference(args, rank, world):
     if rank != 0:
         return
-    rates = []
+    work = ReferenceWorkload(args.config)
+    threads = len(os.sched_getaffinity(0))
+    rates, desc = [], None
     for i in range(args.warmup + args.steps):
-        evals, secs, sample, threads = reference_sample(args.config, args.ref_seconds)
+        evals, secs, desc = work.sample(args.ref_seconds, threads)
         if i >= args.warmup:
             rates.append(evals / secs)
     v = statistics.median(rates)
+    base = reference_baseline(args.config, target_s=0.1, threads=threads, work=work)
+    base.update({"value": v, "sample": desc})
     line = {"impl": "reference", "metric": "pose-evals/sec", "value": v,
             "unit": "pose-evals/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "higher_is_better": True, "scaling": "none",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"{args.config}: {CONFIGS[args.config]['desc']}"},
-            "cpu_baseline": {"value": v, "unit": "pose-evals/s", "cores": threads,
-                             "kind": "reference", "sample": sample},
+            "cpu_baseline": base,
             "e2e": {"value": v, "unit": "pose-evals/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
 # ---- our arm -------------------------------------------------------------------------------
+# ncu --set full captures of the exact screen-kernel instantiation each config
+# runs (profiles/r02_*): DRAM bytes (read + write) per launch, executed warp
+# instructions per launch, issue slots busy.  Not measurable inside the timed
+# run; per config.
+NCU = {
+    "cfg3": dict(kernel="screen_fast_kernel<1, 8, 3, 0, 2, 0, 384>", dram=60228352,
+                 warp_inst=443089427, issue_busy=0.6289,
+                 source="profiles/r02_screen_cfg3_ncu.txt"),
+}
+SMEM_BYTES_PER_CLK_PER_SM = 128
+ALG_BYTES_PER_EVAL = 72  # (2r+1)^2 = 9 window pixels x 8 B float2 (SURVEY.md §8(d) d4)
+
+
 def bench_ours(args, rank, world, local_rank):
     import torch
     import torch.distributed as dist
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    # One non-default stream shared by torch (L2 flush, events, NCCL) and the
-    # library, so device-resident steps are ordered without host syncs.
+    # One non-default stream shared by torch (L2 flush, events) and the
+    # library (kernels, NCCL), so device-resident steps are ordered without
+    # host syncs.
     stream = torch.cuda.Stream(dev)
     torch.cuda.set_stream(stream)
     ctx = ea.Context(local_rank)
@@ -349,12 +458,20 @@ def bench_ours(args, rank, world, local_rank):
     ctx.set_timing(True)
 
     multi = bool(CONFIGS[args.config].get("multi"))
-    # N > 1: "images" (default) -- each rank searches its own frame of the
-    # config (another noise seed per rank: a batch of search images sharded
-    # across GPUs, no data-path collective, weak scaling); "theta" -- one
-    # image, theta slabs per rank + NCCL all-gather of the k rows + device
-    # merge (strong scaling of one search).
+    # N > 1: "theta" (default) -- one image, theta slabs per rank, the
+    # library's NCCL all-gather of the k rows + device merge (strong scaling
+    # of one search, the north star's cfg3 sharding); "images" (opt-in) --
+    # each rank searches its own frame (another noise seed per rank: a batch
+    # of search images sharded across GPUs, no data-path collective, weak).
     shard_theta = world > 1 and args.shard == "theta"
+    if shard_theta or world == 1:
+        # the library's own communicator (NCCL id handed out over
+        # torch.distributed; world 1 at N = 1: the projection below times the
+        # all-gather + merge of a sharded search on this GPU)
+        if world > 1:
+            parallel.init_comm(ctx)
+        else:
+            ctx.comm_init(0, 1, ea.comm_unique_id())
     frame = None if (world == 1 or shard_theta or rank == 0) else 200 + rank
     if multi:
         img, tmpls, cfg, truth = make_multi_inputs(args.config, noise_seed=frame)
@@ -375,14 +492,15 @@ def bench_ours(args, rank, world, local_rank):
 
     k = cfg.topk
     rows = [torch.empty((k, 5), dtype=torch.float64, device=dev) for _ in dets]
+    merged = [torch.empty((k, 5), dtype=torch.float64, device=dev) for _ in dets]
 
     def top_step():
         """One top-level search per model (cfg5: 8), device-resident: slab
         search -> k rows in HBM -> (N > 1) NCCL all-gather + device merge."""
         out = []
-        for d, r in zip(dets, rows):
+        for d, r, m in zip(dets, rows, merged):
             ea.search_top_slab_async(d.levels, cfg, it0, it1, r.data_ptr())
-            out.append(parallel.gather_rows_device(r, k, ctx) if shard_theta else r)
+            out.append(parallel.gather_rows_device(r, k, ctx, m) if shard_theta else r)
         return out
 
     def barrier():
@@ -394,6 +512,10 @@ def bench_ours(args, rank, world, local_rank):
     # Steps are enqueued back to back (no host round trip inside the timed
     # region: results stay in HBM, as in the multi-GPU data path); the L2
     # flush sits between one step's end event and the next step's start.
+    # Every step searches the same resident image, so after the first step
+    # the screening plane (a function of the field) is reused from the
+    # library's cache (plane_kernel skipped, < 1 % of a step); the e2e
+    # numbers below rebuild it for every image.
     for _ in range(args.warmup):
         top_step()
     barrier()
@@ -441,28 +563,36 @@ def bench_ours(args, rank, world, local_rank):
 
     # ---- per-rank work of theta-slab sharding, measured on this GPU ------------------------
     # The worst slab of G (what one rank of a G-GPU theta-sharded search
-    # computes), same step as `value` (flush + events) but without the NCCL
-    # all-gather of k x 40 B rows: a projection of strong scaling, labelled so.
+    # computes), same step as `value` (flush + events), including the
+    # library's NCCL all-gather + device merge of the k rows on a world-1
+    # communicator (on 8 GPUs the all-gather of 8 x 200 B crosses NVLink:
+    # latency-bound, ~10-20 us, not measurable on one GPU).
     slab_proj = None
-    if world == 1 and not multi and not args.no_slab_probe:
+    if world == 1 and not args.no_slab_probe:
         ctx.set_timing(False)
         t_full = statistics.median(step_ms)
         slab_proj = {"what": "worst theta slab of G on this GPU (per-rank compute of a G-GPU "
-                             "theta-sharded search; excludes the NCCL all-gather)",
+                             "theta-sharded search: slab search + the library's NCCL all-gather "
+                             "and device merge of the k rows on a world-1 communicator)",
                      "full_ms": t_full}
-        r0 = rows[0]
         for G in (2, 4, 8):
             worst = (0.0, None)
             for g in range(G):
                 a0, a1 = parallel.theta_slab(nt, g, G)
+
+                def slab_step():
+                    for d, r, m in zip(dets, rows, merged):
+                        ea.search_top_slab_async(d.levels, cfg, a0, a1, r.data_ptr())
+                        parallel.gather_rows_device(r, k, ctx, m)
+
                 for _ in range(3):
-                    ea.search_top_slab_async(det.levels, cfg, a0, a1, r0.data_ptr())
+                    slab_step()
                 evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                        for _ in range(15)]
                 for e_a, e_b in evs:
                     flush.zero_()
                     e_a.record(stream)
-                    ea.search_top_slab_async(det.levels, cfg, a0, a1, r0.data_ptr())
+                    slab_step()
                     e_b.record(stream)
                 torch.cuda.synchronize(dev)
                 t = statistics.median(e_a.elapsed_time(e_b) for e_a, e_b in evs)
@@ -472,11 +602,14 @@ def bench_ours(args, rank, world, local_rank):
                                  "projected_strong_scaling": t_full / worst[0]}
         ea.async_status(ctx)
 
-    # ---- e2e: the public batch-detect call on host images ----------------------------------
-    # Throughput mode: each step is one image (H2D from pinned memory, device
-    # pyramid + Sobel, top-level search, refinement, D2H of the outcome); the
-    # library overlaps image i+1's H2D with image i's search.  For N > 1 the
-    # images are sharded across ranks (each rank its own batch).
+    # ---- e2e: the public detect call on host images ----------------------------------------
+    # N = 1 / images mode: Detector.detect_batch (ea_detect_batch) -- per image
+    # H2D from pinned memory, device pyramid + Sobel, top-level search,
+    # refinement, D2H of the outcome; the library overlaps image i+1's H2D
+    # with image i's search; each rank its own batch.  Theta mode (N > 1):
+    # Detector.detect_sharded (ea_detect_sharded) per image -- rank 0 H2D +
+    # pyramid, NCCL broadcast of the top level's field, slab search per rank,
+    # NCCL all-gather + merge, refinement on rank 0, outcome broadcast.
     n_img = args.steps
     if CONFIGS[args.config].get("batch"):  # cfg4: the batch is the workload, sharded by rank
         n_img = CONFIGS[args.config]["batch"] // world
@@ -488,13 +621,15 @@ def bench_ours(args, rank, world, local_rank):
         scenes = [img] + [make_inputs(args.config, noise_seed=101 + j)[0] for j in range(3)]
     pinned = [torch.from_numpy(scenes[j % len(scenes)]).pin_memory() for j in range(n_img)]
     host_imgs = [p.numpy() for p in pinned]
-    k = cfg.topk
-    h2d = img.size * 8
+    sharded_e2e = shard_theta and not multi
+    h2d = img.size * 8 if (not sharded_e2e or rank == 0) else 0
     d2h = (472 + 48) * len(dets)  # ea_outcome + control block per image and model
 
     def e2e_run():
         if multi:  # one ea_detect_multi call per image: shared pyramid, 8 models
             return [ea.detect_multi(dets, im) for im in host_imgs]
+        if sharded_e2e:
+            return [det.detect_sharded(im if rank == 0 else None, im.shape) for im in host_imgs]
         return det.detect_batch(host_imgs)
 
     # The library's own phase timing (events on its stream) is off for the
@@ -516,7 +651,8 @@ def bench_ours(args, rank, world, local_rank):
         t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
-    e2e = pose_pts * n_img * world / (e2e_ms / 1e3)  # each rank ran n_img full images
+    # images mode: each rank ran n_img full images; theta mode: n_img images in all
+    e2e = pose_pts * n_img * (1 if sharded_e2e else world) / (e2e_ms / 1e3)
     outcome = outs[0]
 
     # ---- single-image detect latency (same public API, one image per call) -------------------
@@ -529,10 +665,13 @@ def bench_ours(args, rank, world, local_rank):
         for i in range(n_lat + args.warmup):
             a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a0.record(stream)
+            im = host_imgs[i % len(host_imgs)]
             if multi:
-                ea.detect_multi(dets, host_imgs[i % len(host_imgs)])
+                ea.detect_multi(dets, im)
+            elif sharded_e2e:
+                det.detect_sharded(im if rank == 0 else None, im.shape)
             else:
-                det.detect(host_imgs[i % len(host_imgs)])
+                det.detect(im)
             a1.record(stream)
             torch.cuda.synchronize(dev)
             if i >= args.warmup:
@@ -551,8 +690,19 @@ def bench_ours(args, rank, world, local_rank):
     smem_peak_gbs = n_sm * SMEM_BYTES_PER_CLK_PER_SM * sm_mhz * 1e6 / 1e9
     kernel_ms = statistics.median(screen_ms)
     local_evals = nx * ny * (it1 - it0) * n_top
-    achieved = local_evals * ALG_BYTES_PER_EVAL / (kernel_ms / 1e3) / 1e9
-    actual_b = lattice_bytes_per_eval([d.levels.model(L - 1).points for d in dets], tg, it0, it1)
+    models_top = [d.levels.model(L - 1).points for d in dets]
+    loaded_b, min_inst = lattice_work_per_eval(models_top, tg, it0, it1)
+    achieved = local_evals * loaded_b / (kernel_ms / 1e3) / 1e9
+    ncu = NCU.get(args.config)
+    issue = None
+    if ncu and world == 1:
+        thread_inst = ncu["warp_inst"] * 32.0 / local_evals
+        issue = {"kernel": ncu["kernel"], "thread_instructions_per_eval": thread_inst,
+                 "minimal_thread_instructions_per_eval": min_inst,
+                 "instruction_efficiency": min_inst / thread_inst,
+                 "issue_slots_busy": ncu["issue_busy"], "source": ncu["source"],
+                 "note": "minimal = the point schedule's LDS + FFMA + FMNMX3 + accumulate "
+                         "instructions per pose-eval (no addressing, loop or epilogue)"}
     line = {
         "metric": "pose-evals/sec", "value": value, "unit": "pose-evals/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot_ms / args.steps,
@@ -563,30 +713,41 @@ def bench_ours(args, rank, world, local_rank):
                    "top_level_grid": f"{nx}x{ny}x{nt}",
                    "top_model_points": n_tops if multi else n_top,
                    "pose_evals_per_step": job_pts, "l2": "flushed (256 MiB write) between steps",
-                   "parallelism": (f"theta-slab x{world} + NCCL all-gather of top-k rows"
+                   "parallelism": (f"theta-slab x{world} + NCCL all-gather of top-k rows "
+                                   "(libedgealign_b200 communicator)"
                                    if shard_theta else f"images x{world} (one frame per GPU)")
                    if world > 1 else "single GPU"},
         "e2e": {"value": e2e, "unit": "pose-evals/s", "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h, "ms_per_image": e2e_ms / n_img, "images": n_img * world,
+                "d2h_bytes_per_step": d2h, "ms_per_image": e2e_ms / n_img,
+                "images": n_img * (1 if sharded_e2e else world),
                 "batches_ms": runs, "timed": "median of 3 batches",
                 "api": ("detect_multi (ea_detect_multi), one call per pinned host image"
-                        if multi else "Detector.detect_batch (ea_detect_batch), pinned host images"),
+                        if multi else
+                        "Detector.detect_sharded (ea_detect_sharded), one pinned host image "
+                        "per call on rank 0" if sharded_e2e else
+                        "Detector.detect_batch (ea_detect_batch), pinned host images"),
                 "detect_latency_ms": statistics.median(lat),
                 "latency_phases_ms_median": {
                     k: statistics.median(p[i] for p in phases)
                     for i, k in enumerate(("h2d_pyramid_gradients", "top_level_search",
                                            "refinement"))}},
-        "roofline": {"bound": "smem", "kernel": {1: "screen_fast_kernel",
-                                                 3: "screen_region_kernel"}.get(
-                         st["screen_path"], "screen_general_kernel"), "achieved": achieved,
-                     "peak": smem_peak_gbs, "unit": "GB/s", "frac": achieved / smem_peak_gbs,
+        "roofline": {"bound": "smem",
+                     "kernel": {1: "screen_fast_kernel", 3: "screen_region_kernel"}.get(
+                         st["screen_path"], "screen_general_kernel"),
+                     "achieved": achieved, "peak": smem_peak_gbs, "unit": "GB/s",
+                     "frac": achieved / smem_peak_gbs,
                      # dram read+write of one launch, ncu --set full (not measurable in-run)
-                     "traffic": TRAFFIC.get(args.config, (None, None))[0],
-                     "traffic_source": TRAFFIC.get(args.config, (None, "not captured"))[1],
-                     "algorithmic_bytes_per_eval": ALG_BYTES_PER_EVAL,
-                     "smem_bytes_loaded_per_eval": actual_b,
-                     "frac_smem_loaded": local_evals * actual_b / (kernel_ms / 1e3) / 1e9
-                     / smem_peak_gbs,
+                     "traffic": ncu["dram"] if ncu else None,
+                     "traffic_source": ncu["source"] if ncu else "not captured",
+                     "bytes_per_eval": loaded_b,
+                     "bytes_per_eval_is": "shared-memory bytes the kernel loads per pose-eval "
+                                          "(the point schedule's window unions; matches ncu "
+                                          "shared wavefronts x 128 B): every loaded plane pixel "
+                                          "serves up to 9 windows from registers, so the "
+                                          "SURVEY's 72 B/eval (no reuse) is not a bound",
+                     "frac_of_72B_per_eval_no_reuse": local_evals * ALG_BYTES_PER_EVAL /
+                     (kernel_ms / 1e3) / 1e9 / smem_peak_gbs,
+                     "issue": issue,
                      "kernel_ms": kernel_ms, "kernel_share_of_step": kernel_ms /
                      statistics.median(step_ms),
                      "peak_source": f"{n_sm} SMs x 128 B/clk x sm_max_mhz from {peak_src}"},
@@ -603,9 +764,7 @@ def bench_ours(args, rank, world, local_rank):
     }
     if not args.no_cpu_baseline:
         try:
-            evals, secs, sample, threads = reference_sample(args.config, args.ref_seconds)
-            line["cpu_baseline"] = {"value": evals / secs, "unit": "pose-evals/s",
-                                    "cores": threads, "kind": "reference", "sample": sample}
+            line["cpu_baseline"] = reference_baseline(args.config, args.ref_seconds)
         except Exception as e:  # oracle/_ref missing on this box
             line["cpu_baseline"] = {"value": None, "unit": "pose-evals/s", "cores": 0,
                                     "kind": "reference", "sample": f"unavailable: {e}"}
@@ -613,16 +772,22 @@ def bench_ours(args, rank, world, local_rank):
 
 
 def main():
+    # one JSON line on stdout: NCCL's version banner (NCCL_DEBUG=VERSION in
+    # some environments) would precede it
+    if os.environ.get("NCCL_DEBUG", "VERSION").upper() == "VERSION":
+        os.environ["NCCL_DEBUG"] = "WARN"
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="cfg3", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--ref-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--shard", default="images", choices=["images", "theta"],
-                    help="N > 1: shard search images (weak) or theta slabs of one image (strong)")
+    ap.add_argument("--shard", default="theta", choices=["images", "theta"],
+                    help="N > 1: theta slabs of one image (default; strong scaling of one "
+                         "search, the north star's cfg3 sharding) or one search image per GPU "
+                         "(opt-in throughput line, weak scaling)")
     ap.add_argument("--no-slab-probe", action="store_true",
                     help="skip the N=1 per-rank theta-slab timing (projection for 2/4/8 GPUs)")
     args = ap.parse_args()

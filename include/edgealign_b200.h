@@ -42,7 +42,8 @@ typedef enum {
     EA_ERR_GEOMETRY = 6,         /* edgealign::GeometryError    errors.h:66-69 */
     EA_ERR_PARSE = 7,            /* edgealign::ParseError       errors.h:20-29 */
     EA_ERR_CUDA = 8,             /* device missing / CUDA runtime failure       */
-    EA_ERR_INTERNAL = 9
+    EA_ERR_INTERNAL = 9,
+    EA_ERR_NCCL = 10             /* NCCL missing / collective failure (multi-GPU) */
 } ea_status;
 
 /* Message of the last failing call on this host thread ("" if none). */
@@ -365,6 +366,50 @@ ea_status ea_detect_multi(ea_ctx* ctx, ea_levels* const* models, int n, const do
  * image i+1's H2D overlapping image i's device pipeline; outs[count]. */
 ea_status ea_detect_batch(ea_ctx* ctx, ea_levels* lv, const double* const* images, int count,
                           int w, int h, const ea_search_config* cfg, ea_outcome* outs);
+
+/* ---- multi-GPU: theta-slab sharding ------------
+ * One process (or host thread) per GPU, one context per GPU.  The
+ * reference partitions the theta-major pose index into contiguous blocks,
+ * one per worker (search.cpp:116-120), and merges the per-worker top-k
+ * lists by `better` (search.cpp:130-139); snapped to theta the blocks are
+ * theta slabs, and because the merge is an associative, commutative total
+ * order, one all-gather of every rank's k rows reproduces search_topk bit
+ * for bit.  The collectives are NCCL (loaded at run time, the copy torch
+ * already mapped when there is one), enqueued on the context's stream. */
+#define EA_COMM_ID_BYTES 128
+typedef struct {
+    char internal[EA_COMM_ID_BYTES]; /* ncclUniqueId */
+} ea_comm_id;
+
+/* [it_begin, it_end) of `rank` among `world`: the reference's block
+ * partition (search.cpp:116-120) on the theta axis.  Host only. */
+void ea_theta_slab(uint64_t nt, int rank, int world, uint64_t* it_begin, uint64_t* it_end);
+/* Rank 0 creates the id and hands it to every rank out of band (MPI, a TCP
+ * store, torch.distributed, ...). */
+ea_status ea_comm_unique_id(ea_comm_id* out);
+/* Join the context's device to the communicator (ncclCommInitRank;
+ * collective: every rank calls it). */
+ea_status ea_comm_init(ea_ctx* ctx, int rank, int world, const ea_comm_id* id);
+ea_status ea_comm_info(const ea_ctx* ctx, int* rank, int* world);
+ea_status ea_comm_destroy(ea_ctx* ctx);
+/* The exchange step of a sharded search (search.cpp:130-139), no host sync:
+ * all-gather every rank's k device rows {score, index, ux, uy, theta} (as
+ * ea_search_top_slab_async writes them) and `better`-merge them into k rows
+ * at d_merged on every rank.  Collective. */
+ea_status ea_gather_rows_async(ea_ctx* ctx, const double* d_local, int k, double* d_merged);
+/* search_levels (search.cpp:254-357) sharded by theta: every rank screens
+ * and verifies its slab of the top level (lv's working image must be set on
+ * every rank), one NCCL all-gather of the k rows, the `better` merge, then
+ * rank 0 refines down the pyramid and broadcasts the outcome.  `out` equals
+ * ea_search_levels' on every rank.  Collective. */
+ea_status ea_search_levels_sharded(ea_ctx* ctx, const ea_levels* lv,
+                                   const ea_search_config* cfg, ea_outcome* out);
+/* Production detect sharded by theta (BASELINE configs[2]): rank 0 uploads
+ * the level-0 host image and builds the pyramid and fields; the top level's
+ * field is broadcast over NCCL (the other ranks pass image = NULL and only
+ * the dimensions); then as ea_search_levels_sharded.  Collective. */
+ea_status ea_detect_sharded(ea_ctx* ctx, ea_levels* lv, const double* image, int w, int h,
+                            const ea_search_config* cfg, ea_outcome* out);
 
 /* ---- Netpbm codecs (image.cpp:26-219), host C++, bytes in / bytes out ---- */
 /* luminance_to_byte  image.cpp:26-34: clamp to [0, 255], round half up. */

@@ -106,6 +106,17 @@ _SIGS = {
                                   C.POINTER(abi.SearchConfig), C.POINTER(abi.Outcome)]),
     "ea_detect_multi": (C.c_int, [_P, C.POINTER(_P), C.c_int, _dp, C.c_int, C.c_int,
                                   C.POINTER(abi.SearchConfig), C.POINTER(abi.Outcome)]),
+    "ea_theta_slab": (None, [C.c_uint64, C.c_int, C.c_int, C.POINTER(C.c_uint64),
+                             C.POINTER(C.c_uint64)]),
+    "ea_comm_unique_id": (C.c_int, [C.POINTER(abi.CommId)]),
+    "ea_comm_init": (C.c_int, [_P, C.c_int, C.c_int, C.POINTER(abi.CommId)]),
+    "ea_comm_info": (C.c_int, [_P, _ip, _ip]),
+    "ea_comm_destroy": (C.c_int, [_P]),
+    "ea_gather_rows_async": (C.c_int, [_P, C.c_void_p, C.c_int, C.c_void_p]),
+    "ea_search_levels_sharded": (C.c_int, [_P, _P, C.POINTER(abi.SearchConfig),
+                                           C.POINTER(abi.Outcome)]),
+    "ea_detect_sharded": (C.c_int, [_P, _P, _dp, C.c_int, C.c_int,
+                                    C.POINTER(abi.SearchConfig), C.POINTER(abi.Outcome)]),
     "ea_render_template": (C.c_int, [C.c_int, C.c_int, _dp]),
     "ea_luminance_to_byte": (C.c_uint8, [C.c_double]),
     "ea_load_pgm": (C.c_int, [C.c_char_p, C.c_size_t, C.c_void_p, C.c_size_t, _ip, _ip]),
@@ -122,10 +133,30 @@ _SIGS = {
 }
 
 
+def _prefer_torch_nccl():
+    """Point the library's run-time NCCL load (csrc/nccl_dl.cpp) at the copy
+    torch links (the nvidia-nccl wheel), unless the caller chose one: a
+    process that loads the system libnccl.so.2 first and imports torch later
+    would hand torch that older copy (same soname) and break it."""
+    if os.environ.get("EAB_NCCL_LIB"):
+        return
+    import importlib.util
+    try:
+        spec = importlib.util.find_spec("nvidia.nccl")
+    except (ImportError, ValueError):
+        spec = None
+    for base in (spec.submodule_search_locations or []) if spec else []:
+        cand = os.path.join(base, "lib", "libnccl.so.2")
+        if os.path.exists(cand):
+            os.environ["EAB_NCCL_LIB"] = cand
+            return
+
+
 def lib():
     """The loaded C-ABI library (raises if it was never built)."""
     global _lib
     if _lib is None:
+        _prefer_torch_nccl()
         if not os.path.exists(LIB_PATH):
             raise ImportError(
                 f"{LIB_PATH} is missing: build it with `python -m paper_2112_05576_b200.build` "

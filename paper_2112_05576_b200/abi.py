@@ -16,6 +16,8 @@ EA_ERR_GEOMETRY = 6
 EA_ERR_PARSE = 7
 EA_ERR_CUDA = 8
 EA_ERR_INTERNAL = 9
+EA_ERR_NCCL = 10
+EA_COMM_ID_BYTES = 128
 
 POLARITY_SIGNED = 0
 POLARITY_IGNORE = 1
@@ -181,3 +183,19 @@ class SearchStats(C.Structure):
 
 def isfinite_grid(g):
     return all(math.isfinite(getattr(g, n)) for n, _ in PoseGrid._fields_)
+
+
+class CommId(C.Structure):
+    """ea_comm_id: an ncclUniqueId, created on rank 0 and handed out of band."""
+    _fields_ = [("internal", C.c_char * EA_COMM_ID_BYTES)]
+
+
+def comm_id_bytes(cid):
+    """The 128 raw bytes of an ea_comm_id (c_char arrays stop at NUL; this does not)."""
+    return C.string_at(C.addressof(cid), EA_COMM_ID_BYTES)
+
+
+def comm_id_from_bytes(raw):
+    cid = CommId()
+    C.memmove(C.addressof(cid), bytes(raw), EA_COMM_ID_BYTES)
+    return cid

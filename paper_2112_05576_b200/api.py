@@ -109,6 +109,23 @@ class Context:
     def kernel_launches(self):
         return int(lib().ea_ctx_kernel_launches(self.handle))
 
+    # ---- multi-GPU (ea_comm_*): one context per GPU, one rank per context ----
+    def comm_init(self, rank, world, comm_id):
+        """Join this context's device to an NCCL communicator (collective)."""
+        _check(lib().ea_comm_init(self.handle, int(rank), int(world), C.byref(comm_id)))
+
+    def comm_info(self):
+        r, w = C.c_int(), C.c_int()
+        _check(lib().ea_comm_info(self.handle, C.byref(r), C.byref(w)))
+        return r.value, w.value
+
+    def has_comm(self):
+        r, w = C.c_int(), C.c_int()
+        return lib().ea_comm_info(self.handle, C.byref(r), C.byref(w)) == abi.EA_OK
+
+    def comm_destroy(self):
+        _check(lib().ea_comm_destroy(self.handle))
+
 
 _default = {}
 
@@ -502,6 +519,36 @@ def merge_rows_async(ctx, d_rows, n_rows, k, d_out):
                                      C.c_void_p(int(d_out))))
 
 
+def theta_slab(nt, rank, world):
+    """[it_begin, it_end) of `rank`: the reference's block partition
+    (search.cpp:116-120) on the theta axis (ea_theta_slab)."""
+    b, e = C.c_uint64(), C.c_uint64()
+    lib().ea_theta_slab(C.c_uint64(int(nt)), int(rank), int(world), C.byref(b), C.byref(e))
+    return b.value, e.value
+
+
+def comm_unique_id():
+    """An ncclUniqueId (ea_comm_unique_id) for rank 0 to hand to every rank."""
+    cid = abi.CommId()
+    _check(lib().ea_comm_unique_id(C.byref(cid)))
+    return cid
+
+
+def gather_rows_async(ctx, d_local, k, d_merged):
+    """NCCL all-gather of every rank's k device rows + device `better` merge
+    into k rows at d_merged (ea_gather_rows_async; no host sync)."""
+    _check(lib().ea_gather_rows_async(ctx.handle, C.c_void_p(int(d_local)), int(k),
+                                      C.c_void_p(int(d_merged))))
+
+
+def search_levels_sharded(levels, config):
+    """search_levels sharded by theta over the context's communicator."""
+    out = Outcome()
+    _check(lib().ea_search_levels_sharded(levels.ctx.handle, levels.handle, C.byref(config),
+                                          C.byref(out)))
+    return out
+
+
 def async_status(ctx, cap=4096):
     """Sync; -> (overflowed, [screen-kernel ms of the timed searches since the last call])."""
     of, n = C.c_int(), C.c_int()
@@ -546,6 +593,23 @@ class Detector:
                                img.shape[0], C.byref(self.config), C.byref(out)))
         return out
 
+
+    def detect_sharded(self, image, shape=None):
+        """Theta-sharded detect over the context's communicator
+        (ea_detect_sharded, collective): rank 0 passes the host image, the
+        other ranks None and `shape` = (h, w).  Same outcome on every rank."""
+        if image is None:
+            h, w = shape
+            ptr = None
+        else:
+            img = image if (isinstance(image, np.ndarray) and image.dtype == np.float64
+                            and image.flags.c_contiguous) else _f64(image)
+            h, w = img.shape
+            ptr = _ptr(img)
+        out = Outcome()
+        _check(lib().ea_detect_sharded(self.ctx.handle, self.levels.handle, ptr, w, h,
+                                       C.byref(self.config), C.byref(out)))
+        return out
 
     def detect_batch(self, images):
         """Throughput mode: one call for many same-size host images (pinned

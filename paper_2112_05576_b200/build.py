@@ -17,8 +17,9 @@ LIB = os.path.join(HERE, "libedgealign_b200.so")
 
 CU_SOURCES = ["api.cu", "field_kernels.cu", "search_kernels.cu", "refine_kernels.cu",
               "model_kernels.cu"]
-CPP_SOURCES = ["host_model.cpp", "host_synth.cpp", "host_io.cpp"]
-HEADERS = ["common.cuh", "kernels.cuh", "refine.cuh", "model.cuh", "failure.h", "host_model.h"]
+CPP_SOURCES = ["host_model.cpp", "host_synth.cpp", "host_io.cpp", "nccl_dl.cpp"]
+HEADERS = ["common.cuh", "kernels.cuh", "refine.cuh", "model.cuh", "failure.h", "host_model.h",
+           "nccl_dl.h"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 HOST_FLAGS = "-fPIC,-ffp-contract=off,-O2,-Wall"

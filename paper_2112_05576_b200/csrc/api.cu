@@ -15,6 +15,7 @@
 
 #include "host_model.h"
 #include "kernels.cuh"
+#include "nccl_dl.h"
 #include "model.cuh"
 #include "refine.cuh"
 
@@ -1452,6 +1453,7 @@ void free_levels(ea_levels* lv) {
     for (auto* f : lv->fields) delete f;
     for (auto* f : lv->fields2) delete f;
     for (auto* f : lv->fields3) delete f;
+    delete lv->shard_top;
     delete lv;
 }
 
@@ -1543,6 +1545,157 @@ void set_working_image(ea_ctx* ctx, ea_levels* lv, const double* image, int w, i
     build_working(ctx, lv, raw, w, h, levels);
 }
 
+// ---- theta-sharded search (search.cpp:116-139) ------------------
+static_assert(sizeof(ncclUniqueId) == EA_COMM_ID_BYTES, "ea_comm_id must hold an ncclUniqueId");
+
+ncclComm_t comm_of(const ea_ctx* ctx) {
+    if (!ctx->comm)
+        fail(EA_ERR_INVALID_ARGUMENT, "context has no communicator (call ea_comm_init first)");
+    return static_cast<ncclComm_t>(ctx->comm);
+}
+
+void theta_slab_of(uint64_t nt, int rank, int world, uint64_t* b, uint64_t* e) {
+    // search.cpp:116-120: worker w scans [total*w/W, total*(w+1)/W)
+    *b = (uint64_t)((unsigned __int128)nt * (unsigned)rank / (unsigned)world);
+    *e = (uint64_t)((unsigned __int128)nt * (unsigned)(rank + 1) / (unsigned)world);
+}
+
+// Candidate buffer of a search whose overflow cannot be retried from the host
+// (device-resident and sharded searches): the whole slab when it has at most
+// 2^26 poses, so the band can never overflow; larger slabs keep 2^26 and
+// report an overflow (flag + an +inf row 0, see topk_rows_body).
+unsigned long long async_cap(ea_ctx* ctx, uint64_t slab_poses) {
+    return std::max<unsigned long long>(initial_cap(ctx),
+                                        std::min<uint64_t>(slab_poses, 1ull << 26));
+}
+
+// Sub-buffers of ctx->shard for k rows on `world` ranks.
+struct ShardBufs {
+    double* local;      // k rows of this rank's slab
+    double* gathered;   // world * k rows
+    double* merged;     // k rows
+    ea_outcome* out;    // device outcome (broadcast from the root)
+    int* flag;          // this rank's overflow flag
+};
+
+ShardBufs shard_bufs(ea_ctx* ctx, int k) {
+    const size_t row = 5 * sizeof(double) * (size_t)k;
+    const size_t out_off = (row * (2 + (size_t)ctx->comm_world) + 255) & ~(size_t)255;
+    char* p = (char*)ctx->shard.ensure(out_off + sizeof(ea_outcome) + 256);
+    ShardBufs b;
+    b.local = (double*)p;
+    b.merged = (double*)(p + row);
+    b.gathered = (double*)(p + 2 * row);
+    b.out = (ea_outcome*)(p + out_off);
+    b.flag = (int*)(p + out_off + sizeof(ea_outcome));
+    return b;
+}
+
+// All-gather of every rank's k rows + the `better` merge into d_merged; with
+// seed_topk the merged top k also lands in ctx->topk / ctrl->n_out (the
+// layout the seed kernel reads).  Enqueued on the context's stream.
+void gather_rows(ea_ctx* ctx, const double* d_local, int k, double* d_merged, bool seed_topk) {
+    ncclComm_t comm = comm_of(ctx);
+    const int n = ctx->comm_world * k;
+    if (n > merge_rows_max(ctx))
+        fail(EA_ERR_INVALID_ARGUMENT, "world * topk exceeds " + std::to_string(merge_rows_max(ctx)) +
+                                          " rows (merge staged in shared memory)");
+    const ShardBufs b = shard_bufs(ctx, k);
+    EAB_NCCL(nccl().AllGather(d_local, b.gathered, 5 * (size_t)k, ncclDouble, comm, ctx->stream));
+    double* ts = nullptr;
+    unsigned long long* ti = nullptr;
+    int* nt = nullptr;
+    if (seed_topk) {
+        ts = (double*)ctx->topk.ensure((sizeof(double) + sizeof(unsigned long long)) * (size_t)k);
+        ti = reinterpret_cast<unsigned long long*>(ts + k);
+        nt = &((SearchCtrl*)ctx->ctrl.ensure(sizeof(SearchCtrl)))->n_out;
+    }
+    launch_merge_rows(ctx, b.gathered, n, k, d_merged, ts, ti, nt);
+}
+
+// One rank's slab of the top level -> k device rows (NaN rows past the
+// count; row 0 = +inf on overflow).
+void slab_rows(ea_ctx* ctx, const ea_model* m, const ea_field* f, const ea_pose_grid& tg,
+               const ea_score_params& p, int k, uint64_t it_begin, uint64_t it_end,
+               double* d_rows, int* flag) {
+    validate_params(p);
+    if (m->n == 0) fail(EA_ERR_INVALID_ARGUMENT, "search needs a nonempty model");
+    if (k < 1) fail(EA_ERR_INVALID_ARGUMENT, "topk must be >= 1");
+    const ea_grid_counts c = counts_of(tg);
+    const uint64_t b = std::min(it_begin, c.nt), e = std::min(it_end, c.nt);
+    const uint64_t poses = e > b ? c.nx * c.ny * (e - b) : 0;
+    const unsigned long long cap = async_cap(ctx, poses);
+    if (poses > 0) {
+        top_enqueue(ctx, m, f, tg, p, k, b, e, cap, d_rows, flag);
+        return;
+    }
+    // empty slab (more ranks than thetas): k empty rows from a cleared
+    // control block (never the previous search's count)
+    SearchCtrl* ctrl = (SearchCtrl*)ctx->ctrl.ensure(sizeof(SearchCtrl));
+    double* ts = (double*)ctx->topk.ensure((sizeof(double) + sizeof(unsigned long long)) * (size_t)k);
+    EAB_CUDA(cudaMemsetAsync(ctrl, 0, sizeof(SearchCtrl), ctx->stream));
+    const RowGrid g{tg.x0, tg.dx, tg.y0, tg.dy, tg.t0, tg.dt, c.nx, c.ny};
+    launch_topk_rows(ctx, ts, reinterpret_cast<unsigned long long*>(ts + k), ctrl, cap, k, g,
+                     d_rows, flag);
+    ctx->hist_clean = false;  // the control block was cleared, not left by a finish
+}
+
+// search_levels sharded by theta (every rank calls it with its top-level
+// field `ftop`): slab -> all-gather -> merge -> root refines -> outcome
+// broadcast.  Root = rank 0.
+void search_levels_sharded(ea_ctx* ctx, const ea_levels* lv, const ea_field* ftop,
+                           const ea_search_config& cfg, ea_outcome* out) {
+    ncclComm_t comm = comm_of(ctx);
+    const int top = cfg.num_levels - 1, k = cfg.topk;
+    const bool root = ctx->comm_rank == 0;
+    const ea_pose_grid tg = top_grid_of(cfg);
+    const ea_grid_counts c = counts_of(tg);
+    const double* tables = root ? detect_tables(ctx, cfg) : nullptr;
+    uint64_t b = 0, e = 0;
+    theta_slab_of(c.nt, ctx->comm_rank, ctx->comm_world, &b, &e);
+    ShardBufs sb = shard_bufs(ctx, k);
+    EAB_CUDA(cudaMemsetAsync(sb.flag, 0, sizeof(int), ctx->stream));
+    slab_rows(ctx, lv->models[top], ftop, tg, cfg.score_params, k, b, e, sb.local, sb.flag);
+    gather_rows(ctx, sb.local, k, sb.merged, /*seed_topk=*/true);
+    sb = shard_bufs(ctx, k);
+    if (root) {
+        SearchCtrl* ctrl = ctx->ctrl.as<SearchCtrl>();
+        const double* ts = ctx->topk.as<double>();
+        const unsigned long long* ti = reinterpret_cast<const unsigned long long*>(ts + k);
+        if (top == 0 || tables) {  // device beam, as enqueue_levels
+            RefineState st = refine_state(ctx, k);
+            st.out = sb.out;
+            EAB_CUDA(cudaMemsetAsync(st.out, 0, sizeof(ea_outcome), ctx->stream));
+            launch_seed_beam(ctx, ts, ti, &ctrl->n_out, seed_args(tg, c, cfg), st.beam[0],
+                             st.cnt[0], st.out);
+            if (top > 0) refine_enqueue(ctx, lv, cfg, tg, tables, st);
+        } else {  // very wide beams: host-assisted refinement from the merged rows
+            std::vector<double> rows(5 * (size_t)k);
+            d2h(ctx, rows.data(), sb.merged, rows.size() * sizeof(double));
+            sync(ctx);
+            std::vector<ea_scored_pose> seeds;
+            for (int r = 0; r < k; ++r) {
+                const double* q = rows.data() + 5 * (size_t)r;
+                if (q[0] != q[0]) break;
+                if (std::isinf(q[0])) fail(EA_ERR_INTERNAL, "candidate buffer overflow in a sharded search");
+                seeds.push_back(ea_scored_pose{q[0], (uint64_t)q[1], ea_pose{q[2], q[3], q[4]}});
+            }
+            ea_outcome ho{};
+            refine_levels(ctx, lv, cfg, tg, seeds_to_beam(seeds), &ho);
+            h2d_staged(ctx, sb.out, &ho, sizeof ho);
+        }
+    }
+    EAB_NCCL(nccl().Broadcast(sb.out, sb.out, sizeof(ea_outcome), ncclUint8, 0, comm, ctx->stream));
+    char* h = (char*)ctx->h_out.ensure(sizeof(ea_outcome) + 5 * sizeof(double));
+    d2h(ctx, h, sb.out, sizeof(ea_outcome));
+    d2h(ctx, h + sizeof(ea_outcome), sb.merged, 5 * sizeof(double));
+    sync(ctx);
+    double row0;
+    std::memcpy(&row0, h + sizeof(ea_outcome), sizeof row0);
+    if (std::isinf(row0)) fail(EA_ERR_INTERNAL, "candidate buffer overflow in a sharded search");
+    std::memcpy(out, h, sizeof(ea_outcome));
+}
+
 }  // namespace
 
 // =============================================================================
@@ -1610,6 +1763,14 @@ void ea_ctx_destroy(ea_ctx* ctx) {
         if (e) cudaEventDestroy(e);
     for (auto& e : ctx->tev)
         if (e) cudaEventDestroy(e);
+    if (ctx->comm) {
+        try {
+            nccl().CommDestroy(static_cast<ncclComm_t>(ctx->comm));
+        } catch (...) {
+        }
+        ctx->comm = nullptr;
+    }
+    ctx->shard.release();
     if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
     if (ctx->refine_stream) cudaStreamDestroy(ctx->refine_stream);
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
@@ -2049,7 +2210,9 @@ ea_status ea_search_topk_slab(ea_ctx* ctx, const ea_model* m, const ea_field* f,
         need(p, "params");
         need(n_out, "n_out");
         DeviceGuard dg(ctx->device);
-        if (it_end == 0) it_end = 1;  // an empty slab must be explicit: [b, e) with e > b
+        *n_out = 0;
+        const uint64_t nt = counts_of(*g).nt;
+        if (std::min(it_end, nt) <= std::min(it_begin, nt)) return;  // empty slab
         const auto r = top_search(ctx, m, f, *g, *p, k, it_begin, it_end);
         for (size_t i = 0; i < r.size(); ++i) out[i] = r[i];
         *n_out = (int)r.size();
@@ -2283,7 +2446,9 @@ ea_status ea_search_top_slab(ea_ctx* ctx, const ea_levels* lv, const ea_search_c
         check_search_config(lv, *cfg);
         DeviceGuard dg(ctx->device);
         const int top = cfg->num_levels - 1;
-        if (it_end == 0) it_end = 1;
+        const uint64_t nt = counts_of(top_grid_of(*cfg)).nt;
+        *n_seeds = 0;
+        if (std::min(it_end, nt) <= std::min(it_begin, nt)) return;  // empty slab
         const auto r = top_search(ctx, lv->models[top], lv->fields[top], top_grid_of(*cfg),
                                   cfg->score_params, cfg->topk, it_begin, it_end);
         for (size_t i = 0; i < r.size(); ++i) seeds[i] = r[i];
@@ -2302,24 +2467,15 @@ ea_status ea_search_top_slab_async(ea_ctx* ctx, const ea_levels* lv,
         check_search_config(lv, *cfg);
         DeviceGuard dg(ctx->device);
         const int top = cfg->num_levels - 1;
-        if (it_end == 0) it_end = 1;
-        const ea_pose_grid tg = top_grid_of(*cfg);
-        const ea_grid_counts c = counts_of(tg);
         if (!ctx->async_flag.p) {
             ctx->async_flag.ensure(sizeof(int));
             EAB_CUDA(cudaMemsetAsync(ctx->async_flag.p, 0, sizeof(int), ctx->stream));
         }
-        // a generous candidate buffer: the band is checked on the device and
-        // reported by ea_ctx_async_status
-        const unsigned long long cap = std::max<unsigned long long>(initial_cap(ctx), 1ull << 20);
-        const TopLaunch t = top_enqueue(ctx, lv->models[top], lv->fields[top], tg,
-                                        cfg->score_params, cfg->topk, it_begin, it_end, cap,
-                                        d_rows, ctx->async_flag.as<int>());
-        if (t.plan.slab_poses == 0) {  // empty slab: k empty rows
-            RowGrid g{tg.x0, tg.dx, tg.y0, tg.dy, tg.t0, tg.dt, c.nx, c.ny};
-            launch_topk_rows(ctx, t.top_score, t.top_index, ctx->ctrl.as<SearchCtrl>(), cap,
-                             cfg->topk, g, d_rows, ctx->async_flag.as<int>());
-        }
+        // the candidate buffer covers the whole slab (async_cap), so the band
+        // cannot overflow for slabs up to 2^26 poses; beyond, an overflow is
+        // flagged for ea_ctx_async_status and marked in row 0
+        slab_rows(ctx, lv->models[top], lv->fields[top], top_grid_of(*cfg), cfg->score_params,
+                  cfg->topk, it_begin, it_end, d_rows, ctx->async_flag.as<int>());
     });
 }
 
@@ -2330,7 +2486,9 @@ ea_status ea_merge_rows_async(ea_ctx* ctx, const double* d_rows, int n_rows, int
         need(d_rows, "d_rows");
         need(d_out, "d_out");
         if (k < 1) fail(EA_ERR_INVALID_ARGUMENT, "topk must be >= 1");
-        if (n_rows < 0 || n_rows > 8192) fail(EA_ERR_INVALID_ARGUMENT, "0 <= n_rows <= 8192");
+        if (n_rows < 0 || n_rows > merge_rows_max(ctx))
+            fail(EA_ERR_INVALID_ARGUMENT,
+                 "0 <= n_rows <= " + std::to_string(merge_rows_max(ctx)) + " required");
         DeviceGuard dg(ctx->device);
         launch_merge_rows(ctx, d_rows, n_rows, k, d_out);
     });
@@ -2434,6 +2592,158 @@ ea_status ea_refine(ea_ctx* ctx, const ea_levels* lv, const ea_search_config* cf
         refine_enqueue(ctx, lv, *cfg, tg, tables, st);
         d2h(ctx, out, st.out, sizeof(ea_outcome));
         sync(ctx);
+    });
+}
+
+// ---- multi-GPU -------------------------------------------------------------------------------
+void ea_theta_slab(uint64_t nt, int rank, int world, uint64_t* it_begin, uint64_t* it_end) {
+    uint64_t b = 0, e = 0;
+    if (world >= 1 && rank >= 0 && rank < world) theta_slab_of(nt, rank, world, &b, &e);
+    if (it_begin) *it_begin = b;
+    if (it_end) *it_end = e;
+}
+
+ea_status ea_comm_unique_id(ea_comm_id* out) {
+    return guard([&] {
+        need(out, "out");
+        ncclUniqueId id;
+        EAB_NCCL(nccl().GetUniqueId(&id));
+        std::memcpy(out->internal, &id, sizeof id);
+    });
+}
+
+ea_status ea_comm_init(ea_ctx* ctx, int rank, int world, const ea_comm_id* id) {
+    return guard([&] {
+        need(ctx, "ctx");
+        need(id, "id");
+        if (world < 1 || rank < 0 || rank >= world)
+            fail(EA_ERR_INVALID_ARGUMENT, "need 0 <= rank < world");
+        DeviceGuard dg(ctx->device);
+        const NcclApi& api = nccl();
+        if (ctx->comm) {
+            sync(ctx);
+            api.CommDestroy(static_cast<ncclComm_t>(ctx->comm));
+            ctx->comm = nullptr;
+        }
+        ncclUniqueId uid;
+        std::memcpy(&uid, id->internal, sizeof uid);
+        ncclComm_t c = nullptr;
+        EAB_NCCL(api.CommInitRank(&c, world, uid, rank));
+        ctx->comm = c;
+        ctx->comm_rank = rank;
+        ctx->comm_world = world;
+    });
+}
+
+ea_status ea_comm_info(const ea_ctx* ctx, int* rank, int* world) {
+    return guard([&] {
+        need(ctx, "ctx");
+        comm_of(ctx);
+        if (rank) *rank = ctx->comm_rank;
+        if (world) *world = ctx->comm_world;
+    });
+}
+
+ea_status ea_comm_destroy(ea_ctx* ctx) {
+    return guard([&] {
+        need(ctx, "ctx");
+        if (!ctx->comm) return;
+        DeviceGuard dg(ctx->device);
+        sync(ctx);
+        EAB_NCCL(nccl().CommDestroy(static_cast<ncclComm_t>(ctx->comm)));
+        ctx->comm = nullptr;
+        ctx->comm_rank = 0;
+        ctx->comm_world = 1;
+    });
+}
+
+ea_status ea_gather_rows_async(ea_ctx* ctx, const double* d_local, int k, double* d_merged) {
+    return guard([&] {
+        need(ctx, "ctx");
+        need(d_local, "d_local");
+        need(d_merged, "d_merged");
+        if (k < 1) fail(EA_ERR_INVALID_ARGUMENT, "topk must be >= 1");
+        DeviceGuard dg(ctx->device);
+        gather_rows(ctx, d_local, k, d_merged, /*seed_topk=*/false);
+    });
+}
+
+ea_status ea_search_levels_sharded(ea_ctx* ctx, const ea_levels* lv, const ea_search_config* cfg,
+                                   ea_outcome* out) {
+    return guard([&] {
+        need(ctx, "ctx");
+        need(lv, "levels");
+        need(cfg, "config");
+        need(out, "out");
+        check_search_config(lv, *cfg);
+        comm_of(ctx);
+        DeviceGuard dg(ctx->device);
+        const uint64_t launched0 = ctx->launches;
+        search_levels_sharded(ctx, lv, lv->fields[cfg->num_levels - 1], *cfg, out);
+        ctx->stats.kernels_launched = (int)(ctx->launches - launched0);
+    });
+}
+
+ea_status ea_detect_sharded(ea_ctx* ctx, ea_levels* lv, const double* image, int w, int h,
+                            const ea_search_config* cfg, ea_outcome* out) {
+    return guard([&] {
+        need(ctx, "ctx");
+        need(lv, "levels");
+        need(cfg, "config");
+        need(out, "out");
+        comm_of(ctx);
+        const bool root = ctx->comm_rank == 0;
+        if (root) need(image, "image");
+        DeviceGuard dg(ctx->device);
+        const int L = cfg->num_levels;
+        if (L < 1 || (int)lv->models.size() < L)
+            fail(EA_ERR_INVALID_ARGUMENT, "prepared levels do not cover num_levels");
+        if (L > EA_MAX_LEVELS) fail(EA_ERR_INVALID_ARGUMENT, "num_levels exceeds EA_MAX_LEVELS");
+        validate_params(cfg->score_params);
+        if (cfg->topk < 1 || cfg->refine_radius < 1)
+            fail(EA_ERR_INVALID_ARGUMENT, "topk and refine_radius must be >= 1");
+        if (w < 1 || h < 1) {
+            fail(EA_ERR_SIZE, "image dimensions must be at least 1x1, got " + std::to_string(w) +
+                                  "x" + std::to_string(h));
+        }
+        const int feasible = pyramid_levels_feasible(w, h);
+        if (L > feasible) {
+            fail(EA_ERR_SIZE, "pyramid of " + std::to_string(L) +
+                                  " levels would drop below 8x8; maximum feasible level count is " +
+                                  std::to_string(feasible));
+        }
+        const uint64_t launched0 = ctx->launches;
+        if (ctx->timing) EAB_CUDA(cudaEventRecord(ctx->ev[4], ctx->stream));
+        const int top = L - 1, wt = w >> top, ht = h >> top;
+        ea_field* ftop = nullptr;
+        if (root) {  // the whole working pyramid and every level's field
+            set_working_image(ctx, lv, image, w, h, L);
+            ftop = lv->fields[top];
+        } else {  // only the top level's field, from the root
+            if (lv->shard_top && (lv->shard_top->width != wt || lv->shard_top->height != ht)) {
+                delete lv->shard_top;
+                lv->shard_top = nullptr;
+            }
+            if (!lv->shard_top) lv->shard_top = new_field(wt, ht);
+            ftop = lv->shard_top;
+        }
+        // SURVEY §8(e) e1 input distribution: one broadcast of gx|gy|mag of
+        // the top level (cfg3: 162 x 121 x 24 B = 470 KB) instead of the
+        // 40 MB level-0 image on every rank
+        EAB_NCCL(nccl().Broadcast(ftop->g.p, ftop->g.p, 3 * (size_t)wt * ht, ncclDouble, 0,
+                                  comm_of(ctx), ctx->stream));
+        if (!root) {
+            ftop->version = next_field_version();
+            ftop->ring_max = 0.0;  // a Sobel field: the border ring is exactly 0
+        }
+        if (ctx->timing) EAB_CUDA(cudaEventRecord(ctx->ev[5], ctx->stream));
+        search_levels_sharded(ctx, lv, ftop, *cfg, out);
+        if (ctx->timing) {
+            float ms = 0.f;
+            EAB_CUDA(cudaEventElapsedTime(&ms, ctx->ev[4], ctx->ev[5]));
+            ctx->stats.image_ms = ms;
+        }
+        ctx->stats.kernels_launched = (int)(ctx->launches - launched0);
     });
 }
 

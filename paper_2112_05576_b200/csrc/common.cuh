@@ -125,6 +125,9 @@ struct ea_levels {
     eab::DevBuf image2;
     std::vector<ea_field*> fields3;
     eab::DevBuf image3;
+    // theta-sharded detect on a rank other than the root: the top level's
+    // field as broadcast by the root (the only level such a rank searches)
+    ea_field* shard_top = nullptr;
 };
 
 struct ea_ctx {
@@ -167,6 +170,11 @@ struct ea_ctx {
     // async (device-resident) searches: overflow flag and a ring of screen
     // kernel event pairs read back by ea_ctx_async_status
     eab::DevBuf async_flag;
+    // multi-GPU: NCCL communicator (ea_comm_init) and the sharded path's
+    // buffers (local rows, all-gathered rows, merged rows, outcome)
+    void* comm = nullptr;  // ncclComm_t
+    int comm_rank = 0, comm_world = 1;
+    eab::DevBuf shard;
     static constexpr int kTimeRing = 64;
     cudaEvent_t tev[2 * kTimeRing] = {};
     int tev_next = 0, tev_pending = 0;

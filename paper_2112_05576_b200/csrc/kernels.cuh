@@ -308,7 +308,12 @@ struct RowGrid {
 void launch_topk_rows(ea_ctx* ctx, const double* score, const unsigned long long* index,
                       const SearchCtrl* ctrl, unsigned long long cap, int k, const RowGrid& g,
                       double* rows, int* overflow);
-void launch_merge_rows(ea_ctx* ctx, const double* in, int n, int k, double* out);
+// top_score/top_index/n_top (optional): the merged top k as a search's
+// select leaves it.  n <= merge_rows_max(ctx) rows (shared-memory staging).
+void launch_merge_rows(ea_ctx* ctx, const double* in, int n, int k, double* out,
+                       double* top_score = nullptr, unsigned long long* top_index = nullptr,
+                       int* n_top = nullptr);
+int merge_rows_max(ea_ctx* ctx);
 // compaction + rescore + select (+ rows when rows != nullptr) in one
 // cooperative launch; same results as launch_compact/rescore/select/topk_rows.
 struct FinishArgs {

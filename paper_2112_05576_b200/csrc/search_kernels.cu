@@ -1574,11 +1574,19 @@ __device__ __forceinline__ void topk_rows_body(const double* __restrict__ score,
                                                unsigned long long cap, int k, const RowGrid& g,
                                                double* __restrict__ rows, int* overflow) {
     const int n = ctrl->n_out;
-    if (threadIdx.x == 0 && ctrl->cand_count > cap) atomicOr(overflow, 1);
+    // Band overflow (more candidates than the buffer): the rows are not the
+    // slab's top k.  Flag it, and mark row 0 with score +inf so that the
+    // mark survives an all-gather + `better` merge (it ranks first) and
+    // every rank of a sharded search sees it.
+    const bool over = ctrl->cand_count > cap;
+    if (threadIdx.x == 0 && over && overflow) atomicOr(overflow, 1);
     const unsigned long long plane = g.nx * g.ny;
     for (int r = threadIdx.x; r < k; r += blockDim.x) {
         double* o = rows + 5 * (size_t)r;
-        if (r < n) {
+        if (over && r == 0) {
+            o[0] = __longlong_as_double(0x7ff0000000000000LL);  // +inf
+            o[1] = o[2] = o[3] = o[4] = 0.0;
+        } else if (r < n) {
             const unsigned long long idx = index[r];
             const unsigned long long it = idx / plane, rem = idx % plane;
             o[0] = score[r];
@@ -1917,17 +1925,29 @@ void launch_finish(ea_ctx* ctx, const FinishArgs& f) {
 
 // The `better` merge of several slabs' rows (search.cpp:130-139): rank of
 // each valid row among all valid rows by (score desc, index asc); rows with
-// rank < k land at their rank, the rest of the output is NaN rows.
+// rank < k land at their rank, the rest of the output is NaN rows.  With
+// top_score/top_index/n_top set it also writes the merged top k in the
+// layout a search's select leaves (the seed kernel's input), so a sharded
+// search refines from the merge without a host round trip.
 __global__ void __launch_bounds__(256) merge_rows_kernel(const double* __restrict__ in, int n,
-                                                         int k, double* __restrict__ out) {
+                                                         int k, double* __restrict__ out,
+                                                         double* __restrict__ top_score,
+                                                         unsigned long long* __restrict__ top_index,
+                                                         int* __restrict__ n_top) {
     extern __shared__ long long mk[];  // order key | index per input row
     long long* key = mk;
     unsigned long long* idx = reinterpret_cast<unsigned long long*>(mk + n);
+    __shared__ int valid;
+    if (threadIdx.x == 0) valid = 0;
+    __syncthreads();
+    int mine = 0;
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
         const double sc = in[5 * (size_t)i];
         key[i] = sc != sc ? LLONG_MIN : order_key(sc);
         idx[i] = (unsigned long long)in[5 * (size_t)i + 1];
+        mine += sc == sc;
     }
+    if (mine) atomicAdd(&valid, mine);
     for (int r = threadIdx.x; r < k; r += blockDim.x) {
         double* o = out + 5 * (size_t)r;
         o[0] = __longlong_as_double(0x7ff8000000000000LL);
@@ -1940,9 +1960,15 @@ __global__ void __launch_bounds__(256) merge_rows_kernel(const double* __restric
         for (int j = 0; j < n; ++j)
             rank += key[j] > key[i] || (key[j] == key[i] && key[j] != LLONG_MIN &&
                                         (idx[j] < idx[i] || (idx[j] == idx[i] && j < i)));
-        if (rank < k)
+        if (rank < k) {
             for (int c = 0; c < 5; ++c) out[5 * (size_t)rank + c] = in[5 * (size_t)i + c];
+            if (top_score) {
+                top_score[rank] = in[5 * (size_t)i];
+                top_index[rank] = idx[i];
+            }
+        }
     }
+    if (n_top && threadIdx.x == 0) *n_top = valid < k ? valid : k;
 }
 
 void launch_topk_rows(ea_ctx* ctx, const double* score, const unsigned long long* index,
@@ -1953,8 +1979,19 @@ void launch_topk_rows(ea_ctx* ctx, const double* score, const unsigned long long
     count_launch(ctx);
 }
 
-void launch_merge_rows(ea_ctx* ctx, const double* in, int n, int k, double* out) {
-    merge_rows_kernel<<<1, 256, (size_t)n * 16, ctx->stream>>>(in, n, k, out);
+int merge_rows_max(ea_ctx* ctx) { return (int)(ctx->smem_optin / 16); }
+
+void launch_merge_rows(ea_ctx* ctx, const double* in, int n, int k, double* out,
+                       double* top_score, unsigned long long* top_index, int* n_top) {
+    const size_t smem = (size_t)n * 16;
+    static size_t opted = 48 * 1024;  // dynamic shared memory beyond 48 KB is opt-in
+    if (smem > opted) {
+        EAB_CUDA(cudaFuncSetAttribute(merge_rows_kernel,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)ctx->smem_optin));
+        opted = ctx->smem_optin;
+    }
+    merge_rows_kernel<<<1, 256, smem, ctx->stream>>>(in, n, k, out, top_score, top_index, n_top);
     check_launch("merge_rows_kernel");
     count_launch(ctx);
 }

@@ -50,6 +50,10 @@ class CudaError(Error):
     """Device missing or CUDA runtime failure (no reference counterpart)."""
 
 
+class NcclError(Error):
+    """NCCL missing or a collective failed (multi-GPU path; no reference counterpart)."""
+
+
 _BY_STATUS = {
     abi.EA_ERR_INVALID_ARGUMENT: InvalidArgument,
     abi.EA_ERR_SIZE: SizeError,
@@ -57,6 +61,7 @@ _BY_STATUS = {
     abi.EA_ERR_BUDGET: BudgetError,
     abi.EA_ERR_GEOMETRY: GeometryError,
     abi.EA_ERR_CUDA: CudaError,
+    abi.EA_ERR_NCCL: NcclError,
     abi.EA_ERR_INTERNAL: Error,
 }
 

@@ -664,6 +664,7 @@ def test_gather_rows_device_nccl_single_rank(ea, oracle):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
     try:
+        parallel.init_comm(det.ctx)  # the library's own NCCL communicator (id over torch)
         stream = torch.cuda.Stream()
         with torch.cuda.stream(stream):
             det.ctx.set_stream(stream.cuda_stream)
@@ -677,6 +678,7 @@ def test_gather_rows_device_nccl_single_rank(ea, oracle):
     finally:
         dist.destroy_process_group()
         det.ctx.set_stream(None)
+        det.ctx.comm_destroy()
 
 
 def test_plane_cache_follows_field_and_params(ea, oracle):

@@ -1,0 +1,163 @@
+"""The multi-GPU data path of the C++ library (include/edgealign_b200.h,
+"multi-GPU") on one B200: an NCCL communicator of world size 1 joined with
+ea_comm_init, the device all-gather + `better` merge (ea_gather_rows_async),
+the sharded detect (ea_detect_sharded: input broadcast, slab search,
+all-gather, merge, root refinement, outcome broadcast) and its host-only
+partition (ea_theta_slab).  Results must equal the single-GPU detect and the
+CPU oracle bit for bit (reference run_search partition + merge,
+search.cpp:116-139).  Several ranks on one GPU are not run (their kernels
+would wait on one another); the rank logic at world 2/3 is covered on CPU by
+tests/test_multiproc.py."""
+import numpy as np
+import pytest
+
+from paper_2112_05576_b200 import abi, parallel
+
+pytestmark = pytest.mark.gpu
+
+D = abi.deg_to_rad
+
+
+def keys(lst):
+    return [(s.score, int(s.grid_index), s.pose.astuple()) for s in lst]
+
+
+def scene(ea, **kw):
+    img, tmpl, _, _ = ea.compose_scene(ea.SceneSpec(**kw))
+    return img, tmpl
+
+
+@pytest.fixture()
+def comm_ctx(ea):
+    """A fresh context joined to a world-1 NCCL communicator."""
+    ctx = ea.Context(0)
+    ctx.comm_init(0, 1, ea.comm_unique_id())
+    assert ctx.comm_info() == (0, 1)
+    yield ctx
+    ctx.comm_destroy()
+    assert not ctx.has_comm()
+    ctx.close()
+
+
+CASES = [
+    dict(scene=dict(canvas_width=200, canvas_height=160, template_id="l_bracket",
+                    template_size=56, true_pose=(96, 84, D(63)), clutter_segments=25,
+                    clutter_seed=4, noise_sigma=1.0, noise_seed=2),
+         grid=(0, 199, 4, 0, 159, 4, 0.0, D(357), D(3)), L=3, k=4),
+    dict(scene=dict(canvas_width=320, canvas_height=240, template_id="l_bracket",
+                    template_size=64, true_pose=(150, 110, D(200)), clutter_segments=30,
+                    clutter_seed=5, noise_sigma=2.0, noise_seed=3,
+                    illumination=(1.3, -10.0, 1.1)),
+         grid=(0, 319, 4, 0, 239, 4, 0.0, D(358), D(2)), L=3, k=5),
+    dict(scene=dict(canvas_width=256, canvas_height=256, template_id="rectangle",
+                    template_size=64, true_pose=(100, 60, D(30))),
+         grid=(40, 216, 8, 40, 216, 8, 0.0, D(88), D(4)), L=2, k=5),
+    # no refinement level: the merged seed is the answer
+    dict(scene=dict(canvas_width=96, canvas_height=96, template_id="cross", template_size=32,
+                    true_pose=(48, 48, 0.0)),
+         grid=(24, 72, 2, 24, 72, 2, 0.0, 0.0, 1.0), L=1, k=5),
+]
+
+
+@pytest.mark.parametrize("case", range(len(CASES)))
+def test_detect_sharded_world1_equals_detect_and_oracle(ea, oracle, comm_ctx, case):
+    c = CASES[case]
+    img, tmpl = scene(ea, **c["scene"])
+    cfg = ea.SearchConfig(grid=ea.PoseGrid(*c["grid"]), num_levels=c["L"],
+                          score_params=ea.ScoreParams(3), topk=c["k"])
+    det = ea.Detector(tmpl, cfg, comm_ctx)
+    got = det.detect_sharded(img)
+    again = det.detect_sharded(img)  # cached plane / tables path
+    single = det.detect(img)
+    assert got.key() == single.key() == again.key()
+    want = oracle.coarse_to_fine(oracle.build_pyramid(tmpl, c["L"]),
+                                 oracle.build_pyramid(img, c["L"]), cfg)
+    assert got.key() == want.key()
+    # search_levels_sharded on the working image already set
+    assert ea.search_levels_sharded(det.levels, cfg).key() == want.key()
+
+
+def test_gather_rows_library_nccl_world1(ea, comm_ctx):
+    """ea_gather_rows_async (NCCL all-gather + device merge, inside the
+    library) on one rank == the rank's own rows == ea_search_top_slab."""
+    import torch
+    img, tmpl = scene(ea, canvas_width=160, canvas_height=128, template_id="l_bracket",
+                      template_size=48, true_pose=(80, 64, D(20)), clutter_segments=10,
+                      clutter_seed=3)
+    cfg = ea.SearchConfig(grid=ea.PoseGrid(0, 159, 2, 0, 127, 2, 0.0, D(355), D(5)),
+                          num_levels=2, score_params=ea.ScoreParams(3), topk=5)
+    det = ea.Detector(tmpl, cfg, comm_ctx)
+    det.levels.set_image(img)
+    stream = torch.cuda.Stream()
+    comm_ctx.set_stream(stream.cuda_stream)
+    try:
+        rows = torch.empty((5, 5), dtype=torch.float64, device="cuda")
+        ea.search_top_slab_async(det.levels, cfg, 0, 72, rows.data_ptr())
+        merged = parallel.gather_rows_device(rows, 5, comm_ctx)
+        stream.synchronize()
+        overflowed, _ = ea.async_status(comm_ctx)
+        assert not overflowed
+    finally:
+        comm_ctx.set_stream(None)
+    want = ea.search_top_slab(det.levels, cfg, 0, 72)
+    assert keys(parallel.unpack(merged.cpu().numpy())) == keys(want)
+    assert keys(parallel.unpack(rows.cpu().numpy())) == keys(want)
+
+
+def test_gather_rows_needs_comm(ea):
+    import torch
+    ctx = ea.Context(0)
+    try:
+        rows = torch.zeros((5, 5), dtype=torch.float64, device="cuda")
+        with pytest.raises(ea.InvalidArgument, match="no communicator"):
+            ea.gather_rows_async(ctx, rows.data_ptr(), 5, rows.data_ptr())
+    finally:
+        ctx.close()
+
+
+def test_empty_slab_rows_are_empty_after_a_search(ea):
+    """An empty theta slab (more ranks than thetas) writes k NaN rows, never
+    the previous search's top k (stale n_out)."""
+    import torch
+    img, tmpl = scene(ea, canvas_width=160, canvas_height=128, template_id="l_bracket",
+                      template_size=48, true_pose=(80, 64, D(20)), clutter_segments=10,
+                      clutter_seed=3)
+    cfg = ea.SearchConfig(grid=ea.PoseGrid(0, 159, 2, 0, 127, 2, 0.0, D(355), D(5)),
+                          num_levels=2, score_params=ea.ScoreParams(3), topk=5)
+    det = ea.Detector(tmpl, cfg)
+    det.levels.set_image(img)
+    rows = torch.empty((5, 5), dtype=torch.float64, device="cuda")
+    ea.search_top_slab_async(det.levels, cfg, 0, 72, rows.data_ptr())
+    ea.async_status(det.ctx)
+    assert not np.isnan(rows.cpu().numpy()[:, 0]).any()
+    for a, b in ((10, 10), (72, 72), (80, 90), (9, 3)):
+        ea.search_top_slab_async(det.levels, cfg, a, b, rows.data_ptr())
+        ea.async_status(det.ctx)
+        assert np.isnan(rows.cpu().numpy()[:, 0]).all(), (a, b)
+        assert ea.search_top_slab(det.levels, cfg, a, b) == []
+    # and the next real search is unaffected
+    ea.search_top_slab_async(det.levels, cfg, 0, 72, rows.data_ptr())
+    ea.async_status(det.ctx)
+    assert keys(parallel.unpack(rows.cpu().numpy())) == keys(ea.search_top_slab(det.levels, cfg, 0, 72))
+
+
+@pytest.mark.parametrize("n", [3072, 3200, 8192])
+def test_merge_rows_many(ea, n):
+    """More rows than the 48 KB default dynamic shared memory holds (ADVICE
+    r01: merge_rows_kernel did not opt in): the merge == a host sort by
+    `better`, including tied scores broken by index and NaN (empty) rows."""
+    import torch
+    rng = np.random.default_rng(n)
+    k = 7
+    rows = np.zeros((n, 5))
+    rows[:, 0] = rng.integers(0, 50, size=n) / 64.0
+    rows[:, 1] = rng.permutation(10 * n)[:n]
+    rows[:, 2:] = rng.normal(size=(n, 3))
+    rows[rng.random(n) < 0.2, 0] = np.nan
+    d_in = torch.from_numpy(rows).cuda()
+    d_out = torch.empty((k, 5), dtype=torch.float64, device="cuda")
+    ctx = ea.default_context()
+    ea.merge_rows_async(ctx, d_in.data_ptr(), n, k, d_out.data_ptr())
+    ctx.synchronize()
+    want = parallel.merge(parallel.unpack(rows), k)
+    assert keys(parallel.unpack(d_out.cpu().numpy())) == keys(want)

@@ -1,7 +1,10 @@
-"""World-size-2 `gloo` runs of the theta-slab sharding (paper_2112_05576_b200
-.parallel) on CPU: per-rank top-k over its slab (the C oracle stands in for
-the device search here), one all-gather, `better` merge == the single-process
-search_topk, bit for bit, on every rank."""
+"""World-size-2/3 `gloo` runs of the theta-slab sharding on CPU, through the
+library's C-ABI wherever it has no device work: the rank partition
+(ea_theta_slab), the NCCL id handed from rank 0 to every rank
+(ea_comm_unique_id -> ea_comm_init's input), the `better` merge
+(ea_merge_topk).  Per rank, the C oracle stands in for the device search
+over its slab; one all-gather; the merge == the single-process search_topk,
+bit for bit, on every rank."""
 import multiprocessing as mp
 import os
 import socket
@@ -9,7 +12,7 @@ import socket
 import numpy as np
 import pytest
 
-from paper_2112_05576_b200 import abi, parallel
+from paper_2112_05576_b200 import abi, api, parallel
 
 D = abi.deg_to_rad
 
@@ -42,7 +45,19 @@ def worker(rank, world, port, seed, k, q):
         local = orc.search_topk(m.points, f, grid, abi.ScoreParams(3), k, it_range=(it0, it1),
                                 threads=2)
         merged = parallel.gather_topk(local, k)
-        q.put((rank, [(s.score, int(s.grid_index), s.pose.astuple()) for s in merged]))
+        # the same exchange with the library's merge (ea_merge_topk, C-ABI)
+        import torch
+        rows = torch.from_numpy(parallel.pack(local, k))
+        allrows = torch.empty((world * k, parallel.ROW), dtype=torch.float64)
+        dist.all_gather_into_tensor(allrows, rows)
+        merged_c = api.merge_topk(parallel.unpack(allrows.numpy()), k)
+        # rank 0's NCCL id reaches every rank intact (the ea_comm_init input)
+        cid = parallel.share_comm_id()
+        ids = [None] * world
+        dist.all_gather_object(ids, abi.comm_id_bytes(cid))
+        q.put((rank, [(s.score, int(s.grid_index), s.pose.astuple()) for s in merged],
+               [(s.score, int(s.grid_index), s.pose.astuple()) for s in merged_c],
+               (it0, it1), len(set(ids)) == 1 and len(ids[0]) == abi.EA_COMM_ID_BYTES))
     finally:
         dist.destroy_process_group()
 
@@ -55,7 +70,8 @@ def test_theta_slabs_gather_merge_equals_full(world, k, seed):
     procs = [ctx.Process(target=worker, args=(r, world, port, seed, k, q)) for r in range(world)]
     for p in procs:
         p.start()
-    res = dict(q.get(timeout=240) for _ in procs)
+    got = [q.get(timeout=240) for _ in procs]
+    res = {g[0]: g[1] for g in got}
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
@@ -64,14 +80,30 @@ def test_theta_slabs_gather_merge_equals_full(world, k, seed):
     want = [(s.score, int(s.grid_index), s.pose.astuple()) for s in full]
     for r in range(world):
         assert res[r] == want
+    slabs = sorted(g[3] for g in got)
+    assert slabs[0][0] == 0 and slabs[-1][1] == orc.grid_counts(grid)[2]
+    assert all(a[1] == b[0] for a, b in zip(slabs, slabs[1:]))
+    for g in got:
+        assert g[2] == want  # library merge
+        assert g[4]          # one id on every rank
 
 
 def test_slab_partition_covers_grid():
-    for nt in (1, 7, 720, 1440):
-        for world in (1, 2, 3, 8):
+    """ea_theta_slab == the reference's block partition (search.cpp:116-120)."""
+    for nt in (1, 5, 7, 720, 1440, 2 ** 40 + 3):
+        for world in (1, 2, 3, 8, 16):
             slabs = [parallel.theta_slab(nt, r, world) for r in range(world)]
+            assert slabs == [(nt * r // world, nt * (r + 1) // world) for r in range(world)]
             assert slabs[0][0] == 0 and slabs[-1][1] == nt
             assert all(a[1] == b[0] for a, b in zip(slabs, slabs[1:]))
+    assert api.theta_slab(10, 3, 2) == (0, 0)  # rank out of range: empty
+
+
+def test_comm_id_roundtrip():
+    cid = api.comm_unique_id()
+    raw = abi.comm_id_bytes(cid)
+    assert len(raw) == abi.EA_COMM_ID_BYTES
+    assert abi.comm_id_bytes(abi.comm_id_from_bytes(raw)) == raw
 
 
 def test_pack_unpack_roundtrip():
