@@ -272,6 +272,23 @@ struct TopOut {
 
 bool is_int(double v) { return std::floor(v) == v && std::fabs(v) <= 1048576.0; }
 
+ExactArgs exact_args(const ea_field* f, const ea_score_params& p, const double* rot,
+                     size_t rot_stride, int n) {
+    ExactArgs x{};
+    x.gx = f->gx();
+    x.gy = f->gy();
+    x.mag = f->mag();
+    x.W = f->width;
+    x.H = f->height;
+    x.R = (p.neighborhood - 1) / 2;
+    x.ignore = p.polarity == EA_POLARITY_IGNORE;
+    x.eps = p.eps_mag;
+    x.rot_exact = rot;
+    x.rot_stride = rot_stride;
+    x.n = n;
+    return x;
+}
+
 // Shared by search_topk, search_top_slab and screen_map: tables, plane and the
 // screening pass.  Returns the fixed-point exponent chosen.
 struct ScreenPlan {
@@ -280,15 +297,28 @@ struct ScreenPlan {
     int fold_e = 0;
     double delta = 0.0;
     bool fast = false;
+    bool fused = false;  // the screen launch also ran the finish (launch_screen_fused)
+    float* cta_top = nullptr;  // top-list mode: the screen's per-CTA lists (FinishArgs::cta_top)
     ItemGeom items{};
     const double* rot = nullptr;  // exact rotation table of the slab (model cache)
     const int* flags = nullptr;   // device count of rounding-ambiguous pairs
 };
 
+// What the fused screen + finish launch needs from the search (top_enqueue).
+struct FusedReq {
+    unsigned long long cap;
+    double* top_score;
+    unsigned long long* top_index;
+    double* d_rows;
+    int* overflow;
+};
+
 // k: the search's top-k (enables the screen kernels' histogram floor when
-// k <= kFloorK); 0 for a plain screening map.
+// k <= kFloorK); 0 for a plain screening map.  req: a top-k search that may
+// run its finish inside the screen launch (plan.fused reports whether it did).
 ScreenPlan screen(ea_ctx* ctx, const ea_model* m, const ea_field* f, const ea_pose_grid& g,
-                  const ea_score_params& p, uint64_t it_begin, uint64_t it_end, int k = 0) {
+                  const ea_score_params& p, uint64_t it_begin, uint64_t it_end, int k = 0,
+                  const FusedReq* req = nullptr) {
     ScreenPlan plan;
     plan.c = counts_of(g);
     if (it_end == 0 || it_end > plan.c.nt) it_end = plan.c.nt;
@@ -470,9 +500,16 @@ ScreenPlan screen(ea_ctx* ctx, const ea_model* m, const ea_field* f, const ea_po
             EAB_CUDA(cudaStreamSynchronize(ctx->stream));
             EAB_CUDA(cudaMemcpy(h, sprof, sizeof h, cudaMemcpyDeviceToHost));
             std::fprintf(stderr, "[screen] ns from first entry: plane landed %lld, last warp loop end "
-                         "%lld, last CTA loop end %lld, last merge %lld\n",
+                         "%lld, last CTA loop end %lld, last merge / barrier 1 %lld",
                          (long long)(h[0] - h[4]), (long long)(h[1] - h[4]),
                          (long long)(h[2] - h[4]), (long long)(h[3] - h[4]));
+            if (h[5])  // fused finish phases
+                std::fprintf(stderr, ", threshold %lld, compaction %lld, barrier 2 %lld, rescore %lld, "
+                             "select+rows %lld",
+                             (long long)(h[8] - h[4]), (long long)(h[9] - h[4]),
+                             (long long)(h[5] - h[4]), (long long)(h[6] - h[4]),
+                             (long long)(h[7] - h[4]));
+            std::fprintf(stderr, "\n");
         }
         EAB_CUDA(cudaStreamSynchronize(ctx->stream));
         for (int i = 0; i < 16; ++i) h[i] = (i == 0 || i == 4) ? ~0ull : 0ull;
@@ -480,7 +517,89 @@ ScreenPlan screen(ea_ctx* ctx, const ea_model* m, const ea_field* f, const ea_po
         ++nsprof;
         a.prof = sprof;
     }
-    if (plan.slab_poses) {
+    static unsigned long long* wtrace = nullptr;  // EAB_SCREEN_TRACE: per-warp unit stamps
+    static int nwtrace = 0;
+    if (std::getenv("EAB_SCREEN_TRACE") && plan.slab_poses) {
+        const size_t nw = (size_t)ctx->sm_count * 16;
+        if (!wtrace) {
+            EAB_CUDA(cudaMalloc(&wtrace, nw * 8 * sizeof(unsigned long long)));
+        } else if (nwtrace > 0) {
+            EAB_CUDA(cudaStreamSynchronize(ctx->stream));
+            std::vector<unsigned long long> h(nw * 8);
+            EAB_CUDA(cudaMemcpy(h.data(), wtrace, h.size() * 8, cudaMemcpyDeviceToHost));
+            unsigned long long t0 = ~0ull;
+            for (size_t w = 0; w < nw; ++w)
+                if (h[8 * w]) t0 = std::min(t0, h[8 * w]);
+            std::vector<double> first, last, start;
+            std::vector<int> cnt(8, 0);
+            const unsigned long long m56 = (1ull << 56) - 1;
+            for (size_t w = 0; w < nw; ++w) {
+                if (!h[8 * w]) continue;
+                const int u = (int)(h[8 * w + 7] >> 56);
+                ++cnt[std::min(u, 7)];
+                start.push_back((double)(h[8 * w] - t0) * 1e-3);
+                if (u >= 2) first.push_back((double)(h[8 * w + 1] - t0) * 1e-3);
+                last.push_back((double)((h[8 * w + 7] & m56) - (t0 & m56)) * 1e-3);
+            }
+            auto pct = [](std::vector<double> v, double q) {
+                if (v.empty()) return 0.0;
+                std::sort(v.begin(), v.end());
+                return v[(size_t)(q * (v.size() - 1))];
+            };
+            std::fprintf(stderr, "[trace] warps %zu; units/warp:", start.size());
+            for (int u = 0; u < 8; ++u) std::fprintf(stderr, " %d:%d", u, cnt[u]);
+            std::fprintf(stderr, " | start us p0/50/100 %.1f/%.1f/%.1f | first unit end %.1f/%.1f/%.1f"
+                         " | loop end %.1f/%.1f/%.1f/%.1f(p90)\n",
+                         pct(start, 0), pct(start, .5), pct(start, 1), pct(first, 0),
+                         pct(first, .5), pct(first, 1), pct(last, 0), pct(last, .5), pct(last, 1),
+                         pct(last, .9));
+        }
+        EAB_CUDA(cudaStreamSynchronize(ctx->stream));
+        EAB_CUDA(cudaMemset(wtrace, 0, (size_t)ctx->sm_count * 16 * 8 * sizeof(unsigned long long)));
+        ++nwtrace;
+        a.wtrace = wtrace;
+    }
+    // Top-list mode for a top-k search on the smem lattice kernel: no
+    // histogram, band threshold M_k - 2 delta from the k-th largest tile
+    // maximum (see fused_threshold) -- fewer candidates than the histogram
+    // bin's lower edge, and no per-pose histogram atomics in the screen.
+    if (plan.slab_poses && req && ctx->toplist && ctx->fused_finish && lattice && !region &&
+        mm->n_flagged == 0 && k >= 1 && k <= kTopK && ctx->sm_count <= 512) {
+        a.cta_top = (float*)ctx->cta_top.ensure(sizeof(float) * kTopK * (size_t)ctx->sm_count);
+        plan.cta_top = a.cta_top;
+    }
+    if (plan.slab_poses && req && ctx->fused_screen && plan.cta_top) {
+        // screen + finish in one cooperative launch (no histogram)
+        FinishArgs fa{};
+        fa.map = map;
+        fa.item_max = item_max;
+        fa.items = screen_items(a, true);
+        fa.ctrl = ctrl;
+        fa.cap = req->cap;
+        fa.cand = (unsigned*)ctx->cand.ensure(sizeof(unsigned) * req->cap);
+        fa.cand_score = (double*)ctx->cand_score.ensure(sizeof(double) * req->cap);
+        fa.k = k;
+        fa.delta = plan.delta;
+        fa.flags = nullptr;
+        ExactArgs x = exact_args(f, p, rot, slab_pairs, n);
+        x.nx = plan.c.nx;
+        x.ny = plan.c.ny;
+        x.it_begin = plan.it_begin;
+        x.x0 = g.x0;
+        x.dx = g.dx;
+        x.y0 = g.y0;
+        x.dy = g.dy;
+        fa.x = x;
+        fa.index_base = plan.it_begin * plan.c.nx * plan.c.ny;
+        fa.out_score = req->top_score;
+        fa.out_index = req->top_index;
+        fa.rg = RowGrid{g.x0, g.dx, g.y0, g.dy, g.t0, g.dt, plan.c.nx, plan.c.ny};
+        fa.rows = req->d_rows;
+        fa.overflow = req->overflow;
+        fa.cta_top = plan.cta_top;
+        plan.fused = plan.fast = launch_screen_fused(ctx, a, fa);
+    }
+    if (plan.slab_poses && !plan.fused) {
         if (lattice) plan.fast = region ? launch_screen_region(ctx, a) : launch_screen_fast(ctx, a);
         if (!plan.fast) launch_screen_general(ctx, a);
         else if (mm->n_flagged > 0) launch_screen_flagged(ctx, a);  // thetas the lattice kernel skipped
@@ -494,23 +613,6 @@ ScreenPlan screen(ea_ctx* ctx, const ea_model* m, const ea_field* f, const ea_po
     ctx->stats.screen_path = plan.fast ? (region ? 3 : 1) : 2;
     plan.items = screen_items(a, plan.fast);
     return plan;
-}
-
-ExactArgs exact_args(const ea_field* f, const ea_score_params& p, const double* rot,
-                     size_t rot_stride, int n) {
-    ExactArgs x{};
-    x.gx = f->gx();
-    x.gy = f->gy();
-    x.mag = f->mag();
-    x.W = f->width;
-    x.H = f->height;
-    x.R = (p.neighborhood - 1) / 2;
-    x.ignore = p.polarity == EA_POLARITY_IGNORE;
-    x.eps = p.eps_mag;
-    x.rot_exact = rot;
-    x.rot_stride = rot_stride;
-    x.n = n;
-    return x;
 }
 
 // run_search (search.cpp:95-140) on theta indices [it_begin, it_end), split in
@@ -536,17 +638,22 @@ TopLaunch top_enqueue(ea_ctx* ctx, const ea_model* m, const ea_field* f, const e
     ctx->stats = ea_search_stats{};
     if (ctx->timing) EAB_CUDA(cudaEventRecord(ctx->ev[0], ctx->stream));
     TopLaunch t;
-    t.plan = screen(ctx, m, f, g, p, it_begin, it_end, k);
+    double* tk = (double*)ctx->topk.ensure((sizeof(double) + sizeof(unsigned long long)) * (size_t)k);
+    t.top_score = tk;
+    t.top_index = reinterpret_cast<unsigned long long*>(tk + k);
+    const FusedReq req{cap, t.top_score, t.top_index, d_rows, overflow};
+    t.plan = screen(ctx, m, f, g, p, it_begin, it_end, k, &req);
     t.k = k;
     t.n = m->n;
     t.cap = cap;
     ctx->stats.poses = t.plan.slab_poses;
     ctx->stats.pose_points = t.plan.slab_poses * (uint64_t)m->n;
     SearchCtrl* ctrl = ctx->ctrl.as<SearchCtrl>();
-    double* tk = (double*)ctx->topk.ensure((sizeof(double) + sizeof(unsigned long long)) * (size_t)k);
-    t.top_score = tk;
-    t.top_index = reinterpret_cast<unsigned long long*>(tk + k);
     if (t.plan.slab_poses == 0) return t;
+    if (t.plan.fused) {  // the screen launch ran the finish; the histogram was not touched
+        ctx->hist_clean = true;
+        return t;
+    }
 
     const size_t slab_pairs = t.plan.it_count * (size_t)t.n;
     ExactArgs x = exact_args(f, p, t.plan.rot, slab_pairs, t.n);
@@ -583,6 +690,8 @@ TopLaunch top_enqueue(ea_ctx* ctx, const ea_model* m, const ea_field* f, const e
         fa.rg = rg;
         fa.rows = d_rows;
         fa.overflow = overflow;
+        fa.cta_top = t.plan.fast ? t.plan.cta_top : nullptr;
+        fa.n_lists = ctx->screen_ctas;
         launch_finish(ctx, fa);
         ctx->hist_clean = true;
         return t;
@@ -1751,7 +1860,8 @@ void ea_ctx_destroy(ea_ctx* ctx) {
                       &ctx->item_max, &ctx->tail,
                       &ctx->hist, &ctx->ctrl, &ctx->cand, &ctx->cand_score, &ctx->topk,
                       &ctx->refine_poses, &ctx->refine_scores, &ctx->beam, &ctx->accum64,
-                      &ctx->work, &ctx->ttab, &ctx->rstate, &ctx->rslots, &ctx->mscratch})
+                      &ctx->work, &ctx->ttab, &ctx->rstate, &ctx->rslots, &ctx->mscratch,
+                      &ctx->cta_top})
         b->release();
     ctx->h_stage.release();
     ctx->h_out.release();

@@ -151,10 +151,21 @@ struct ea_ctx {
     // one cooperative finish launch after the screen (EAB_NO_FUSED_FINISH=1:
     // the separate compact/rescore/select/rows launches, for A/B measurements)
     bool fused_finish = std::getenv("EAB_NO_FUSED_FINISH") == nullptr;
+    // screen + finish in one cooperative launch where eligible (top-list
+    // mode); off by default: measured on B200 it saves the finish launch on a
+    // full search (-13 us of 650) but costs a theta slab +6 us (the
+    // cooperative launch waits for the whole GPU) and batch detect +3 %
+    // (a cooperative grid cannot overlap the refinement stream);
+    // EAB_FUSED_SCREEN=1 enables it (tested)
+    bool fused_screen = std::getenv("EAB_FUSED_SCREEN") != nullptr &&
+                        std::getenv("EAB_NO_FUSED_FINISH") == nullptr;
+    // top-list mode of the smem lattice kernel (see screen(), api.cu);
+    // EAB_NO_TOPLIST=1: the histogram threshold (A/B, tested both ways)
+    bool toplist = std::getenv("EAB_NO_TOPLIST") == nullptr;
     cudaEvent_t ev[8] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
     // scratch
     eab::DevBuf cs, rot_exact, rot_screen, plane, map, item_max, tail, hist, ctrl, cand, cand_score, topk,
-        refine_poses, refine_scores, beam, accum64, work, mscratch;
+        refine_poses, refine_scores, beam, accum64, work, mscratch, cta_top;
     eab::HostBuf h_stage, h_out;
     // glibc cos/sin tables of theta grids, cached per (t0, dt, nt)
     std::map<std::vector<double>, std::vector<double>> cs_cache;
@@ -174,6 +185,7 @@ struct ea_ctx {
     // buffers (local rows, all-gathered rows, merged rows, outcome)
     void* comm = nullptr;  // ncclComm_t
     int comm_rank = 0, comm_world = 1;
+    int screen_ctas = 0;  // grid of the last smem lattice screen launch
     eab::DevBuf shard;
     static constexpr int kTimeRing = 64;
     cudaEvent_t tev[2 * kTimeRing] = {};

@@ -247,6 +247,11 @@ struct ScreenArgs {
     unsigned* hist;   // kHistBins
     SearchCtrl* ctrl;
     unsigned long long* prof;  // optional phase timestamps (EAB_SCREEN_PROF)
+    unsigned long long* wtrace;  // optional per-warp unit end stamps [warp][8] (EAB_SCREEN_TRACE)
+    // top-list mode (smem lattice kernel, 1 <= kf <= 8, no flagged theta):
+    // no histogram; each CTA writes its kf largest tile maxima here
+    // ([CTA][kTopK]) and the finish takes the band threshold from them
+    float* cta_top;
 };
 
 // Dynamic shared memory the lattice kernel needs for a plane.
@@ -337,8 +342,17 @@ struct FinishArgs {
     double* rows;
     int* overflow;
     unsigned long long* prof;  // optional phase timestamps (EAB_FINISH_PROF)
+    float* cta_top;            // top-list mode: [CTA][kTopK] largest tile maxima per screen CTA
+    int n_lists;               // screen CTAs that wrote cta_top
 };
 void launch_finish(ea_ctx* ctx, const FinishArgs& f);
+// Screen + finish in ONE cooperative launch (smem lattice kernel, k <= 8,
+// no flagged theta): the band threshold comes from the exact k-th largest
+// screen score (per-CTA top k, merged after a grid barrier) instead of the
+// histogram.  false = not eligible: use the launch_screen_fast +
+// launch_finish pair.
+bool launch_screen_fused(ea_ctx* ctx, const ScreenArgs& a, const FinishArgs& f);
+constexpr int kTopK = 8;  // largest k of the fused path (per-warp top-k lists)
 // Dense exact map (score_map search.cpp:169-202).
 void launch_exact_map(ea_ctx* ctx, const ExactArgs& a, unsigned long long total, double* out);
 

@@ -589,7 +589,7 @@ __device__ __forceinline__ void floor_insert(float* wtop, float best, int lane) 
     __syncwarp();
 }
 
-template <int S>
+template <int S, bool HIST = true>
 __device__ __forceinline__ float emit_tile(const ScreenArgs& a, const int (&acc)[S][kTW],
                                            const int X, const int Y, unsigned long long itr,
                                            unsigned long long item, unsigned* hist,
@@ -606,7 +606,8 @@ __device__ __forceinline__ float emit_tile(const ScreenArgs& a, const int (&acc)
                 const float sc = (float)acc[s][j] * a.scale;
                 out[iy * a.nx + ix] = sc;
                 best = fmaxf(best, sc);
-                if (sc >= floor) atomicAdd(&hist[hist_bin(sc)], 1u);
+                if constexpr (HIST)
+                    if (hist && sc >= floor) atomicAdd(&hist[hist_bin(sc)], 1u);
             }
         }
     }
@@ -616,247 +617,113 @@ __device__ __forceinline__ float emit_tile(const ScreenArgs& a, const int (&acc)
     return best;
 }
 
-template <int R, int S, int SHIFT, bool IGNORE, int XG, bool EDGE, int THREADS>
-__global__ void __launch_bounds__(THREADS, 1)
-    screen_fast_kernel(const ScreenArgs a, const unsigned nwx, const unsigned nwy,
-                       const TailPlan tp, const int vec16) {
-    extern __shared__ __align__(16) unsigned char smem[];
-    unsigned* hist = reinterpret_cast<unsigned*>(smem);
-    float2* P = reinterpret_cast<float2*>(smem + kHistBins * sizeof(unsigned));
-    __shared__ float wtop_all[16][kFloorK];
-    __shared__ __align__(8) unsigned long long plane_bar;
-    float* wtop = wtop_all[threadIdx.x >> 5];
-    if ((threadIdx.x & 31) < kFloorK) wtop[threadIdx.x & 31] = -INFINITY;
-    if (a.prof && threadIdx.x == 0) atomicMin(a.prof + 4, gtimer());  // first CTA entry
-    if (blockIdx.x == 0 && threadIdx.x == 0) a.ctrl->cand_count = 0ull;  // for the finish
-    // The plane arrives by bulk copy (TMA engine, one thread issues it) while
-    // the threads clear the histogram.
-    if (threadIdx.x == 0) {
-        mbar_init(&plane_bar, 1);
-        bulk_copy_to_smem(P, a.plane, (unsigned)vec16 * 16u, &plane_bar);
+// k largest values (with multiplicity) of up to 32*Q descending lists of
+// kTopK floats (list i at src + i * kTopK, 16-byte aligned), by one warp:
+// each lane folds its lists into a register top-kTopK (insertion network),
+// then k rounds of a warp max over the lanes' heads, the winning lane
+// popping one instance per round.  Returns the k-th largest (-inf if fewer
+// than k finite values); lane 0 writes the k values to out (if given).
+template <int Q, bool GLOBAL>
+__device__ __forceinline__ float warp_kth_of_lists(const float* src, int nlists, int k, float* out,
+                                                   int lane) {
+    float L[kTopK];
+#pragma unroll
+    for (int i = 0; i < kTopK; ++i) L[i] = -INFINITY;
+    float4 buf[Q][2];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {  // all loads first: one round trip
+        const int li = lane + 32 * q;
+        const float4* p = reinterpret_cast<const float4*>(src + (size_t)li * kTopK);
+        const float4 ninf = make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+        buf[q][0] = li < nlists ? (GLOBAL ? __ldcg(p) : p[0]) : ninf;
+        buf[q][1] = li < nlists ? (GLOBAL ? __ldcg(p + 1) : p[1]) : ninf;
     }
-    for (int i = threadIdx.x; i < kHistBins; i += blockDim.x) hist[i] = 0u;
-    __syncthreads();
-    mbar_wait_parity(&plane_bar, 0);
-    if (a.prof && threadIdx.x == 0) atomicMin(a.prof + 0, gtimer());  // first plane landed
-
-    constexpr int NACC = S * kTW;
-    const int lane = threadIdx.x & 31;
-    constexpr int YG = 32 / XG;  // lane strips along y; XG groups of 8 columns along x
-    const int yg = lane % YG, xg = lane / YG;
-    const float K = a.K;
-    const unsigned long long total = tp.n_main + tp.n_tail * (unsigned long long)tp.f;
-    const size_t sstride = 1 + 2 * (size_t)a.n;
-
-    LaneGeom g;
-    g.P = P;
-    g.PW = a.geom.PW;
-    g.XL = a.geom.PW - 1;
-    g.cx_lo = 1 + a.geom.PL;
-    g.cx_hi = a.geom.W + a.geom.PL;
-    g.H1 = a.geom.H + 1;
-    g.Z = a.geom.zero;
-    g.ry_lo = 1;
-    g.ry_hi = a.geom.H;
-    g.wspan = 8 * (XG - 1);
-
-    for (;;) {
-        unsigned long long work = 0;
-        if (lane == 0) work = atomicAdd(&a.ctrl->work_counter, 1ull);
-        work = __shfl_sync(0xffffffffu, work, 0);
-        if (work >= total) break;
-        unsigned long long item = work;
-        long long tslot = -1;
-        int ch = 0;
-        if (work >= tp.n_main) {
-            const unsigned long long m = work - tp.n_main;
-            tslot = (long long)(m / (unsigned)tp.f);
-            ch = (int)(m % (unsigned)tp.f);
-            item = tp.n_main + (unsigned long long)tslot;
-        }
-        const unsigned wx = (unsigned)(item % nwx);
-        const unsigned long long rest = item / nwx;
-        const unsigned wy = (unsigned)(rest % nwy);
-        const unsigned long long itr = rest / nwy;
-        const int X0 = (int)wx * (8 * XG);
-        const int X = X0 + xg * kTW;
-        const int Y = (int)wy * (YG * S) + yg * S;
-        if (__ldg(a.amb + itr) != 0) {  // flagged theta: the general kernel scores it
-            if (lane == 0) a.item_max[item] = INFINITY;
-            continue;
-        }
-        const int4* sch = a.sched + itr * sstride;
-        const int4 hdr = __ldg(sch);
-        const int n_ent = hdr.x + hdr.y + hdr.z + hdr.w;
-        int e0 = 0, e1 = n_ent;
-        if (tslot >= 0) {
-            e0 = (int)((long long)ch * n_ent / tp.f);
-            e1 = (int)((long long)(ch + 1) * n_ent / tp.f);
-        }
-        g.cbase = a.ix0 + X - R + g.cx_lo;   // padded column of the window start - ox
-        g.rbase = a.iy0 + Y - R + 1;         // padded row of the window start - oy
-        g.cwbase = a.ix0 + X0 - R + g.cx_lo; // warp's first column - ox
-
-        unsigned acc[S][kTW];
 #pragma unroll
-        for (int s = 0; s < S; ++s)
+    for (int q = 0; q < Q; ++q) {
+        const float v[kTopK] = {buf[q][0].x, buf[q][0].y, buf[q][0].z, buf[q][0].w,
+                                buf[q][1].x, buf[q][1].y, buf[q][1].z, buf[q][1].w};
 #pragma unroll
-            for (int j = 0; j < kTW; ++j) acc[s][j] = 0u;
-        const int done = run_entries<R, S, SHIFT, IGNORE, EDGE, true>(sch + 1, hdr, e0, e1, g, K, acc);
-        int sc[S][kTW];
-        const unsigned corr = (unsigned)done * a.B3;
+        for (int j = 0; j < kTopK; ++j) {
+            float x = v[j];
 #pragma unroll
-        for (int s = 0; s < S; ++s)
-#pragma unroll
-            for (int j = 0; j < kTW; ++j) sc[s][j] = (int)(acc[s][j] - corr);
-        if (tslot >= 0) {  // micro-item: merge, last arrival finalises
-            int* part = tp.part + (size_t)tslot * NACC * 32;
-#pragma unroll
-            for (int s = 0; s < S; ++s)
-#pragma unroll
-                for (int j = 0; j < kTW; ++j) atomicAdd(part + (s * kTW + j) * 32 + lane, sc[s][j]);
-            __threadfence();
-            unsigned old = 0;
-            if (lane == 0) old = atomicAdd(tp.done + tslot, 1u);
-            old = __shfl_sync(0xffffffffu, old, 0);
-            if (old != (unsigned)tp.f - 1u) continue;
-            __threadfence();
-            // read the merged sums and leave the slot zeroed for the next
-            // launch (no per-launch memset of the partial buffer)
-#pragma unroll
-            for (int s = 0; s < S; ++s)
-#pragma unroll
-                for (int j = 0; j < kTW; ++j) {
-                    sc[s][j] = __ldcg(part + (s * kTW + j) * 32 + lane);
-                    __stcg(part + (s * kTW + j) * 32 + lane, 0);
-                }
-            if (lane == 0) tp.done[tslot] = 0u;
-        }
-        const float best = emit_tile<S>(a, sc, X, Y, itr, item, hist, lane,
-                                        warp_floor(wtop, a.kf));
-        floor_insert(wtop, best, lane);
-    }
-    if (a.prof && (threadIdx.x & 31) == 0) atomicMax(a.prof + 1, gtimer());  // last warp's loop end
-    __syncthreads();
-    if (a.prof && threadIdx.x == 0) atomicMax(a.prof + 2, gtimer());  // last CTA's loop end
-    merge_hist(hist, a.hist, a.kf);
-    if (a.prof && threadIdx.x == 0) atomicMax(a.prof + 3, gtimer());  // last merge end
-}
-
-template <int R, int S, int SHIFT, bool IGNORE, int XG, bool EDGE, int THREADS>
-static void run_fast(ea_ctx* ctx, const ScreenArgs& a) {
-    constexpr int YG = 32 / XG;
-    const unsigned nwx = (unsigned)((a.nx + 8 * XG - 1) / (8 * XG));
-    const unsigned nwy = (unsigned)((a.ny + YG * S - 1) / (YG * S));
-    const unsigned long long items = (unsigned long long)nwx * nwy * a.it_count;
-    const size_t plane_bytes = (a.geom.bytes() + 15) & ~(size_t)15;
-    const size_t smem = kHistBins * sizeof(unsigned) + plane_bytes;
-    auto kern = screen_fast_kernel<R, S, SHIFT, IGNORE, XG, EDGE, THREADS>;
-    EAB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    constexpr int threads = THREADS;
-    const unsigned long long warps_per_cta = threads / 32;
-    const bool split = std::getenv("EAB_NO_TAIL_SPLIT") == nullptr;
-    // Full grid (one CTA per SM) whenever the items can be split into enough
-    // point-chunks to occupy it: a theta slab of a sharded search (or any
-    // small grid) has fewer warp tiles than the P resident warps.
-    const int fmax = split && a.n >= 8 ? std::min(a.n / 4, 64) : 1;
-    unsigned long long ctas = (items * (unsigned long long)fmax + warps_per_cta - 1) / warps_per_cta;
-    if (ctas > (unsigned long long)ctx->sm_count) ctas = ctx->sm_count;
-    if (ctas == 0) ctas = 1;
-    // tail split (see TailPlan): the last partial round of `rem` items is cut
-    // into f chunks, f minimising the tail's makespan in item units
-    //   max(rem * (1 + c*f) / P, 1/f + c)
-    // -- warps pull micro-items dynamically, so the tail ends when either its
-    // total work (spread over P warps) or one chunk's latency is done; c ~ 6%
-    // of an item is a chunk's fixed cost (prologue, partial-sum merge,
-    // finalise).  Fitted on the B200 (profiles/r01.md, EAB_TAIL_F sweep): a
-    // 1/8 theta slab of cfg2 (900 items on 1776 warps) is fastest at f = 2
-    // (0.095 ms screen vs 0.118 at the f = 7 the older ceil-rounds model
-    // chose), cfg3's slab at f = 6-9; a tail of nearly a full round (full
-    // cfg3: 1632 items on 1776 warps) stays unsplit -- f = 2 measured +4%.
-    TailPlan tp{items, 0, 1, nullptr, nullptr};
-    const unsigned long long P = ctas * warps_per_cta;
-    const unsigned long long rem = items % P;
-    if (rem > 0 && fmax >= 2) {
-        constexpr double c = 0.06;
-        auto makespan = [&](int ff) {  // an unsplit item pays no chunk cost
-            const double cf = ff > 1 ? c : 0.0;
-            return std::max((double)rem * (1.0 + cf * ff) / (double)P, 1.0 / ff + cf);
-        };
-        int f = 1;
-        double best = makespan(1);
-        for (int ff = 2; ff <= fmax; ++ff) {
-            const double cost = makespan(ff);
-            if (cost < best - 1e-9) {
-                best = cost;
-                f = ff;
+            for (int i = 0; i < kTopK; ++i) {
+                const float hi = fmaxf(L[i], x);
+                x = fminf(L[i], x);
+                L[i] = hi;
             }
         }
-        if (const char* ef = std::getenv("EAB_TAIL_F")) {  // diagnostic A/B of the split factor
-            const int v = std::atoi(ef);
-            if (v >= 1 && v <= fmax) f = v;
-        }
-        if (f >= 2) {
-            tp.n_main = items - rem;
-            tp.n_tail = rem;
-            tp.f = f;
-            // Partial sums and arrival counters are zero between launches:
-            // cleared once at allocation, then by each slot's finaliser.
-            const size_t part_bytes = rem * (size_t)S * kTW * 32 * sizeof(int);
-            const size_t bytes = part_bytes + rem * sizeof(unsigned);
-            const void* before = ctx->tail.p;
-            const size_t cap_before = ctx->tail.cap;
-            char* buf = (char*)ctx->tail.ensure(bytes);
-            if (buf != before || ctx->tail.cap != cap_before)
-                EAB_CUDA(cudaMemsetAsync(buf, 0, ctx->tail.cap, ctx->stream));
-            // layout: partials of slot i at [i], counters after the largest
-            // partial block the buffer can hold, so a slot's counter never
-            // aliases another launch's partials
-            tp.part = (int*)buf;
-            tp.done = (unsigned*)(buf + ctx->tail.cap - rem * sizeof(unsigned));
-        }
     }
-    kern<<<(unsigned)ctas, threads, smem, ctx->stream>>>(a, nwx, nwy, tp, (int)(plane_bytes / 16));
-    check_launch("screen_fast_kernel");
-    count_launch(ctx);
+    float t = -INFINITY;
+    for (int r = 0; r < k; ++r) {
+        float m = L[0];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+        const int win = __ffs(__ballot_sync(0xffffffffu, L[0] == m)) - 1;
+        if (lane == win) {
+#pragma unroll
+            for (int i = 0; i + 1 < kTopK; ++i) L[i] = L[i + 1];
+            L[kTopK - 1] = -INFINITY;
+        }
+        if (out && lane == 0) out[r] = m;
+        t = m;
+    }
+    return t;
 }
 
-size_t fast_smem_bytes(const PlaneGeom& g) {
-    return kHistBins * sizeof(unsigned) + ((g.bytes() + 15) & ~(size_t)15);
-}
-
-bool launch_screen_fast(ea_ctx* ctx, const ScreenArgs& a) {
-    if (fast_smem_bytes(a.geom) > ctx->smem_optin) return false;
-    if (a.geom.shift != 3) return false;  // 8-row lane strips
-    if (a.geom.elem_bytes != 8) return false;
-    const bool ig = a.ignore != 0;
-    // Windows that may leave the padded plane (padding shrunk to fit shared
-    // memory) need the clamping variant; fully padded planes run the lighter
-    // kernel, whose register budget allows kFastThreads threads.
-    const bool edge = a.edge != 0;
-#define EAB_FAST_XG(RR, XGV)                                                          \
-    if (edge) {                                                                       \
-        if (ig) run_fast<RR, 8, 3, true, XGV, true, 256>(ctx, a);                     \
-        else run_fast<RR, 8, 3, false, XGV, true, 256>(ctx, a);                       \
-    } else {                                                                          \
-        if (ig) run_fast<RR, 8, 3, true, XGV, false, kFastThreads>(ctx, a);           \
-        else run_fast<RR, 8, 3, false, XGV, false, kFastThreads>(ctx, a);             \
+// Fused path: band threshold thr = M_k - 2 delta, M_k the kf-th largest
+// TILE maximum, from the CTAs' lists (cta_top[G][kTopK], each descending, of
+// their warps' largest tile maxima).  The k tiles whose maxima are >= M_k
+// hold k distinct poses with S_f >= M_k, so M_k <= T_f (the k-th largest S_f)
+// and every pose of the true top k has S_f >= T_f - 2 delta >= M_k - 2 delta
+// (DESIGN.md §4).  M_k is a map value, so the comparison is exact.
+//
+// Compact, rolled code on purpose: everything after the screen loop runs
+// once, from a cold instruction cache (the loop's ~50 KB of SASS evicted it
+// and the step's L2 flush evicted L2), so its cost tracks its code size --
+// a fully unrolled warp merge measured 8.7 us here against 3.2 us rolled.
+__device__ __forceinline__ float fused_threshold(const FinishArgs& f, float* ttop) {
+    __shared__ float thr_s;
+    const int n = f.n_lists * kTopK;  // the screen launch's CTAs (not this grid's)
+    for (int i = threadIdx.x; i < n; i += blockDim.x) ttop[i] = __ldcg(f.cta_top + i);
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        const int lane = threadIdx.x;
+        // lane owns lists lane, lane + 32, ... (head index per list in a bit
+        // field: 4 bits each, kTopK <= 8; up to 16 lists per lane)
+        const int G = f.n_lists;
+        unsigned long long heads = 0ull;
+        float t = -INFINITY;
+        for (int r = 0; r < f.k; ++r) {
+            float mine = -INFINITY;
+            int src = -1;
+#pragma unroll 1
+            for (int q = 0; q < 16 && lane + 32 * q < G; ++q) {
+                const int h = (int)((heads >> (4 * q)) & 15ull);
+                const float x = h < kTopK ? ttop[(lane + 32 * q) * kTopK + h] : -INFINITY;
+                if (x > mine) {
+                    mine = x;
+                    src = q;
+                }
+            }
+            float m = mine;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+            const int win = __ffs(__ballot_sync(0xffffffffu, mine == m && src >= 0)) - 1;
+            if (lane == win) heads += 1ull << (4 * src);
+            t = m;
+        }
+        if (lane == 0) {
+            float thr = -INFINITY;
+            if (t > -INFINITY) {  // else fewer than k poses: every pose is a candidate
+                const double th = (double)t - 2.0 * f.delta;
+                thr = (float)th;
+                if ((double)thr > th) thr = nextafterf(thr, -INFINITY);
+            }
+            thr_s = thr;
+        }
     }
-#define EAB_FAST(RR)                                                        \
-    if (a.R == RR) {                                                        \
-        if (a.xg == 2) {                                                    \
-            EAB_FAST_XG(RR, 2)                                              \
-        } else {                                                            \
-            EAB_FAST_XG(RR, 4)                                              \
-        }                                                                   \
-        return true;                                                        \
-    }
-    EAB_FAST(1)
-    EAB_FAST(0)
-    EAB_FAST(2)
-#undef EAB_FAST
-#undef EAB_FAST_XG
-    return false;
+    __syncthreads();
+    return thr_s;
 }
 
 // Region-tiled lattice kernel: the plane lives in global memory (zero ring,
@@ -1463,16 +1330,26 @@ __device__ __forceinline__ Best pick(Best x, Best y) {
     return better_k(x.k, x.i, y.k, y.i) ? x : y;
 }
 
+constexpr int kStage = 2048;  // candidates staged in shared memory by select_body
+// Shared-memory scratch of select_body (static in select_kernel /
+// finish_kernel; carved from the plane's dynamic shared memory in the fused
+// screen kernel, whose plane is dead by then).
+struct SelectSmem {
+    long long skey[kStage];
+    unsigned long long sidx[kStage];
+    Best warp_best[32];
+    Best prev;
+};
+
 __device__ __forceinline__ void select_body(const unsigned* __restrict__ cand,
                                             const double* __restrict__ score, SearchCtrl* ctrl,
                                             unsigned long long cap, int k,
                                             unsigned long long index_base, double* out_score,
-                                            unsigned long long* out_index) {
-    constexpr int kStage = 2048;  // candidates staged in shared memory
-    __shared__ long long skey[kStage];
-    __shared__ unsigned long long sidx[kStage];
-    __shared__ Best warp_best[8];
-    __shared__ Best prev;
+                                            unsigned long long* out_index, SelectSmem& sm) {
+    long long* skey = sm.skey;
+    unsigned long long* sidx = sm.sidx;
+    Best* warp_best = sm.warp_best;
+    Best& prev = sm.prev;
     unsigned long long nc = ctrl->cand_count;
     if (nc > cap) nc = cap;
     const int t = threadIdx.x, lane = t & 31, w = t >> 5;
@@ -1552,7 +1429,8 @@ __global__ void __launch_bounds__(256) select_kernel(const unsigned* __restrict_
                                                      int k, unsigned long long index_base,
                                                      double* out_score,
                                                      unsigned long long* out_index) {
-    select_body(cand, score, ctrl, cap, k, index_base, out_score, out_index);
+    __shared__ SelectSmem sm;
+    select_body(cand, score, ctrl, cap, k, index_base, out_score, out_index, sm);
 }
 
 void launch_select(ea_ctx* ctx, const unsigned* cand, const double* score, SearchCtrl* ctrl,
@@ -1733,9 +1611,10 @@ __device__ __forceinline__ void finish_tile(const FinishArgs& f, unsigned long l
 }
 
 // C: exact fp64 score of candidate c with the whole CTA (reference order).
+constexpr int kMaxFinishThreads = 384;  // finish phases run with 256 (finish_kernel) or 384 threads
+
 __device__ __forceinline__ void finish_rescore(const ExactArgs& a, unsigned rel_idx,
-                                               double* out) {
-    __shared__ double votes[256];
+                                               double* out, double* votes /* smem, blockDim */) {
     const unsigned long long plane = a.nx * a.ny;
     const unsigned long long itl = rel_idx / plane, rem = rel_idx % plane;
     const double ux = lattice(a.x0, rem % a.nx, a.dx);
@@ -1743,7 +1622,8 @@ __device__ __forceinline__ void finish_rescore(const ExactArgs& a, unsigned rel_
     const size_t S = a.rot_stride, base = (size_t)itl * a.n;
     const int t = threadIdx.x;
     double sum = 0.0;
-    for (int p0 = 0; p0 < a.n; p0 += 256) {
+    const int nt = blockDim.x;
+    for (int p0 = 0; p0 < a.n; p0 += nt) {
         const int i = p0 + t;
         double v = 0.0;  // off-field centre / guarded coordinate: vote 0 (x + 0.0 == x)
         if (i < a.n) {
@@ -1761,7 +1641,7 @@ __device__ __forceinline__ void finish_rescore(const ExactArgs& a, unsigned rel_
         votes[t] = v;
         __syncthreads();
         if (t == 0) {
-            const int cn = min(256, a.n - p0);
+            const int cn = min(nt, a.n - p0);
             int j = 0;
             for (; j + 8 <= cn; j += 8) {  // 8 loads in flight, then the ordered adds
                 double b[8];
@@ -1779,9 +1659,8 @@ __device__ __forceinline__ void finish_rescore(const ExactArgs& a, unsigned rel_
 
 // D: top k by `better` (score desc, index asc) as ranks; n_out = min(k, nc).
 constexpr int kRankMax = 512;  // candidates ranked in one pass; more: select_body rounds
-__device__ __forceinline__ void finish_select(const FinishArgs& f, unsigned long long nc) {
-    __shared__ long long skey[kRankMax];
-    __shared__ unsigned long long sidx[kRankMax];
+__device__ __forceinline__ void finish_select(const FinishArgs& f, unsigned long long nc,
+                                              long long* skey, unsigned long long* sidx) {
     const int t = threadIdx.x;
     for (unsigned long long c = t; c < nc; c += blockDim.x) {
         skey[c] = order_key(__ldcg(f.cand_score + c));
@@ -1808,58 +1687,55 @@ __device__ __forceinline__ void finish_select(const FinishArgs& f, unsigned long
         if (threadIdx.x == 0) atomicMax(f.prof + (slot), gtimer() - f.prof[15]);          \
     }
 
-__global__ void __launch_bounds__(256) finish_kernel(const FinishArgs f) {
-    cg::grid_group grid = cg::this_grid();
-    if (f.prof && blockIdx.x == 0 && threadIdx.x == 0) {
-        f.prof[15] = gtimer();
-        __threadfence();
-    }
-    if (f.prof) grid.sync();
+// B: warps take 32 consecutive items per item_max load.  Lane l of warp w
+// tests item w + l*nwarps (+ 32*nwarps per round): the qualifying tiles
+// cluster around the peaks (same translation tile, adjacent thetas) and this
+// spreads them over warps.
+__device__ __forceinline__ void finish_compact_phase(const FinishArgs& f, float thr) {
     const int lane = threadIdx.x & 31;
-    if (blockIdx.x == 0 && threadIdx.x == 0 && f.flags) f.ctrl->flags = *f.flags;
-    const float thr = finish_threshold(f.hist, f.k, f.delta);
-    if (blockIdx.x == 0 && threadIdx.x == 0) f.ctrl->thr = thr;
-    EAB_PROF(0)
-    {   // B: warps take 32 consecutive items per item_max load
-        const unsigned long long warp = ((unsigned long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-        const unsigned long long nwarps = ((unsigned long long)gridDim.x * blockDim.x) >> 5;
-        // Lane l of warp w tests item w + l*nwarps (+ 32*nwarps per round):
-        // the qualifying tiles cluster around the peaks (same translation
-        // tile, adjacent thetas) and this spreads them over warps.
-        unsigned long long tb0 = f.prof ? gtimer() : 0;
-        unsigned ntiles = 0;
-        for (unsigned long long b0 = warp; b0 < f.items.n_items; b0 += nwarps * 32) {
-            const unsigned long long it = b0 + (unsigned long long)lane * nwarps;
-            const float m = it < f.items.n_items ? __ldcg(f.item_max + it)
-                                                 : __int_as_float(0x7fffffff);  // NaN: skip
-            unsigned mask = __ballot_sync(0xffffffffu, m >= thr);
-            while (mask) {
-                const int j = __ffs(mask) - 1;
-                mask &= mask - 1;
-                finish_tile(f, b0 + (unsigned long long)j * nwarps, thr, lane);
-                ++ntiles;
-            }
-        }
-        if (f.prof && lane == 0) {
-            atomicMax(f.prof + 8, (unsigned long long)ntiles);
-            atomicMax(f.prof + 10, gtimer() - tb0);
+    const unsigned long long warp = ((unsigned long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const unsigned long long nwarps = ((unsigned long long)gridDim.x * blockDim.x) >> 5;
+    unsigned long long tb0 = f.prof ? gtimer() : 0;
+    unsigned ntiles = 0;
+    for (unsigned long long b0 = warp; b0 < f.items.n_items; b0 += nwarps * 32) {
+        const unsigned long long it = b0 + (unsigned long long)lane * nwarps;
+        const float m = it < f.items.n_items ? __ldcg(f.item_max + it)
+                                             : __int_as_float(0x7fffffff);  // NaN: skip
+        unsigned mask = __ballot_sync(0xffffffffu, m >= thr);
+        while (mask) {
+            const int j = __ffs(mask) - 1;
+            mask &= mask - 1;
+            finish_tile(f, b0 + (unsigned long long)j * nwarps, thr, lane);
+            ++ntiles;
         }
     }
-    EAB_PROF(1)
-    grid.sync();
-    EAB_PROF(2)
-    // Every CTA has read the histogram: leave it zero, and the screen's work
-    // counter at 0, for the next search (which may skip the plane kernel that
-    // would otherwise clear them).
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < kHistBins; i += gridDim.x * blockDim.x)
-        f.hist_rw[i] = 0u;
-    if (blockIdx.x == 0 && threadIdx.x == 0) f.ctrl->work_counter = 0ull;
+    if (f.prof && lane == 0) {
+        atomicMax(f.prof + 8, (unsigned long long)ntiles);
+        atomicMax(f.prof + 10, gtimer() - tb0);
+    }
+}
+
+// C: one CTA per candidate (after a grid barrier: the count is final).
+// Shared-memory scratch of the finish phases C and D.
+constexpr int kMaxScreenCtas = 512;  // per-CTA top lists merged by fused_threshold
+union FinishSmem {
+    double votes[kMaxFinishThreads];
+    SelectSmem sel;
+    float ttop[kMaxScreenCtas * kTopK];
+};
+
+__device__ __forceinline__ unsigned long long finish_rescore_phase(const FinishArgs& f,
+                                                                   FinishSmem& sm) {
     unsigned long long nc = __ldcg(&f.ctrl->cand_count);
     if (nc > f.cap) nc = f.cap;  // overflow: reported, the caller retries with a larger cap
     for (unsigned long long c = blockIdx.x; c < nc; c += gridDim.x)
-        finish_rescore(f.x, __ldcg(f.cand + c), f.cand_score + c);
-    EAB_PROF(3)
-    // D on the CTA that finishes C last
+        finish_rescore(f.x, __ldcg(f.cand + c), f.cand_score + c, sm.votes);
+    return nc;
+}
+
+// D on the CTA that finishes C last: select + rows; resets the ticket.
+__device__ __forceinline__ void finish_select_phase(const FinishArgs& f, unsigned long long nc,
+                                                    FinishSmem& sm) {
     __shared__ int last;
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -1869,19 +1745,395 @@ __global__ void __launch_bounds__(256) finish_kernel(const FinishArgs f) {
     __syncthreads();
     if (!last) return;
     __threadfence();
+    __syncthreads();  // the rescore's vote scratch is reused below
     if (nc <= (unsigned long long)kRankMax)
-        finish_select(f, nc);
+        finish_select(f, nc, sm.sel.skey, sm.sel.sidx);
     else
         select_body(f.cand, f.cand_score, f.ctrl, f.cap, f.k, f.index_base, f.out_score,
-                    f.out_index);
+                    f.out_index, sm.sel);
     if (threadIdx.x == 0) f.ctrl->finish_ticket = 0u;
-    EAB_PROF(4)
     __syncthreads();
     if (f.rows) topk_rows_body(f.out_score, f.out_index, f.ctrl, f.cap, f.k, f.rg, f.rows,
                                f.overflow);
+}
+
+__global__ void __launch_bounds__(256) finish_kernel(const FinishArgs f) {
+    cg::grid_group grid = cg::this_grid();
+    if (f.prof && blockIdx.x == 0 && threadIdx.x == 0) {
+        f.prof[15] = gtimer();
+        __threadfence();
+    }
+    if (f.prof) grid.sync();
+    if (blockIdx.x == 0 && threadIdx.x == 0 && f.flags) f.ctrl->flags = *f.flags;
+    __shared__ FinishSmem sm;
+    // band threshold: from the screen's per-CTA lists of largest tile maxima
+    // (top-list mode) or from the histogram
+    const float thr = f.cta_top ? fused_threshold(f, sm.ttop) : finish_threshold(f.hist, f.k, f.delta);
+    if (blockIdx.x == 0 && threadIdx.x == 0) f.ctrl->thr = thr;
+    EAB_PROF(0)
+    finish_compact_phase(f, thr);
+    EAB_PROF(1)
+    grid.sync();
+    EAB_PROF(2)
+    // Every CTA has read the histogram: leave it zero, and the screen's work
+    // counter at 0, for the next search (which may skip the plane kernel that
+    // would otherwise clear them).  (Top-list mode never touched it.)
+    if (!f.cta_top)
+        for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < kHistBins;
+             i += gridDim.x * blockDim.x)
+            f.hist_rw[i] = 0u;
+    if (blockIdx.x == 0 && threadIdx.x == 0) f.ctrl->work_counter = 0ull;
+    const unsigned long long nc = finish_rescore_phase(f, sm);
+    EAB_PROF(3)
+    finish_select_phase(f, nc, sm);
+    EAB_PROF(4)
     EAB_PROF(5)
 }
 #undef EAB_PROF
+
+// ---- the smem lattice kernel (after the finish phases: its fused variant runs them)
+// FUSED: the finish (band threshold from the exact k-th largest score,
+// compaction, exact rescore, select, rows) runs in the same cooperative
+// launch after grid barriers; no histogram (its 16 KB go to the plane).
+template <int R, int S, int SHIFT, bool IGNORE, int XG, bool EDGE, int THREADS, bool FUSED>
+__global__ void __launch_bounds__(THREADS, 1)
+    screen_fast_kernel(const ScreenArgs a, const unsigned nwx, const unsigned nwy,
+                       const TailPlan tp, const int vec16, const FinishArgs fa) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    unsigned* hist = reinterpret_cast<unsigned*>(smem);
+    float2* P = reinterpret_cast<float2*>(smem + (FUSED ? 0 : kHistBins * sizeof(unsigned)));
+    static_assert(kFloorK == kTopK, "one per-warp list serves both paths");
+    __shared__ __align__(16) float wtop_all[16][kFloorK];
+    __shared__ __align__(8) unsigned long long plane_bar;
+    float* wtop = wtop_all[threadIdx.x >> 5];
+    if ((threadIdx.x & 31) < kFloorK) wtop[threadIdx.x & 31] = -INFINITY;
+    if (a.prof && threadIdx.x == 0) atomicMin(a.prof + 4, gtimer());  // first CTA entry
+    if (blockIdx.x == 0 && threadIdx.x == 0) a.ctrl->cand_count = 0ull;  // for the finish
+    // The plane arrives by bulk copy (TMA engine, one thread issues it) while
+    // the threads clear the histogram.
+    if (threadIdx.x == 0) {
+        mbar_init(&plane_bar, 1);
+        bulk_copy_to_smem(P, a.plane, (unsigned)vec16 * 16u, &plane_bar);
+    }
+    // top-list mode (fused, or a.cta_top set): no histogram -- the band
+    // threshold comes from the CTAs' lists of their largest tile maxima
+    const bool toplist = FUSED || a.cta_top != nullptr;
+    if (!toplist)
+        for (int i = threadIdx.x; i < kHistBins; i += blockDim.x) hist[i] = 0u;
+    __syncthreads();
+    mbar_wait_parity(&plane_bar, 0);
+    if (a.prof && threadIdx.x == 0) atomicMin(a.prof + 0, gtimer());  // first plane landed
+
+    constexpr int NACC = S * kTW;
+    const int lane = threadIdx.x & 31;
+    constexpr int YG = 32 / XG;  // lane strips along y; XG groups of 8 columns along x
+    const int yg = lane % YG, xg = lane / YG;
+    const float K = a.K;
+    const unsigned long long total = tp.n_main + tp.n_tail * (unsigned long long)tp.f;
+    const size_t sstride = 1 + 2 * (size_t)a.n;
+
+    LaneGeom g;
+    g.P = P;
+    g.PW = a.geom.PW;
+    g.XL = a.geom.PW - 1;
+    g.cx_lo = 1 + a.geom.PL;
+    g.cx_hi = a.geom.W + a.geom.PL;
+    g.H1 = a.geom.H + 1;
+    g.Z = a.geom.zero;
+    g.ry_lo = 1;
+    g.ry_hi = a.geom.H;
+    g.wspan = 8 * (XG - 1);
+
+    unsigned long long* wt = a.wtrace ? a.wtrace + 8 * (size_t)(blockIdx.x * (blockDim.x >> 5) +
+                                                                 (threadIdx.x >> 5))
+                                      : nullptr;
+    int units = 0;
+    if (wt && lane == 0) wt[0] = gtimer();
+    for (;;) {
+        if (wt && lane == 0 && units > 0 && units < 7) wt[units] = gtimer();
+        unsigned long long work = 0;
+        if (lane == 0) work = atomicAdd(&a.ctrl->work_counter, 1ull);
+        work = __shfl_sync(0xffffffffu, work, 0);
+        if (work >= total) break;
+        ++units;
+        unsigned long long item = work;
+        long long tslot = -1;
+        int ch = 0;
+        if (work >= tp.n_main) {
+            const unsigned long long m = work - tp.n_main;
+            tslot = (long long)(m / (unsigned)tp.f);
+            ch = (int)(m % (unsigned)tp.f);
+            item = tp.n_main + (unsigned long long)tslot;
+        }
+        const unsigned wx = (unsigned)(item % nwx);
+        const unsigned long long rest = item / nwx;
+        const unsigned wy = (unsigned)(rest % nwy);
+        const unsigned long long itr = rest / nwy;
+        const int X0 = (int)wx * (8 * XG);
+        const int X = X0 + xg * kTW;
+        const int Y = (int)wy * (YG * S) + yg * S;
+        if (__ldg(a.amb + itr) != 0) {  // flagged theta: the general kernel scores it
+            if (lane == 0) a.item_max[item] = INFINITY;
+            continue;
+        }
+        const int4* sch = a.sched + itr * sstride;
+        const int4 hdr = __ldg(sch);
+        const int n_ent = hdr.x + hdr.y + hdr.z + hdr.w;
+        int e0 = 0, e1 = n_ent;
+        if (tslot >= 0) {
+            e0 = (int)((long long)ch * n_ent / tp.f);
+            e1 = (int)((long long)(ch + 1) * n_ent / tp.f);
+        }
+        g.cbase = a.ix0 + X - R + g.cx_lo;   // padded column of the window start - ox
+        g.rbase = a.iy0 + Y - R + 1;         // padded row of the window start - oy
+        g.cwbase = a.ix0 + X0 - R + g.cx_lo; // warp's first column - ox
+
+        unsigned acc[S][kTW];
+#pragma unroll
+        for (int s = 0; s < S; ++s)
+#pragma unroll
+            for (int j = 0; j < kTW; ++j) acc[s][j] = 0u;
+        const int done = run_entries<R, S, SHIFT, IGNORE, EDGE, true>(sch + 1, hdr, e0, e1, g, K, acc);
+        int sc[S][kTW];
+        const unsigned corr = (unsigned)done * a.B3;
+#pragma unroll
+        for (int s = 0; s < S; ++s)
+#pragma unroll
+            for (int j = 0; j < kTW; ++j) sc[s][j] = (int)(acc[s][j] - corr);
+        if (tslot >= 0) {  // micro-item: merge, last arrival finalises
+            int* part = tp.part + (size_t)tslot * NACC * 32;
+#pragma unroll
+            for (int s = 0; s < S; ++s)
+#pragma unroll
+                for (int j = 0; j < kTW; ++j) atomicAdd(part + (s * kTW + j) * 32 + lane, sc[s][j]);
+            __threadfence();
+            unsigned old = 0;
+            if (lane == 0) old = atomicAdd(tp.done + tslot, 1u);
+            old = __shfl_sync(0xffffffffu, old, 0);
+            if (old != (unsigned)tp.f - 1u) continue;
+            __threadfence();
+            // read the merged sums and leave the slot zeroed for the next
+            // launch (no per-launch memset of the partial buffer)
+#pragma unroll
+            for (int s = 0; s < S; ++s)
+#pragma unroll
+                for (int j = 0; j < kTW; ++j) {
+                    sc[s][j] = __ldcg(part + (s * kTW + j) * 32 + lane);
+                    __stcg(part + (s * kTW + j) * 32 + lane, 0);
+                }
+            if (lane == 0) tp.done[tslot] = 0u;
+        }
+        // fused: no histogram; wtop keeps the warp's 8 largest tile maxima
+        const float best = emit_tile<S, !FUSED>(a, sc, X, Y, itr, item, toplist ? nullptr : hist,
+                                                lane, warp_floor(wtop, a.kf));
+        floor_insert(wtop, best, lane);
+    }
+    if (wt && lane == 0) wt[7] = ((unsigned long long)units << 56) | (gtimer() & ((1ull << 56) - 1));
+    if (a.prof && (threadIdx.x & 31) == 0) atomicMax(a.prof + 1, gtimer());  // last warp's loop end
+    __syncthreads();
+    if (a.prof && threadIdx.x == 0) atomicMax(a.prof + 2, gtimer());  // last CTA's loop end
+    if (toplist) {
+        // the CTA's kf largest tile maxima (merge of its warps' lists, warp 0)
+        if (threadIdx.x < 32) {
+            float* out = a.cta_top + blockIdx.x * kTopK;
+            warp_kth_of_lists<1, false>(&wtop_all[0][0], blockDim.x >> 5, a.kf, out, threadIdx.x);
+            if (threadIdx.x >= a.kf && threadIdx.x < kTopK) out[threadIdx.x] = -INFINITY;
+        }
+    } else {
+        merge_hist(hist, a.hist, a.kf);
+    }
+    if (a.prof && threadIdx.x == 0) atomicMax(a.prof + 3, gtimer());  // last merge end
+    if constexpr (FUSED) {
+        cg::grid_group grid = cg::this_grid();
+        grid.sync();  // every CTA's list is written; the work counter is free
+        if (a.prof && threadIdx.x == 0) atomicMax(a.prof + 11, gtimer());  // barrier 1 passed
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            a.ctrl->work_counter = 0ull;
+            a.ctrl->flags = 0;
+        }
+        // the plane is dead: its shared memory becomes the finish's scratch
+        const float thr = fused_threshold(fa, reinterpret_cast<float*>(smem));
+        if (blockIdx.x == 0 && threadIdx.x == 0) a.ctrl->thr = thr;
+        if (a.prof && threadIdx.x == 0) atomicMax(a.prof + 8, gtimer());  // threshold known
+        finish_compact_phase(fa, thr);
+        if (a.prof && threadIdx.x == 0) atomicMax(a.prof + 9, gtimer());  // compaction done
+        grid.sync();
+        if (a.prof && threadIdx.x == 0) atomicMax(a.prof + 5, gtimer());  // barrier 2 passed
+        FinishSmem& fsm = *reinterpret_cast<FinishSmem*>(smem);
+        const unsigned long long nc = finish_rescore_phase(fa, fsm);
+        if (a.prof && threadIdx.x == 0) atomicMax(a.prof + 6, gtimer());  // rescore done
+        finish_select_phase(fa, nc, fsm);
+        if (a.prof && threadIdx.x == 0) atomicMax(a.prof + 7, gtimer());  // select + rows done
+    }
+}
+
+template <int R, int S, int SHIFT, bool IGNORE, int XG, bool EDGE, int THREADS, bool FUSED>
+static void run_fast(ea_ctx* ctx, const ScreenArgs& a, const FinishArgs* fin) {
+    constexpr int YG = 32 / XG;
+    const unsigned nwx = (unsigned)((a.nx + 8 * XG - 1) / (8 * XG));
+    const unsigned nwy = (unsigned)((a.ny + YG * S - 1) / (YG * S));
+    const unsigned long long items = (unsigned long long)nwx * nwy * a.it_count;
+    const size_t plane_bytes = (a.geom.bytes() + 15) & ~(size_t)15;
+    // fused: no histogram; the plane's bytes are reused by the finish phases
+    const size_t smem =
+        FUSED ? std::max({plane_bytes, sizeof(FinishSmem),
+                          (size_t)ctx->sm_count * kTopK * sizeof(float)})
+              : kHistBins * sizeof(unsigned) + plane_bytes;
+    auto kern = screen_fast_kernel<R, S, SHIFT, IGNORE, XG, EDGE, THREADS, FUSED>;
+    EAB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    constexpr int threads = THREADS;
+    const unsigned long long warps_per_cta = threads / 32;
+    const bool split = std::getenv("EAB_NO_TAIL_SPLIT") == nullptr;
+    // Full grid (one CTA per SM) whenever the items can be split into enough
+    // point-chunks to occupy it: a theta slab of a sharded search (or any
+    // small grid) has fewer warp tiles than the P resident warps.
+    const int fmax = split && a.n >= 8 ? std::min(a.n / 4, 64) : 1;
+    unsigned long long ctas = (items * (unsigned long long)fmax + warps_per_cta - 1) / warps_per_cta;
+    if (ctas > (unsigned long long)ctx->sm_count) ctas = ctx->sm_count;
+    if (ctas == 0) ctas = 1;
+    // tail split (see TailPlan): the last partial round of `rem` items is cut
+    // into f chunks, f minimising the tail's makespan in item units
+    //   max(rem * (1 + c*f) / P, 1/f + c)
+    // -- warps pull micro-items dynamically, so the tail ends when either its
+    // total work (spread over P warps) or one chunk's latency is done; c ~ 6%
+    // of an item is a chunk's fixed cost (prologue, partial-sum merge,
+    // finalise).  Fitted on the B200 (profiles/r01.md, EAB_TAIL_F sweep): a
+    // 1/8 theta slab of cfg2 (900 items on 1776 warps) is fastest at f = 2
+    // (0.095 ms screen vs 0.118 at the f = 7 the older ceil-rounds model
+    // chose), cfg3's slab at f = 6-9; a tail of nearly a full round (full
+    // cfg3: 1632 items on 1776 warps) stays unsplit -- f = 2 measured +4%.
+    TailPlan tp{items, 0, 1, nullptr, nullptr};
+    const unsigned long long P = ctas * warps_per_cta;
+    const unsigned long long rem = items % P;
+    if (rem > 0 && fmax >= 2) {
+        constexpr double c = 0.06;
+        auto makespan = [&](int ff) {  // an unsplit item pays no chunk cost
+            const double cf = ff > 1 ? c : 0.0;
+            return std::max((double)rem * (1.0 + cf * ff) / (double)P, 1.0 / ff + cf);
+        };
+        int f = 1;
+        double best = makespan(1);
+        for (int ff = 2; ff <= fmax; ++ff) {
+            const double cost = makespan(ff);
+            if (cost < best - 1e-9) {
+                best = cost;
+                f = ff;
+            }
+        }
+        // A chunk count just above P puts a second wave of chunks at the
+        // end: with near-uniform item costs (cfg3: 49 points, per-theta cost
+        // spread 0.9%) its 1/8 theta slab (204 tail items on 1776 warps) ended
+        // its loop at 94-98 us with f = 9 (1836 chunks); cut to the largest f
+        // that still fits one wave when that keeps a split.
+        if (f >= 2 && rem * (unsigned long long)f > P && rem * (unsigned long long)f * 5 < P * 6 &&
+            P / rem >= 2)
+            f = (int)(P / rem);
+        if (const char* ef = std::getenv("EAB_TAIL_F")) {  // diagnostic A/B of the split factor
+            const int v = std::atoi(ef);
+            if (v >= 1 && v <= fmax) f = v;
+        }
+        if (f >= 2) {
+            tp.n_main = items - rem;
+            tp.n_tail = rem;
+            tp.f = f;
+            // Partial sums and arrival counters are zero between launches:
+            // cleared once at allocation, then by each slot's finaliser.
+            const size_t part_bytes = rem * (size_t)S * kTW * 32 * sizeof(int);
+            const size_t bytes = part_bytes + rem * sizeof(unsigned);
+            const void* before = ctx->tail.p;
+            const size_t cap_before = ctx->tail.cap;
+            char* buf = (char*)ctx->tail.ensure(bytes);
+            if (buf != before || ctx->tail.cap != cap_before)
+                EAB_CUDA(cudaMemsetAsync(buf, 0, ctx->tail.cap, ctx->stream));
+            // layout: partials of slot i at [i], counters after the largest
+            // partial block the buffer can hold, so a slot's counter never
+            // aliases another launch's partials
+            tp.part = (int*)buf;
+            tp.done = (unsigned*)(buf + ctx->tail.cap - rem * sizeof(unsigned));
+        }
+    }
+    ctx->screen_ctas = (int)ctas;  // the finish merges this many per-CTA top lists
+    const int vec16 = (int)(plane_bytes / 16);
+    if constexpr (FUSED) {
+        // every CTA must be resident for the grid barriers (one per SM)
+        FinishArgs fa = *fin;
+        fa.n_lists = (int)ctas;
+        ScreenArgs sa = a;
+        unsigned gx = nwx, gy = nwy;
+        TailPlan t = tp;
+        int v16 = vec16;
+        void* args[] = {&sa, &gx, &gy, &t, &v16, &fa};
+        EAB_CUDA(cudaLaunchCooperativeKernel((const void*)kern, dim3((unsigned)ctas), dim3(threads),
+                                             args, smem, ctx->stream));
+        check_launch("screen_fast_kernel(fused)");
+    } else {
+        kern<<<(unsigned)ctas, threads, smem, ctx->stream>>>(a, nwx, nwy, tp, vec16, FinishArgs{});
+        check_launch("screen_fast_kernel");
+    }
+    count_launch(ctx);
+}
+
+size_t fast_smem_bytes(const PlaneGeom& g) {
+    return kHistBins * sizeof(unsigned) + ((g.bytes() + 15) & ~(size_t)15);
+}
+
+bool launch_screen_fast(ea_ctx* ctx, const ScreenArgs& a) {
+    if (fast_smem_bytes(a.geom) > ctx->smem_optin) return false;
+    if (a.geom.shift != 3) return false;  // 8-row lane strips
+    if (a.geom.elem_bytes != 8) return false;
+    const bool ig = a.ignore != 0;
+    // Windows that may leave the padded plane (padding shrunk to fit shared
+    // memory) need the clamping variant; fully padded planes run the lighter
+    // kernel, whose register budget allows kFastThreads threads.
+    const bool edge = a.edge != 0;
+#define EAB_FAST_XG(RR, XGV)                                                                  \
+    if (edge) {                                                                               \
+        if (ig) run_fast<RR, 8, 3, true, XGV, true, 256, false>(ctx, a, nullptr);            \
+        else run_fast<RR, 8, 3, false, XGV, true, 256, false>(ctx, a, nullptr);              \
+    } else {                                                                                  \
+        if (ig) run_fast<RR, 8, 3, true, XGV, false, kFastThreads, false>(ctx, a, nullptr);  \
+        else run_fast<RR, 8, 3, false, XGV, false, kFastThreads, false>(ctx, a, nullptr);    \
+    }
+#define EAB_FAST(RR)                                                        \
+    if (a.R == RR) {                                                        \
+        if (a.xg == 2) {                                                    \
+            EAB_FAST_XG(RR, 2)                                              \
+        } else {                                                            \
+            EAB_FAST_XG(RR, 4)                                              \
+        }                                                                   \
+        return true;                                                        \
+    }
+    EAB_FAST(1)
+    EAB_FAST(0)
+    EAB_FAST(2)
+#undef EAB_FAST
+#undef EAB_FAST_XG
+    return false;
+}
+
+bool launch_screen_fused(ea_ctx* ctx, const ScreenArgs& a, const FinishArgs& f) {
+    if (fast_smem_bytes(a.geom) > ctx->smem_optin) return false;
+    if (a.geom.shift != 3 || a.geom.elem_bytes != 8) return false;
+    if (a.edge != 0 || a.kf < 1 || a.kf > kTopK || f.k != a.kf || !f.cta_top) return false;
+    const bool ig = a.ignore != 0;
+#define EAB_FUSED(RR)                                                                         \
+    if (a.R == RR) {                                                                          \
+        if (a.xg == 2) {                                                                      \
+            if (ig) run_fast<RR, 8, 3, true, 2, false, kFastThreads, true>(ctx, a, &f);       \
+            else run_fast<RR, 8, 3, false, 2, false, kFastThreads, true>(ctx, a, &f);         \
+        } else {                                                                              \
+            if (ig) run_fast<RR, 8, 3, true, 4, false, kFastThreads, true>(ctx, a, &f);       \
+            else run_fast<RR, 8, 3, false, 4, false, kFastThreads, true>(ctx, a, &f);         \
+        }                                                                                     \
+        return true;                                                                          \
+    }
+    EAB_FUSED(1)
+    EAB_FUSED(0)
+    EAB_FUSED(2)
+#undef EAB_FUSED
+    return false;
+}
+
 
 void launch_finish(ea_ctx* ctx, const FinishArgs& f) {
     static int per_sm = -1;  // co-resident CTAs per SM (same binary for every device)
@@ -1984,8 +2236,10 @@ int merge_rows_max(ea_ctx* ctx) { return (int)(ctx->smem_optin / 16); }
 void launch_merge_rows(ea_ctx* ctx, const double* in, int n, int k, double* out,
                        double* top_score, unsigned long long* top_index, int* n_top) {
     const size_t smem = (size_t)n * 16;
-    static size_t opted = 48 * 1024;  // dynamic shared memory beyond 48 KB is opt-in
-    if (smem > opted) {
+    // dynamic shared memory beyond 48 KB (minus the kernel's static bytes) is
+    // opt-in: raise the limit once, to the context's budget
+    static size_t opted = 0;
+    if (smem + 1024 > 48 * 1024 && opted < ctx->smem_optin) {
         EAB_CUDA(cudaFuncSetAttribute(merge_rows_kernel,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)ctx->smem_optin));

@@ -80,8 +80,11 @@ def main():
             _, times = ea.async_status(ctx)
             step = statistics.median(a.elapsed_time(b) for a, b in ev)
             scr = statistics.median(times) if times else None
+            ea.search_top_slab(det.levels, cfg, it0, it1)  # synchronous: fills the stats
+            st = ctx.stats()
             rec = {"slab": [it0, it1], "step_ms": step, "screen_ms": scr, "host_enqueue_ms": host_ms,
-                   "other_ms": step - scr if scr is not None else None}
+                   "other_ms": step - scr if scr is not None else None,
+                   "candidates": st["candidates"], "threshold": st["threshold"]}
             allrec.append((round(step, 4), round(scr, 4) if scr else None))
             if worst is None or step > worst["step_ms"]:
                 worst = rec

@@ -736,6 +736,57 @@ def test_unfused_finish_path_matches(ea, oracle, monkeypatch, case):
     ctx_fused.close()
 
 
+@pytest.mark.parametrize("case", [0, 1, 2, 3, 4, 5, len(SEARCH_CASES) - 1])
+def test_screen_threshold_modes_match(ea, oracle, monkeypatch, case):
+    """Three ways to the band threshold, all equal to the oracle for every k,
+    on contexts used back to back (shared model caches, plane cache):
+    top-list mode (default for k <= 8 on the smem lattice kernel: no
+    histogram, threshold from the k-th largest tile maximum), the histogram
+    (EAB_NO_TOPLIST=1, and always for k > 8), and the screen with the finish
+    inside its cooperative launch (EAB_FUSED_SCREEN=1)."""
+    size, w, h, g, nb, pol = SEARCH_CASES[case]
+    rng = np.random.default_rng(900 + case)
+    m = rand_model(oracle, rng, size)
+    f = oracle.compute_gradients(rand_image(rng, w, h))
+    grid = ea.PoseGrid(*g)
+    params = ea.ScoreParams(nb, pol)
+    monkeypatch.setenv("EAB_NO_TOPLIST", "1")
+    ctx_hist = ea.Context(0)
+    monkeypatch.delenv("EAB_NO_TOPLIST")
+    monkeypatch.setenv("EAB_FUSED_SCREEN", "1")
+    ctx_fused = ea.Context(0)
+    monkeypatch.delenv("EAB_FUSED_SCREEN")
+    ctx_top = ea.Context(0)
+    for k in (1, 2, 5, 8, 9):
+        want = keys(oracle.search_topk(m.points, f, grid, params, k))
+        for ctx in (ctx_top, ctx_hist, ctx_fused, ctx_top, ctx_fused):
+            assert keys(ea.search_topk(m, f, grid, params, k=k, ctx=ctx)) == want, (k, ctx)
+    for c in (ctx_hist, ctx_fused, ctx_top):
+        c.close()
+
+
+def test_fused_screen_ties_and_tiny_grids(ea, oracle, monkeypatch):
+    """Top-list and fused path edge cases: a flat field (every pose ties at 0: the k-th
+    largest is 0 and every pose is a candidate), grids with fewer poses than
+    k, and one-theta grids."""
+    rng = np.random.default_rng(77)
+    m = rand_model(oracle, rng, 10)
+    flat = oracle.compute_gradients(np.full((24, 20), 42.0))
+    f = oracle.compute_gradients(rand_image(rng, 24, 20))
+    params = ea.ScoreParams(3)
+    monkeypatch.setenv("EAB_FUSED_SCREEN", "1")
+    ctx_fused = ea.Context(0)
+    monkeypatch.delenv("EAB_FUSED_SCREEN")
+    for field, ctx in ((flat, None), (f, None), (flat, ctx_fused), (f, ctx_fused)):
+        for g in ((0, 19, 1, 0, 23, 1, 0.0, D(20), D(10)), (3, 4, 1, 5, 5, 1, 0.0, 0.0, 1.0),
+                  (0, 1, 1, 0, 1, 1, 0.0, D(10), D(10)), (0, 19, 1, 0, 23, 1, D(7), D(7), 1.0)):
+            grid = ea.PoseGrid(*g)
+            for k in (1, 3, 8):
+                want = keys(oracle.search_topk(m.points, field, grid, params, k))
+                assert keys(ea.search_topk(m, field, grid, params, k=k, ctx=ctx)) == want, (g, k)
+    ctx_fused.close()
+
+
 @pytest.mark.parametrize("w,h,L", [(160, 160, 1), (333, 257, 4), (162, 121, 2), (648, 486, 5),
                                    (517, 389, 6), (97, 64, 3)])
 def test_fused_pyramid_fields_bit_exact(ea, oracle, monkeypatch, w, h, L):
