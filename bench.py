@@ -494,9 +494,31 @@ def bench_ours(args, rank, world, local_rank):
     rows = [torch.empty((k, 5), dtype=torch.float64, device=dev) for _ in dets]
     merged = [torch.empty((k, 5), dtype=torch.float64, device=dev) for _ in dets]
 
+    # cfg5 (several models): the (model, theta slab) work items of
+    # ea_plan_multi, one all-gather of every model's rows
+    nm = len(dets)
+    local_all = torch.empty((nm * k, 5), dtype=torch.float64, device=dev)
+    merged_all = torch.empty((nm * k, 5), dtype=torch.float64, device=dev)
+
+    def multi_items(G, r):
+        return [(m, b, e) for rr, m, b, e, _ in
+                ea.plan_multi([nx * ny] * nm, [nt] * nm, n_tops, G) if rr == r]
+
+    my_items = multi_items(world if shard_theta else 1, rank if shard_theta else 0)
+
+    def multi_step(items, gather):
+        local_all.fill_(float("nan"))  # rows of models without a slab here
+        for m, b, e in items:
+            ea.search_top_slab_async(dets[m].levels, cfg, b, e, local_all[m * k:(m + 1) * k].data_ptr())
+        if gather:
+            ea.gather_rows_multi_async(ctx, local_all.data_ptr(), nm, k, merged_all.data_ptr())
+
     def top_step():
         """One top-level search per model (cfg5: 8), device-resident: slab
         search -> k rows in HBM -> (N > 1) NCCL all-gather + device merge."""
+        if multi:
+            multi_step(my_items, shard_theta)
+            return [merged_all if shard_theta else local_all]
         out = []
         for d, r, m in zip(dets, rows, merged):
             ea.search_top_slab_async(d.levels, cfg, it0, it1, r.data_ptr())
@@ -548,7 +570,7 @@ def bench_ours(args, rank, world, local_rank):
     overflowed, times = ea.async_status(ctx)
     if overflowed:
         raise RuntimeError("candidate buffer overflow in the device-resident search")
-    per_step = len(dets)
+    per_step = len(my_items) if multi else len(dets)
     screen_ms = [sum(times[i:i + per_step]) for i in range(0, len(times) - per_step + 1, per_step)]
     tot_ms = sum(step_ms)
     if world > 1:
@@ -575,12 +597,21 @@ def bench_ours(args, rank, world, local_rank):
                              "theta-sharded search: slab search + the library's NCCL all-gather "
                              "and device merge of the k rows on a world-1 communicator)",
                      "full_ms": t_full}
+        if multi:
+            slab_proj["what"] = ("worst rank of G on this GPU (per-rank compute of a G-GPU "
+                                 "multi-model sharded search: the rank's ea_plan_multi (model, "
+                                 "theta slab) items + the library's NCCL all-gather and per-model "
+                                 "merge of every model's rows on a world-1 communicator)")
         for G in (2, 4, 8):
             worst = (0.0, None)
             for g in range(G):
                 a0, a1 = parallel.theta_slab(nt, g, G)
+                items_g = multi_items(G, g) if multi else None
 
                 def slab_step():
+                    if multi:
+                        multi_step(items_g, True)
+                        return
                     for d, r, m in zip(dets, rows, merged):
                         ea.search_top_slab_async(d.levels, cfg, a0, a1, r.data_ptr())
                         parallel.gather_rows_device(r, k, ctx, m)
@@ -597,7 +628,7 @@ def bench_ours(args, rank, world, local_rank):
                 torch.cuda.synchronize(dev)
                 t = statistics.median(e_a.elapsed_time(e_b) for e_a, e_b in evs)
                 if t > worst[0]:
-                    worst = (t, [a0, a1])
+                    worst = (t, [list(x) for x in items_g] if multi else [a0, a1])
             slab_proj[str(G)] = {"worst_slab_ms": worst[0], "slab": worst[1],
                                  "projected_strong_scaling": t_full / worst[0]}
         ea.async_status(ctx)
@@ -621,11 +652,14 @@ def bench_ours(args, rank, world, local_rank):
         scenes = [img] + [make_inputs(args.config, noise_seed=101 + j)[0] for j in range(3)]
     pinned = [torch.from_numpy(scenes[j % len(scenes)]).pin_memory() for j in range(n_img)]
     host_imgs = [p.numpy() for p in pinned]
-    sharded_e2e = shard_theta and not multi
+    sharded_e2e = shard_theta
     h2d = img.size * 8 if (not sharded_e2e or rank == 0) else 0
     d2h = (472 + 48) * len(dets)  # ea_outcome + control block per image and model
 
     def e2e_run():
+        if multi and sharded_e2e:  # ea_detect_multi_sharded per image (e3)
+            return [ea.detect_multi_sharded(dets, im if rank == 0 else None, im.shape)
+                    for im in host_imgs]
         if multi:  # one ea_detect_multi call per image: shared pyramid, 8 models
             return [ea.detect_multi(dets, im) for im in host_imgs]
         if sharded_e2e:
@@ -666,7 +700,9 @@ def bench_ours(args, rank, world, local_rank):
             a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a0.record(stream)
             im = host_imgs[i % len(host_imgs)]
-            if multi:
+            if multi and sharded_e2e:
+                ea.detect_multi_sharded(dets, im if rank == 0 else None, im.shape)
+            elif multi:
                 ea.detect_multi(dets, im)
             elif sharded_e2e:
                 det.detect_sharded(im if rank == 0 else None, im.shape)
@@ -689,7 +725,8 @@ def bench_ours(args, rank, world, local_rank):
     n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
     smem_peak_gbs = n_sm * SMEM_BYTES_PER_CLK_PER_SM * sm_mhz * 1e6 / 1e9
     kernel_ms = statistics.median(screen_ms)
-    local_evals = nx * ny * (it1 - it0) * n_top
+    local_evals = (sum(nx * ny * (e - b) * n_tops[m] for m, b, e in my_items) if multi
+                   else nx * ny * (it1 - it0) * n_top)
     models_top = [d.levels.model(L - 1).points for d in dets]
     loaded_b, min_inst = lattice_work_per_eval(models_top, tg, it0, it1)
     achieved = local_evals * loaded_b / (kernel_ms / 1e3) / 1e9
@@ -713,7 +750,10 @@ def bench_ours(args, rank, world, local_rank):
                    "top_level_grid": f"{nx}x{ny}x{nt}",
                    "top_model_points": n_tops if multi else n_top,
                    "pose_evals_per_step": job_pts, "l2": "flushed (256 MiB write) between steps",
-                   "parallelism": (f"theta-slab x{world} + NCCL all-gather of top-k rows "
+                   "parallelism": (f"(model x theta-slab) items of ea_plan_multi on {world} "
+                                   "ranks + one NCCL all-gather of every model's top-k rows"
+                                   if multi and shard_theta else
+                                   f"theta-slab x{world} + NCCL all-gather of top-k rows "
                                    "(libedgealign_b200 communicator)"
                                    if shard_theta else f"images x{world} (one frame per GPU)")
                    if world > 1 else "single GPU"},
@@ -721,7 +761,9 @@ def bench_ours(args, rank, world, local_rank):
                 "d2h_bytes_per_step": d2h, "ms_per_image": e2e_ms / n_img,
                 "images": n_img * (1 if sharded_e2e else world),
                 "batches_ms": runs, "timed": "median of 3 batches",
-                "api": ("detect_multi (ea_detect_multi), one call per pinned host image"
+                "api": ("detect_multi_sharded (ea_detect_multi_sharded), one call per pinned "
+                        "host image on rank 0" if multi and sharded_e2e else
+                        "detect_multi (ea_detect_multi), one call per pinned host image"
                         if multi else
                         "Detector.detect_sharded (ea_detect_sharded), one pinned host image "
                         "per call on rank 0" if sharded_e2e else

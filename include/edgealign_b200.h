@@ -411,6 +411,43 @@ ea_status ea_search_levels_sharded(ea_ctx* ctx, const ea_levels* lv,
 ea_status ea_detect_sharded(ea_ctx* ctx, ea_levels* lv, const double* image, int w, int h,
                             const ea_search_config* cfg, ea_outcome* out);
 
+/* Multi-model sharding (BASELINE configs[4]): the
+ * reference searches each model with its own search_topk (search.cpp:
+ * 155-167); here every (model, theta slab) is a work item costed in
+ * pose-evals (poses x top-level model points, + fixed_evals per search for
+ * the launch / finish overhead), big models split into slabs of about one
+ * rank's share, small ones kept whole, assigned longest-first to the least
+ * loaded rank that holds no other slab of the model.  Deterministic: every
+ * rank computes the same plan. */
+typedef struct {
+    int32_t rank;
+    int32_t model;
+    uint64_t it_begin, it_end; /* theta slab [it_begin, it_end) of the model */
+    double cost;               /* pose-evals + fixed_evals */
+} ea_work_item;
+
+/* plane_poses[m] = nx * ny, thetas[m] = nt, n_top[m] = top-level model
+ * points.  items: cap entries; *n_items receives the count (<= n_models *
+ * world).  Host only. */
+ea_status ea_plan_multi(const uint64_t* plane_poses, const uint64_t* thetas, const int* n_top,
+                        int n_models, int world, double fixed_evals, ea_work_item* items,
+                        int cap, int* n_items);
+/* The exchange step of a multi-model sharded search: all-gather every
+ * rank's n_models x k device rows (model m's k rows at d_local + 5*k*m;
+ * NaN rows for models the rank has no slab of) and `better`-merge them per
+ * model into d_merged (same layout).  Collective, no host sync. */
+ea_status ea_gather_rows_multi_async(ea_ctx* ctx, const double* d_local, int n_models, int k,
+                                     double* d_merged);
+/* Multi-model detect sharded over the communicator (collective): rank 0
+ * uploads the host image and builds the shared pyramid (into models[0]'s
+ * working side), the top level's field is broadcast, every rank searches
+ * its ea_plan_multi items, one NCCL all-gather of all models' k rows, a
+ * `better` merge per model, rank 0 refines every model and broadcasts the
+ * outcomes.  outs[n] equals ea_detect_multi's on every rank. */
+ea_status ea_detect_multi_sharded(ea_ctx* ctx, ea_levels* const* models, int n,
+                                  const double* image, int w, int h,
+                                  const ea_search_config* cfg, ea_outcome* outs);
+
 /* ---- Netpbm codecs (image.cpp:26-219), host C++, bytes in / bytes out ---- */
 /* luminance_to_byte  image.cpp:26-34: clamp to [0, 255], round half up. */
 uint8_t ea_luminance_to_byte(double v);

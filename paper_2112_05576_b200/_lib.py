@@ -117,6 +117,11 @@ _SIGS = {
                                            C.POINTER(abi.Outcome)]),
     "ea_detect_sharded": (C.c_int, [_P, _P, _dp, C.c_int, C.c_int,
                                     C.POINTER(abi.SearchConfig), C.POINTER(abi.Outcome)]),
+    "ea_plan_multi": (C.c_int, [C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), _ip, C.c_int,
+                                C.c_int, C.c_double, C.POINTER(abi.WorkItem), C.c_int, _ip]),
+    "ea_gather_rows_multi_async": (C.c_int, [_P, C.c_void_p, C.c_int, C.c_int, C.c_void_p]),
+    "ea_detect_multi_sharded": (C.c_int, [_P, C.POINTER(_P), C.c_int, _dp, C.c_int, C.c_int,
+                                          C.POINTER(abi.SearchConfig), C.POINTER(abi.Outcome)]),
     "ea_render_template": (C.c_int, [C.c_int, C.c_int, _dp]),
     "ea_luminance_to_byte": (C.c_uint8, [C.c_double]),
     "ea_load_pgm": (C.c_int, [C.c_char_p, C.c_size_t, C.c_void_p, C.c_size_t, _ip, _ip]),

@@ -199,3 +199,12 @@ def comm_id_from_bytes(raw):
     cid = CommId()
     C.memmove(C.addressof(cid), bytes(raw), EA_COMM_ID_BYTES)
     return cid
+
+
+class WorkItem(C.Structure):
+    """ea_work_item: one (model, theta slab) of a multi-model sharded search."""
+    _fields_ = [("rank", C.c_int32), ("model", C.c_int32), ("it_begin", C.c_uint64),
+                ("it_end", C.c_uint64), ("cost", C.c_double)]
+
+    def astuple(self):
+        return (self.rank, self.model, self.it_begin, self.it_end, self.cost)

@@ -647,6 +647,53 @@ def detect_multi(detectors, image):
     return list(outs)
 
 
+def plan_multi(plane_poses, thetas, n_top, world, fixed_evals=6.6e7):
+    """ea_plan_multi: the (model, theta slab) work items of a multi-model
+    sharded search, as (rank, model, it_begin, it_end, cost) tuples."""
+    n = len(n_top)
+    pp = (C.c_uint64 * max(n, 1))(*[int(x) for x in plane_poses])
+    th = (C.c_uint64 * max(n, 1))(*[int(x) for x in thetas])
+    nt = (C.c_int * max(n, 1))(*[int(x) for x in n_top])
+    cap = max(n * int(world), 1)
+    items = (abi.WorkItem * cap)()
+    cnt = C.c_int()
+    _check(lib().ea_plan_multi(pp, th, nt, n, int(world), float(fixed_evals), items, cap,
+                               C.byref(cnt)))
+    return [items[i].astuple() for i in range(cnt.value)]
+
+
+def gather_rows_multi_async(ctx, d_local, n_models, k, d_merged):
+    """NCCL all-gather of every rank's n_models x k device rows + per-model
+    `better` merge into d_merged (ea_gather_rows_multi_async; no host sync)."""
+    _check(lib().ea_gather_rows_multi_async(ctx.handle, C.c_void_p(int(d_local)), int(n_models),
+                                            int(k), C.c_void_p(int(d_merged))))
+
+
+def detect_multi_sharded(detectors, image, shape=None):
+    """Multi-model detect sharded over the first detector's communicator
+    (ea_detect_multi_sharded, collective): rank 0 passes the host image, the
+    other ranks None and `shape` = (h, w).  -> one Outcome per detector."""
+    if not detectors:
+        return []
+    ctx, cfg = detectors[0].ctx, detectors[0].config
+    for d in detectors:
+        if d.ctx is not ctx:
+            raise ValueError("detect_multi_sharded needs detectors on one context")
+    if image is None:
+        h, w = shape
+        ptr = None
+    else:
+        img = image if (isinstance(image, np.ndarray) and image.dtype == np.float64
+                        and image.flags.c_contiguous) else _f64(image)
+        h, w = img.shape
+        ptr = _ptr(img)
+    hs = (C.c_void_p * len(detectors))(*[d.levels.handle for d in detectors])
+    outs = (Outcome * len(detectors))()
+    _check(lib().ea_detect_multi_sharded(ctx.handle, hs, len(detectors), ptr, w, h,
+                                         C.byref(cfg), outs))
+    return list(outs)
+
+
 # ---- Netpbm codecs (image.cpp:26-219) -------------------------------------------------
 def luminance_to_byte(v):
     return int(lib().ea_luminance_to_byte(float(v)))

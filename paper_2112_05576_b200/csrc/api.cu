@@ -1805,6 +1805,237 @@ void search_levels_sharded(ea_ctx* ctx, const ea_levels* lv, const ea_field* fto
     std::memcpy(out, h, sizeof(ea_outcome));
 }
 
+
+// ---- multi-model sharding ----------------------------------------
+// (model, theta slab) work items, costed in pose-evals; see ea_plan_multi in
+// the header.  Deterministic (every rank computes the same plan).
+// LPT assignment of the slabs of `s[m]` per model (theta block partition,
+// search.cpp:116-120): longest first, to the least loaded rank holding no
+// other slab of that model; ties broken by model, slab, rank -- a total
+// order, so every rank computes the same plan.  Returns the makespan.
+double assign_lpt(const std::vector<double>& cost, const uint64_t* thetas,
+                  const std::vector<uint64_t>& s, int world, double fixed_evals,
+                  std::vector<ea_work_item>* out) {
+    const int n_models = (int)cost.size();
+    std::vector<ea_work_item> items;
+    for (int m = 0; m < n_models; ++m) {
+        for (uint64_t j = 0; j < s[m]; ++j) {
+            ea_work_item it{};
+            it.rank = -1;
+            it.model = m;
+            theta_slab_of(thetas[m], (int)j, (int)s[m], &it.it_begin, &it.it_end);
+            it.cost = cost[m] * (double)(it.it_end - it.it_begin) / (double)thetas[m] + fixed_evals;
+            items.push_back(it);
+        }
+    }
+    std::stable_sort(items.begin(), items.end(), [](const ea_work_item& x, const ea_work_item& y) {
+        if (x.cost != y.cost) return x.cost > y.cost;
+        if (x.model != y.model) return x.model < y.model;
+        return x.it_begin < y.it_begin;
+    });
+    std::vector<double> load(world, 0.0);
+    std::vector<std::vector<char>> holds(world, std::vector<char>(n_models, 0));
+    for (ea_work_item& it : items) {
+        int best = -1;
+        for (int r = 0; r < world; ++r) {
+            if (holds[r][it.model]) continue;  // one slab of a model per rank
+            if (best < 0 || load[r] < load[best]) best = r;
+        }
+        it.rank = best;
+        load[best] += it.cost;
+        holds[best][it.model] = 1;
+    }
+    std::stable_sort(items.begin(), items.end(), [](const ea_work_item& x, const ea_work_item& y) {
+        if (x.rank != y.rank) return x.rank < y.rank;
+        if (x.model != y.model) return x.model < y.model;
+        return x.it_begin < y.it_begin;
+    });
+    *out = std::move(items);
+    return *std::max_element(load.begin(), load.end());
+}
+
+// The plan with the smallest makespan among slab sizes of about 1/d of a
+// rank's share (d = 1, 2, 3, 4, 6, 8) and every model cut into `world`
+// slabs: coarse slabs pay fewer fixed costs, fine slabs pack better.
+std::vector<ea_work_item> plan_multi(const uint64_t* plane_poses, const uint64_t* thetas,
+                                     const int* n_top, int n_models, int world,
+                                     double fixed_evals) {
+    if (n_models < 0 || world < 1) fail(EA_ERR_INVALID_ARGUMENT, "need n_models >= 0, world >= 1");
+    double total = 0.0;
+    std::vector<double> cost(n_models);
+    for (int m = 0; m < n_models; ++m) {
+        if (n_top[m] < 0) fail(EA_ERR_INVALID_ARGUMENT, "n_top must be >= 0");
+        cost[m] = (thetas[m] == 0 || plane_poses[m] == 0)
+                      ? 0.0
+                      : (double)plane_poses[m] * (double)thetas[m] * (double)n_top[m];
+        total += cost[m];
+    }
+    const double share = total / world;
+    std::vector<ea_work_item> best;
+    double best_span = 0.0;
+    for (int d : {1, 2, 3, 4, 6, 8, 0}) {  // 0: every model in `world` slabs
+        std::vector<uint64_t> s(n_models, 0);
+        for (int m = 0; m < n_models; ++m) {
+            if (thetas[m] == 0 || plane_poses[m] == 0) continue;
+            uint64_t q = d == 0 ? (uint64_t)world
+                         : share > 0.0 ? (uint64_t)std::ceil(cost[m] * d / share - 1e-9) : 1;
+            s[m] = std::max<uint64_t>(1, std::min<uint64_t>({q, (uint64_t)world, thetas[m]}));
+        }
+        std::vector<ea_work_item> items;
+        const double span = assign_lpt(cost, thetas, s, world, fixed_evals, &items);
+        if (best.empty() || span < best_span * (1 - 1e-12)) {
+            best = std::move(items);
+            best_span = span;
+        }
+    }
+    return best;
+}
+
+// Per-search overhead of one slab search in pose-evals (the finish and the
+// launch boundaries, ~30 us at ~2.2e12 pose-evals/s on B200).
+constexpr double kSearchFixedEvals = 6.6e7;
+
+void detect_multi_sharded(ea_ctx* ctx, ea_levels* const* models, int n, const double* image,
+                          int w, int h, const ea_search_config& cfg, ea_outcome* outs) {
+    ncclComm_t comm = comm_of(ctx);
+    const bool root = ctx->comm_rank == 0;
+    const int L = cfg.num_levels, top = L - 1, k = cfg.topk, world = ctx->comm_world;
+    for (int i = 0; i < n; ++i) {
+        need(models[i], "models[i]");
+        if ((int)models[i]->models.size() < L)
+            fail(EA_ERR_INVALID_ARGUMENT, "prepared levels of model " + std::to_string(i) +
+                                              " do not cover num_levels");
+    }
+    if (L < 1 || L > EA_MAX_LEVELS) fail(EA_ERR_INVALID_ARGUMENT, "num_levels out of range");
+    validate_params(cfg.score_params);
+    if (k < 1 || cfg.refine_radius < 1)
+        fail(EA_ERR_INVALID_ARGUMENT, "topk and refine_radius must be >= 1");
+    if (w < 1 || h < 1) {
+        fail(EA_ERR_SIZE, "image dimensions must be at least 1x1, got " + std::to_string(w) + "x" +
+                              std::to_string(h));
+    }
+    if (L > pyramid_levels_feasible(w, h)) {
+        fail(EA_ERR_SIZE, "pyramid of " + std::to_string(L) +
+                              " levels would drop below 8x8; maximum feasible level count is " +
+                              std::to_string(pyramid_levels_feasible(w, h)));
+    }
+    if (world * k > merge_rows_max(ctx))
+        fail(EA_ERR_INVALID_ARGUMENT, "world * topk exceeds the merge's shared memory");
+    ea_levels* work = models[0];
+    const int wt = w >> top, ht = h >> top;
+    ea_field* ftop = nullptr;
+    if (root) {
+        set_working_image(ctx, work, image, w, h, L);
+        ftop = work->fields[top];
+    } else {
+        if (work->shard_top && (work->shard_top->width != wt || work->shard_top->height != ht)) {
+            delete work->shard_top;
+            work->shard_top = nullptr;
+        }
+        if (!work->shard_top) work->shard_top = new_field(wt, ht);
+        ftop = work->shard_top;
+    }
+    EAB_NCCL(nccl().Broadcast(ftop->g.p, ftop->g.p, 3 * (size_t)wt * ht, ncclDouble, 0, comm,
+                              ctx->stream));
+    if (!root) {
+        ftop->version = next_field_version();
+        ftop->ring_max = 0.0;
+    }
+    // the plan (same on every rank)
+    const ea_pose_grid tg = top_grid_of(cfg);
+    const ea_grid_counts c = counts_of(tg);
+    std::vector<uint64_t> planes(n, c.nx * c.ny), thetas(n, c.nt);
+    std::vector<int> ntop(n);
+    for (int i = 0; i < n; ++i) ntop[i] = models[i]->models[top]->n;
+    const std::vector<ea_work_item> items =
+        plan_multi(planes.data(), thetas.data(), ntop.data(), n, world, kSearchFixedEvals);
+    // buffers: local rows [n][k], gathered [world][n][k], merged [n][k], seeds, outcomes
+    const size_t rows_b = 5 * sizeof(double) * (size_t)n * k;
+    const size_t seeds_b = (sizeof(double) + sizeof(unsigned long long)) * (size_t)n * k;
+    size_t off = 0;
+    auto carve = [&](size_t bytes) {
+        const size_t o = off;
+        off = (off + bytes + 255) & ~(size_t)255;
+        return o;
+    };
+    const size_t o_local = carve(rows_b), o_gath = carve(rows_b * world), o_merged = carve(rows_b),
+                 o_score = carve(seeds_b), o_cnt = carve(sizeof(int) * n),
+                 o_out = carve(sizeof(ea_outcome) * n), o_flag = carve(sizeof(int));
+    char* base = (char*)ctx->shard.ensure(off);
+    double* local = (double*)(base + o_local);
+    double* gathered = (double*)(base + o_gath);
+    double* merged = (double*)(base + o_merged);
+    double* tscore = (double*)(base + o_score);
+    unsigned long long* tindex = reinterpret_cast<unsigned long long*>(tscore + (size_t)n * k);
+    int* tcount = (int*)(base + o_cnt);
+    ea_outcome* d_outs = (ea_outcome*)(base + o_out);
+    int* flag = (int*)(base + o_flag);
+    // NaN rows for the models this rank has no slab of (0xff.. is a NaN)
+    EAB_CUDA(cudaMemsetAsync(local, 0xff, rows_b, ctx->stream));
+    EAB_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), ctx->stream));
+    for (const ea_work_item& it : items) {
+        if (it.rank != ctx->comm_rank) continue;
+        slab_rows(ctx, models[it.model]->models[top], ftop, tg, cfg.score_params, k, it.it_begin,
+                  it.it_end, local + 5 * (size_t)it.model * k, flag);
+    }
+    EAB_NCCL(nccl().AllGather(local, gathered, 5 * (size_t)n * k, ncclDouble, comm, ctx->stream));
+    launch_merge_rows_multi(ctx, gathered, world, n, k, merged, tscore, tindex, tcount);
+    if (root) {
+        struct View {
+            ea_levels lv;
+            ~View() {
+                lv.models.clear();
+                lv.fields.clear();
+            }
+        };
+        const double* tables = detect_tables(ctx, cfg);
+        EAB_CUDA(cudaMemsetAsync(d_outs, 0, sizeof(ea_outcome) * n, ctx->stream));
+        std::vector<double> hrows;
+        if (top > 0 && !tables) {  // very wide beams: host-assisted refinement
+            hrows.resize(5 * (size_t)n * k);
+            d2h(ctx, hrows.data(), merged, rows_b);
+            sync(ctx);
+        }
+        for (int i = 0; i < n; ++i) {
+            View v;
+            v.lv.models = models[i]->models;
+            v.lv.fields = work->fields;
+            if (top == 0 || tables) {
+                RefineState st = refine_state(ctx, k);
+                st.out = d_outs + i;
+                launch_seed_beam(ctx, tscore + (size_t)i * k, tindex + (size_t)i * k, tcount + i,
+                                 seed_args(tg, c, cfg), st.beam[0], st.cnt[0], st.out);
+                if (top > 0) refine_enqueue(ctx, &v.lv, cfg, tg, tables, st);
+            } else {
+                std::vector<ea_scored_pose> seeds;
+                for (int r = 0; r < k; ++r) {
+                    const double* q = hrows.data() + 5 * ((size_t)i * k + r);
+                    if (q[0] != q[0]) break;
+                    if (std::isinf(q[0]))
+                        fail(EA_ERR_INTERNAL, "candidate buffer overflow in a sharded search");
+                    seeds.push_back(ea_scored_pose{q[0], (uint64_t)q[1], ea_pose{q[2], q[3], q[4]}});
+                }
+                ea_outcome ho{};
+                refine_levels(ctx, &v.lv, cfg, tg, seeds_to_beam(seeds), &ho);
+                h2d_staged(ctx, d_outs + i, &ho, sizeof ho);
+            }
+        }
+    }
+    EAB_NCCL(nccl().Broadcast(d_outs, d_outs, sizeof(ea_outcome) * n, ncclUint8, 0, comm,
+                              ctx->stream));
+    char* hb = (char*)ctx->h_out.ensure(sizeof(ea_outcome) * n + rows_b);
+    d2h(ctx, hb, d_outs, sizeof(ea_outcome) * n);
+    d2h(ctx, hb + sizeof(ea_outcome) * n, merged, rows_b);
+    sync(ctx);
+    for (int i = 0; i < n; ++i) {
+        double row0;
+        std::memcpy(&row0, hb + sizeof(ea_outcome) * n + 5 * sizeof(double) * (size_t)i * k,
+                    sizeof row0);
+        if (std::isinf(row0)) fail(EA_ERR_INTERNAL, "candidate buffer overflow in a sharded search");
+    }
+    std::memcpy(outs, hb, sizeof(ea_outcome) * n);
+}
+
 }  // namespace
 
 // =============================================================================
@@ -2853,6 +3084,67 @@ ea_status ea_detect_sharded(ea_ctx* ctx, ea_levels* lv, const double* image, int
             EAB_CUDA(cudaEventElapsedTime(&ms, ctx->ev[4], ctx->ev[5]));
             ctx->stats.image_ms = ms;
         }
+        ctx->stats.kernels_launched = (int)(ctx->launches - launched0);
+    });
+}
+
+ea_status ea_plan_multi(const uint64_t* plane_poses, const uint64_t* thetas, const int* n_top,
+                        int n_models, int world, double fixed_evals, ea_work_item* items,
+                        int cap, int* n_items) {
+    return guard([&] {
+        need(n_items, "n_items");
+        if (n_models > 0) {
+            need(plane_poses, "plane_poses");
+            need(thetas, "thetas");
+            need(n_top, "n_top");
+        }
+        const std::vector<ea_work_item> v =
+            plan_multi(plane_poses, thetas, n_top, n_models, world, fixed_evals);
+        *n_items = (int)v.size();
+        if ((int)v.size() > cap) fail(EA_ERR_INVALID_ARGUMENT, "items buffer too small");
+        for (size_t i = 0; i < v.size(); ++i) items[i] = v[i];
+    });
+}
+
+ea_status ea_gather_rows_multi_async(ea_ctx* ctx, const double* d_local, int n_models, int k,
+                                     double* d_merged) {
+    return guard([&] {
+        need(ctx, "ctx");
+        need(d_local, "d_local");
+        need(d_merged, "d_merged");
+        if (k < 1 || n_models < 1) fail(EA_ERR_INVALID_ARGUMENT, "need topk >= 1, n_models >= 1");
+        ncclComm_t comm = comm_of(ctx);
+        const int world = ctx->comm_world;
+        if (world * k > merge_rows_max(ctx))
+            fail(EA_ERR_INVALID_ARGUMENT, "world * topk exceeds the merge's shared memory");
+        DeviceGuard dg(ctx->device);
+        const size_t rows = 5 * (size_t)n_models * k;
+        const size_t o_seed = (sizeof(double) * rows * world + 255) & ~(size_t)255;
+        const size_t seeds = (sizeof(double) + sizeof(unsigned long long)) * (size_t)n_models * k;
+        char* base = (char*)ctx->mscratch.ensure(o_seed + seeds + sizeof(int) * n_models);
+        double* gathered = (double*)base;
+        double* ts = (double*)(base + o_seed);
+        EAB_NCCL(nccl().AllGather(d_local, gathered, rows, ncclDouble, comm, ctx->stream));
+        launch_merge_rows_multi(ctx, gathered, world, n_models, k, d_merged, ts,
+                                reinterpret_cast<unsigned long long*>(ts + (size_t)n_models * k),
+                                (int*)(base + o_seed + seeds));
+    });
+}
+
+ea_status ea_detect_multi_sharded(ea_ctx* ctx, ea_levels* const* models, int n,
+                                  const double* image, int w, int h,
+                                  const ea_search_config* cfg, ea_outcome* outs) {
+    return guard([&] {
+        need(ctx, "ctx");
+        need(cfg, "config");
+        if (n <= 0) return;
+        need(models, "models");
+        need(outs, "outs");
+        comm_of(ctx);
+        if (ctx->comm_rank == 0) need(image, "image");
+        DeviceGuard dg(ctx->device);
+        const uint64_t launched0 = ctx->launches;
+        detect_multi_sharded(ctx, models, n, image, w, h, *cfg, outs);
         ctx->stats.kernels_launched = (int)(ctx->launches - launched0);
     });
 }

@@ -319,6 +319,12 @@ void launch_merge_rows(ea_ctx* ctx, const double* in, int n, int k, double* out,
                        double* top_score = nullptr, unsigned long long* top_index = nullptr,
                        int* n_top = nullptr);
 int merge_rows_max(ea_ctx* ctx);
+// Per-model merge of a multi-model all-gather: rank r's rows of model m at
+// in[(r * n_models + m) * k ..]; model m's merged rows at out[m * k ..] and
+// its seeds at top_score/top_index[m * k ..], n_top[m].
+void launch_merge_rows_multi(ea_ctx* ctx, const double* in, int world, int n_models, int k,
+                             double* out, double* top_score, unsigned long long* top_index,
+                             int* n_top);
 // compaction + rescore + select (+ rows when rows != nullptr) in one
 // cooperative launch; same results as launch_compact/rescore/select/topk_rows.
 struct FinishArgs {

@@ -2231,6 +2231,68 @@ void launch_topk_rows(ea_ctx* ctx, const double* score, const unsigned long long
     count_launch(ctx);
 }
 
+// Per-model `better` merge of a multi-model all-gather (one CTA per model):
+// rank r's rows of model m are in[(r * n_models + m) * k + j], j < k.
+// Writes model m's k merged rows to out[m * k ..] and its seeds to
+// top_score/top_index[m * k ..], n_top[m].
+__global__ void __launch_bounds__(256) merge_rows_multi_kernel(
+    const double* __restrict__ in, int world, int n_models, int k, double* __restrict__ out,
+    double* __restrict__ top_score, unsigned long long* __restrict__ top_index,
+    int* __restrict__ n_top) {
+    extern __shared__ long long mk[];
+    const int m = blockIdx.x, n = world * k;
+    long long* key = mk;
+    unsigned long long* idx = reinterpret_cast<unsigned long long*>(mk + n);
+    __shared__ int valid;
+    if (threadIdx.x == 0) valid = 0;
+    __syncthreads();
+    auto row = [&](int i) { return in + 5 * ((size_t)((i / k) * n_models + m) * k + i % k); };
+    int mine = 0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const double sc = row(i)[0];
+        key[i] = sc != sc ? LLONG_MIN : order_key(sc);
+        idx[i] = (unsigned long long)row(i)[1];
+        mine += sc == sc;
+    }
+    if (mine) atomicAdd(&valid, mine);
+    double* o = out + 5 * (size_t)m * k;
+    for (int r = threadIdx.x; r < k; r += blockDim.x) {
+        o[5 * r] = __longlong_as_double(0x7ff8000000000000LL);
+        o[5 * r + 1] = o[5 * r + 2] = o[5 * r + 3] = o[5 * r + 4] = 0.0;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        if (key[i] == LLONG_MIN) continue;
+        int rank = 0;
+        for (int j = 0; j < n; ++j)
+            rank += key[j] > key[i] || (key[j] == key[i] && key[j] != LLONG_MIN &&
+                                        (idx[j] < idx[i] || (idx[j] == idx[i] && j < i)));
+        if (rank < k) {
+            for (int c = 0; c < 5; ++c) o[5 * rank + c] = row(i)[c];
+            top_score[(size_t)m * k + rank] = row(i)[0];
+            top_index[(size_t)m * k + rank] = idx[i];
+        }
+    }
+    if (threadIdx.x == 0) n_top[m] = valid < k ? valid : k;
+}
+
+void launch_merge_rows_multi(ea_ctx* ctx, const double* in, int world, int n_models, int k,
+                             double* out, double* top_score, unsigned long long* top_index,
+                             int* n_top) {
+    const size_t smem = (size_t)world * k * 16;
+    static size_t opted = 0;
+    if (smem + 1024 > 48 * 1024 && opted < ctx->smem_optin) {
+        EAB_CUDA(cudaFuncSetAttribute(merge_rows_multi_kernel,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)ctx->smem_optin));
+        opted = ctx->smem_optin;
+    }
+    merge_rows_multi_kernel<<<n_models, 256, smem, ctx->stream>>>(in, world, n_models, k, out,
+                                                                 top_score, top_index, n_top);
+    check_launch("merge_rows_multi_kernel");
+    count_launch(ctx);
+}
+
 int merge_rows_max(ea_ctx* ctx) { return (int)(ctx->smem_optin / 16); }
 
 void launch_merge_rows(ea_ctx* ctx, const double* in, int n, int k, double* out,

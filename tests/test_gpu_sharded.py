@@ -161,3 +161,40 @@ def test_merge_rows_many(ea, n):
     ctx.synchronize()
     want = parallel.merge(parallel.unpack(rows), k)
     assert keys(parallel.unpack(d_out.cpu().numpy())) == keys(want)
+
+
+def test_detect_multi_sharded_world1(ea, oracle, comm_ctx):
+    """ea_detect_multi_sharded (plan, input broadcast, per-item slab searches,
+    one all-gather of every model's rows, per-model merge, root refinement,
+    outcome broadcast) on a world-1 communicator == detect_multi == oracle,
+    twice (cached plane and tables), on a region-tiled top level."""
+    stamps = [("l_bracket", 64, (150.0, 130.0, D(40))), ("cross", 96, (460.0, 140.0, D(15))),
+              ("ring", 80, (170.0, 350.0, 0.0)), ("rectangle", 72, (470.0, 340.0, D(200)))]
+    spec = ea.SceneSpec(640, 480, "rectangle", 0, (0, 0, 0), 60, 5, None, (1.1, 4.0, 1.0), 1.5, 9)
+    img = ea.compose_multi(spec, stamps)
+    cfg = ea.SearchConfig(grid=ea.PoseGrid(0, 639, 2, 0, 479, 2, 0.0, D(350), D(10)),
+                          num_levels=2, score_params=ea.ScoreParams(3), topk=3)
+    tmpls = [ea.render_template(t, s) for t, s, _ in stamps]
+    dets = [ea.Detector(t, cfg, comm_ctx) for t in tmpls]
+    got = ea.detect_multi_sharded(dets, img)
+    again = ea.detect_multi_sharded(dets, img)
+    single = ea.detect_multi(dets, img)
+    wp = oracle.build_pyramid(img, 2)
+    for t, a, b, c in zip(tmpls, got, again, single):
+        want = oracle.coarse_to_fine(oracle.build_pyramid(t, 2), wp, cfg)
+        assert a.key() == b.key() == c.key() == want.key()
+
+
+def test_detect_multi_sharded_lattice_world1(ea, oracle, comm_ctx):
+    """Same on a small (shared-memory) top level with three refinement levels."""
+    stamps = [("l_bracket", 48, (70.0, 60.0, D(33))), ("cross", 40, (150.0, 100.0, D(80)))]
+    spec = ea.SceneSpec(224, 160, "rectangle", 0, (0, 0, 0), 20, 3, None, (1.0, 0.0, 1.0), 0.0, 0)
+    img = ea.compose_multi(spec, stamps)
+    cfg = ea.SearchConfig(grid=ea.PoseGrid(0, 223, 4, 0, 159, 4, 0.0, D(357), D(3)),
+                          num_levels=3, score_params=ea.ScoreParams(3), topk=4)
+    tmpls = [ea.render_template(t, s) for t, s, _ in stamps]
+    dets = [ea.Detector(t, cfg, comm_ctx) for t in tmpls]
+    got = ea.detect_multi_sharded(dets, img)
+    wp = oracle.build_pyramid(img, 3)
+    for t, a in zip(tmpls, got):
+        assert a.key() == oracle.coarse_to_fine(oracle.build_pyramid(t, 3), wp, cfg).key()

@@ -111,3 +111,112 @@ def test_pack_unpack_roundtrip():
     back = parallel.unpack(parallel.pack(s, 3))
     assert len(back) == 1 and back[0].grid_index == 2 ** 40 + 3
     assert back[0].score == 0.5 and back[0].pose.astuple() == (1.5, -2.25, 0.125)
+
+
+# ---- multi-model sharding: ea_plan_multi ---------------------------
+def check_plan(items, thetas, world):
+    """Every model's theta range is covered exactly once by contiguous slabs,
+    one slab per (rank, model), ranks in range."""
+    by_model = {}
+    seen = set()
+    for r, m, b, e, c in items:
+        assert 0 <= r < world and b < e and c > 0
+        assert (r, m) not in seen
+        seen.add((r, m))
+        by_model.setdefault(m, []).append((b, e))
+    for m, nt in enumerate(thetas):
+        sl = sorted(by_model.get(m, []))
+        if nt == 0:
+            assert not sl
+            continue
+        assert sl[0][0] == 0 and sl[-1][1] == nt
+        assert all(a[1] == b[0] for a, b in zip(sl, sl[1:]))
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 4, 8, 16])
+def test_plan_multi_covers_and_balances(world):
+    ntop = [11, 20, 35, 57, 75, 144, 210, 292]  # cfg5's top-level model sizes
+    planes, thetas = [324 * 243] * 8, [720] * 8
+    items = api.plan_multi(planes, thetas, ntop, world)
+    check_plan(items, thetas, world)
+    assert items == api.plan_multi(planes, thetas, ntop, world)  # deterministic
+    load = [0.0] * world
+    for r, m, b, e, c in items:
+        load[r] += c
+    ideal = sum(p * t * n for p, t, n in zip(planes, thetas, ntop)) / world
+    # within the fixed per-search cost of one slab per model of the ideal
+    assert max(load) <= ideal * 1.15 + 8 * 6.6e7
+    # never worse than cutting every model into `world` slabs
+    uniform = ideal + 8 * 6.6e7
+    assert max(load) <= uniform * 1.0001
+
+
+def test_plan_multi_edge_cases():
+    assert api.plan_multi([], [], [], 4) == []
+    items = api.plan_multi([100, 100], [3, 0], [5, 7], 8)  # fewer thetas than ranks; empty model
+    check_plan(items, [3, 0], 8)
+    assert all(m == 0 for _, m, _, _, _ in items) and len(items) <= 3
+    from paper_2112_05576_b200.errors import InvalidArgument
+    with pytest.raises(InvalidArgument):
+        api.plan_multi([1], [1], [1], 0)
+
+
+def multi_case(seed):
+    from oracle.pyoracle import OracleC
+    orc = OracleC()
+    img, _, _, _ = orc.compose_scene(abi.SceneSpec(96, 80, "cross", 30, (40, 36, D(20)), 14,
+                                                   seed))
+    models = []
+    for shape, size in (("l_bracket", 32), ("cross", 30), ("ring", 24)):
+        models.append(orc.prepare_model(orc.render_template(shape, size)))
+    f = orc.compute_gradients(img)
+    grid = abi.PoseGrid(0, 95, 1, 0, 79, 1, 0.0, D(350), D(10))
+    return orc, models, f, grid
+
+
+def multi_worker(rank, world, port, seed, k, q):
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        orc, models, f, grid = multi_case(seed)
+        nx, ny, nt = orc.grid_counts(grid)
+        n = len(models)
+        items = api.plan_multi([nx * ny] * n, [nt] * n, [len(m.points) for m in models], world)
+        rows = np.full((n * k, parallel.ROW), np.nan)
+        for r, m, b, e, _ in items:  # this rank's (model, slab) items; oracle stands in
+            if r == rank:
+                part = orc.search_topk(models[m].points, f, grid, abi.ScoreParams(3), k,
+                                       it_range=(b, e), threads=2)
+                rows[m * k:(m + 1) * k] = parallel.pack(part, k)
+        allrows = torch.empty((world * n * k, parallel.ROW), dtype=torch.float64)
+        dist.all_gather_into_tensor(allrows, torch.from_numpy(rows))
+        got = allrows.numpy().reshape(world, n, k, parallel.ROW)
+        out = []
+        for m in range(n):
+            merged = api.merge_topk(parallel.unpack(got[:, m]), k)
+            out.append([(s.score, int(s.grid_index)) for s in merged])
+        q.put((rank, out))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,k,seed", [(2, 5, 1), (3, 4, 2)])
+def test_multi_model_plan_gather_merge_equals_full(world, k, seed):
+    ctx = mp.get_context("fork")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=multi_worker, args=(r, world, port, seed, k, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=240) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    orc, models, f, grid = multi_case(seed)
+    want = [[(s.score, int(s.grid_index)) for s in
+             orc.search_topk(m.points, f, grid, abi.ScoreParams(3), k)] for m in models]
+    for r in range(world):
+        assert res[r] == want
