@@ -299,6 +299,7 @@ struct ScreenPlan {
     bool fast = false;
     bool fused = false;  // the screen launch also ran the finish (launch_screen_fused)
     float* cta_top = nullptr;  // top-list mode: the screen's per-CTA lists (FinishArgs::cta_top)
+    const unsigned char* zero_tiles = nullptr;  // exact-zero tile flags (lattice kernel)
     ItemGeom items{};
     const double* rot = nullptr;  // exact rotation table of the slab (model cache)
     const int* flags = nullptr;   // device count of rounding-ambiguous pairs
@@ -478,6 +479,29 @@ ScreenPlan screen(ea_ctx* ctx, const ea_model* m, const ea_field* f, const ea_po
     a.edge = edge ? 1 : 0;
     a.amb = amb;
     a.kf = (k >= 1 && k <= 8) ? k : 0;
+    // Exact-zero translation tiles of the smem lattice kernel (a function of
+    // the field, eps, the lattice origin, the tile shape and the model
+    // radius: cached like the plane).  Flat regions skip the screen work, and
+    // a featureless frame no longer floods the band with every pose (only the
+    // first k poses of each zero tile can rank; finish_tile).
+    if (lattice && !region && plan.slab_poses) {
+        const int tw = 8 * xg, th = (32 / xg) * 8;
+        const unsigned nwx = (unsigned)((plan.c.nx + tw - 1) / tw);
+        const unsigned nwy = (unsigned)((plan.c.ny + th - 1) / th);
+        const int halo = ro_int + R;
+        unsigned char* zt = (unsigned char*)ctx->ztiles.ensure((size_t)nwx * nwy);
+        const std::vector<double> zkey{(double)reinterpret_cast<uintptr_t>(f), (double)f->version,
+                                       p.eps_mag, g.x0, g.y0, (double)nwx, (double)nwy,
+                                       (double)xg, (double)halo,
+                                       (double)reinterpret_cast<uintptr_t>(zt)};
+        if (zkey != ctx->ztiles_key) {
+            ctx->ztiles_key.clear();
+            launch_zero_tiles(ctx, f, p.eps_mag, (int)g.x0, (int)g.y0, nwx, nwy, tw, th, halo, zt);
+            ctx->ztiles_key = zkey;
+        }
+        a.zero_tiles = zt;
+        plan.zero_tiles = zt;
+    }
     a.K = K;
     a.B3 = B3;
     a.scale = (float)(std::ldexp(1.0, e - 22) / (double)n);
@@ -597,6 +621,7 @@ ScreenPlan screen(ea_ctx* ctx, const ea_model* m, const ea_field* f, const ea_po
         fa.rows = req->d_rows;
         fa.overflow = req->overflow;
         fa.cta_top = plan.cta_top;
+        fa.zero_tiles = plan.zero_tiles;
         plan.fused = plan.fast = launch_screen_fused(ctx, a, fa);
     }
     if (plan.slab_poses && !plan.fused) {
@@ -692,6 +717,7 @@ TopLaunch top_enqueue(ea_ctx* ctx, const ea_model* m, const ea_field* f, const e
         fa.overflow = overflow;
         fa.cta_top = t.plan.fast ? t.plan.cta_top : nullptr;
         fa.n_lists = ctx->screen_ctas;
+        fa.zero_tiles = t.plan.fast && ctx->stats.screen_path == 1 ? t.plan.zero_tiles : nullptr;
         launch_finish(ctx, fa);
         ctx->hist_clean = true;
         return t;
@@ -2092,7 +2118,7 @@ void ea_ctx_destroy(ea_ctx* ctx) {
                       &ctx->hist, &ctx->ctrl, &ctx->cand, &ctx->cand_score, &ctx->topk,
                       &ctx->refine_poses, &ctx->refine_scores, &ctx->beam, &ctx->accum64,
                       &ctx->work, &ctx->ttab, &ctx->rstate, &ctx->rslots, &ctx->mscratch,
-                      &ctx->cta_top})
+                      &ctx->cta_top, &ctx->ztiles})
         b->release();
     ctx->h_stage.release();
     ctx->h_out.release();

@@ -248,6 +248,11 @@ struct ScreenArgs {
     SearchCtrl* ctrl;
     unsigned long long* prof;  // optional phase timestamps (EAB_SCREEN_PROF)
     unsigned long long* wtrace;  // optional per-warp unit end stamps [warp][8] (EAB_SCREEN_TRACE)
+    // exact-zero translation tiles (nwx * nwy flags, theta-independent; null
+    // = none known): no edge pixel (|g| >= eps) within any window of any
+    // pose of the tile, so every such pose scores exactly 0 (similarity.cpp:
+    // 102-118, kernels_scalar.cpp:44-50) -- the screen skips their work
+    const unsigned char* zero_tiles;
     // top-list mode (smem lattice kernel, 1 <= kf <= 8, no flagged theta):
     // no histogram; each CTA writes its kf largest tile maxima here
     // ([CTA][kTopK]) and the finish takes the band threshold from them
@@ -263,6 +268,12 @@ bool launch_screen_fast(ea_ctx* ctx, const ScreenArgs& a);
 // Returns false when even one halo region does not fit.
 bool launch_screen_region(ea_ctx* ctx, const ScreenArgs& a);
 void launch_screen_general(ea_ctx* ctx, const ScreenArgs& a);
+// Exact-zero flags of the lattice kernel's translation tiles (nwx x nwy tiles
+// of tw x th poses from lattice origin (ix0, iy0)): 1 when no pixel of the
+// field within `halo` of the tile has |g| >= eps.
+void launch_zero_tiles(ea_ctx* ctx, const ea_field* f, double eps, int ix0, int iy0,
+                       unsigned nwx, unsigned nwy, int tw, int th, int halo,
+                       unsigned char* out);
 // The general kernel over the flagged thetas of a lattice launch only.
 void launch_screen_flagged(ea_ctx* ctx, const ScreenArgs& a);
 
@@ -348,6 +359,7 @@ struct FinishArgs {
     double* rows;
     int* overflow;
     unsigned long long* prof;  // optional phase timestamps (EAB_FINISH_PROF)
+    const unsigned char* zero_tiles;  // exact-zero translation tiles (ScreenArgs::zero_tiles)
     float* cta_top;            // top-list mode: [CTA][kTopK] largest tile maxima per screen CTA
     int n_lists;               // screen CTAs that wrote cta_top
 };

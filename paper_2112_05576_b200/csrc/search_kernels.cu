@@ -976,6 +976,39 @@ __global__ void __launch_bounds__(256)
     merge_hist(hist, a.hist, a.kf);
 }
 
+// One CTA per translation tile: any |g| >= eps within the tile's halo?
+__global__ void __launch_bounds__(256) zero_tiles_kernel(const double* __restrict__ mag, int W,
+                                                         int H, double eps, int ix0, int iy0,
+                                                         unsigned nwx, int tw, int th, int halo,
+                                                         unsigned char* __restrict__ out) {
+    const unsigned t = blockIdx.x;
+    const int wx = (int)(t % nwx), wy = (int)(t / nwx);
+    const int x0 = max(ix0 + wx * tw - halo, 0), x1 = min(ix0 + wx * tw + tw - 1 + halo, W - 1);
+    const int y0 = max(iy0 + wy * th - halo, 0), y1 = min(iy0 + wy * th + th - 1 + halo, H - 1);
+    int any = 0;
+    if (x0 <= x1 && y0 <= y1) {
+        const int cols = x1 - x0 + 1;
+        const long long n = (long long)cols * (y1 - y0 + 1);
+        for (long long i = threadIdx.x; i < n && !any; i += blockDim.x) {
+            const int y = y0 + (int)(i / cols), x = x0 + (int)(i % cols);
+            any = __ldg(mag + (size_t)y * W + x) >= eps;
+        }
+    }
+    any = __syncthreads_or(any);
+    if (threadIdx.x == 0) out[t] = any ? 0 : 1;
+}
+
+void launch_zero_tiles(ea_ctx* ctx, const ea_field* f, double eps, int ix0, int iy0,
+                       unsigned nwx, unsigned nwy, int tw, int th, int halo,
+                       unsigned char* out) {
+    const unsigned long long n = (unsigned long long)nwx * nwy;
+    if (n == 0) return;
+    zero_tiles_kernel<<<(unsigned)n, 256, 0, ctx->stream>>>(f->mag(), f->width, f->height, eps,
+                                                            ix0, iy0, nwx, tw, th, halo, out);
+    check_launch("zero_tiles_kernel");
+    count_launch(ctx);
+}
+
 void launch_screen_general(ea_ctx* ctx, const ScreenArgs& a) {
     const unsigned long long total = a.nx * a.ny * a.it_count;
     unsigned long long blocks = (total + 255) / 256;
@@ -1558,6 +1591,23 @@ __device__ __forceinline__ float finish_threshold(const unsigned* __restrict__ h
 __device__ __forceinline__ void finish_tile(const FinishArgs& f, unsigned long long it,
                                             float thr, int lane) {
     const ItemGeom& g = f.items;
+    if (f.zero_tiles && g.lattice && __ldg(f.zero_tiles + it % ((unsigned long long)g.nwx * g.nwy))) {
+        // exact-zero tile: every pose scores 0 (and 0 >= thr, or none is a
+        // candidate); only its first k poses in index order can rank -- any
+        // other has k poses of equal score and smaller index in this tile
+        if (lane == 0 && 0.0f >= thr) {
+            const unsigned long long wx = it % g.nwx, rest = it / g.nwx;
+            const unsigned long long wy = rest % g.nwy, itr = rest / g.nwy;
+            const unsigned long long x0 = wx * g.cols, y0 = wy * g.rows;
+            int got = 0;
+            for (unsigned long long y = y0; y < y0 + g.rows && y < g.ny && got < f.k; ++y)
+                for (unsigned long long x = x0; x < x0 + g.cols && x < g.nx && got < f.k; ++x, ++got) {
+                    const unsigned long long slot = atomicAdd(&f.ctrl->cand_count, 1ull);
+                    if (slot < f.cap) f.cand[slot] = (unsigned)(itr * (g.nx * g.ny) + y * g.nx + x);
+                }
+        }
+        return;
+    }
     constexpr int kMaxSteps = 64;  // 32 lanes x 64 = one 2048-pose lattice tile
     const float kNaN = __int_as_float(0x7fffffff);  // never >= thr, even thr = -inf
     const float* p;
@@ -1884,6 +1934,8 @@ __global__ void __launch_bounds__(THREADS, 1)
             e0 = (int)((long long)ch * n_ent / tp.f);
             e1 = (int)((long long)(ch + 1) * n_ent / tp.f);
         }
+        // exact-zero tile: no entries, every score the fixed-point 0
+        if (a.zero_tiles && __ldg(a.zero_tiles + (size_t)wy * nwx + wx)) e0 = e1 = 0;
         g.cbase = a.ix0 + X - R + g.cx_lo;   // padded column of the window start - ox
         g.rbase = a.iy0 + Y - R + 1;         // padded row of the window start - oy
         g.cwbase = a.ix0 + X0 - R + g.cx_lo; // warp's first column - ox

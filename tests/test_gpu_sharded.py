@@ -198,3 +198,31 @@ def test_detect_multi_sharded_lattice_world1(ea, oracle, comm_ctx):
     wp = oracle.build_pyramid(img, 3)
     for t, a in zip(tmpls, got):
         assert a.key() == oracle.coarse_to_fine(oracle.build_pyramid(t, 3), wp, cfg).key()
+
+
+@pytest.mark.parametrize("k", [1, 5, 8])
+def test_blank_frame_async_and_sync(ea, k):
+    """A featureless 1280x1024 frame (every pose scores exactly 0):
+    the device-resident slab search no longer floods the band -- exact-zero
+    tiles contribute only their first k poses -- and returns the reference's
+    answer: the k smallest grid indices, score 0 (better: ties by index)."""
+    import torch
+    blank = np.full((1024, 1280), 117.0)
+    tmpl = ea.render_template("l_bracket", 200)
+    cfg = ea.SearchConfig(grid=ea.PoseGrid(0, 1279, 8, 0, 1023, 8, 0.0, D(359.5), D(0.5)),
+                          num_levels=4, score_params=ea.ScoreParams(3), topk=k)
+    det = ea.Detector(tmpl, cfg)
+    det.levels.set_image(blank)
+    rows = torch.empty((k, 5), dtype=torch.float64, device="cuda")
+    ea.search_top_slab_async(det.levels, cfg, 0, 720, rows.data_ptr())
+    overflowed, _ = ea.async_status(det.ctx)
+    assert not overflowed
+    got = parallel.unpack(rows.cpu().numpy())
+    tg = ea.PoseGrid(0, 1279 / 8, 1, 0, 1023 / 8, 1, 0.0, D(359.5), D(0.5))
+    want = [(0.0, i, ea.pose_at(tg, i).astuple()) for i in range(k)]
+    assert [(s.score, int(s.grid_index), s.pose.astuple()) for s in got] == want
+    sync = ea.search_top_slab(det.levels, cfg, 0, 720)
+    assert keys(sync) == keys(got)
+    assert det.ctx.stats()["candidates"] <= 720 * 10 * k  # k per zero tile, not every pose
+    out = det.detect(blank)
+    assert not out.found and out.score == 0.0
