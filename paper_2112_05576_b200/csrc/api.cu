@@ -745,9 +745,61 @@ unsigned long long initial_cap(ea_ctx* ctx) {
     return std::max<size_t>(ctx->cand.cap / sizeof(unsigned), 1u << 16);
 }
 
+// Grids larger than one screening launch takes (the candidate indices are
+// 32-bit and the fp32 map is 4 B/pose) are searched in theta chunks of at
+// most kChunkPoses poses whose top-k lists are `better`-merged -- the merge
+// is the reference's own (search.cpp:130-139), so the result is the same as
+// one pass; the reference indexes poses with size_t (search.cpp:105-106).
+constexpr uint64_t kChunkPoses = 1ull << 26;
+
+// Candidate buffer of a search whose overflow cannot be retried from the host
+// (device-resident and sharded searches): the whole slab when it has at most
+// 2^26 poses, so the band can never overflow; larger slabs keep 2^26 and
+// report an overflow (flag + an +inf row 0, see topk_rows_body).
+unsigned long long async_cap(ea_ctx* ctx, uint64_t slab_poses) {
+    return std::max<unsigned long long>(initial_cap(ctx),
+                                        std::min<uint64_t>(slab_poses, 1ull << 26));
+}
+
+std::vector<std::pair<uint64_t, uint64_t>> theta_chunks(const ea_grid_counts& c, uint64_t b,
+                                                        uint64_t e) {
+    const uint64_t plane = c.nx * c.ny;
+    if (plane >= (1ull << 32))
+        fail(EA_ERR_INVALID_ARGUMENT, "one theta of the pose grid exceeds 2^32 translations");
+    const uint64_t per = std::max<uint64_t>(1, kChunkPoses / std::max<uint64_t>(plane, 1));
+    std::vector<std::pair<uint64_t, uint64_t>> out;
+    for (uint64_t x = b; x < e; x += per) out.emplace_back(x, std::min(x + per, e));
+    return out;
+}
+
+std::vector<ea_scored_pose> top_search_one(ea_ctx* ctx, const ea_model* m, const ea_field* f,
+                                           const ea_pose_grid& g, const ea_score_params& p, int k,
+                                           uint64_t it_begin, uint64_t it_end);
+
 std::vector<ea_scored_pose> top_search(ea_ctx* ctx, const ea_model* m, const ea_field* f,
                                        const ea_pose_grid& g, const ea_score_params& p, int k,
                                        uint64_t it_begin, uint64_t it_end) {
+    const ea_grid_counts c = counts_of(g);
+    if (it_end == 0 || it_end > c.nt) it_end = c.nt;
+    if (it_begin > it_end) it_begin = it_end;
+    if ((it_end - it_begin) * c.nx * c.ny <= kChunkPoses)
+        return top_search_one(ctx, m, f, g, p, k, it_begin, it_end);
+    std::vector<ea_scored_pose> all;
+    for (const auto& ch : theta_chunks(c, it_begin, it_end)) {
+        const auto part = top_search_one(ctx, m, f, g, p, k, ch.first, ch.second);
+        all.insert(all.end(), part.begin(), part.end());
+    }
+    std::stable_sort(all.begin(), all.end(), [](const ea_scored_pose& x, const ea_scored_pose& y) {
+        if (x.score != y.score) return x.score > y.score;  // better: search.cpp:36-41
+        return x.grid_index < y.grid_index;
+    });
+    if ((int)all.size() > k) all.resize(k);
+    return all;
+}
+
+std::vector<ea_scored_pose> top_search_one(ea_ctx* ctx, const ea_model* m, const ea_field* f,
+                                           const ea_pose_grid& g, const ea_score_params& p, int k,
+                                           uint64_t it_begin, uint64_t it_end) {
     unsigned long long cap = initial_cap(ctx);
     for (int attempt = 0; attempt < 3; ++attempt) {
         const TopLaunch t = top_enqueue(ctx, m, f, g, p, k, it_begin, it_end, cap);
@@ -1236,8 +1288,27 @@ TopLaunch enqueue_levels(ea_ctx* ctx, const ea_levels* lv, const ea_search_confi
     const int k = cfg.topk;
     const ea_pose_grid tg = top_grid_of(cfg);
     const ea_grid_counts c = counts_of(tg);
-    const TopLaunch t = top_enqueue(ctx, lv->models[top], lv->fields[top], tg, cfg.score_params, k,
-                                    0, 0, cap);
+    TopLaunch t;
+    if (c.nx * c.ny * c.nt > kChunkPoses) {
+        // theta chunks (see kChunkPoses) merged on the device into the seeds;
+        // an overflowing chunk marks its row 0 +inf, which ranks first and
+        // surfaces as the outcome's top-level trace score (search_levels_device)
+        const auto chunks = theta_chunks(c, 0, c.nt);
+        const int n = (int)chunks.size() * k;
+        if (n > merge_rows_max(ctx))
+            fail(EA_ERR_INVALID_ARGUMENT, "pose grid too large for the chunk merge");
+        double* tmp = (double*)ctx->chunk_rows.ensure(5 * sizeof(double) * ((size_t)n + k));
+        for (size_t i = 0; i < chunks.size(); ++i) {
+            const uint64_t cp = c.nx * c.ny * (chunks[i].second - chunks[i].first);
+            t = top_enqueue(ctx, lv->models[top], lv->fields[top], tg, cfg.score_params, k,
+                            chunks[i].first, chunks[i].second, async_cap(ctx, cp),
+                            tmp + 5 * (size_t)k * i, nullptr);
+        }
+        launch_merge_rows(ctx, tmp, n, k, tmp + 5 * (size_t)n, t.top_score, t.top_index,
+                          &ctx->ctrl.as<SearchCtrl>()->n_out);
+    } else {
+        t = top_enqueue(ctx, lv->models[top], lv->fields[top], tg, cfg.score_params, k, 0, 0, cap);
+    }
     if (ctx->timing) EAB_CUDA(cudaEventRecord(ctx->ev[3], ctx->stream));
     RefineState st = refine_state(ctx, k);
     st.out = d_out;
@@ -1289,6 +1360,8 @@ void search_levels_device(ea_ctx* ctx, const ea_levels* lv, const ea_search_conf
         std::memcpy(&hc, h + sizeof(ea_outcome), sizeof hc);
         if (top_stats(ctx, t, hc)) {
             std::memcpy(out, h, sizeof(ea_outcome));
+            if (std::isinf(out->trace[0].score))  // a theta chunk overflowed (enqueue_levels)
+                fail(EA_ERR_INTERNAL, "candidate buffer overflow in a chunked search");
             return;
         }
         cap = hc.cand_count;  // band admitted more than the buffer: grow, redo
@@ -1302,7 +1375,10 @@ void detect_batch(ea_ctx* ctx, ea_levels* lv, const double* const* images, int c
                   int h, const ea_search_config& cfg, ea_outcome* outs) {
     const int L = cfg.num_levels;
     const double* tables = detect_tables(ctx, cfg);
-    if (L > 1 && !tables) {  // host-assisted refinement: no overlap, one by one
+    const ea_grid_counts gc0 = counts_of(top_grid_of(cfg));
+    if ((L > 1 && !tables) || gc0.nx * gc0.ny * gc0.nt > kChunkPoses) {
+        // host-assisted refinement, or a grid searched in theta chunks
+        // (search_levels_device): no overlap, one by one
         for (int i = 0; i < count; ++i) {
             set_working_image(ctx, lv, images[i], w, h, L);
             search_levels_device(ctx, lv, cfg, outs + i);
@@ -1695,15 +1771,6 @@ void theta_slab_of(uint64_t nt, int rank, int world, uint64_t* b, uint64_t* e) {
     *e = (uint64_t)((unsigned __int128)nt * (unsigned)(rank + 1) / (unsigned)world);
 }
 
-// Candidate buffer of a search whose overflow cannot be retried from the host
-// (device-resident and sharded searches): the whole slab when it has at most
-// 2^26 poses, so the band can never overflow; larger slabs keep 2^26 and
-// report an overflow (flag + an +inf row 0, see topk_rows_body).
-unsigned long long async_cap(ea_ctx* ctx, uint64_t slab_poses) {
-    return std::max<unsigned long long>(initial_cap(ctx),
-                                        std::min<uint64_t>(slab_poses, 1ull << 26));
-}
-
 // Sub-buffers of ctx->shard for k rows on `world` ranks.
 struct ShardBufs {
     double* local;      // k rows of this rank's slab
@@ -1759,6 +1826,20 @@ void slab_rows(ea_ctx* ctx, const ea_model* m, const ea_field* f, const ea_pose_
     const ea_grid_counts c = counts_of(tg);
     const uint64_t b = std::min(it_begin, c.nt), e = std::min(it_end, c.nt);
     const uint64_t poses = e > b ? c.nx * c.ny * (e - b) : 0;
+    if (poses > kChunkPoses) {  // theta chunks, rows merged on the device
+        const auto chunks = theta_chunks(c, b, e);
+        const int n = (int)chunks.size() * k;
+        if (n > merge_rows_max(ctx))
+            fail(EA_ERR_INVALID_ARGUMENT, "pose grid too large for the chunk merge");
+        double* tmp = (double*)ctx->chunk_rows.ensure(5 * sizeof(double) * (size_t)n);
+        for (size_t i = 0; i < chunks.size(); ++i) {
+            const uint64_t cp = c.nx * c.ny * (chunks[i].second - chunks[i].first);
+            top_enqueue(ctx, m, f, tg, p, k, chunks[i].first, chunks[i].second, async_cap(ctx, cp),
+                        tmp + 5 * (size_t)k * i, flag);
+        }
+        launch_merge_rows(ctx, tmp, n, k, d_rows);
+        return;
+    }
     const unsigned long long cap = async_cap(ctx, poses);
     if (poses > 0) {
         top_enqueue(ctx, m, f, tg, p, k, b, e, cap, d_rows, flag);
@@ -2118,7 +2199,7 @@ void ea_ctx_destroy(ea_ctx* ctx) {
                       &ctx->hist, &ctx->ctrl, &ctx->cand, &ctx->cand_score, &ctx->topk,
                       &ctx->refine_poses, &ctx->refine_scores, &ctx->beam, &ctx->accum64,
                       &ctx->work, &ctx->ttab, &ctx->rstate, &ctx->rslots, &ctx->mscratch,
-                      &ctx->cta_top, &ctx->ztiles})
+                      &ctx->cta_top, &ctx->ztiles, &ctx->chunk_rows})
         b->release();
     ctx->h_stage.release();
     ctx->h_out.release();

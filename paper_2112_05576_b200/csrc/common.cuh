@@ -165,7 +165,7 @@ struct ea_ctx {
     cudaEvent_t ev[8] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
     // scratch
     eab::DevBuf cs, rot_exact, rot_screen, plane, map, item_max, tail, hist, ctrl, cand, cand_score, topk,
-        refine_poses, refine_scores, beam, accum64, work, mscratch, cta_top, ztiles;
+        refine_poses, refine_scores, beam, accum64, work, mscratch, cta_top, ztiles, chunk_rows;
     std::vector<double> ztiles_key;  // what ztiles holds (see screen(), api.cu)
     eab::HostBuf h_stage, h_out;
     // glibc cos/sin tables of theta grids, cached per (t0, dt, nt)

@@ -226,3 +226,34 @@ def test_blank_frame_async_and_sync(ea, k):
     assert det.ctx.stats()["candidates"] <= 720 * 10 * k  # k per zero tile, not every pose
     out = det.detect(blank)
     assert not out.found and out.score == 0.0
+
+
+@pytest.mark.slow
+def test_grid_over_2_32_poses_chunked(ea, oracle):
+    """A pose grid of more than 2^32 poses (the reference indexes poses with
+    size_t, search.cpp:105-106): searched in theta chunks whose top-k lists
+    are `better`-merged.  The sync search, the device-resident slab rows and
+    the detect path agree with each other and with the merge of explicit
+    sub-slab searches; the returned scores are the oracle's pose scores."""
+    import torch
+    rng = np.random.default_rng(42)
+    img = rng.integers(0, 256, size=(72, 72)).astype(np.float64)
+    f = oracle.compute_gradients(img)
+    m = oracle.extract_edge_model(oracle.compute_gradients(
+        rng.integers(0, 256, size=(6, 6)).astype(np.float64)), (0.0, 0.0), 0)
+    nt = (2 ** 32) // (64 * 64) + 50_000  # > 2^32 poses
+    dt = 2e-6
+    grid = ea.PoseGrid(4, 67, 1, 4, 67, 1, 0.0, (nt - 1) * dt, dt)
+    nx, ny, ntt = ea.grid_counts(grid)
+    assert nx * ny * ntt > 2 ** 32
+    params = ea.ScoreParams(3)
+    k = 5
+    full = ea.search_topk(m, f, grid, params, k=k)
+    cuts = [0, 300_001, 700_000, ntt // 2 + 17, ntt]
+    parts = []
+    for a, b in zip(cuts, cuts[1:]):
+        parts += ea.search_topk_slab(m, f, grid, params, k, a, b)
+    assert keys(full) == keys(ea.merge_topk(parts, k))
+    for s in full:
+        want, _ = oracle.pose_score(m.points, s.pose.astuple(), f, params)
+        assert s.score == want
