@@ -337,13 +337,18 @@ ScreenPlan screen(ea_ctx* ctx, const ea_model* m, const ea_field* f, const ea_po
     const size_t nth = plan.it_count;
     const size_t slab_pairs = nth * (size_t)n;
     ea_model* mm = const_cast<ea_model*>(m);
-    const std::vector<double> key{g.t0, g.dt, (double)plan.c.nt, (double)it_begin, (double)nth};
+    // (R: twins in the schedule only for R <= 1)
+    const std::vector<double> key{g.t0, g.dt, (double)plan.c.nt, (double)it_begin, (double)nth,
+                                  (double)std::min(R, 2)};
     double* rot = (double*)mm->rot.ensure(sizeof(double) * 4 * (slab_pairs ? slab_pairs : 1));
     int4* scr = (int4*)mm->scr.ensure(sizeof(int4) * (slab_pairs ? slab_pairs : 1));
     // per-theta ambiguous-point counts, the flagged-theta list (ScreenArgs::amb)
     // and, in the last slot, the total of ambiguous pairs
-    int* amb = (int*)mm->amb.ensure(sizeof(int) * (2 * nth + 3));
-    int4* sched = (int4*)mm->sched.ensure(sizeof(int4) * (nth ? nth : 1) * (1 + 2 * (size_t)n));
+    // (+ a 64-bit count of twinned points for the schedule mode, 8-aligned)
+    const size_t amb_words = 2 * nth + 3, tw_off = (amb_words + 1) & ~(size_t)1;
+    int* amb = (int*)mm->amb.ensure(sizeof(int) * tw_off + sizeof(unsigned long long));
+    unsigned long long* twinned = reinterpret_cast<unsigned long long*>(amb + tw_off);
+    int4* sched = (int4*)mm->sched.ensure(sizeof(int4) * (nth ? nth : 1) * sched_stride(n));
     if (key != mm->tab_key) {
         mm->tab_key.clear();
         double* d_cs = (double*)ctx->cs.ensure(sizeof(double) * 2 * (nth ? nth : 1));
@@ -353,15 +358,27 @@ ScreenPlan screen(ea_ctx* ctx, const ea_model* m, const ea_field* f, const ea_po
             h2d_staged(ctx, d_cs, cs_all.data() + 2 * it_begin, sizeof(double) * 2 * nth);
             ctx->cs_dev_key = key;
         }
-        EAB_CUDA(cudaMemsetAsync(amb, 0, sizeof(int) * (2 * nth + 3), ctx->stream));
+        EAB_CUDA(cudaMemsetAsync(amb, 0, sizeof(int) * tw_off + sizeof(unsigned long long),
+                                 ctx->stream));
         launch_rotate(ctx, m->pts.as<double>(), n, d_cs, (int)nth, rot, scr, amb + 2 * nth + 2,
                       amb);
-        launch_schedule(ctx, scr, n, (int)nth, sched);
+        // Schedule mode: twins (mode 1) when R <= 1, unless fewer than a fifth
+        // of the points pair up as twins (round templates) -- then pairs.
+        static const bool no_twins = std::getenv("EAB_NO_TWINS") != nullptr;
+        int mode = (R <= 1 && !no_twins) ? 1 : 0;
+        launch_schedule(ctx, scr, n, (int)nth, sched, mode, twinned);
         // once per model and slab: does any theta need the general kernel?
         int n_flagged = 0;
+        unsigned long long n_twinned = 0;
         d2h(ctx, &n_flagged, amb + nth, sizeof n_flagged);
+        d2h(ctx, &n_twinned, twinned, sizeof n_twinned);
         sync(ctx);
+        if (mode == 1 && n_twinned * 5 < (unsigned long long)nth * n) {
+            mode = 0;
+            launch_schedule(ctx, scr, n, (int)nth, sched, mode, nullptr);
+        }
         mm->n_flagged = n_flagged;
+        mm->sched_mode = mode;
         mm->tab_key = key;
     }
     SearchCtrl* ctrl = (SearchCtrl*)ctx->ctrl.ensure(sizeof(SearchCtrl));
@@ -430,7 +447,19 @@ ScreenPlan screen(ea_ctx* ctx, const ea_model* m, const ea_field* f, const ea_po
         edge = PL < PL0 || PR < PR0;
         if (region) PL = PR = 0;  // halo regions are zero-filled instead
     }
-    const PlaneGeom geom = plane_geom(f->width, f->height, shift, PL, PR, elem);
+    PlaneGeom geom = plane_geom(f->width, f->height, shift, PL, PR, elem);
+    // Twin schedules run 4-row lane strips (32 accumulators, 16 warps per SM,
+    // half the unrolled body per entry kind): with 8-row strips the twin
+    // kernel's bodies overflowed the instruction cache (no_instructions 23%
+    // of stall samples, IPC 2.05); with 4-row strips the cache holds them
+    // (IPC 2.53) and shared-memory bandwidth binds (L1 94%).  Measured on
+    // B200: cfg3 screen 0.636 -> 0.617 ms, cfg2 0.430 -> 0.402, cfg1 0.275 ->
+    // 0.253 against 8-row pair schedules.  EAB_S8=1 keeps 8-row strips.
+    static const bool s8 = std::getenv("EAB_S8") != nullptr;
+    if (!s8 && mm->sched_mode == 1 && lattice && !region && !edge && R <= 1) {
+        const PlaneGeom g4 = plane_geom(f->width, f->height, 2, PL, PR, elem);
+        if (fast_smem_bytes(g4) <= ctx->smem_optin) geom = g4;
+    }
     void* plane = ctx->plane.ensure(geom.bytes());
     // The plane is a function of the image (field), eps and the geometry:
     // rebuilt only when one of them changed.  Its kernel also clears the
@@ -475,6 +504,7 @@ ScreenPlan screen(ea_ctx* ctx, const ea_model* m, const ea_field* f, const ea_po
     a.ignore = p.polarity == EA_POLARITY_IGNORE;
     a.xg = xg;
     a.sched = sched;
+    a.sched_mode = mm->sched_mode;
     a.ro = ro_int;
     a.edge = edge ? 1 : 0;
     a.amb = amb;
@@ -485,7 +515,7 @@ ScreenPlan screen(ea_ctx* ctx, const ea_model* m, const ea_field* f, const ea_po
     // a featureless frame no longer floods the band with every pose (only the
     // first k poses of each zero tile can rank; finish_tile).
     if (lattice && !region && plan.slab_poses) {
-        const int tw = 8 * xg, th = (32 / xg) * 8;
+        const int tw = 8 * xg, th = (32 / xg) * (geom.shift == 2 ? 4 : 8);
         const unsigned nwx = (unsigned)((plan.c.nx + tw - 1) / tw);
         const unsigned nwy = (unsigned)((plan.c.ny + th - 1) / th);
         const int halo = ro_int + R;

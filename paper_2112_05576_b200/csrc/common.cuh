@@ -114,6 +114,7 @@ struct ea_model {
     std::vector<double> tab_key;
     eab::DevBuf rot, scr, amb, sched;
     int n_flagged = 0;  // flagged thetas of the cached slab
+    int sched_mode = 0;  // entry kinds of the cached schedule (launch_schedule)
 };
 
 struct ea_levels {

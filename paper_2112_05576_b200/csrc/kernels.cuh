@@ -210,9 +210,14 @@ void launch_plane(ea_ctx* ctx, const ea_field* f, double eps, const PlaneGeom& g
 // count and the list of thetas that have any (AmbList); flags: their total.
 void launch_rotate(ea_ctx* ctx, const double* pts_soa, int n, const double* cs, int nth,
                    double* rot_exact, int4* rot_screen, int* flags, int* amb = nullptr);
-// Lattice point schedule per theta: points sorted by (oy, ox), same-row
-// neighbours paired (see search_kernels.cu).  sched: nth x (1 + 2n) int4.
-void launch_schedule(ea_ctx* ctx, const int4* rot_screen, int n, int nth, int4* sched);
+// Lattice point schedule per theta: points sorted by (oy, ox) and combined
+// into entries -- mode 0: same-row neighbour pairs; mode 1: twins (same
+// direction, offsets (1,0) / (0,1); R <= 1) -- see search_kernels.cu.
+// sched: nth x sched_stride(n) int4.  twinned (mode 1, optional): += points
+// in twin entries.
+__host__ __device__ inline size_t sched_stride(size_t n) { return 1 + 2 * n; }
+void launch_schedule(ea_ctx* ctx, const int4* rot_screen, int n, int nth, int4* sched, int mode,
+                     unsigned long long* twinned);
 
 struct ScreenArgs {
     const void* plane;        // float2 or __half2 elements (geom.elem_bytes)
@@ -231,6 +236,7 @@ struct ScreenArgs {
     int R;
     int ignore;
     int xg;           // lattice warp tile: xg * 8 columns x (32 / xg) * 8 rows
+    int sched_mode;   // schedule entry kinds: 0 singles/pairs, 1 singles/twins (launch_schedule)
     int ro;           // region kernel: bound on |lattice offset| of every rotated point
     int edge;         // smem kernel: zero columns shrunk to fit, windows may need clamping
     // Thetas with a rounding-ambiguous lattice offset (amb[it] > 0) are left

@@ -356,26 +356,127 @@ __device__ __forceinline__ void point_rows(const float2* __restrict__ P, const i
     }
 }
 
+// A twin entry (two points with the same screening direction whose lattice
+// offsets differ by (0,0): TW = 1, (1,0): TW = 2, (0,1): TW = 3) over a
+// lane's 8 x S pose block: one candidate per pixel of the union window, one
+// horizontal max per union column and one vertical max per union row serve
+// both points; the second point's votes are the first's shifted by the
+// offset, so acc += bits(V[s][j]) + bits(V[s + DY][j + DX]) (IADD3).  R <= 1
+// (the zero ring stands in for the window-centre masks).
+template <int R, int S, int SHIFT, bool IGNORE, bool CLAMP, bool STRIP, int TW>
+__device__ __forceinline__ void twin_rows(const float2* __restrict__ P, const int PW,
+                                          const int XL, const int H1, const int Z, const int cb,
+                                          const int rb, const float dx, const float dy,
+                                          const float K, unsigned (&acc)[S][kTW]) {
+    static_assert(R <= 1, "twins need the zero ring (R <= 1)");
+    constexpr int DX = TW == 2 ? 1 : 0, DY = TW == 3 ? 1 : 0;
+    constexpr int NC = kTW + 2 * R + DX;  // union columns
+    constexpr int NH = kTW + DX;          // horizontal maxima (window starts)
+    constexpr int NR = S + 2 * R + DY;    // union rows
+    constexpr int HP = 2 * R > 0 ? 2 * R : 1;
+    int col[CLAMP ? NC : 1];
+    if constexpr (CLAMP) {
+#pragma unroll
+        for (int m = 0; m < NC; ++m) col[m] = min(max(cb + m, 0), XL);
+    }
+    float hprev[HP][NH];
+    float vprev[DY ? kTW : 1];
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+        constexpr int kBankMask = 128 / (int)sizeof(float2) - 1;
+        const int yv = rb + r;
+        const int va = yv * PW + (yv >> SHIFT);
+        const float2* row = P + (!STRIP || (unsigned)yv <= (unsigned)H1 ? va : Z + (va & kBankMask));
+        if constexpr (!CLAMP) row += cb;
+        float c[NC];
+#pragma unroll
+        for (int m = 0; m < NC; ++m) {
+            const float2 v = CLAMP ? row[col[m]] : row[m];
+            if constexpr (IGNORE) c[m] = fabsf(fmaf(dy, v.y, dx * v.x));
+            else c[m] = fmaf(dy, v.y, fmaf(dx, v.x, K));
+        }
+        float h[NH];
+#pragma unroll
+        for (int j = 0; j < NH; ++j) h[j] = max_run<2 * R + 1>(c + j);
+        if (r >= 2 * R) {
+            const int q = r - 2 * R;  // union output row
+            float V[NH];
+#pragma unroll
+            for (int j = 0; j < NH; ++j) {
+                float cv[2 * R + 1];
+#pragma unroll
+                for (int t = 0; t < 2 * R; ++t) cv[t] = hprev[t][j];
+                cv[2 * R] = h[j];
+                V[j] = max_run<2 * R + 1>(cv);
+                if constexpr (IGNORE) V[j] = V[j] + K;
+            }
+            if constexpr (TW == 1) {
+#pragma unroll
+                for (int j = 0; j < kTW; ++j)
+                    acc[q][j] += __float_as_uint(V[j]) + __float_as_uint(V[j]);
+            } else if constexpr (TW == 2) {
+#pragma unroll
+                for (int j = 0; j < kTW; ++j)
+                    acc[q][j] += __float_as_uint(V[j]) + __float_as_uint(V[j + 1]);
+            } else {
+                if (q >= 1) {
+#pragma unroll
+                    for (int j = 0; j < kTW; ++j)
+                        acc[q - 1][j] += __float_as_uint(vprev[j]) + __float_as_uint(V[j]);
+                }
+#pragma unroll
+                for (int j = 0; j < kTW; ++j) vprev[j] = V[j];
+            }
+        }
+        if constexpr (R > 0) {
+#pragma unroll
+            for (int t = 0; t + 1 < 2 * R; ++t)
+#pragma unroll
+                for (int j = 0; j < NH; ++j) hprev[t][j] = hprev[t + 1][j];
+#pragma unroll
+            for (int j = 0; j < NH; ++j) hprev[2 * R - 1][j] = h[j];
+        }
+    }
+}
+
 // ---- point schedule ------------------------------------------------------------
 // Per theta, the lattice kernels walk a schedule instead of the raw point
-// list: points sorted by (oy, ox) and paired greedily when they share a
-// lattice row and their windows start at most kMaxPairDx columns apart.
-// Layout per theta (stride 1 + 2n int4): header {singles, pairs dx=0, pairs
-// dx=1, 0}, then 2 int4 per entry {ox, oy, dxf, dyf} x {second point or
-// unused}, singles first, then pairs by dx.  The sum over points is integer and
+// list.  Points are sorted by (oy, ox) and combined into entries of one of
+// three kinds; which three is the schedule's mode (each mode is its own
+// kernel instantiation: a kernel that unrolls more bodies than three
+// overflows the instruction cache -- six bodies measured IPC 2.51 -> 1.87,
+// no_instructions stalls 4% -> 28%):
+//  * mode 0 (pairs): singles; same-row neighbours whose windows start 0 or 1
+//    column apart, sharing their window loads;
+//  * mode 1 (twins): singles; two points with the SAME screening direction
+//    (fp32 dx, dy bit patterns) whose lattice offsets differ by (1,0) or
+//    (0,1) -- points along a straight template edge rotate to identical
+//    directions -- sharing their candidates (one dot product per pixel for
+//    both) and their horizontal and vertical window maxima (the second
+//    point's windows are the first's shifted): ~4.3 instructions per
+//    pose-eval instead of ~7.9.  R <= 1 only (the R >= 2 centre masks are
+//    per point).
+// The host builds mode 1 when R <= 1 and switches to mode 0 when fewer than
+// a fifth of the points are twinned (round templates).  Layout per theta
+// (stride sched_stride(n) = 1 + 2n int4): header {kind-0, kind-1, kind-2
+// counts, 0}, then 2 int4 per entry {ox, oy, dxf, dyf} x {second point of a
+// pair, or unused}, in kind order.  The sum over points is integer and
 // order-free, so the schedule does not change a score.
 constexpr int kMaxPairDx = 1;  // dx = 2 pairs: a fourth unrolled body, net loss (icache)
 constexpr int kPairMaxN = 1024;  // larger models: singles only
 
 __global__ void __launch_bounds__(256) schedule_kernel(const int4* __restrict__ scr, int n,
                                                        int4* __restrict__ sched, int dmin,
-                                                       int dmax) {
+                                                       int dmax, int mode,
+                                                       unsigned long long* __restrict__ twinned) {
     const int th = blockIdx.x;
     const int4* pts = scr + (size_t)th * n;
-    int4* out = sched + (size_t)th * (1 + 2 * (size_t)n);
+    int4* out = sched + (size_t)th * sched_stride(n);
     __shared__ int4 sp[kPairMaxN];       // the theta's points
     __shared__ short order[kPairMaxN];   // sorted position -> point
-    __shared__ short slot[kPairMaxN];    // sorted position -> output entry (-1: second of a pair)
+    __shared__ short part[kPairMaxN];    // sorted position -> partner position (-1: none)
+    __shared__ unsigned char kind[kPairMaxN];  // entry kind at the first position; 255: second
+    __shared__ short slot[kPairMaxN];    // sorted position -> output entry
     if (n > kPairMaxN) {
         if (threadIdx.x == 0) out[0] = make_int4(n, 0, 0, 0);
         for (int i = threadIdx.x; i < n; i += blockDim.x) out[1 + 2 * i] = __ldg(pts + i);
@@ -393,45 +494,90 @@ __global__ void __launch_bounds__(256) schedule_kernel(const int4* __restrict__ 
         }
         order[rank] = (short)i;
     }
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        part[i] = -1;
+        kind[i] = 0;
+    }
     __syncthreads();
-    if (threadIdx.x == 0) {  // greedy pairing along the sorted list, then output slots
-        int c[3] = {0, 0, 0};
-        for (int i = 0; i < n;) {
-            const int4 a = sp[order[i]];
-            int kind = 0;
-            if (i + 1 < n) {
-                const int4 b = sp[order[i + 1]];
-                const int d = b.x - a.x;
-                if (b.y == a.y && d >= dmin && d <= dmax) kind = 1 + d;
+    if (threadIdx.x == 0) {
+        if (mode == 1) {
+            // twins, greedily along the sorted list: (1,0) first (just after
+            // i on its row), then (0,1) (binary search of the next row)
+            for (int i = 0; i < n; ++i) {
+                if (part[i] >= 0 || kind[i] == 255) continue;
+                const int4 a = sp[order[i]];
+                int mate = -1, k = 0;
+                for (int j = i + 1; j < n; ++j) {
+                    const int4 b = sp[order[j]];
+                    if (b.y != a.y || b.x > a.x + 1) break;
+                    if (b.x != a.x + 1 || part[j] >= 0 || kind[j] == 255 || b.z != a.z ||
+                        b.w != a.w)
+                        continue;
+                    mate = j;
+                    k = 1;
+                    break;
+                }
+                if (mate < 0) {  // (0, 1): lower bound of (a.y + 1, a.x)
+                    int lo = i + 1, hi = n;
+                    while (lo < hi) {
+                        const int mid = (lo + hi) >> 1;
+                        const int4 b = sp[order[mid]];
+                        if (b.y < a.y + 1 || (b.y == a.y + 1 && b.x < a.x)) lo = mid + 1;
+                        else hi = mid;
+                    }
+                    for (int j = lo; j < n; ++j) {
+                        const int4 b = sp[order[j]];
+                        if (b.y != a.y + 1 || b.x != a.x) break;
+                        if (part[j] >= 0 || kind[j] == 255 || b.z != a.z || b.w != a.w) continue;
+                        mate = j;
+                        k = 2;
+                        break;
+                    }
+                }
+                if (mate >= 0) {
+                    part[i] = (short)mate;
+                    kind[i] = (unsigned char)k;
+                    kind[mate] = 255;
+                }
             }
-            slot[i] = (short)(kind << 12);  // type now, entry index below
-            if (kind) slot[i + 1] = -1;
-            ++c[kind];
-            i += kind ? 2 : 1;
+        } else {
+            // pairs: consecutive points of one row, windows dmin..dmax apart
+            for (int i = 0; i + 1 < n;) {
+                const int4 a = sp[order[i]], b = sp[order[i + 1]];
+                const int d = b.x - a.x;
+                if (b.y == a.y && d >= dmin && d <= dmax) {
+                    part[i] = (short)(i + 1);
+                    kind[i] = (unsigned char)(1 + d);
+                    kind[i + 1] = 255;
+                    i += 2;
+                } else {
+                    ++i;
+                }
+            }
         }
+        int c[3] = {0, 0, 0};
+        for (int i = 0; i < n; ++i)
+            if (kind[i] != 255) ++c[kind[i]];
         int cur[3] = {0, c[0], c[0] + c[1]};
-        for (int i = 0; i < n; ++i) {
-            if (slot[i] < 0) continue;
-            const int kind = slot[i] >> 12;
-            slot[i] = (short)(cur[kind]++ | (kind ? 0x4000 : 0));
-        }
+        for (int i = 0; i < n; ++i) slot[i] = kind[i] == 255 ? (short)-1 : (short)cur[kind[i]]++;
         out[0] = make_int4(c[0], c[1], c[2], 0);
+        if (twinned && mode == 1) atomicAdd(twinned, 2ull * (unsigned long long)(c[1] + c[2]));
     }
     __syncthreads();
     for (int i = threadIdx.x; i < n; i += blockDim.x) {  // scatter the entries
-        const int sl = slot[i];
-        if (sl < 0) continue;
-        const int e = sl & 0x3fff;
+        const int e = slot[i];
+        if (e < 0) continue;
         out[1 + 2 * e] = sp[order[i]];
-        if (sl & 0x4000) out[2 + 2 * e] = sp[order[i + 1]];
+        if (part[i] >= 0) out[2 + 2 * e] = sp[order[part[i]]];
     }
 }
 
-void launch_schedule(ea_ctx* ctx, const int4* scr, int n, int nth, int4* sched) {
+void launch_schedule(ea_ctx* ctx, const int4* scr, int n, int nth, int4* sched, int mode,
+                     unsigned long long* twinned) {
     if (nth == 0 || n == 0) return;
     // EAB_NO_PAIRS=1: singles only (A/B measurements)
     static const int dmax = std::getenv("EAB_NO_PAIRS") ? -1 : kMaxPairDx;
-    schedule_kernel<<<nth, 256, 0, ctx->stream>>>(scr, n, sched, 0, dmax);
+    schedule_kernel<<<nth, 256, 0, ctx->stream>>>(scr, n, sched, 0, dmax, mode, twinned);
     check_launch("schedule_kernel");
     count_launch(ctx);
 }
@@ -466,12 +612,32 @@ __device__ __forceinline__ void one_entry(const LaneGeom& g, const int4 p, const
                                                            dx1, dy1, dx2, dy2, K, acc);
 }
 
-// One lane block over schedule entries [e0, e1): singles, then pairs by dx.
+template <int R, int S, int SHIFT, bool IGNORE, bool EDGE, bool STRIP, int TW>
+__device__ __forceinline__ void twin_entry(const LaneGeom& g, const int4 p, const float K,
+                                           unsigned (&acc)[S][kTW]) {
+    const float dx = __int_as_float(p.z), dy = __int_as_float(p.w);
+    const int cb = p.x + g.cbase, rb = p.y + g.rbase;
+    constexpr int NC = kTW + 2 * R + (TW == 2 ? 1 : 0);
+    if constexpr (EDGE) {
+        const int cw = p.x + g.cwbase;  // warp-uniform
+        if (!(cw >= 0 && cw + g.wspan + NC - 1 <= g.XL)) {
+            twin_rows<R, S, SHIFT, IGNORE, true, STRIP, TW>(g.P, g.PW, g.XL, g.H1, g.Z, cb, rb,
+                                                           dx, dy, K, acc);
+            return;
+        }
+    }
+    twin_rows<R, S, SHIFT, IGNORE, false, STRIP, TW>(g.P, g.PW, g.XL, g.H1, g.Z, cb, rb, dx, dy,
+                                                    K, acc);
+}
+
+// One lane block over schedule entries [e0, e1): singles, pairs by dx, then
+// twins by offset (entry kinds in schedule order).
 // Returns the number of model points processed (for the bits(K) correction).
-template <int R, int S, int SHIFT, bool IGNORE, bool EDGE, bool STRIP>
+template <int R, int S, int SHIFT, bool IGNORE, bool EDGE, bool STRIP, int MODE>
 __device__ __forceinline__ int run_entries(const int4* __restrict__ ent, const int4 hdr, int e0,
                                            int e1, const LaneGeom& g, const float K,
                                            unsigned (&acc)[S][kTW]) {
+    static_assert(MODE == 0 || R <= 1, "twin schedules need R <= 1");
     int done = 0;
     int lo = 0;
     const int bounds[3] = {hdr.x, hdr.y, hdr.z};
@@ -480,28 +646,6 @@ __device__ __forceinline__ int run_entries(const int4* __restrict__ ent, const i
     for (int t = 0; t < 3; ++t) {
         const int hi = lo + bounds[t];
         const int b = max(lo, e0), e = min(hi, e1);
-#ifdef EAB_ENTRY_PREFETCH
-        if (b < e) {
-            int4 p = __ldg(ent + 2 * b), q = __ldg(ent + 2 * b + 1);
-            for (int i = b; i < e; ++i) {
-                // prefetch the next entry: its loads overlap this entry's rows
-                const int in = i + 1 < e ? i + 1 : i;
-                const int4 pn = __ldg(ent + 2 * in);
-                const int4 qn = t == 0 ? q : __ldg(ent + 2 * in + 1);
-                if (t == 0) {
-                    one_entry<R, S, SHIFT, IGNORE, EDGE, STRIP, 1, 0>(g, p, 0.f, 0.f, K, acc);
-                } else {
-                    const float dx2 = __int_as_float(q.z), dy2 = __int_as_float(q.w);
-                    if (t == 1)
-                        one_entry<R, S, SHIFT, IGNORE, EDGE, STRIP, 2, 0>(g, p, dx2, dy2, K, acc);
-                    else
-                        one_entry<R, S, SHIFT, IGNORE, EDGE, STRIP, 2, 1>(g, p, dx2, dy2, K, acc);
-                }
-                p = pn;
-                q = qn;
-            }
-        }
-#else
         // Entries arrive 32 at a time, one per lane, and are broadcast by
         // shuffles: no global load sits inside the row loop (a per-entry
         // prefetch shared a scoreboard with the shared-memory loads and
@@ -511,7 +655,7 @@ __device__ __forceinline__ int run_entries(const int4* __restrict__ ent, const i
             int4 pl = make_int4(0, 0, 0, 0), ql = make_int4(0, 0, 0, 0);
             if (mine < e) {
                 pl = __ldg(ent + 2 * mine);
-                if (t != 0) ql = __ldg(ent + 2 * mine + 1);
+                if (MODE == 0 && t != 0) ql = __ldg(ent + 2 * mine + 1);
             }
             const int cnt = min(32, e - base);
             for (int j = 0; j < cnt; ++j) {
@@ -522,17 +666,21 @@ __device__ __forceinline__ int run_entries(const int4* __restrict__ ent, const i
                 p.w = __shfl_sync(0xffffffffu, pl.w, j);
                 if (t == 0) {
                     one_entry<R, S, SHIFT, IGNORE, EDGE, STRIP, 1, 0>(g, p, 0.f, 0.f, K, acc);
-                } else {
+                } else if constexpr (MODE == 0) {
                     const float dx2 = __int_as_float(__shfl_sync(0xffffffffu, ql.z, j));
                     const float dy2 = __int_as_float(__shfl_sync(0xffffffffu, ql.w, j));
                     if (t == 1)
                         one_entry<R, S, SHIFT, IGNORE, EDGE, STRIP, 2, 0>(g, p, dx2, dy2, K, acc);
                     else
                         one_entry<R, S, SHIFT, IGNORE, EDGE, STRIP, 2, 1>(g, p, dx2, dy2, K, acc);
+                } else if constexpr (R <= 1) {
+                    if (t == 1)
+                        twin_entry<R, S, SHIFT, IGNORE, EDGE, STRIP, 2>(g, p, K, acc);
+                    else
+                        twin_entry<R, S, SHIFT, IGNORE, EDGE, STRIP, 3>(g, p, K, acc);
                 }
             }
         }
-#endif
         if (e > b) done += (e - b) * (t == 0 ? 1 : 2);
         lo = hi;
     }
@@ -749,7 +897,7 @@ struct RegionPlan {
 #endif
 constexpr int kGroup = EAB_REGION_WARPS;  // thetas per CTA item (= warps per CTA)
 
-template <int R, int S, int SHIFT, bool IGNORE, int XG>
+template <int R, int S, int SHIFT, bool IGNORE, int XG, int MODE>
 __global__ void __launch_bounds__(kGroup * 32, 1)
     screen_region_kernel(const ScreenArgs a, const unsigned nwx, const unsigned nwy,
                          const RegionPlan rp) {
@@ -821,7 +969,7 @@ __global__ void __launch_bounds__(kGroup * 32, 1)
         lg.ry_lo = 1 - R0;
         lg.ry_hi = a.geom.H - R0;
         lg.cwbase = lg.wspan = 0;
-        const int4* sch = a.sched + itr * (1 + 2 * (size_t)a.n);
+        const int4* sch = a.sched + itr * sched_stride(a.n);
         const int4 hdr = __ldg(sch);
 
         unsigned uacc[S][kTW];
@@ -829,8 +977,8 @@ __global__ void __launch_bounds__(kGroup * 32, 1)
         for (int s = 0; s < S; ++s)
 #pragma unroll
             for (int j = 0; j < kTW; ++j) uacc[s][j] = 0u;
-        const int done = run_entries<R, S, SHIFT, IGNORE, false, false>(
-            sch + 1, hdr, 0, hdr.x + hdr.y + hdr.z + hdr.w, lg, K, uacc);
+        const int done = run_entries<R, S, SHIFT, IGNORE, false, false, MODE>(
+            sch + 1, hdr, 0, hdr.x + hdr.y + hdr.z, lg, K, uacc);
         int acc[S][kTW];
         const unsigned corr = (unsigned)done * a.B3;
 #pragma unroll
@@ -862,7 +1010,7 @@ static size_t region_smem(const RegionPlan& rp) {
     return kHistBins * sizeof(unsigned) + (size_t)rp.elems16 * 16;
 }
 
-template <int R, bool IGNORE, int XG>
+template <int R, bool IGNORE, int XG, int MODE>
 static void run_region(ea_ctx* ctx, const ScreenArgs& a, RegionPlan rp) {
     constexpr int S = 8, YG = 32 / XG;
     const unsigned nwx = (unsigned)((a.nx + 8 * XG - 1) / (8 * XG));
@@ -870,7 +1018,7 @@ static void run_region(ea_ctx* ctx, const ScreenArgs& a, RegionPlan rp) {
     rp.groups = (unsigned)((a.it_count + kGroup - 1) / kGroup);
     rp.n_items = (unsigned long long)nwx * nwy * rp.groups;
     const size_t smem = region_smem(rp);
-    auto kern = screen_region_kernel<R, S, 3, IGNORE, XG>;
+    auto kern = screen_region_kernel<R, S, 3, IGNORE, XG, MODE>;
     EAB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     unsigned long long ctas = std::min<unsigned long long>(rp.n_items, (unsigned)ctx->sm_count);
     if (ctas == 0) ctas = 1;
@@ -881,24 +1029,35 @@ static void run_region(ea_ctx* ctx, const ScreenArgs& a, RegionPlan rp) {
 
 bool launch_screen_region(ea_ctx* ctx, const ScreenArgs& a) {
     if (a.geom.shift != 3 || a.geom.elem_bytes != 8 || a.R > 2) return false;
+    if (a.sched_mode == 1 && a.R > 1) return false;
     const RegionPlan rp = region_plan(a, a.R);
     if (region_smem(rp) > ctx->smem_optin) return false;
     const bool ig = a.ignore != 0;
+#define EAB_REGION_M(RR, MM)                                                    \
+    if (a.xg == 2) {                                                            \
+        if (ig) run_region<RR, true, 2, MM>(ctx, a, rp);                        \
+        else run_region<RR, false, 2, MM>(ctx, a, rp);                          \
+    } else {                                                                    \
+        if (ig) run_region<RR, true, 4, MM>(ctx, a, rp);                        \
+        else run_region<RR, false, 4, MM>(ctx, a, rp);                          \
+    }
 #define EAB_REGION(RR)                                                          \
     if (a.R == RR) {                                                            \
-        if (a.xg == 2) {                                                        \
-            if (ig) run_region<RR, true, 2>(ctx, a, rp);                        \
-            else run_region<RR, false, 2>(ctx, a, rp);                          \
+        if (a.sched_mode == 1) {                                                \
+            EAB_REGION_M(RR, 1)                                                 \
         } else {                                                                \
-            if (ig) run_region<RR, true, 4>(ctx, a, rp);                        \
-            else run_region<RR, false, 4>(ctx, a, rp);                          \
+            EAB_REGION_M(RR, 0)                                                 \
         }                                                                       \
         return true;                                                            \
     }
     EAB_REGION(1)
     EAB_REGION(0)
-    EAB_REGION(2)
+    if (a.R == 2) {
+        EAB_REGION_M(2, 0)
+        return true;
+    }
 #undef EAB_REGION
+#undef EAB_REGION_M
     return false;
 }
 
@@ -1197,7 +1356,7 @@ ItemGeom screen_items(const ScreenArgs& a, bool fast) {
     g.ny = a.ny;
     g.total = a.nx * a.ny * a.it_count;
     if (fast) {
-        const unsigned S = a.geom.shift == 3 ? 8u : 16u;
+        const unsigned S = a.geom.shift == 3 ? 8u : a.geom.shift == 2 ? 4u : 16u;
         const unsigned XG = a.xg == 2 ? 2u : 4u;
         g.lattice = 1;
         g.cols = 8 * XG;
@@ -1845,7 +2004,8 @@ __global__ void __launch_bounds__(256) finish_kernel(const FinishArgs f) {
 // FUSED: the finish (band threshold from the exact k-th largest score,
 // compaction, exact rescore, select, rows) runs in the same cooperative
 // launch after grid barriers; no histogram (its 16 KB go to the plane).
-template <int R, int S, int SHIFT, bool IGNORE, int XG, bool EDGE, int THREADS, bool FUSED>
+template <int R, int S, int SHIFT, bool IGNORE, int XG, bool EDGE, int THREADS, bool FUSED,
+          int MODE>
 __global__ void __launch_bounds__(THREADS, 1)
     screen_fast_kernel(const ScreenArgs a, const unsigned nwx, const unsigned nwy,
                        const TailPlan tp, const int vec16, const FinishArgs fa) {
@@ -1880,7 +2040,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int yg = lane % YG, xg = lane / YG;
     const float K = a.K;
     const unsigned long long total = tp.n_main + tp.n_tail * (unsigned long long)tp.f;
-    const size_t sstride = 1 + 2 * (size_t)a.n;
+    const size_t sstride = sched_stride(a.n);
 
     LaneGeom g;
     g.P = P;
@@ -1928,7 +2088,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         const int4* sch = a.sched + itr * sstride;
         const int4 hdr = __ldg(sch);
-        const int n_ent = hdr.x + hdr.y + hdr.z + hdr.w;
+        const int n_ent = hdr.x + hdr.y + hdr.z;
         int e0 = 0, e1 = n_ent;
         if (tslot >= 0) {
             e0 = (int)((long long)ch * n_ent / tp.f);
@@ -1945,7 +2105,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         for (int s = 0; s < S; ++s)
 #pragma unroll
             for (int j = 0; j < kTW; ++j) acc[s][j] = 0u;
-        const int done = run_entries<R, S, SHIFT, IGNORE, EDGE, true>(sch + 1, hdr, e0, e1, g, K, acc);
+        const int done = run_entries<R, S, SHIFT, IGNORE, EDGE, true, MODE>(sch + 1, hdr, e0, e1,
+                                                                           g, K, acc);
         int sc[S][kTW];
         const unsigned corr = (unsigned)done * a.B3;
 #pragma unroll
@@ -2019,7 +2180,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
 }
 
-template <int R, int S, int SHIFT, bool IGNORE, int XG, bool EDGE, int THREADS, bool FUSED>
+template <int R, int S, int SHIFT, bool IGNORE, int XG, bool EDGE, int THREADS, bool FUSED,
+          int MODE>
 static void run_fast(ea_ctx* ctx, const ScreenArgs& a, const FinishArgs* fin) {
     constexpr int YG = 32 / XG;
     const unsigned nwx = (unsigned)((a.nx + 8 * XG - 1) / (8 * XG));
@@ -2031,7 +2193,7 @@ static void run_fast(ea_ctx* ctx, const ScreenArgs& a, const FinishArgs* fin) {
         FUSED ? std::max({plane_bytes, sizeof(FinishSmem),
                           (size_t)ctx->sm_count * kTopK * sizeof(float)})
               : kHistBins * sizeof(unsigned) + plane_bytes;
-    auto kern = screen_fast_kernel<R, S, SHIFT, IGNORE, XG, EDGE, THREADS, FUSED>;
+    auto kern = screen_fast_kernel<R, S, SHIFT, IGNORE, XG, EDGE, THREADS, FUSED, MODE>;
     EAB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     constexpr int threads = THREADS;
     const unsigned long long warps_per_cta = threads / 32;
@@ -2131,34 +2293,63 @@ size_t fast_smem_bytes(const PlaneGeom& g) {
 
 bool launch_screen_fast(ea_ctx* ctx, const ScreenArgs& a) {
     if (fast_smem_bytes(a.geom) > ctx->smem_optin) return false;
-    if (a.geom.shift != 3) return false;  // 8-row lane strips
     if (a.geom.elem_bytes != 8) return false;
+    if (a.sched_mode == 1 && a.R > 1) return false;
     const bool ig = a.ignore != 0;
+    if (a.geom.shift == 2) {  // 4-row lane strips: 32 accumulators, 16 warps (EAB_S4)
+        if (a.edge != 0 || a.R > 1) return false;
+#define EAB_FAST4(RR, MM)                                                                    \
+    if (a.xg == 2) {                                                                         \
+        if (ig) run_fast<RR, 4, 2, true, 2, false, 512, false, MM>(ctx, a, nullptr);        \
+        else run_fast<RR, 4, 2, false, 2, false, 512, false, MM>(ctx, a, nullptr);          \
+    } else {                                                                                 \
+        if (ig) run_fast<RR, 4, 2, true, 4, false, 512, false, MM>(ctx, a, nullptr);        \
+        else run_fast<RR, 4, 2, false, 4, false, 512, false, MM>(ctx, a, nullptr);          \
+    }
+        if (a.R == 1) {
+            if (a.sched_mode == 1) { EAB_FAST4(1, 1) } else { EAB_FAST4(1, 0) }
+        } else {
+            if (a.sched_mode == 1) { EAB_FAST4(0, 1) } else { EAB_FAST4(0, 0) }
+        }
+#undef EAB_FAST4
+        return true;
+    }
+    if (a.geom.shift != 3) return false;  // 8-row lane strips
     // Windows that may leave the padded plane (padding shrunk to fit shared
     // memory) need the clamping variant; fully padded planes run the lighter
     // kernel, whose register budget allows kFastThreads threads.
     const bool edge = a.edge != 0;
-#define EAB_FAST_XG(RR, XGV)                                                                  \
-    if (edge) {                                                                               \
-        if (ig) run_fast<RR, 8, 3, true, XGV, true, 256, false>(ctx, a, nullptr);            \
-        else run_fast<RR, 8, 3, false, XGV, true, 256, false>(ctx, a, nullptr);              \
-    } else {                                                                                  \
-        if (ig) run_fast<RR, 8, 3, true, XGV, false, kFastThreads, false>(ctx, a, nullptr);  \
-        else run_fast<RR, 8, 3, false, XGV, false, kFastThreads, false>(ctx, a, nullptr);    \
+#define EAB_FAST_XG(RR, XGV, MM)                                                                \
+    if (edge) {                                                                                 \
+        if (ig) run_fast<RR, 8, 3, true, XGV, true, 256, false, MM>(ctx, a, nullptr);          \
+        else run_fast<RR, 8, 3, false, XGV, true, 256, false, MM>(ctx, a, nullptr);            \
+    } else {                                                                                    \
+        if (ig) run_fast<RR, 8, 3, true, XGV, false, kFastThreads, false, MM>(ctx, a, nullptr);\
+        else run_fast<RR, 8, 3, false, XGV, false, kFastThreads, false, MM>(ctx, a, nullptr);  \
+    }
+#define EAB_FAST_M(RR, MM)                                                  \
+    if (a.xg == 2) {                                                        \
+        EAB_FAST_XG(RR, 2, MM)                                              \
+    } else {                                                                \
+        EAB_FAST_XG(RR, 4, MM)                                              \
     }
 #define EAB_FAST(RR)                                                        \
     if (a.R == RR) {                                                        \
-        if (a.xg == 2) {                                                    \
-            EAB_FAST_XG(RR, 2)                                              \
+        if (a.sched_mode == 1) {                                            \
+            EAB_FAST_M(RR, 1)                                               \
         } else {                                                            \
-            EAB_FAST_XG(RR, 4)                                              \
+            EAB_FAST_M(RR, 0)                                               \
         }                                                                   \
         return true;                                                        \
     }
     EAB_FAST(1)
     EAB_FAST(0)
-    EAB_FAST(2)
+    if (a.R == 2) {
+        EAB_FAST_M(2, 0)
+        return true;
+    }
 #undef EAB_FAST
+#undef EAB_FAST_M
 #undef EAB_FAST_XG
     return false;
 }
@@ -2167,22 +2358,33 @@ bool launch_screen_fused(ea_ctx* ctx, const ScreenArgs& a, const FinishArgs& f) 
     if (fast_smem_bytes(a.geom) > ctx->smem_optin) return false;
     if (a.geom.shift != 3 || a.geom.elem_bytes != 8) return false;
     if (a.edge != 0 || a.kf < 1 || a.kf > kTopK || f.k != a.kf || !f.cta_top) return false;
+    if (a.sched_mode == 1 && a.R > 1) return false;
     const bool ig = a.ignore != 0;
-#define EAB_FUSED(RR)                                                                         \
-    if (a.R == RR) {                                                                          \
-        if (a.xg == 2) {                                                                      \
-            if (ig) run_fast<RR, 8, 3, true, 2, false, kFastThreads, true>(ctx, a, &f);       \
-            else run_fast<RR, 8, 3, false, 2, false, kFastThreads, true>(ctx, a, &f);         \
-        } else {                                                                              \
-            if (ig) run_fast<RR, 8, 3, true, 4, false, kFastThreads, true>(ctx, a, &f);       \
-            else run_fast<RR, 8, 3, false, 4, false, kFastThreads, true>(ctx, a, &f);         \
-        }                                                                                     \
-        return true;                                                                          \
+#define EAB_FUSED_M(RR, MM)                                                                       \
+    if (a.xg == 2) {                                                                              \
+        if (ig) run_fast<RR, 8, 3, true, 2, false, kFastThreads, true, MM>(ctx, a, &f);           \
+        else run_fast<RR, 8, 3, false, 2, false, kFastThreads, true, MM>(ctx, a, &f);             \
+    } else {                                                                                      \
+        if (ig) run_fast<RR, 8, 3, true, 4, false, kFastThreads, true, MM>(ctx, a, &f);           \
+        else run_fast<RR, 8, 3, false, 4, false, kFastThreads, true, MM>(ctx, a, &f);             \
+    }
+#define EAB_FUSED(RR)                                                                             \
+    if (a.R == RR) {                                                                              \
+        if (a.sched_mode == 1) {                                                                  \
+            EAB_FUSED_M(RR, 1)                                                                    \
+        } else {                                                                                  \
+            EAB_FUSED_M(RR, 0)                                                                    \
+        }                                                                                         \
+        return true;                                                                              \
     }
     EAB_FUSED(1)
     EAB_FUSED(0)
-    EAB_FUSED(2)
+    if (a.R == 2) {
+        EAB_FUSED_M(2, 0)
+        return true;
+    }
 #undef EAB_FUSED
+#undef EAB_FUSED_M
     return false;
 }
 
