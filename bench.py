@@ -174,45 +174,99 @@ def make_multi_inputs(name, noise_seed=None):
     return img, tmpls, cfg, [p for _, _, p in stamps]
 
 
-def lattice_work_per_eval(models, tg, it0, it1, R=1, S=8):
-    """Per pose-evaluation, from the lattice kernel's point schedule
-    (search_kernels.cu schedule_kernel, restated): (shared-memory bytes
-    loaded, minimal thread instructions).  Per theta the points are sorted by
-    (oy, ox) and same-row neighbours with dx <= 1 paired; per lane block of
-    8 x S poses a single loads (8+2R)(S+2R) float2 and issues per window row
-    8+2R LDS, 2(8+2R) FFMA, 8 FMNMX3 (horizontal) and per pose row 8 FMNMX3
-    (vertical) + 8 accumulates; a pair loads its (8+2R+dx)(S+2R) union once,
-    doubles the FFMA and FMNMX3 and adds both votes with one IADD3.  Host
-    cos/sin may differ from glibc's in the last bit, which can move a rounding
-    tie: a model, not a count."""
+def _schedule(ox, oy, fx, fy, mode):
+    """schedule_kernel's entries for one theta (search_kernels.cu, restated):
+    mode 1: twins (same fp32 direction, offsets (1,0) then (0,1)) + singles;
+    mode 0: same-row pairs with dx <= 1 + singles.  -> list of (kind, dx, dy)."""
+    n = len(ox)
+    order = sorted(range(n), key=lambda i: (oy[i], ox[i], i))
+    pos = {}
+    for r, i in enumerate(order):
+        pos.setdefault((oy[i], ox[i]), []).append(r)
+    used = [False] * n
+    out = []
+    if mode == 1:
+        for r, i in enumerate(order):
+            if used[r]:
+                continue
+            mate = None
+            for key, kind in (((oy[i], ox[i] + 1), "t10"), ((oy[i] + 1, ox[i]), "t01")):
+                for q in pos.get(key, []):
+                    j = order[q]
+                    if q > r and not used[q] and fx[j] == fx[i] and fy[j] == fy[i]:
+                        mate = (q, kind)
+                        break
+                if mate:
+                    break
+            used[r] = True
+            if mate:
+                used[mate[0]] = True
+                out.append(mate[1])
+            else:
+                out.append("s")
+        return out
+    r = 0
+    while r < n:
+        i = order[r]
+        if r + 1 < n:
+            j = order[r + 1]
+            d = ox[j] - ox[i]
+            if oy[j] == oy[i] and 0 <= d <= 1:
+                out.append("p%d" % d)
+                r += 2
+                continue
+        out.append("s")
+        r += 1
+    return out
+
+
+def lattice_work_per_eval(models, tg, it0, it1, R=1):
+    """Per pose-evaluation, from the lattice kernel's point schedule and lane
+    strip (api.cu screen(), search_kernels.cu schedule_kernel, restated):
+    (shared-memory bytes loaded, minimal thread instructions, mode).  Mode 1
+    (twins, 4-row strips) when R <= 1 and at least a fifth of the points are
+    twinned, else mode 0 (pairs, 8-row strips).  Per lane block of 8 x S
+    poses an entry loads its union window once (float2, 8 B per pixel) and
+    issues per union row one LDS and two FFMA per column and one FMNMX3 per
+    horizontal window, per output row one FMNMX3 per vertical window and one
+    accumulate per pose (IADD3 for two points).  Host cos/sin may differ from
+    glibc's in the last bit, which can move a rounding tie: a model, not a
+    count."""
     import math
-    px_total = evals = inst = 0
-    NR, NC = S + 2 * R, 8 + 2 * R
-    for pts in models:
-        pts = np.asarray(pts)
-        for it in range(it0, it1):
-            t = tg.t0 + it * tg.dt
-            c, s_ = math.cos(t), math.sin(t)
-            ox = np.floor(c * pts[:, 0] - s_ * pts[:, 1] + 0.5).astype(np.int64)
-            oy = np.floor(s_ * pts[:, 0] + c * pts[:, 1] + 0.5).astype(np.int64)
-            order = np.lexsort((np.arange(len(pts)), ox, oy))
-            i, n = 0, len(order)
-            while i < n:
-                a = order[i]
-                if i + 1 < n:
-                    b = order[i + 1]
-                    d = ox[b] - ox[a]
-                    if oy[b] == oy[a] and 0 <= d <= 1:
-                        px_total += (NC + d) * NR
-                        inst += NR * ((NC + d) + 4 * NC + 16) + S * (16 + 8)
-                        i += 2
-                        continue
-                px_total += NC * NR
-                inst += NR * (NC + 2 * NC + 8) + S * (8 + 8)
-                i += 1
-            evals += n * 8 * S
-    evals = max(evals, 1)
-    return px_total * 8.0 / evals, inst / evals
+    NC = 8 + 2 * R
+    per = {}  # mode -> [bytes, inst, evals, twinned points, points]
+    for mode in ((1, 0) if R <= 1 else (0,)):
+        S = 4 if mode == 1 else 8
+        NR = S + 2 * R
+        cost = {  # (pixels, instructions, points) per entry
+            "s": (NC * NR, NR * (3 * NC + 8) + S * 16, 1),
+            "p0": (NC * NR, NR * (NC + 4 * NC + 16) + S * 24, 2),
+            "p1": ((NC + 1) * NR, NR * ((NC + 1) + 4 * NC + 16) + S * 24, 2),
+            "t10": ((NC + 1) * NR, NR * (3 * (NC + 1) + 9) + S * (9 + 8), 2),
+            "t01": (NC * (NR + 1), (NR + 1) * (3 * NC + 8) + (S + 1) * 8 + S * 8, 2),
+        }
+        px = inst = evals = tw = pts_n = 0
+        for pts in models:
+            pts = np.asarray(pts)
+            for it in range(it0, it1):
+                t = tg.t0 + it * tg.dt
+                c, s_ = math.cos(t), math.sin(t)
+                x, y, dx, dy = pts[:, 0], pts[:, 1], pts[:, 2], pts[:, 3]
+                ox = np.floor(c * x - s_ * y + 0.5).astype(np.int64)
+                oy = np.floor(s_ * x + c * y + 0.5).astype(np.int64)
+                rx, ry = c * dx - s_ * dy, s_ * dx + c * dy
+                nrm = np.sqrt(rx * rx + ry * ry)
+                fx, fy = (rx / nrm).astype(np.float32), (ry / nrm).astype(np.float32)
+                for kind in _schedule(list(ox), list(oy), list(fx), list(fy), mode):
+                    p_, i_, n_ = cost[kind]
+                    px += p_
+                    inst += i_
+                    evals += n_ * 8 * S
+                    tw += 2 if kind[0] == "t" else 0
+                pts_n += len(pts)
+        per[mode] = (px * 8.0 / max(evals, 1), inst / max(evals, 1), tw, pts_n)
+    mode = 1 if 1 in per and per[1][2] * 5 >= per[1][3] else 0
+    return per[mode][0], per[mode][1], mode
 
 
 def top_grid(cfg):
@@ -434,8 +488,9 @@ def bench_reference(args, rank, world):
 # instructions per launch, issue slots busy.  Not measurable inside the timed
 # run; per config.
 NCU = {
-    "cfg3": dict(kernel="screen_fast_kernel<1, 8, 3, 0, 2, 0, 384>", dram=60228352,
-                 warp_inst=443089427, issue_busy=0.6289,
+    "cfg3": dict(kernel="screen_fast_kernel<1, 4, 2, 0, 2, 0, 512, 0, 1>", dram=69324800,
+                 warp_inst=443125272, issue_busy=0.6327, smem_wavefronts=148444936,
+                 l1_busy=0.9403, ncu_ms=0.61312,
                  source="profiles/r02_screen_cfg3_ncu.txt"),
 }
 SMEM_BYTES_PER_CLK_PER_SM = 128
@@ -728,18 +783,24 @@ def bench_ours(args, rank, world, local_rank):
     local_evals = (sum(nx * ny * (e - b) * n_tops[m] for m, b, e in my_items) if multi
                    else nx * ny * (it1 - it0) * n_top)
     models_top = [d.levels.model(L - 1).points for d in dets]
-    loaded_b, min_inst = lattice_work_per_eval(models_top, tg, it0, it1)
+    loaded_b, min_inst, sched_mode = lattice_work_per_eval(models_top, tg, it0, it1)
     achieved = local_evals * loaded_b / (kernel_ms / 1e3) / 1e9
     ncu = NCU.get(args.config)
     issue = None
     if ncu and world == 1:
         thread_inst = ncu["warp_inst"] * 32.0 / local_evals
         issue = {"kernel": ncu["kernel"], "thread_instructions_per_eval": thread_inst,
+                 "smem_bytes_per_eval_ncu": ncu["smem_wavefronts"] * 128.0 / local_evals,
+                 "frac_smem_ncu_wavefronts": ncu["smem_wavefronts"] * 128.0 / (kernel_ms / 1e3)
+                 / 1e9 / smem_peak_gbs,
+                 "l1tex_throughput_ncu": ncu["l1_busy"],
                  "minimal_thread_instructions_per_eval": min_inst,
                  "instruction_efficiency": min_inst / thread_inst,
                  "issue_slots_busy": ncu["issue_busy"], "source": ncu["source"],
                  "note": "minimal = the point schedule's LDS + FFMA + FMNMX3 + accumulate "
-                         "instructions per pose-eval (no addressing, loop or epilogue)"}
+                         "instructions per pose-eval (no addressing, loop or epilogue)",
+                 "schedule": "twins, 4-row lane strips" if sched_mode == 1 else
+                             "pairs, 8-row lane strips"}
     line = {
         "metric": "pose-evals/sec", "value": value, "unit": "pose-evals/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot_ms / args.steps,
