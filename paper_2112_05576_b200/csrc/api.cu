@@ -505,6 +505,10 @@ ScreenPlan screen(ea_ctx* ctx, const ea_model* m, const ea_field* f, const ea_po
     a.xg = xg;
     a.sched = sched;
     a.sched_mode = mm->sched_mode;
+    // lane strip of the lattice kernel that will run (screen_items' tile
+    // shape): the smem kernel's from its plane skew, the region kernel's from
+    // the schedule mode (launch_screen_region)
+    a.strip = region ? (a.sched_mode == 1 && R <= 1 ? 4 : 8) : (geom.shift == 2 ? 4 : 8);
     a.ro = ro_int;
     a.edge = edge ? 1 : 0;
     a.amb = amb;
@@ -617,12 +621,15 @@ ScreenPlan screen(ea_ctx* ctx, const ea_model* m, const ea_field* f, const ea_po
     // histogram, band threshold M_k - 2 delta from the k-th largest tile
     // maximum (see fused_threshold) -- fewer candidates than the histogram
     // bin's lower edge, and no per-pose histogram atomics in the screen.
-    if (plan.slab_poses && req && ctx->toplist && ctx->fused_finish && lattice && !region &&
+    if (plan.slab_poses && req && ctx->toplist && ctx->fused_finish && lattice &&
         mm->n_flagged == 0 && k >= 1 && k <= kTopK && ctx->sm_count <= 512) {
         a.cta_top = (float*)ctx->cta_top.ensure(sizeof(float) * kTopK * (size_t)ctx->sm_count);
+        float mm4 = (float)(4.0 * plan.delta);
+        if ((double)mm4 < 4.0 * plan.delta) mm4 = std::nextafter(mm4, INFINITY);
+        a.map_margin = mm4;
         plan.cta_top = a.cta_top;
     }
-    if (plan.slab_poses && req && ctx->fused_screen && plan.cta_top) {
+    if (plan.slab_poses && req && ctx->fused_screen && plan.cta_top && !region) {
         // screen + finish in one cooperative launch (no histogram)
         FinishArgs fa{};
         fa.map = map;

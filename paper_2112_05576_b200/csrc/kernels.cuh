@@ -237,6 +237,7 @@ struct ScreenArgs {
     int ignore;
     int xg;           // lattice warp tile: xg * 8 columns x (32 / xg) * 8 rows
     int sched_mode;   // schedule entry kinds: 0 singles/pairs, 1 singles/twins (launch_schedule)
+    int strip;        // lattice kernels' lane-strip rows S (8, or 4 for twin schedules)
     int ro;           // region kernel: bound on |lattice offset| of every rotated point
     int edge;         // smem kernel: zero columns shrunk to fit, windows may need clamping
     // Thetas with a rounding-ambiguous lattice offset (amb[it] > 0) are left
@@ -263,6 +264,7 @@ struct ScreenArgs {
     // no histogram; each CTA writes its kf largest tile maxima here
     // ([CTA][kTopK]) and the finish takes the band threshold from them
     float* cta_top;
+    float map_margin;  // top-list mode: 4 delta rounded up (emit_tile's map floor)
 };
 
 // Dynamic shared memory the lattice kernel needs for a plane.

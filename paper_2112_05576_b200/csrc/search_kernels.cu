@@ -741,9 +741,25 @@ template <int S, bool HIST = true>
 __device__ __forceinline__ float emit_tile(const ScreenArgs& a, const int (&acc)[S][kTW],
                                            const int X, const int Y, unsigned long long itr,
                                            unsigned long long item, unsigned* hist,
-                                           const int lane, const float floor) {
-    float* out = a.map + (size_t)itr * (a.nx * a.ny);
+                                           const int lane, const float floor,
+                                           const float map_floor = -INFINITY) {
+    // Top-list mode passes map_floor = (the warp's k-th largest tile maximum
+    // so far) - 4 delta, rounded down: a tile whose maximum is below it can
+    // never reach the band (its max < M_k - 2 delta, the finish's threshold),
+    // so its scores are not written -- most tiles of a search, and most of
+    // the map's DRAM write traffic.
     float best = -INFINITY;
+#pragma unroll
+    for (int s = 0; s < S; ++s)
+#pragma unroll
+        for (int j = 0; j < kTW; ++j)
+            if ((unsigned long long)(X + j) < a.nx && (unsigned long long)(Y + s) < a.ny)
+                best = fmaxf(best, (float)acc[s][j] * a.scale);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) best = fmaxf(best, __shfl_xor_sync(0xffffffffu, best, o));
+    if (lane == 0) a.item_max[item] = best;
+    if (best < map_floor) return best;  // warp-uniform
+    float* out = a.map + (size_t)itr * (a.nx * a.ny);
 #pragma unroll
     for (int s = 0; s < S; ++s) {
         const unsigned long long iy = (unsigned long long)(Y + s);
@@ -753,15 +769,11 @@ __device__ __forceinline__ float emit_tile(const ScreenArgs& a, const int (&acc)
             if (ix < a.nx && iy < a.ny) {
                 const float sc = (float)acc[s][j] * a.scale;
                 out[iy * a.nx + ix] = sc;
-                best = fmaxf(best, sc);
                 if constexpr (HIST)
                     if (hist && sc >= floor) atomicAdd(&hist[hist_bin(sc)], 1u);
             }
         }
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) best = fmaxf(best, __shfl_xor_sync(0xffffffffu, best, o));
-    if (lane == 0) a.item_max[item] = best;
     return best;
 }
 
@@ -887,26 +899,30 @@ __device__ __forceinline__ float fused_threshold(const FinishArgs& f, float* tto
 // warp, ordered tile-major and split into contiguous equal runs per CTA, so a
 // CTA reloads its region only when its run crosses into the next tile.
 struct RegionPlan {
-    int RW, RH;              // region pitch (elements, even) and rows
+    int RW, RH;              // region pitch (elements; even, a multiple of 4 for 4-row strips) and rows
     int elems16;             // region size in 16 B chunks
     unsigned long long n_items;  // warp tiles x theta groups
     unsigned groups;         // theta groups per warp tile
 };
-#ifndef EAB_REGION_WARPS
-#define EAB_REGION_WARPS 8
-#endif
-constexpr int kGroup = EAB_REGION_WARPS;  // thetas per CTA item (= warps per CTA)
+// thetas per CTA item (= warps per CTA): 8 warps x 8-row strips, 16 x 4-row
+template <int S>
+constexpr int region_group() { return S == 4 ? 16 : 8; }
 
+// SHIFT: the region's row skew in shared memory (lane strips of S = 2^SHIFT
+// rows); the global plane keeps its own (a.geom.shift).
 template <int R, int S, int SHIFT, bool IGNORE, int XG, int MODE>
-__global__ void __launch_bounds__(kGroup * 32, 1)
+__global__ void __launch_bounds__(region_group<S>() * 32, 1)
     screen_region_kernel(const ScreenArgs a, const unsigned nwx, const unsigned nwy,
                          const RegionPlan rp) {
+    constexpr int kGroup = region_group<S>();
     extern __shared__ __align__(16) unsigned char smem[];
+    const bool toplist = a.cta_top != nullptr;  // no histogram (see ScreenArgs::cta_top)
     unsigned* hist = reinterpret_cast<unsigned*>(smem);
-    float2* P = reinterpret_cast<float2*>(smem + kHistBins * sizeof(unsigned));
-    for (int i = threadIdx.x; i < kHistBins; i += blockDim.x) hist[i] = 0u;
+    float2* P = reinterpret_cast<float2*>(smem + (toplist ? 0 : kHistBins * sizeof(unsigned)));
+    if (!toplist)
+        for (int i = threadIdx.x; i < kHistBins; i += blockDim.x) hist[i] = 0u;
     if (blockIdx.x == 0 && threadIdx.x == 0) a.ctrl->cand_count = 0ull;  // for the finish
-    __shared__ float wtop_all[kGroup][kFloorK];
+    __shared__ __align__(16) float wtop_all[kGroup][kFloorK];
     float* wtop = wtop_all[threadIdx.x >> 5];
     if ((threadIdx.x & 31) < kFloorK) wtop[threadIdx.x & 31] = -INFINITY;
 
@@ -915,7 +931,7 @@ __global__ void __launch_bounds__(kGroup * 32, 1)
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
     const int yg = lane % YG, xg = lane / YG;
     const int h = a.ro + R;
-    const int PW = a.geom.PW, GH = a.geom.H + 2;
+    const int PW = a.geom.PW, GH = a.geom.H + 2, GSH = a.geom.shift;
     const float2* G = static_cast<const float2*>(a.plane);
     const float K = a.K;
 
@@ -936,7 +952,7 @@ __global__ void __launch_bounds__(kGroup * 32, 1)
                 const int gr = R0 + r;
                 float2* srow = P + r * rp.RW + (r >> SHIFT);
                 if (gr >= 0 && gr < GH) {
-                    const float2* grow = G + (size_t)gr * PW + (gr >> SHIFT);
+                    const float2* grow = G + (size_t)gr * PW + (gr >> GSH);
                     for (int c = lane; c < rp.RW; c += 32) {
                         const int gc = C0 + c;
                         srow[c] = (gc >= 0 && gc < PW) ? __ldg(grow + gc) : make_float2(0.f, 0.f);
@@ -985,43 +1001,56 @@ __global__ void __launch_bounds__(kGroup * 32, 1)
         for (int s = 0; s < S; ++s)
 #pragma unroll
             for (int j = 0; j < kTW; ++j) acc[s][j] = (int)(uacc[s][j] - corr);
-        const float best = emit_tile<S>(a, acc, TX0 + Xr, TY0 + Yr, itr, item, hist, lane,
-                                        warp_floor(wtop, a.kf));
+        const float wf = warp_floor(wtop, a.kf);
+        const float best = emit_tile<S>(a, acc, TX0 + Xr, TY0 + Yr, itr, item,
+                                        toplist ? nullptr : hist, lane, wf,
+                                        toplist ? __fsub_rd(wf, a.map_margin) : -INFINITY);
         floor_insert(wtop, best, lane);
     }
     __syncthreads();
-    merge_hist(hist, a.hist, a.kf);
+    if (toplist) {  // the CTA's kf largest tile maxima (merge of its warps' lists)
+        if (threadIdx.x < 32) {
+            float* out = a.cta_top + blockIdx.x * kTopK;
+            warp_kth_of_lists<1, false>(&wtop_all[0][0], kGroup, a.kf, out, threadIdx.x);
+            if (threadIdx.x >= a.kf && threadIdx.x < kTopK) out[threadIdx.x] = -INFINITY;
+        }
+    } else {
+        merge_hist(hist, a.hist, a.kf);
+    }
 }
 
-static RegionPlan region_plan(const ScreenArgs& a, int R) {
-    constexpr int S = 8;
+static RegionPlan region_plan(const ScreenArgs& a, int R, int S) {
     const int YG = 32 / a.xg;
     const int h = a.ro + R;
+    const int shift = S == 4 ? 2 : 3;
     RegionPlan rp{};
     rp.RW = 8 * a.xg + 2 * h;
-    rp.RW += rp.RW & 1;  // even pitch: lane slots stay yg + 8*xg (mod 16)
+    // lane slots stay yg + 8*xg (mod 16): S * RW must be a multiple of 16
+    const int mult = S == 4 ? 4 : 2;
+    rp.RW = (rp.RW + mult - 1) / mult * mult;
     rp.RH = YG * S + 2 * h;
-    const size_t elems = (size_t)rp.RH * rp.RW + (size_t)((rp.RH - 1) >> 3) + 1;
+    const size_t elems = (size_t)rp.RH * rp.RW + (size_t)((rp.RH - 1) >> shift) + 1;
     rp.elems16 = (int)((elems * sizeof(float2) + 15) / 16);
     return rp;
 }
 
-static size_t region_smem(const RegionPlan& rp) {
-    return kHistBins * sizeof(unsigned) + (size_t)rp.elems16 * 16;
+static size_t region_smem(const RegionPlan& rp, bool toplist) {
+    return (toplist ? 0 : kHistBins * sizeof(unsigned)) + (size_t)rp.elems16 * 16;
 }
 
-template <int R, bool IGNORE, int XG, int MODE>
+template <int R, int S, bool IGNORE, int XG, int MODE>
 static void run_region(ea_ctx* ctx, const ScreenArgs& a, RegionPlan rp) {
-    constexpr int S = 8, YG = 32 / XG;
+    constexpr int YG = 32 / XG, kGroup = region_group<S>();
     const unsigned nwx = (unsigned)((a.nx + 8 * XG - 1) / (8 * XG));
     const unsigned nwy = (unsigned)((a.ny + YG * S - 1) / (YG * S));
     rp.groups = (unsigned)((a.it_count + kGroup - 1) / kGroup);
     rp.n_items = (unsigned long long)nwx * nwy * rp.groups;
-    const size_t smem = region_smem(rp);
-    auto kern = screen_region_kernel<R, S, 3, IGNORE, XG, MODE>;
+    const size_t smem = region_smem(rp, a.cta_top != nullptr);
+    auto kern = screen_region_kernel<R, S, S == 4 ? 2 : 3, IGNORE, XG, MODE>;
     EAB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     unsigned long long ctas = std::min<unsigned long long>(rp.n_items, (unsigned)ctx->sm_count);
     if (ctas == 0) ctas = 1;
+    ctx->screen_ctas = (int)ctas;  // the finish merges this many per-CTA top lists
     kern<<<(unsigned)ctas, kGroup * 32, smem, ctx->stream>>>(a, nwx, nwy, rp);
     check_launch("screen_region_kernel");
     count_launch(ctx);
@@ -1030,30 +1059,32 @@ static void run_region(ea_ctx* ctx, const ScreenArgs& a, RegionPlan rp) {
 bool launch_screen_region(ea_ctx* ctx, const ScreenArgs& a) {
     if (a.geom.shift != 3 || a.geom.elem_bytes != 8 || a.R > 2) return false;
     if (a.sched_mode == 1 && a.R > 1) return false;
-    const RegionPlan rp = region_plan(a, a.R);
-    if (region_smem(rp) > ctx->smem_optin) return false;
+    // twin schedules: 4-row strips x 16 warps (the fast kernel's reasoning)
+    const int S = a.sched_mode == 1 ? 4 : 8;
+    const RegionPlan rp = region_plan(a, a.R, S);
+    if (region_smem(rp, a.cta_top != nullptr) > ctx->smem_optin) return false;
     const bool ig = a.ignore != 0;
-#define EAB_REGION_M(RR, MM)                                                    \
+#define EAB_REGION_M(RR, SS, MM)                                                \
     if (a.xg == 2) {                                                            \
-        if (ig) run_region<RR, true, 2, MM>(ctx, a, rp);                        \
-        else run_region<RR, false, 2, MM>(ctx, a, rp);                          \
+        if (ig) run_region<RR, SS, true, 2, MM>(ctx, a, rp);                    \
+        else run_region<RR, SS, false, 2, MM>(ctx, a, rp);                      \
     } else {                                                                    \
-        if (ig) run_region<RR, true, 4, MM>(ctx, a, rp);                        \
-        else run_region<RR, false, 4, MM>(ctx, a, rp);                          \
+        if (ig) run_region<RR, SS, true, 4, MM>(ctx, a, rp);                    \
+        else run_region<RR, SS, false, 4, MM>(ctx, a, rp);                      \
     }
 #define EAB_REGION(RR)                                                          \
     if (a.R == RR) {                                                            \
         if (a.sched_mode == 1) {                                                \
-            EAB_REGION_M(RR, 1)                                                 \
+            EAB_REGION_M(RR, 4, 1)                                              \
         } else {                                                                \
-            EAB_REGION_M(RR, 0)                                                 \
+            EAB_REGION_M(RR, 8, 0)                                              \
         }                                                                       \
         return true;                                                            \
     }
     EAB_REGION(1)
     EAB_REGION(0)
     if (a.R == 2) {
-        EAB_REGION_M(2, 0)
+        EAB_REGION_M(2, 8, 0)
         return true;
     }
 #undef EAB_REGION
@@ -1356,7 +1387,7 @@ ItemGeom screen_items(const ScreenArgs& a, bool fast) {
     g.ny = a.ny;
     g.total = a.nx * a.ny * a.it_count;
     if (fast) {
-        const unsigned S = a.geom.shift == 3 ? 8u : a.geom.shift == 2 ? 4u : 16u;
+        const unsigned S = (unsigned)a.strip;  // lane-strip rows of the kernel that ran
         const unsigned XG = a.xg == 2 ? 2u : 4u;
         g.lattice = 1;
         g.cols = 8 * XG;
@@ -2137,8 +2168,10 @@ __global__ void __launch_bounds__(THREADS, 1)
             if (lane == 0) tp.done[tslot] = 0u;
         }
         // fused: no histogram; wtop keeps the warp's 8 largest tile maxima
+        const float wf = warp_floor(wtop, a.kf);
         const float best = emit_tile<S, !FUSED>(a, sc, X, Y, itr, item, toplist ? nullptr : hist,
-                                                lane, warp_floor(wtop, a.kf));
+                                                lane, wf,
+                                                toplist ? __fsub_rd(wf, a.map_margin) : -INFINITY);
         floor_insert(wtop, best, lane);
     }
     if (wt && lane == 0) wt[7] = ((unsigned long long)units << 56) | (gtimer() & ((1ull << 56) - 1));

@@ -252,7 +252,7 @@ REGION_CASES = [
     ("l_bracket", 64, 360, 360, (0, 359, 1, 0, 359, 1, 0.0, D(300), D(60)), 3, 1),
     # plane fits shared memory only with shrunk zero columns -> clamping variant
     ("l_bracket", 72, 300, 85, (0, 299, 1, 0, 84, 1, 0.0, D(330), D(30)), 3, 0),
-    # halo region of a 96 px model exceeds shared memory -> general kernel
+    # halo region of a 96 px model: general kernel, or region kernel when it fits
     ("l_bracket", 96, 360, 360, (0, 359, 1, 0, 359, 1, 0.0, D(300), D(60)), 3, 0),
 ]
 
@@ -267,7 +267,10 @@ def test_region_search_bit_exact(ea, oracle, case):
     params = ea.ScoreParams(nb, pol)
     for k in (1, 9):
         got = ea.search_topk(tm, f, grid, params, k=k)
-        assert ea.default_context().stats()["screen_path"] == (2 if size > 90 else 1 if h < 100 else 3)
+        path = ea.default_context().stats()["screen_path"]
+        # a 96 px model's halo region fits shared memory only without the
+        # histogram (top-list mode, k <= 8) and with 4-row strips (twins)
+        assert path == (1 if h < 100 else 3) if size <= 90 else path in (2, 3)
         want = oracle.search_topk(tm.points, f, grid, params, k)
         assert keys(got) == keys(want)
 
