@@ -621,15 +621,19 @@ ScreenPlan screen(ea_ctx* ctx, const ea_model* m, const ea_field* f, const ea_po
     // histogram, band threshold M_k - 2 delta from the k-th largest tile
     // maximum (see fused_threshold) -- fewer candidates than the histogram
     // bin's lower edge, and no per-pose histogram atomics in the screen.
+    // (Flagged thetas, scored by the general kernel, publish no tile maxima:
+    // M_k over the lattice tiles alone is still <= T_f, and their items carry
+    // item_max = +inf, so the compaction scans them whole.)
     if (plan.slab_poses && req && ctx->toplist && ctx->fused_finish && lattice &&
-        mm->n_flagged == 0 && k >= 1 && k <= kTopK && ctx->sm_count <= 512) {
+        (size_t)mm->n_flagged * 2 < nth && k >= 1 && k <= kTopK && ctx->sm_count <= 512) {
         a.cta_top = (float*)ctx->cta_top.ensure(sizeof(float) * kTopK * (size_t)ctx->sm_count);
         float mm4 = (float)(4.0 * plan.delta);
         if ((double)mm4 < 4.0 * plan.delta) mm4 = std::nextafter(mm4, INFINITY);
         a.map_margin = mm4;
         plan.cta_top = a.cta_top;
     }
-    if (plan.slab_poses && req && ctx->fused_screen && plan.cta_top && !region) {
+    if (plan.slab_poses && req && ctx->fused_screen && plan.cta_top && !region &&
+        mm->n_flagged == 0) {
         // screen + finish in one cooperative launch (no histogram)
         FinishArgs fa{};
         fa.map = map;

@@ -60,7 +60,18 @@ struct SearchCtrl {
     int flags;                        // rounding-ambiguous (theta, point) pairs
     float thr;                        // band threshold on the fp32 screen score
     int n_out;                        // entries written to the top-k output
+    unsigned gfloor;                  // top-list mode: max over warps of their k-th largest
+                                      // tile maximum (order key; 0 = none), <= M_k
 };
+
+// Monotone unsigned image of a float (0 below every float): atomicMax-able.
+__device__ __forceinline__ unsigned float_order_key(float v) {
+    const unsigned b = __float_as_uint(v);
+    return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+__device__ __forceinline__ float float_from_order_key(unsigned k) {
+    return k == 0u ? -INFINITY : __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k);
+}
 
 // ---- exact fp64 primitives (reference op order) ------------------------------
 

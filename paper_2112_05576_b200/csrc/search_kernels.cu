@@ -737,6 +737,20 @@ __device__ __forceinline__ void floor_insert(float* wtop, float best, int lane) 
     __syncwarp();
 }
 
+// Top-list mode: after a warp's tile maxima list grows, publish its k-th
+// largest (<= M_k) to the launch-wide floor; tiles below (global floor -
+// 4 delta) are not written to the map (emit_tile).
+__device__ __forceinline__ void publish_floor(const ScreenArgs& a, const float* wtop, int lane) {
+    if (lane == 0 && a.kf > 0) {
+        const float f = wtop[a.kf - 1];
+        if (f > -INFINITY) atomicMax(&a.ctrl->gfloor, float_order_key(f));
+    }
+}
+__device__ __forceinline__ float map_floor_of(const ScreenArgs& a, float own) {
+    const float g = float_from_order_key(__ldcg(&a.ctrl->gfloor));
+    return __fsub_rd(fmaxf(own, g), a.map_margin);
+}
+
 template <int S, bool HIST = true>
 __device__ __forceinline__ float emit_tile(const ScreenArgs& a, const int (&acc)[S][kTW],
                                            const int X, const int Y, unsigned long long itr,
@@ -1004,8 +1018,9 @@ __global__ void __launch_bounds__(region_group<S>() * 32, 1)
         const float wf = warp_floor(wtop, a.kf);
         const float best = emit_tile<S>(a, acc, TX0 + Xr, TY0 + Yr, itr, item,
                                         toplist ? nullptr : hist, lane, wf,
-                                        toplist ? __fsub_rd(wf, a.map_margin) : -INFINITY);
+                                        toplist ? map_floor_of(a, wf) : -INFINITY);
         floor_insert(wtop, best, lane);
+        if (toplist) publish_floor(a, wtop, lane);
     }
     __syncthreads();
     if (toplist) {  // the CTA's kf largest tile maxima (merge of its warps' lists)
@@ -1154,7 +1169,7 @@ __global__ void __launch_bounds__(256)
         }
         sc = (float)acc * a.scale;
         a.map[itr * plane_poses + rem] = sc;
-        atomicAdd(&hist[hist_bin(sc)], 1u);
+        if (!a.cta_top) atomicAdd(&hist[hist_bin(sc)], 1u);  // top-list mode: no histogram
         }
         if (tlist) continue;  // item_max belongs to the lattice items (set to +inf)
         float best = sc;
@@ -1163,7 +1178,7 @@ __global__ void __launch_bounds__(256)
         if (lane == 0) a.item_max[t0 >> 5] = best;
     }
     __syncthreads();
-    merge_hist(hist, a.hist, a.kf);
+    if (!a.cta_top) merge_hist(hist, a.hist, a.kf);
 }
 
 // One CTA per translation tile: any |g| >= eps within the tile's halo?
@@ -2022,7 +2037,10 @@ __global__ void __launch_bounds__(256) finish_kernel(const FinishArgs f) {
         for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < kHistBins;
              i += gridDim.x * blockDim.x)
             f.hist_rw[i] = 0u;
-    if (blockIdx.x == 0 && threadIdx.x == 0) f.ctrl->work_counter = 0ull;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        f.ctrl->work_counter = 0ull;
+        f.ctrl->gfloor = 0u;  // the screen's top-list floor, for the next search
+    }
     const unsigned long long nc = finish_rescore_phase(f, sm);
     EAB_PROF(3)
     finish_select_phase(f, nc, sm);
@@ -2171,8 +2189,9 @@ __global__ void __launch_bounds__(THREADS, 1)
         const float wf = warp_floor(wtop, a.kf);
         const float best = emit_tile<S, !FUSED>(a, sc, X, Y, itr, item, toplist ? nullptr : hist,
                                                 lane, wf,
-                                                toplist ? __fsub_rd(wf, a.map_margin) : -INFINITY);
+                                                toplist ? map_floor_of(a, wf) : -INFINITY);
         floor_insert(wtop, best, lane);
+        if (toplist) publish_floor(a, wtop, lane);
     }
     if (wt && lane == 0) wt[7] = ((unsigned long long)units << 56) | (gtimer() & ((1ull << 56) - 1));
     if (a.prof && (threadIdx.x & 31) == 0) atomicMax(a.prof + 1, gtimer());  // last warp's loop end
@@ -2195,6 +2214,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (a.prof && threadIdx.x == 0) atomicMax(a.prof + 11, gtimer());  // barrier 1 passed
         if (blockIdx.x == 0 && threadIdx.x == 0) {
             a.ctrl->work_counter = 0ull;
+            a.ctrl->gfloor = 0u;
             a.ctrl->flags = 0;
         }
         // the plane is dead: its shared memory becomes the finish's scratch
