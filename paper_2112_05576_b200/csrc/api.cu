@@ -401,9 +401,18 @@ ScreenPlan screen(ea_ctx* ctx, const ea_model* m, const ea_field* f, const ea_po
     // Integer origin + unit steps: every translation is an exact integer,
     // so centre = floor(px + 0.5) + u (lattice_offset); x1/y1 only bound the
     // counts and must keep |u| < 2^20.
+    // Integer steps sx, sy > 1 (the paper's 3 px grid) run the same kernels
+    // on the unit lattice that covers the grid and emit only the grid's poses
+    // (emit_tile_strided): sx * sy times the screening work of the grid, at
+    // the lattice kernels' per-pose cost instead of the general kernel's.
+    const bool int_steps = is_int(g.dx) && is_int(g.dy) && g.dx >= 1.0 && g.dy >= 1.0 &&
+                           g.dx <= 64.0 && g.dy <= 64.0;
     const bool lattice = is_int(g.x0) && is_int(g.y0) && std::fabs(g.x1) <= 1048576.0 &&
-                         std::fabs(g.y1) <= 1048576.0 && g.dx == 1.0 && g.dy == 1.0 && R <= 2 &&
+                         std::fabs(g.y1) <= 1048576.0 && int_steps && R <= 2 &&
                          f->ring_max < p.eps_mag;
+    const int sx = lattice ? (int)g.dx : 1, sy = lattice ? (int)g.dy : 1;
+    const uint64_t lnx = lattice ? (plan.c.nx - 1) * (uint64_t)sx + 1 : plan.c.nx;
+    const uint64_t lny = lattice ? (plan.c.ny - 1) * (uint64_t)sy + 1 : plan.c.ny;
     // Lane strips of 8 rows (64 accumulators, 8 warps/SM) measured faster
     // than 16 rows (128 accumulators: spills) on B200.
     const int shift = 3;
@@ -416,7 +425,7 @@ ScreenPlan screen(ea_ctx* ctx, const ea_model* m, const ea_field* f, const ea_po
     int xg = 4;
     {   // warp tile 32x64 or 16x128: whichever pads the translation grid least
         auto padded = [&](uint64_t cols, uint64_t rows) {
-            return ((plan.c.nx + cols - 1) / cols * cols) * ((plan.c.ny + rows - 1) / rows * rows);
+            return ((lnx + cols - 1) / cols * cols) * ((lny + rows - 1) / rows * rows);
         };
         xg = padded(16, 128) < padded(32, 64) ? 2 : 4;
     }
@@ -433,7 +442,7 @@ ScreenPlan screen(ea_ctx* ctx, const ea_model* m, const ea_field* f, const ea_po
         const long ro = (long)std::ceil(rmax) + 2;
         ro_int = (int)std::min<long>(ro, 1 << 20);
         const long tw = 8L * xg;  // warp tile width: the lanes' last window column
-        const long ix0 = (long)g.x0, span = (long)((plan.c.nx + tw - 1) / tw) * tw;
+        const long ix0 = (long)g.x0, span = (long)((lnx + tw - 1) / tw) * tw;
         PL = (int)std::max(0L, ro + R - 1 - ix0);
         PR = (int)std::max(0L, ix0 + span + ro + R - f->width - 1);
         const size_t budget = ctx->smem_optin;  // hist + plane must fit one CTA
@@ -481,7 +490,9 @@ ScreenPlan screen(ea_ctx* ctx, const ea_model* m, const ea_field* f, const ea_po
     ctx->hist_clean = false;
     float* map = (float*)ctx->map.ensure(sizeof(float) * (plan.slab_poses ? plan.slab_poses : 1));
     float* item_max =
-        (float*)ctx->item_max.ensure(sizeof(float) * (plan.slab_poses / 32 + plan.it_count * 64 + 64));
+        (float*)ctx->item_max.ensure(sizeof(float) * (std::max<uint64_t>(plan.slab_poses,
+                                                                           lnx * lny * plan.it_count) /
+                                                         32 + plan.it_count * 64 + 64));
 
     ScreenArgs a{};
     a.plane = plane;
@@ -494,6 +505,10 @@ ScreenPlan screen(ea_ctx* ctx, const ea_model* m, const ea_field* f, const ea_po
     a.it_count = plan.it_count;
     a.nx = plan.c.nx;
     a.ny = plan.c.ny;
+    a.sx = sx;
+    a.sy = sy;
+    a.lnx = lnx;
+    a.lny = lny;
     a.ix0 = lattice ? (int)g.x0 : 0;
     a.iy0 = lattice ? (int)g.y0 : 0;
     a.x0 = g.x0;
@@ -520,8 +535,8 @@ ScreenPlan screen(ea_ctx* ctx, const ea_model* m, const ea_field* f, const ea_po
     // first k poses of each zero tile can rank; finish_tile).
     if (lattice && !region && plan.slab_poses) {
         const int tw = 8 * xg, th = (32 / xg) * (geom.shift == 2 ? 4 : 8);
-        const unsigned nwx = (unsigned)((plan.c.nx + tw - 1) / tw);
-        const unsigned nwy = (unsigned)((plan.c.ny + th - 1) / th);
+        const unsigned nwx = (unsigned)((lnx + tw - 1) / tw);
+        const unsigned nwy = (unsigned)((lny + th - 1) / th);
         const int halo = ro_int + R;
         unsigned char* zt = (unsigned char*)ctx->ztiles.ensure((size_t)nwx * nwy);
         const std::vector<double> zkey{(double)reinterpret_cast<uintptr_t>(f), (double)f->version,

@@ -249,6 +249,12 @@ struct ScreenArgs {
     int xg;           // lattice warp tile: xg * 8 columns x (32 / xg) * 8 rows
     int sched_mode;   // schedule entry kinds: 0 singles/pairs, 1 singles/twins (launch_schedule)
     int strip;        // lattice kernels' lane-strip rows S (8, or 4 for twin schedules)
+    // Integer steps sx, sy >= 1 (the paper's 3 px grid): the lattice kernels
+    // tile the UNIT lattice of lnx x lny translations from (ix0, iy0) and
+    // emit only the poses on the grid, (ix, iy) = (X / sx, Y / sy); unit
+    // grids have sx = sy = 1, lnx = nx, lny = ny.
+    int sx, sy;
+    unsigned long long lnx, lny;
     int ro;           // region kernel: bound on |lattice offset| of every rotated point
     int edge;         // smem kernel: zero columns shrunk to fit, windows may need clamping
     // Thetas with a rounding-ambiguous lattice offset (amb[it] > 0) are left
@@ -305,6 +311,7 @@ struct ItemGeom {
     int lattice;           // 1: items are (theta, wy, wx) tiles of cols x rows poses
     unsigned nwx, nwy, rows, cols;
     unsigned long long nx, ny, total;
+    int sx, sy;            // lattice steps (tiles are on the unit lattice; see ScreenArgs)
 };
 ItemGeom screen_items(const ScreenArgs& a, bool fast);
 // Compaction with the band threshold (see launch_threshold) computed in-kernel.

@@ -751,6 +751,48 @@ __device__ __forceinline__ float map_floor_of(const ScreenArgs& a, float own) {
     return __fsub_rd(fmaxf(own, g), a.map_margin);
 }
 
+// emit_tile for integer steps sx, sy > 1: the lane's 8 x S block is on the
+// unit lattice; only translations X % sx == 0, Y % sy == 0 are grid poses
+// (ix, iy) = (X / sx, Y / sy).  Kept out of line of the unit-step path.
+template <int S, bool HIST>
+__device__ __noinline__ float emit_tile_strided(const ScreenArgs& a, const int (&acc)[S][kTW],
+                                                const int X, const int Y, unsigned long long itr,
+                                                unsigned long long item, unsigned* hist,
+                                                const int lane, const float floor,
+                                                const float map_floor) {
+    float best = -INFINITY;
+#pragma unroll
+    for (int s = 0; s < S; ++s)
+#pragma unroll
+        for (int j = 0; j < kTW; ++j) {
+            const int ux = X + j, uy = Y + s;
+            if (ux % a.sx == 0 && uy % a.sy == 0 &&
+                (unsigned long long)(ux / a.sx) < a.nx && (unsigned long long)(uy / a.sy) < a.ny)
+                best = fmaxf(best, (float)acc[s][j] * a.scale);
+        }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) best = fmaxf(best, __shfl_xor_sync(0xffffffffu, best, o));
+    if (lane == 0) a.item_max[item] = best;
+    if (best < map_floor) return best;  // warp-uniform
+    float* out = a.map + (size_t)itr * (a.nx * a.ny);
+#pragma unroll
+    for (int s = 0; s < S; ++s)
+#pragma unroll
+        for (int j = 0; j < kTW; ++j) {
+            const int ux = X + j, uy = Y + s;
+            if (ux % a.sx != 0 || uy % a.sy != 0) continue;
+            const unsigned long long ix = (unsigned long long)(ux / a.sx);
+            const unsigned long long iy = (unsigned long long)(uy / a.sy);
+            if (ix < a.nx && iy < a.ny) {
+                const float sc = (float)acc[s][j] * a.scale;
+                out[iy * a.nx + ix] = sc;
+                if constexpr (HIST)
+                    if (hist && sc >= floor) atomicAdd(&hist[hist_bin(sc)], 1u);
+            }
+        }
+    return best;
+}
+
 template <int S, bool HIST = true>
 __device__ __forceinline__ float emit_tile(const ScreenArgs& a, const int (&acc)[S][kTW],
                                            const int X, const int Y, unsigned long long itr,
@@ -762,6 +804,8 @@ __device__ __forceinline__ float emit_tile(const ScreenArgs& a, const int (&acc)
     // never reach the band (its max < M_k - 2 delta, the finish's threshold),
     // so its scores are not written -- most tiles of a search, and most of
     // the map's DRAM write traffic.
+    if (a.sx != 1 || a.sy != 1)  // integer steps > 1: only the grid's poses
+        return emit_tile_strided<S, HIST>(a, acc, X, Y, itr, item, hist, lane, floor, map_floor);
     float best = -INFINITY;
 #pragma unroll
     for (int s = 0; s < S; ++s)
@@ -1056,8 +1100,8 @@ static size_t region_smem(const RegionPlan& rp, bool toplist) {
 template <int R, int S, bool IGNORE, int XG, int MODE>
 static void run_region(ea_ctx* ctx, const ScreenArgs& a, RegionPlan rp) {
     constexpr int YG = 32 / XG, kGroup = region_group<S>();
-    const unsigned nwx = (unsigned)((a.nx + 8 * XG - 1) / (8 * XG));
-    const unsigned nwy = (unsigned)((a.ny + YG * S - 1) / (YG * S));
+    const unsigned nwx = (unsigned)((a.lnx + 8 * XG - 1) / (8 * XG));
+    const unsigned nwy = (unsigned)((a.lny + YG * S - 1) / (YG * S));
     rp.groups = (unsigned)((a.it_count + kGroup - 1) / kGroup);
     rp.n_items = (unsigned long long)nwx * nwy * rp.groups;
     const size_t smem = region_smem(rp, a.cta_top != nullptr);
@@ -1407,8 +1451,10 @@ ItemGeom screen_items(const ScreenArgs& a, bool fast) {
         g.lattice = 1;
         g.cols = 8 * XG;
         g.rows = (32 / XG) * S;
-        g.nwx = (unsigned)((a.nx + g.cols - 1) / g.cols);
-        g.nwy = (unsigned)((a.ny + g.rows - 1) / g.rows);
+        g.nwx = (unsigned)((a.lnx + g.cols - 1) / g.cols);
+        g.nwy = (unsigned)((a.lny + g.rows - 1) / g.rows);
+        g.sx = a.sx;
+        g.sy = a.sy;
         g.n_items = (unsigned long long)g.nwx * g.nwy * a.it_count;
     } else {
         g.lattice = 0;
@@ -1793,9 +1839,52 @@ __device__ __forceinline__ float finish_threshold(const unsigned* __restrict__ h
 // B: one warp, one qualifying work item: every pose with S_f >= thr.  Lane
 // addresses are one pointer + a 32-bit row stride, so the 64 loads issue back
 // to back (64-bit index math per load made this a 4 us instruction chain).
+// finish_tile for integer steps > 1: the unit-lattice tile's grid poses are
+// the rectangle [ceil(x0/sx), ceil(x1/sx)) x [ceil(y0/sy), ceil(y1/sy)) of
+// the grid; lanes walk it row-major (an exact-zero tile: its first k).
+__device__ __noinline__ void finish_tile_strided(const FinishArgs& f, unsigned long long it,
+                                                  float thr, int lane) {
+    const ItemGeom& g = f.items;
+    const unsigned long long wx = it % g.nwx, rest = it / g.nwx;
+    const unsigned long long wy = rest % g.nwy, itr = rest / g.nwy;
+    const unsigned long long sx = (unsigned)g.sx, sy = (unsigned)g.sy;
+    const unsigned long long ix0 = (wx * g.cols + sx - 1) / sx;
+    const unsigned long long ix1 = min(((wx + 1) * g.cols + sx - 1) / sx, g.nx);
+    const unsigned long long iy0 = (wy * g.rows + sy - 1) / sy;
+    const unsigned long long iy1 = min(((wy + 1) * g.rows + sy - 1) / sy, g.ny);
+    if (ix0 >= ix1 || iy0 >= iy1) return;
+    const unsigned long long w = ix1 - ix0, n = w * (iy1 - iy0);
+    const unsigned long long base = itr * (g.nx * g.ny);
+    const bool zero = f.zero_tiles && __ldg(f.zero_tiles + it % ((unsigned long long)g.nwx * g.nwy));
+    const unsigned long long lim = zero ? min(n, (unsigned long long)f.k) : n;
+    for (unsigned long long i0 = 0; i0 < lim; i0 += 32) {
+        const unsigned long long i = i0 + lane;
+        bool take = false;
+        unsigned long long idx = 0;
+        if (i < lim) {
+            idx = base + (iy0 + i / w) * g.nx + ix0 + i % w;
+            take = zero ? 0.0f >= thr : __ldcg(f.map + idx) >= thr;
+        }
+        const unsigned mask = __ballot_sync(0xffffffffu, take);
+        if (!mask) continue;
+        const int leader = __ffs(mask) - 1;
+        unsigned long long slot0 = 0;
+        if (lane == leader) slot0 = atomicAdd(&f.ctrl->cand_count, (unsigned long long)__popc(mask));
+        slot0 = __shfl_sync(0xffffffffu, slot0, leader);
+        if (take) {
+            const unsigned long long slot = slot0 + __popc(mask & ((1u << lane) - 1u));
+            if (slot < f.cap) f.cand[slot] = (unsigned)idx;
+        }
+    }
+}
+
 __device__ __forceinline__ void finish_tile(const FinishArgs& f, unsigned long long it,
                                             float thr, int lane) {
     const ItemGeom& g = f.items;
+    if (g.lattice && (g.sx != 1 || g.sy != 1)) {  // integer steps > 1: the tile's grid poses
+        finish_tile_strided(f, it, thr, lane);
+        return;
+    }
     if (f.zero_tiles && g.lattice && __ldg(f.zero_tiles + it % ((unsigned long long)g.nwx * g.nwy))) {
         // exact-zero tile: every pose scores 0 (and 0 >= thr, or none is a
         // candidate); only its first k poses in index order can rank -- any
@@ -2237,8 +2326,8 @@ template <int R, int S, int SHIFT, bool IGNORE, int XG, bool EDGE, int THREADS, 
           int MODE>
 static void run_fast(ea_ctx* ctx, const ScreenArgs& a, const FinishArgs* fin) {
     constexpr int YG = 32 / XG;
-    const unsigned nwx = (unsigned)((a.nx + 8 * XG - 1) / (8 * XG));
-    const unsigned nwy = (unsigned)((a.ny + YG * S - 1) / (YG * S));
+    const unsigned nwx = (unsigned)((a.lnx + 8 * XG - 1) / (8 * XG));
+    const unsigned nwy = (unsigned)((a.lny + YG * S - 1) / (YG * S));
     const unsigned long long items = (unsigned long long)nwx * nwy * a.it_count;
     const size_t plane_bytes = (a.geom.bytes() + 15) & ~(size_t)15;
     // fused: no histogram; the plane's bytes are reused by the finish phases

@@ -813,3 +813,51 @@ def test_fused_pyramid_fields_bit_exact(ea, oracle, monkeypatch, w, h, L):
             for a, b in zip(lv.field(l), want[l]):
                 assert np.array_equal(a, b), (fused, l)
     monkeypatch.delenv("EAB_NO_FUSED_PYRAMID", raising=False)
+
+
+# ---- integer steps > 1 on the lattice kernels (unit lattice, strided emit) --------------
+STRIDE_CASES = [
+    # (model size, field w, h, grid, nb, polarity)
+    (12, 64, 48, (0, 63, 2, 0, 47, 2, 0.0, D(350), D(10)), 3, 0),
+    (12, 64, 48, (1, 62, 3, 2, 47, 3, 0.0, D(350), D(10)), 3, 0),
+    (10, 60, 50, (-7, 66, 2, -5, 52, 3, 0.1, D(300), D(25)), 3, 0),   # off-image overhang
+    (14, 64, 64, (0, 63, 3, 0, 63, 1, 0.0, D(357), D(3)), 1, 0),
+    (14, 64, 64, (3, 60, 4, 3, 60, 4, 0.0, D(350), D(10)), 5, 1),
+    (12, 300, 260, (0, 299, 3, 0, 259, 3, 0.0, D(345), D(15)), 3, 0),  # region-tiled plane
+]
+
+
+@pytest.mark.parametrize("case", range(len(STRIDE_CASES)))
+def test_strided_lattice_bit_exact(ea, oracle, case):
+    """Integer steps > 1 (the paper's 3 px / 3 px grid) run the lattice
+    kernels over the unit lattice covering the grid and emit only the grid's
+    poses: same top k as the oracle for k in and beyond the top-list range."""
+    size, w, h, g, nb, pol = STRIDE_CASES[case]
+    rng = np.random.default_rng(700 + case)
+    m = rand_model(oracle, rng, size)
+    f = oracle.compute_gradients(rand_image(rng, w, h, real=case % 2 == 1))
+    grid = ea.PoseGrid(*g)
+    params = ea.ScoreParams(nb, pol)
+    for k in (1, 5, 11):
+        got = ea.search_topk(m, f, grid, params, k=k)
+        assert ea.default_context().stats()["screen_path"] in (1, 3)  # a lattice kernel
+        assert keys(got) == keys(oracle.search_topk(m.points, f, grid, params, k)), k
+
+
+@pytest.mark.slow
+def test_paper_geometry_detect_bit_exact(ea, oracle):
+    """The paper's own experiment geometry: an
+    812 x 617 search image, steps of 3 px / 3 px / 3 deg over the full
+    rotation, searched at level 0 -- the strided lattice path; detect ==
+    the oracle's coarse_to_fine bit for bit."""
+    img, tmpl = scene(ea, canvas_width=812, canvas_height=617, template_id="l_bracket",
+                      template_size=96, true_pose=(400, 300, D(42)), clutter_segments=40,
+                      clutter_seed=21, noise_sigma=1.5, noise_seed=4)
+    cfg = ea.SearchConfig(grid=ea.PoseGrid(0, 811, 3, 0, 616, 3, 0.0, D(357), D(3)),
+                          num_levels=1, score_params=ea.ScoreParams(3), topk=5)
+    got = ea.Detector(tmpl, cfg).detect(img)
+    assert ea.default_context().stats()["screen_path"] == 3
+    want = oracle.coarse_to_fine(oracle.build_pyramid(tmpl, 1), oracle.build_pyramid(img, 1), cfg,
+                                 threads=16)
+    assert got.key() == want.key()
+    assert got.found
