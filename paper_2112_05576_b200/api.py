@@ -797,3 +797,57 @@ def compose_scene(spec):
     _check(lib().ea_compose_scene(C.byref(spec), _ptr(canvas), _ptr(tmpl), C.byref(pose),
                                   C.byref(occ)))
     return canvas, tmpl, pose.astuple(), occ.value
+
+
+# ---- BenchRow CSV (SPEC.md cmd_bench, "sample,backend,workers,run,elapsed_ms") ----------
+BENCH_CSV_HEADER = "sample,backend,workers,run,elapsed_ms"
+
+
+def bench_rows(samples, reps=5, warmup=1, backends=("cuda",), config=None, ctx=None):
+    """The reference's bench rows (SPEC.md BenchRow / cmd_bench) for this
+    library: for each (name, template, image) sample, `warmup` untimed then
+    `reps` timed detects per backend; only the search is timed (models are
+    prepared before, I/O excluded).  The CUDA backend is the only backend of
+    this library (every BackendKind runs on the device, search.h:14-20);
+    a sample whose backends disagree on the pose raises (cmd_bench exit 3).
+    -> list of dict rows {sample, backend, workers, run, elapsed_ms}."""
+    import time
+    rows = []
+    for name, tmpl, img in samples:
+        cfg = config or SearchConfig()
+        det = Detector(tmpl, cfg, ctx)
+        det.levels.set_image(img)
+        poses = set()
+        for backend in backends:
+            kind = {"serial": BACKEND_SERIAL, "parallel": BACKEND_PARALLEL,
+                    "cuda": BACKEND_CUDA}[backend]
+            bcfg = SearchConfig(grid=cfg.grid, num_levels=cfg.num_levels,
+                                score_params=cfg.score_params, min_score=cfg.min_score,
+                                topk=cfg.topk, refine_radius=cfg.refine_radius,
+                                backend_kind=kind, worker_count=cfg.worker_count)
+            for run in range(warmup + reps):
+                t0 = time.perf_counter()
+                out = search_levels(det.levels, bcfg)
+                ms = (time.perf_counter() - t0) * 1e3
+                if run >= warmup:
+                    rows.append({"sample": name, "backend": backend,
+                                 "workers": int(cfg.worker_count), "run": run - warmup,
+                                 "elapsed_ms": ms})
+            poses.add(out.key()[:2])  # found + pose
+        if len(poses) > 1:
+            raise Error(f"backends disagree on the pose of sample {name}")
+    return rows
+
+
+def bench_csv(rows):
+    """BenchRow CSV text with the reference's exact header."""
+    lines = [BENCH_CSV_HEADER]
+    for r in rows:
+        if not r["elapsed_ms"] > 0:
+            raise ValueError("BenchRow invariant: elapsed_ms > 0")
+        name = str(r["sample"])
+        if any(c in name for c in ',"\n'):
+            name = '"' + name.replace('"', '""') + '"'
+        lines.append(f"{name},{r['backend']},{int(r['workers'])},{int(r['run'])},"
+                     f"{float(r['elapsed_ms']):.6f}")
+    return "\n".join(lines) + "\n"

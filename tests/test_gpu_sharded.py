@@ -259,3 +259,22 @@ def test_grid_over_2_32_poses_chunked(ea, oracle):
     for s in full:
         want, _ = oracle.pose_score(m.points, s.pose.astuple(), f, params)
         assert s.score == want
+
+
+def test_bench_rows_suite(ea):
+    """cmd_bench's rows on the device: samples x backends x reps rows, all
+    backends (every kind runs on the device) agreeing on the pose."""
+    samples = []
+    for i in range(2):
+        img, tmpl = scene(ea, canvas_width=160, canvas_height=128, template_id="cross",
+                          template_size=40, true_pose=(70 + 10 * i, 60, D(15 * i)),
+                          clutter_segments=6, clutter_seed=i)
+        samples.append((f"s{i}", tmpl, img))
+    cfg = ea.SearchConfig(grid=ea.PoseGrid(0, 159, 2, 0, 127, 2, 0.0, D(355), D(5)),
+                          num_levels=2, score_params=ea.ScoreParams(3))
+    rows = ea.bench_rows(samples, reps=2, warmup=1, backends=("serial", "parallel", "cuda"),
+                         config=cfg)
+    assert len(rows) == 2 * 3 * 2
+    assert all(r["elapsed_ms"] > 0 for r in rows)
+    text = ea.bench_csv(rows)
+    assert text.splitlines()[0] == "sample,backend,workers,run,elapsed_ms"

@@ -102,3 +102,21 @@ def test_detect_result_json_keys():
     assert d["pose"] == {"x": 10.5, "y": 20.25, "theta_deg": 90.0}
     assert [t["level"] for t in d["level_trace"]] == [1, 0]
     assert d["level_trace"][0]["theta_deg"] == 90.0
+
+
+def test_bench_csv_format():
+    """BenchRow CSV (SPEC.md cmd_bench): the exact header, one row per
+    sample x backend x rep, elapsed_ms > 0 enforced, quoting of names."""
+    import paper_2112_05576_b200 as ea
+    rows = [{"sample": s, "backend": b, "workers": 0, "run": r, "elapsed_ms": 1.25 + r}
+            for s in ("a", "b,c") for b in ("cuda",) for r in range(2)]
+    text = ea.bench_csv(rows)
+    lines = text.splitlines()
+    assert lines[0] == "sample,backend,workers,run,elapsed_ms"
+    assert len(lines) == 1 + 4
+    assert lines[1] == "a,cuda,0,0,1.250000"
+    assert lines[3] == '"b,c",cuda,0,0,1.250000'
+    import pytest
+    with pytest.raises(ValueError):
+        ea.bench_csv([{"sample": "x", "backend": "cuda", "workers": 0, "run": 0,
+                       "elapsed_ms": 0.0}])
