@@ -488,9 +488,9 @@ def bench_reference(args, rank, world):
 # instructions per launch, issue slots busy.  Not measurable inside the timed
 # run; per config.
 NCU = {
-    "cfg3": dict(kernel="screen_fast_kernel<1, 4, 2, 0, 2, 0, 512, 0, 1>", dram=69324800,
-                 warp_inst=443125272, issue_busy=0.6327, smem_wavefronts=148444936,
-                 l1_busy=0.9403, ncu_ms=0.61312,
+    "cfg3": dict(kernel="screen_fast_kernel<1, 4, 2, 0, 2, 0, 512, 0, 1>", dram=17905664,
+                 warp_inst=450993934, issue_busy=0.6787, smem_wavefronts=144345164,
+                 l1_busy=0.9238, ncu_ms=0.60358,
                  source="profiles/r02_screen_cfg3_ncu.txt"),
 }
 SMEM_BYTES_PER_CLK_PER_SM = 128

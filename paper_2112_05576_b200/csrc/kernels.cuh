@@ -61,7 +61,7 @@ struct SearchCtrl {
     float thr;                        // band threshold on the fp32 screen score
     int n_out;                        // entries written to the top-k output
     unsigned gfloor;                  // top-list mode: max over warps of their k-th largest
-                                      // tile maximum (order key; 0 = none), <= M_k
+                                      // listed lane maximum (order key; 0 = none), <= M_k
 };
 
 // Monotone unsigned image of a float (0 below every float): atomicMax-able.

@@ -737,6 +737,25 @@ __device__ __forceinline__ void floor_insert(float* wtop, float best, int lane) 
     __syncwarp();
 }
 
+// Inserts a finished tile's largest lane maxima (up to kf of them; each lane
+// maximum is the score of a distinct pose, so after ONE tile the warp's
+// kf-th entry is a lower bound of T_f, the kf-th largest score -- with tile
+// maxima alone it took kf tiles, and most of a launch's map was written
+// before the floor rose).  Warp-uniform: one redux per round, rounds stop
+// at the first value that does not enter the list.
+__device__ __forceinline__ void floor_insert_lanes(float* wtop, float v, int kf, int lane) {
+    const int rounds = kf > 0 ? kf : 1;
+    for (int r = 0; r < rounds; ++r) {
+        const unsigned key = float_order_key(v);
+        const unsigned top = __reduce_max_sync(0xffffffffu, key);
+        const float m = float_from_order_key(top);
+        if (!(m > wtop[kFloorK - 1])) break;
+        floor_insert(wtop, m, lane);
+        const unsigned who = __ballot_sync(0xffffffffu, key == top);
+        if (lane == __ffs(who) - 1) v = -INFINITY;
+    }
+}
+
 // Top-list mode: after a warp's tile maxima list grows, publish its k-th
 // largest (<= M_k) to the launch-wide floor; tiles below (global floor -
 // 4 delta) are not written to the map (emit_tile).
@@ -759,7 +778,7 @@ __device__ __noinline__ float emit_tile_strided(const ScreenArgs& a, const int (
                                                 const int X, const int Y, unsigned long long itr,
                                                 unsigned long long item, unsigned* hist,
                                                 const int lane, const float floor,
-                                                const float map_floor) {
+                                                const float map_floor, float& lbest) {
     float best = -INFINITY;
 #pragma unroll
     for (int s = 0; s < S; ++s)
@@ -770,6 +789,7 @@ __device__ __noinline__ float emit_tile_strided(const ScreenArgs& a, const int (
                 (unsigned long long)(ux / a.sx) < a.nx && (unsigned long long)(uy / a.sy) < a.ny)
                 best = fmaxf(best, (float)acc[s][j] * a.scale);
         }
+    lbest = best;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) best = fmaxf(best, __shfl_xor_sync(0xffffffffu, best, o));
     if (lane == 0) a.item_max[item] = best;
@@ -798,14 +818,15 @@ __device__ __forceinline__ float emit_tile(const ScreenArgs& a, const int (&acc)
                                            const int X, const int Y, unsigned long long itr,
                                            unsigned long long item, unsigned* hist,
                                            const int lane, const float floor,
-                                           const float map_floor = -INFINITY) {
+                                           const float map_floor, float& lbest) {
     // Top-list mode passes map_floor = (the warp's k-th largest tile maximum
     // so far) - 4 delta, rounded down: a tile whose maximum is below it can
     // never reach the band (its max < M_k - 2 delta, the finish's threshold),
     // so its scores are not written -- most tiles of a search, and most of
     // the map's DRAM write traffic.
     if (a.sx != 1 || a.sy != 1)  // integer steps > 1: only the grid's poses
-        return emit_tile_strided<S, HIST>(a, acc, X, Y, itr, item, hist, lane, floor, map_floor);
+        return emit_tile_strided<S, HIST>(a, acc, X, Y, itr, item, hist, lane, floor, map_floor,
+                                          lbest);
     float best = -INFINITY;
 #pragma unroll
     for (int s = 0; s < S; ++s)
@@ -813,6 +834,7 @@ __device__ __forceinline__ float emit_tile(const ScreenArgs& a, const int (&acc)
         for (int j = 0; j < kTW; ++j)
             if ((unsigned long long)(X + j) < a.nx && (unsigned long long)(Y + s) < a.ny)
                 best = fmaxf(best, (float)acc[s][j] * a.scale);
+    lbest = best;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) best = fmaxf(best, __shfl_xor_sync(0xffffffffu, best, o));
     if (lane == 0) a.item_max[item] = best;
@@ -962,9 +984,13 @@ struct RegionPlan {
     unsigned long long n_items;  // warp tiles x theta groups
     unsigned groups;         // theta groups per warp tile
 };
-// thetas per CTA item (= warps per CTA): 8 warps x 8-row strips, 16 x 4-row
+// thetas per CTA item (= warps per CTA): 12 warps x 8-row strips (168 regs; 8
+// warps measured 1.2% slower), 16 x 4-row
 template <int S>
-constexpr int region_group() { return S == 4 ? 16 : 8; }
+#ifndef EAB_REGION_GROUP8
+#define EAB_REGION_GROUP8 12
+#endif
+constexpr int region_group() { return S == 4 ? 16 : EAB_REGION_GROUP8; }
 
 // SHIFT: the region's row skew in shared memory (lane strips of S = 2^SHIFT
 // rows); the global plane keeps its own (a.geom.shift).
@@ -1060,10 +1086,10 @@ __global__ void __launch_bounds__(region_group<S>() * 32, 1)
 #pragma unroll
             for (int j = 0; j < kTW; ++j) acc[s][j] = (int)(uacc[s][j] - corr);
         const float wf = warp_floor(wtop, a.kf);
-        const float best = emit_tile<S>(a, acc, TX0 + Xr, TY0 + Yr, itr, item,
-                                        toplist ? nullptr : hist, lane, wf,
-                                        toplist ? map_floor_of(a, wf) : -INFINITY);
-        floor_insert(wtop, best, lane);
+        float lbest;
+        emit_tile<S>(a, acc, TX0 + Xr, TY0 + Yr, itr, item, toplist ? nullptr : hist, lane, wf,
+                     toplist ? map_floor_of(a, wf) : -INFINITY, lbest);
+        floor_insert_lanes(wtop, lbest, a.kf, lane);
         if (toplist) publish_floor(a, wtop, lane);
     }
     __syncthreads();
@@ -2276,10 +2302,10 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         // fused: no histogram; wtop keeps the warp's 8 largest tile maxima
         const float wf = warp_floor(wtop, a.kf);
-        const float best = emit_tile<S, !FUSED>(a, sc, X, Y, itr, item, toplist ? nullptr : hist,
-                                                lane, wf,
-                                                toplist ? map_floor_of(a, wf) : -INFINITY);
-        floor_insert(wtop, best, lane);
+        float lbest;
+        emit_tile<S, !FUSED>(a, sc, X, Y, itr, item, toplist ? nullptr : hist, lane, wf,
+                             toplist ? map_floor_of(a, wf) : -INFINITY, lbest);
+        floor_insert_lanes(wtop, lbest, a.kf, lane);
         if (toplist) publish_floor(a, wtop, lane);
     }
     if (wt && lane == 0) wt[7] = ((unsigned long long)units << 56) | (gtimer() & ((1ull << 56) - 1));

@@ -1,6 +1,8 @@
 import csv, io, subprocess, sys, collections
 rep = sys.argv[1]
-out = subprocess.run(["ncu","-i",rep,"--page","source","--csv","--print-source","sass"],capture_output=True,text=True).stdout
+# an .ncu-rep, or the csv of `ncu -i REP --page source --csv --print-source sass`
+out = (open(rep).read() if rep.endswith(".csv") else
+       subprocess.run(["ncu","-i",rep,"--page","source","--csv","--print-source","sass"],capture_output=True,text=True).stdout)
 lines = out.splitlines()
 rows = list(csv.reader(io.StringIO("\n".join(lines[1:]))))
 h = rows[0]; ie = h.index("Instructions Executed"); src = h.index("Source"); st=h.index("Warp Stall Sampling (All Samples)")
