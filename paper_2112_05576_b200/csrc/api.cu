@@ -489,10 +489,12 @@ ScreenPlan screen(ea_ctx* ctx, const ea_model* m, const ea_field* f, const ea_po
     // state) has been enqueued -- see top_enqueue
     ctx->hist_clean = false;
     float* map = (float*)ctx->map.ensure(sizeof(float) * (plan.slab_poses ? plan.slab_poses : 1));
-    float* item_max =
-        (float*)ctx->item_max.ensure(sizeof(float) * (std::max<uint64_t>(plan.slab_poses,
-                                                                           lnx * lny * plan.it_count) /
-                                                         32 + plan.it_count * 64 + 64));
+    // per-item maxima: lattice warp tiles are >= 16 columns x 32 rows (a
+    // bound that holds for any grid shape, however thin); the general kernel
+    // keeps one per 32 poses
+    const uint64_t lattice_items = ((lnx + 15) / 16) * ((lny + 31) / 32) * plan.it_count;
+    float* item_max = (float*)ctx->item_max.ensure(
+        sizeof(float) * (std::max<uint64_t>(plan.slab_poses / 32 + 1, lattice_items) + 64));
 
     ScreenArgs a{};
     a.plane = plane;

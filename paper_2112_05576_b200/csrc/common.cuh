@@ -9,6 +9,7 @@
 #include <cstdint>
 #include <cstring>
 #include <map>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -212,6 +213,23 @@ inline void count_launch(ea_ctx* ctx, int n = 1) {
             ctx->trace.emplace_back(last_launch_name(), e);
         }
     }
+}
+
+// Raises kernel `fn`'s dynamic shared-memory limit to at least `bytes` on
+// the context's device.  Function attributes are per device, so the record
+// of what was raised is keyed by (function, device) -- not a process-wide
+// flag -- and guarded for contexts driven from several host threads.
+inline void raise_smem_limit(const ea_ctx* ctx, const void* fn, size_t bytes) {
+    static std::mutex mu;
+    static std::map<std::pair<const void*, int>, size_t> raised;
+    std::lock_guard<std::mutex> lock(mu);
+    size_t& cur = raised[{fn, ctx->device}];
+    if (cur >= bytes) return;
+    const cudaError_t e =
+        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e != cudaSuccess)
+        fail(EA_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
+    cur = bytes;
 }
 
 inline void check_launch(const char* what) {

@@ -226,12 +226,7 @@ bool launch_pyramid_fields(ea_ctx* ctx, const PyramidFieldsArgs& a_in) {
     const size_t smem = pyramid_fields_smem(a.levels, tile);
     if (smem > 100 * 1024) return false;
     a.tile = tile;
-    static bool attr_set = false;
-    if (!attr_set) {
-        EAB_CUDA(cudaFuncSetAttribute(pyramid_fields_kernel,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
-        attr_set = true;
-    }
+    raise_smem_limit(ctx, (const void*)pyramid_fields_kernel, 100 * 1024);
     const int T0 = tile << (a.levels - 1);
     dim3 grid((a.w[0] + T0 - 1) / T0, (a.h[0] + T0 - 1) / T0);
     pyramid_fields_kernel<<<grid, 256, smem, ctx->stream>>>(a);

@@ -241,13 +241,7 @@ void launch_refine_level(ea_ctx* ctx, const RefineArgs& a_in) {
     const int e_max = a.max_parents * a.side * a.side * a.side;
     const size_t smem = sizeof(double) * (size_t)a.n;
     a.votes_in_smem = smem <= kRefineSmemMax ? 1 : 0;
-    static bool attr_set = false;
-    if (!attr_set) {
-        EAB_CUDA(cudaFuncSetAttribute(refine_entry_kernel,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)kRefineSmemMax));
-        attr_set = true;
-    }
+    raise_smem_limit(ctx, (const void*)refine_entry_kernel, kRefineSmemMax);
     refine_entry_kernel<<<e_max, kRefineThreads, a.votes_in_smem ? smem : 0, ctx->stream>>>(a);
     check_launch("refine_entry_kernel");
     refine_rank_kernel<<<(e_max * 32 + 255) / 256, 256, 0, ctx->stream>>>(a);

@@ -1132,7 +1132,7 @@ static void run_region(ea_ctx* ctx, const ScreenArgs& a, RegionPlan rp) {
     rp.n_items = (unsigned long long)nwx * nwy * rp.groups;
     const size_t smem = region_smem(rp, a.cta_top != nullptr);
     auto kern = screen_region_kernel<R, S, S == 4 ? 2 : 3, IGNORE, XG, MODE>;
-    EAB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    raise_smem_limit(ctx, (const void*)kern, smem);
     unsigned long long ctas = std::min<unsigned long long>(rp.n_items, (unsigned)ctx->sm_count);
     if (ctas == 0) ctas = 1;
     ctx->screen_ctas = (int)ctas;  // the finish merges this many per-CTA top lists
@@ -2362,7 +2362,7 @@ static void run_fast(ea_ctx* ctx, const ScreenArgs& a, const FinishArgs* fin) {
                           (size_t)ctx->sm_count * kTopK * sizeof(float)})
               : kHistBins * sizeof(unsigned) + plane_bytes;
     auto kern = screen_fast_kernel<R, S, SHIFT, IGNORE, XG, EDGE, THREADS, FUSED, MODE>;
-    EAB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    raise_smem_limit(ctx, (const void*)kern, smem);
     constexpr int threads = THREADS;
     const unsigned long long warps_per_cta = threads / 32;
     const bool split = std::getenv("EAB_NO_TAIL_SPLIT") == nullptr;
@@ -2702,13 +2702,8 @@ void launch_merge_rows_multi(ea_ctx* ctx, const double* in, int world, int n_mod
                              double* out, double* top_score, unsigned long long* top_index,
                              int* n_top) {
     const size_t smem = (size_t)world * k * 16;
-    static size_t opted = 0;
-    if (smem + 1024 > 48 * 1024 && opted < ctx->smem_optin) {
-        EAB_CUDA(cudaFuncSetAttribute(merge_rows_multi_kernel,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)ctx->smem_optin));
-        opted = ctx->smem_optin;
-    }
+    if (smem + 1024 > 48 * 1024)
+        raise_smem_limit(ctx, (const void*)merge_rows_multi_kernel, ctx->smem_optin);
     merge_rows_multi_kernel<<<n_models, 256, smem, ctx->stream>>>(in, world, n_models, k, out,
                                                                  top_score, top_index, n_top);
     check_launch("merge_rows_multi_kernel");
@@ -2722,13 +2717,8 @@ void launch_merge_rows(ea_ctx* ctx, const double* in, int n, int k, double* out,
     const size_t smem = (size_t)n * 16;
     // dynamic shared memory beyond 48 KB (minus the kernel's static bytes) is
     // opt-in: raise the limit once, to the context's budget
-    static size_t opted = 0;
-    if (smem + 1024 > 48 * 1024 && opted < ctx->smem_optin) {
-        EAB_CUDA(cudaFuncSetAttribute(merge_rows_kernel,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)ctx->smem_optin));
-        opted = ctx->smem_optin;
-    }
+    if (smem + 1024 > 48 * 1024)
+        raise_smem_limit(ctx, (const void*)merge_rows_kernel, ctx->smem_optin);
     merge_rows_kernel<<<1, 256, smem, ctx->stream>>>(in, n, k, out, top_score, top_index, n_top);
     check_launch("merge_rows_kernel");
     count_launch(ctx);
