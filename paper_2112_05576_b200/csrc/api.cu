@@ -1088,13 +1088,11 @@ void refine_levels(ea_ctx* ctx, const ea_levels* lv, const ea_search_config& cfg
     int* dcnt[2] = {(int*)(db + sizeof(ea_outcome) + 2 * beam_bytes),
                     (int*)(db + sizeof(ea_outcome) + 2 * beam_bytes) + 1};
     const double* dtab = (const double*)(db + head);
-    const size_t rot_elems = (size_t)4 * k * side * std::max(n_max, 1);
     double* votes =
-        (double*)ctx->refine_scores.ensure(sizeof(double) * ((size_t)std::max(n_max, 1) * E + rot_elems));
-    double* rotbuf = votes + (size_t)std::max(n_max, 1) * E;
-    // entries: score|ux|uy|theta rows, pose SoA, order keys, dup flags
-    double* entries = (double*)ctx->beam.ensure((sizeof(double) * 8 + sizeof(int)) * E);
-    int* dup = (int*)(entries + 8 * E);
+        (double*)ctx->refine_scores.ensure(sizeof(double) * (size_t)std::max(n_max, 1) * E);
+    // entries: score|ux|uy|theta rows, order keys, dup flags
+    double* entries = (double*)ctx->beam.ensure((sizeof(double) * 5 + sizeof(int)) * E);
+    int* dup = (int*)(entries + 5 * E);
     const ea_score_params& sp = cfg.score_params;
     int cur = 0;
     for (int d = 1; d <= top; ++d) {
@@ -1128,10 +1126,8 @@ void refine_levels(ea_ctx* ctx, const ea_levels* lv, const ea_search_config& cfg
         a.beam_out = dbeam[cur ^ 1];
         a.beam_count_out = dcnt[cur ^ 1];
         a.votes = votes;
-        a.rot = rotbuf;
         a.entries = entries;
-        a.poses = entries + 4 * E;
-        a.keys = reinterpret_cast<long long*>(entries + 7 * E);
+        a.keys = reinterpret_cast<long long*>(entries + 4 * E);
         a.dup = dup;
         a.outcome = dout;
         launch_refine_level(ctx, a);
@@ -1218,13 +1214,11 @@ void refine_enqueue(ea_ctx* ctx, const ea_levels* lv, const ea_search_config& cf
     const size_t E = (size_t)k * side * side * side;
     int n_max = 0;
     for (int l = 0; l < top; ++l) n_max = std::max(n_max, lv->models[l]->n);
-    const size_t rot_elems = (size_t)4 * k * side * std::max(n_max, 1);
     double* votes =
-        (double*)ctx->refine_scores.ensure(sizeof(double) * ((size_t)std::max(n_max, 1) * E + rot_elems));
-    double* rotbuf = votes + (size_t)std::max(n_max, 1) * E;
-    // entries: score|ux|uy|theta rows, pose SoA, order keys, dup flags
-    double* entries = (double*)ctx->beam.ensure((sizeof(double) * 8 + sizeof(int)) * E);
-    int* dup = (int*)(entries + 8 * E);
+        (double*)ctx->refine_scores.ensure(sizeof(double) * (size_t)std::max(n_max, 1) * E);
+    // entries: score|ux|uy|theta rows, order keys, dup flags
+    double* entries = (double*)ctx->beam.ensure((sizeof(double) * 5 + sizeof(int)) * E);
+    int* dup = (int*)(entries + 5 * E);
     const ea_score_params& sp = cfg.score_params;
     double step_x = tg.dx, step_y = tg.dy;
     int cur = 0;
@@ -1261,10 +1255,8 @@ void refine_enqueue(ea_ctx* ctx, const ea_levels* lv, const ea_search_config& cf
         a.beam_out = st.beam[cur ^ 1];
         a.beam_count_out = st.cnt[cur ^ 1];
         a.votes = votes;
-        a.rot = rotbuf;
         a.entries = entries;
-        a.poses = entries + 4 * E;
-        a.keys = reinterpret_cast<long long*>(entries + 7 * E);
+        a.keys = reinterpret_cast<long long*>(entries + 4 * E);
         a.dup = dup;
         a.outcome = st.out;
         launch_refine_level(ctx, a);

@@ -31,10 +31,8 @@ struct RefineArgs {
     BeamDev* beam_out;
     int* beam_count_out;
     double* votes;        // [entry][point] vote rows when they do not fit shared memory
-    double* rot;          // [parent * side + kt][px | py | dx | dy][point]
     int votes_in_smem;    // set by launch_refine_level
     double* entries;      // [entry] score, ux, uy, theta
-    double* poses;        // ux[E] | uy[E] | theta[E] (refine_rotate_kernel)
     long long* keys;      // order_key(score), LLONG_MIN for duplicates
     int* dup;             // [entry] an earlier entry has the same pose
     ea_outcome* outcome;  // device copy of the result

@@ -6,11 +6,11 @@
 // host evaluates glibc cos/sin for all paths of the k seeds once (k * sum
 // side^d values) and the levels run without host round trips:
 //
-//   refine_rotate_kernel  exact rotation of the model for each (parent, kt)
-//                         (similarity.cpp:79-86), shared by its side^2 poses.
-//   refine_entry_kernel   one CTA per pose: exact votes of all points into a
-//                         shared-memory row, ordered fp64 sum (model-point
-//                         order, then /n) + "an earlier entry has this pose".
+//   refine_entry_kernel   one CTA per pose: the pose and the model's exact
+//                         rotation (similarity.cpp:79-86), exact votes of all
+//                         points into a shared-memory row, ordered fp64 sum
+//                         (model-point order, then /n) + "an earlier entry
+//                         has this pose".
 //   refine_rank_kernel    one warp per pose: rank among first occurrences in
 //                         the stable-sort order -> new beam slot, trace,
 //                         final outcome.
@@ -22,49 +22,34 @@
 
 namespace eab {
 
-// Exact rotation (similarity.cpp:79-86) of every model point for each
-// (parent, kt): shared by the side^2 lattice poses of that pair.
-__global__ void __launch_bounds__(128) refine_rotate_kernel(const RefineArgs a) {
-    const int side = a.side;
-    const int pk = blockIdx.x;  // parent * side + (kt + R)
-    if (pk / side >= *a.beam_count) return;
-    const BeamDev parent = a.beam[pk / side];
+// Lattice pose e of a level (search.cpp:295-312): parent = e / side^3, kt
+// path step (e / side^2) % side, (ky, kx) from e % side^2 -- the same
+// arithmetic the host loop uses (2 * parent + k * step, no contraction).
+__device__ __forceinline__ void refine_pose(const RefineArgs& a, int e, double& ux, double& uy,
+                                            double& th, double& c, double& s) {
+    const int side = a.side, ss = side * side;
+    const int pk = e / ss, j = e % ss;
+    const BeamDev& parent = a.beam[pk / side];
     const int path = parent.path * side + (pk % side);
-    const double c = a.table[3 * path + 1], s = a.table[3 * path + 2];
-    if (blockIdx.y == 0) {  // the pair's side^2 lattice poses (search.cpp:305-312)
-        const int ss = side * side, E = a.max_parents * side * ss;
-        const double cx = __dmul_rn(parent.ux, 2.0), cy = __dmul_rn(parent.uy, 2.0);
-        const double th = a.table[3 * path];
-        for (int j = threadIdx.x; j < ss; j += blockDim.x) {
-            const int ky = j / side - a.R, kx = j % side - a.R;
-            const int e = pk * ss + j;
-            a.poses[e] = __dadd_rn(cx, __dmul_rn((double)kx, a.step_x));
-            a.poses[E + e] = __dadd_rn(cy, __dmul_rn((double)ky, a.step_y));
-            a.poses[2 * E + e] = th;
-        }
-    }
-    double* out = a.rot + (size_t)pk * 4 * a.n;
-    for (int i = blockIdx.y * blockDim.x + threadIdx.x; i < a.n; i += gridDim.y * blockDim.x) {
-        const double x = a.pts[i], y = a.pts[a.n + i];
-        const double dx = a.pts[2 * a.n + i], dy = a.pts[3 * a.n + i];
-        const double rx = __dsub_rn(__dmul_rn(c, dx), __dmul_rn(s, dy));
-        const double ry = __dadd_rn(__dmul_rn(s, dx), __dmul_rn(c, dy));
-        const double norm = __dsqrt_rn(__dadd_rn(__dmul_rn(rx, rx), __dmul_rn(ry, ry)));
-        out[i] = __dsub_rn(__dmul_rn(c, x), __dmul_rn(s, y));
-        out[a.n + i] = __dadd_rn(__dmul_rn(s, x), __dmul_rn(c, y));
-        out[2 * a.n + i] = __ddiv_rn(rx, norm);
-        out[3 * a.n + i] = __ddiv_rn(ry, norm);
-    }
+    th = a.table[3 * path];
+    c = a.table[3 * path + 1];
+    s = a.table[3 * path + 2];
+    const int ky = j / side - a.R, kx = j % side - a.R;
+    ux = __dadd_rn(__dmul_rn(parent.ux, 2.0), __dmul_rn((double)kx, a.step_x));
+    uy = __dadd_rn(__dmul_rn(parent.uy, 2.0), __dmul_rn((double)ky, a.step_y));
 }
 
 // Score of each lattice pose (score_rotated, similarity.cpp:102-118): one
-// CTA per pose.  Threads compute the exact votes of the model points
-// (strided) into a vote row (shared memory, or global for very large models);
-// then thread 0 adds them in model-point order -- the reference's sequential
-// fp64 sum, bit for bit -- and divides by n, while warp 1 checks whether an
-// earlier entry in generation order has the identical pose: identical poses
-// score identically, so after the stable sort the first occurrence is the one
-// kept (search.cpp:330-345).
+// CTA per pose.  Threads rotate the model points for the pose's theta
+// (rotate_model, similarity.cpp:79-86: glibc cos/sin from the path table)
+// and compute their exact votes into a vote row (shared memory, or global
+// for very large models); then thread 0 adds them in model-point order --
+// the reference's sequential fp64 sum, bit for bit -- and divides by n,
+// while warp 1 checks whether an earlier entry in generation order has the
+// identical pose: identical poses score identically, so after the stable
+// sort the first occurrence is the one kept (search.cpp:330-345).  (The
+// rotation is recomputed by each of a (parent, kt) pair's side^2 poses: a
+// separate rotation launch cost more than the arithmetic.)
 __global__ void __launch_bounds__(kRefineThreads) refine_entry_kernel(const RefineArgs a) {
     extern __shared__ double sv[];
     __shared__ int dup_s;
@@ -72,27 +57,31 @@ __global__ void __launch_bounds__(kRefineThreads) refine_entry_kernel(const Refi
     const int E = *a.beam_count * side * ss;
     const int e = blockIdx.x;
     if (e >= E) return;  // whole CTA
-    const int EM = a.max_parents * side * ss;  // pose array stride
-    const double px = a.poses[e], py = a.poses[EM + e], pt = a.poses[2 * EM + e];
+    double px, py, pt, c, s;
+    refine_pose(a, e, px, py, pt, c, s);
     const int n = a.n;
-    const double* rot = a.rot + (size_t)(e / ss) * 4 * n;
     double* vb = a.votes_in_smem ? sv : a.votes + (size_t)e * n;
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const double x = a.pts[i], y = a.pts[n + i];
+        const double dx = a.pts[2 * n + i], dy = a.pts[3 * n + i];
+        const double rx = __dsub_rn(__dmul_rn(c, dx), __dmul_rn(s, dy));
+        const double ry = __dadd_rn(__dmul_rn(s, dx), __dmul_rn(c, dy));
+        const double norm = __dsqrt_rn(__dadd_rn(__dmul_rn(rx, rx), __dmul_rn(ry, ry)));
         int inb;
-        vb[i] = point_term_exact(rot[i], rot[n + i], rot[2 * n + i], rot[3 * n + i], px, py,
-                                 a.gx, a.gy, a.mag, a.W, a.H, a.vote_R, a.eps, a.ignore != 0,
-                                 &inb);
+        vb[i] = point_term_exact(__dsub_rn(__dmul_rn(c, x), __dmul_rn(s, y)),
+                                 __dadd_rn(__dmul_rn(s, x), __dmul_rn(c, y)),
+                                 __ddiv_rn(rx, norm), __ddiv_rn(ry, norm), px, py, a.gx, a.gy,
+                                 a.mag, a.W, a.H, a.vote_R, a.eps, a.ignore != 0, &inb);
     }
     __syncthreads();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (warp == 1) {
         int dup = 0;
-        // (unrolled: the pose loads of eight earlier entries in flight per lane
-        // instead of one L2 round trip per 32 entries)
-#pragma unroll 8
-        for (int q = lane; q < e; q += 32)
-            dup |= (a.poses[q] == px && a.poses[EM + q] == py && a.poses[2 * EM + q] == pt) ? 1
-                                                                                              : 0;
+        for (int q = lane; q < e; q += 32) {
+            double qx, qy, qt, qc, qs;
+            refine_pose(a, q, qx, qy, qt, qc, qs);
+            dup |= (qx == px && qy == py && qt == pt) ? 1 : 0;
+        }
         dup = __any_sync(0xffffffffu, dup);
         if (lane == 0) dup_s = dup;
     }
@@ -234,19 +223,16 @@ void launch_seed_beam(ea_ctx* ctx, const double* top_score, const unsigned long 
 
 void launch_refine_level(ea_ctx* ctx, const RefineArgs& a_in) {
     RefineArgs a = a_in;
-    const int pairs = a.max_parents * a.side;
-    const int gy = std::max(1, std::min((a.n + 127) / 128, 8));
-    refine_rotate_kernel<<<dim3(pairs, gy), 128, 0, ctx->stream>>>(a);
-    check_launch("refine_rotate_kernel");
     const int e_max = a.max_parents * a.side * a.side * a.side;
     const size_t smem = sizeof(double) * (size_t)a.n;
     a.votes_in_smem = smem <= kRefineSmemMax ? 1 : 0;
     raise_smem_limit(ctx, (const void*)refine_entry_kernel, kRefineSmemMax);
     refine_entry_kernel<<<e_max, kRefineThreads, a.votes_in_smem ? smem : 0, ctx->stream>>>(a);
     check_launch("refine_entry_kernel");
+    count_launch(ctx);
     refine_rank_kernel<<<(e_max * 32 + 255) / 256, 256, 0, ctx->stream>>>(a);
     check_launch("refine_rank_kernel");
-    count_launch(ctx, 3);
+    count_launch(ctx);
 }
 
 }  // namespace eab
