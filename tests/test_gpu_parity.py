@@ -459,6 +459,14 @@ def test_detect_batch_matches_single(ea, oracle):
     for img, got in zip(imgs, batch):
         assert got.key() == det.detect(img).key()
         assert got.key() == oracle.coarse_to_fine(tp, oracle.build_pyramid(img, 2), cfg).key()
+    # the same images staged in the library's pinned buffers (ea_host_alloc)
+    pinned = []
+    for img in imgs:
+        buf = ea.host_array(img.shape)
+        buf[...] = img
+        pinned.append(buf)
+    assert [o.key() for o in det.detect_batch(pinned)] == [o.key() for o in batch]
+    assert det.detect(pinned[2]).key() == batch[2].key()
 
 
 @pytest.mark.slow
