@@ -2225,9 +2225,11 @@ ea_status ea_ctx_create(int device, ea_ctx** out) {
         auto* c = new ea_ctx;
         c->device = device;
         c->sm_count = prop.multiProcessorCount;
-        // dynamic shared memory budget: the opt-in limit minus 1 KB for the
-        // screen kernels' static arrays (per-warp histogram floors)
-        c->smem_optin = prop.sharedMemPerBlockOptin - 1024;
+        // dynamic shared-memory budget of the lattice kernels: the opt-in
+        // limit minus their static shared memory (per-warp lists, the plane
+        // barrier, merge_hist's chunk sums; checked per kernel at launch by
+        // raise_smem_limit -- a 1 KB reserve let a plane near the limit fail)
+        c->smem_optin = prop.sharedMemPerBlockOptin - kLatticeStaticSmem;
         cudaError_t se = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
         if (se != cudaSuccess) {
             delete c;

@@ -219,12 +219,23 @@ inline void count_launch(ea_ctx* ctx, int n = 1) {
 // the context's device.  Function attributes are per device, so the record
 // of what was raised is keyed by (function, device) -- not a process-wide
 // flag -- and guarded for contexts driven from several host threads.
+// Static shared memory the lattice kernels may declare on top of their
+// dynamic budget (ea_ctx::smem_optin = opt-in limit - this).
+constexpr size_t kLatticeStaticSmem = 2688;
+
 inline void raise_smem_limit(const ea_ctx* ctx, const void* fn, size_t bytes) {
     static std::mutex mu;
     static std::map<std::pair<const void*, int>, size_t> raised;
     std::lock_guard<std::mutex> lock(mu);
     size_t& cur = raised[{fn, ctx->device}];
     if (cur >= bytes) return;
+    cudaFuncAttributes fa{};
+    if (cudaFuncGetAttributes(&fa, fn) == cudaSuccess &&
+        bytes + fa.sharedSizeBytes > ctx->smem_optin + kLatticeStaticSmem)
+        fail(EA_ERR_INTERNAL, "kernel needs " + std::to_string(bytes) + " B dynamic + " +
+                                  std::to_string(fa.sharedSizeBytes) +
+                                  " B static shared memory, over the opt-in limit "
+                                  "(raise kLatticeStaticSmem)");
     const cudaError_t e =
         cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
     if (e != cudaSuccess)

@@ -776,6 +776,32 @@ def test_screen_threshold_modes_match(ea, oracle, monkeypatch, case):
         c.close()
 
 
+@pytest.mark.parametrize("tid,size", [("cross", 40), ("rectangle", 48), ("ring", 36)])
+def test_toplist_clustered_peak(ea, oracle, monkeypatch, tid, size):
+    """A lone clean object on a blank canvas: the k best poses all sit in the
+    peak's warp tile (adjacent translations and thetas).  The top lists then
+    hold that tile's lane maxima -- distinct poses, so the band threshold
+    stays <= T_f -- and the map floor rises after the first tile.  Default
+    (top lists) and histogram paths == the oracle for k up to 8 and 9."""
+    img, tmpl = scene(ea, canvas_width=160, canvas_height=120, template_id=tid,
+                      template_size=size, true_pose=(80, 60, D(25)), clutter_segments=0,
+                      clutter_seed=1, noise_sigma=0.0, noise_seed=1)
+    m = oracle.prepare_model(tmpl)
+    f = oracle.compute_gradients(img)
+    grid = ea.PoseGrid(0, 159, 1, 0, 119, 1, 0.0, D(359), D(1))
+    params = ea.ScoreParams(3)
+    monkeypatch.setenv("EAB_NO_TOPLIST", "1")
+    ctx_hist = ea.Context(0)
+    monkeypatch.delenv("EAB_NO_TOPLIST")
+    ctx_top = ea.Context(0)
+    for k in (1, 5, 8, 9):
+        want = keys(oracle.search_topk(m.points, f, grid, params, k))
+        for ctx in (ctx_top, ctx_hist):
+            assert keys(ea.search_topk(m, f, grid, params, k=k, ctx=ctx)) == want, (k, ctx)
+    ctx_hist.close()
+    ctx_top.close()
+
+
 def test_fused_screen_ties_and_tiny_grids(ea, oracle, monkeypatch):
     """Top-list and fused path edge cases: a flat field (every pose ties at 0: the k-th
     largest is 0 and every pose is a candidate), grids with fewer poses than
