@@ -275,6 +275,43 @@ def test_region_search_bit_exact(ea, oracle, case):
         assert keys(got) == keys(want)
 
 
+GEOMETRY_SWEEP = [
+    # (shape, size, w, h, grid): planes around the shared-memory limit for
+    # 8- and 4-row strips, very wide and very thin fields and grids (one
+    # translation row, one column), grids overhanging the field
+    ("rectangle", 40, 280, 96, None),
+    ("l_bracket", 56, 310, 90, None),
+    ("rectangle", 40, 330, 80, None),
+    ("l_bracket", 48, 512, 50, None),
+    ("cross", 40, 900, 24, None),
+    ("rectangle", 32, 1500, 12, None),
+    ("l_bracket", 40, 1200, 40, (0, 1199, 1, 20, 20, 1, 0.0, D(270), D(90))),
+    ("rectangle", 40, 64, 900, (30, 30, 1, 0, 899, 1, 0.0, D(270), D(90))),
+    ("ring", 30, 200, 150, (-40, 239, 1, -30, 179, 1, 0.0, D(300), D(60))),
+    # integer strides > 1 on a plane too large for shared memory (region
+    # kernel, strided emit) and on a fitting one
+    ("l_bracket", 48, 640, 480, (0, 639, 3, 0, 479, 3, 0.0, D(270), D(90))),
+    ("rectangle", 40, 300, 200, (1, 298, 2, 2, 197, 4, 0.0, D(270), D(90))),
+]
+
+
+@pytest.mark.parametrize("case", range(len(GEOMETRY_SWEEP)))
+def test_search_geometry_sweep(ea, oracle, case):
+    """Field and grid shapes at the lattice kernels' limits (plane bytes vs
+    the shared-memory budget, padding shrunk or not, region tiling, warp
+    tiles much wider or taller than the grid) == the oracle."""
+    shape, size, w, h, g = GEOMETRY_SWEEP[case]
+    rng = np.random.default_rng(4000 + case)
+    tm = oracle.prepare_model(oracle.render_template(shape, size))
+    f = oracle.compute_gradients(rand_image(rng, w, h, real=case % 2 == 0))
+    grid = ea.PoseGrid(*(g or (0, w - 1, 1, 0, h - 1, 1, 0.0, D(270), D(90))))
+    params = ea.ScoreParams(3)
+    for k in (1, 5, 9):
+        got = ea.search_topk(tm, f, grid, params, k=k)
+        want = oracle.search_topk(tm.points, f, grid, params, k)
+        assert keys(got) == keys(want), (k, ea.default_context().stats()["screen_path"])
+
+
 @pytest.mark.parametrize("nb,pol", [(3, 0), (5, 1), (1, 0)])
 def test_region_screen_bound(ea, oracle, nb, pol):
     rng = np.random.default_rng(40 + nb)
