@@ -411,6 +411,37 @@ def test_coarse_to_fine_bit_exact(ea, oracle, case):
     assert det.key() == want.key()
 
 
+C2F_SWEEP = [
+    # (template, size, canvas, pose, L, grid step at level 0, dtheta, topk,
+    #  refine_radius, nb, polarity)
+    ("l_bracket", 48, (200, 160), (97, 81, 33), 3, 4, 3, 1, 1, 3, 0),
+    ("cross", 40, (190, 150), (90, 70, 10), 2, 2, 5, 8, 2, 5, 0),
+    ("rectangle", 56, (230, 170), (120, 90, 75), 3, 4, 4, 3, 3, 3, 1),
+    ("ring", 36, (160, 160), (80, 80, 0), 2, 2, 6, 20, 2, 1, 0),
+    ("l_bracket", 64, (260, 200), (131, 97, 250), 4, 8, 2, 5, 2, 3, 0),
+    ("cross", 36, (170, 130), (84, 66, 45), 2, 3, 5, 4, 1, 3, 0),
+]
+
+
+@pytest.mark.parametrize("case", range(len(C2F_SWEEP)))
+def test_coarse_to_fine_sweep(ea, oracle, case):
+    """search_levels across beam widths (topk 1..20), refinement radii 1-3,
+    neighbourhoods 1/3/5, both polarities, 2-4 levels and grid steps that
+    do and do not divide the level scale (a step of 3 at level 0 is a
+    non-integer top-level step): Detector.detect == the oracle's
+    coarse_to_fine, outcome and per-level trace."""
+    tid, size, (W, H), (px, py, pt), L, st, dt, k, rr, nb, pol = C2F_SWEEP[case]
+    img, tmpl = scene(ea, canvas_width=W, canvas_height=H, template_id=tid, template_size=size,
+                      true_pose=(px, py, D(pt)), clutter_segments=12, clutter_seed=case,
+                      noise_sigma=1.0, noise_seed=50 + case)
+    cfg = ea.SearchConfig(grid=ea.PoseGrid(0, W - 1, st, 0, H - 1, st, 0.0, D(360 - dt), D(dt)),
+                          num_levels=L, score_params=ea.ScoreParams(nb, pol), topk=k,
+                          refine_radius=rr, min_score=0.3)
+    tp, wp = oracle.build_pyramid(tmpl, L), oracle.build_pyramid(img, L)
+    want = oracle.coarse_to_fine(tp, wp, cfg)
+    assert ea.Detector(tmpl, cfg).detect(img).key() == want.key()
+
+
 def test_flat_scene_no_detection(ea, oracle):
     flat = np.full((96, 96), 180.0)
     tmpl = oracle.render_template("rectangle", 32)
