@@ -473,7 +473,8 @@ def bench_reference(args, rank, world):
     base.update({"value": v, "sample": desc})
     line = {"impl": "reference", "metric": "pose-evals/sec", "value": v,
             "unit": "pose-evals/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "higher_is_better": True, "scaling": "none",
+            "warmup": args.warmup, "higher_is_better": True,
+            "scaling": "strong" if args.shard == "theta" else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"{args.config}: {CONFIGS[args.config]['desc']}"},
             "cpu_baseline": base,
@@ -812,7 +813,9 @@ def bench_ours(args, rank, world, local_rank):
         "metric": "pose-evals/sec", "value": value, "unit": "pose-evals/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot_ms / args.steps,
         "higher_is_better": True,
-        "scaling": ("strong" if shard_theta else "weak") if world > 1 else "none",
+        # the mode the N > 1 runs of this command use (theta slabs of one
+        # search: strong; --shard images: weak), also at N = 1
+        "scaling": "strong" if args.shard == "theta" else "weak",
         "vs_baseline": None, "dtype": "f32 screen + f64 exact verify", "data": "synthetic",
         "config": {"workload": f"{args.config}: {CONFIGS[args.config]['desc']}",
                    "top_level_grid": f"{nx}x{ny}x{nt}",
