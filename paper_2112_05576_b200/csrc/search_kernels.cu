@@ -985,20 +985,18 @@ struct RegionPlan {
     unsigned groups;         // theta groups per warp tile
 };
 // thetas per CTA item (= warps per CTA): 12 warps x 8-row strips (168 regs; 8
-// warps measured 1.2% slower), 16 x 4-row
-template <int S>
-#ifndef EAB_REGION_GROUP8
-#define EAB_REGION_GROUP8 12
-#endif
-constexpr int region_group() { return S == 4 ? 16 : EAB_REGION_GROUP8; }
+// warps measured 1.2% slower for 3x3 windows and 19% slower for 5x5, where
+// 12 warps spill ~650 B), 16 x 4-row
+template <int R, int S>
+constexpr int region_group() { return S == 4 ? 16 : 12; }
 
 // SHIFT: the region's row skew in shared memory (lane strips of S = 2^SHIFT
 // rows); the global plane keeps its own (a.geom.shift).
 template <int R, int S, int SHIFT, bool IGNORE, int XG, int MODE>
-__global__ void __launch_bounds__(region_group<S>() * 32, 1)
+__global__ void __launch_bounds__(region_group<R, S>() * 32, 1)
     screen_region_kernel(const ScreenArgs a, const unsigned nwx, const unsigned nwy,
                          const RegionPlan rp) {
-    constexpr int kGroup = region_group<S>();
+    constexpr int kGroup = region_group<R, S>();
     extern __shared__ __align__(16) unsigned char smem[];
     const bool toplist = a.cta_top != nullptr;  // no histogram (see ScreenArgs::cta_top)
     unsigned* hist = reinterpret_cast<unsigned*>(smem);
@@ -1125,7 +1123,7 @@ static size_t region_smem(const RegionPlan& rp, bool toplist) {
 
 template <int R, int S, bool IGNORE, int XG, int MODE>
 static void run_region(ea_ctx* ctx, const ScreenArgs& a, RegionPlan rp) {
-    constexpr int YG = 32 / XG, kGroup = region_group<S>();
+    constexpr int YG = 32 / XG, kGroup = region_group<R, S>();
     const unsigned nwx = (unsigned)((a.lnx + 8 * XG - 1) / (8 * XG));
     const unsigned nwy = (unsigned)((a.lny + YG * S - 1) / (YG * S));
     rp.groups = (unsigned)((a.it_count + kGroup - 1) / kGroup);
@@ -2455,6 +2453,11 @@ static void run_fast(ea_ctx* ctx, const ScreenArgs& a, const FinishArgs* fin) {
     count_launch(ctx);
 }
 
+// CTA size of the fully padded 8-row kernel: kFastThreads (12 warps x 168
+// registers) for 3x3 windows; 8 warps for 5x5 (R = 2 spilled ~600 B at 168
+// registers; cfg2 at nb 5: 1.167 -> 1.101 ms).
+constexpr int fast_threads(int R) { return R >= 2 ? 256 : kFastThreads; }
+
 size_t fast_smem_bytes(const PlaneGeom& g) {
     return kHistBins * sizeof(unsigned) + ((g.bytes() + 15) & ~(size_t)15);
 }
@@ -2492,8 +2495,8 @@ bool launch_screen_fast(ea_ctx* ctx, const ScreenArgs& a) {
         if (ig) run_fast<RR, 8, 3, true, XGV, true, 256, false, MM>(ctx, a, nullptr);          \
         else run_fast<RR, 8, 3, false, XGV, true, 256, false, MM>(ctx, a, nullptr);            \
     } else {                                                                                    \
-        if (ig) run_fast<RR, 8, 3, true, XGV, false, kFastThreads, false, MM>(ctx, a, nullptr);\
-        else run_fast<RR, 8, 3, false, XGV, false, kFastThreads, false, MM>(ctx, a, nullptr);  \
+        if (ig) run_fast<RR, 8, 3, true, XGV, false, fast_threads(RR), false, MM>(ctx, a, nullptr);\
+        else run_fast<RR, 8, 3, false, XGV, false, fast_threads(RR), false, MM>(ctx, a, nullptr);  \
     }
 #define EAB_FAST_M(RR, MM)                                                  \
     if (a.xg == 2) {                                                        \
