@@ -442,6 +442,38 @@ def test_coarse_to_fine_sweep(ea, oracle, case):
     assert ea.Detector(tmpl, cfg).detect(img).key() == want.key()
 
 
+def test_shared_context_interleaved_detects(ea, oracle):
+    """Two detectors of different templates, image sizes, grids and
+    neighbourhoods on ONE context, interleaved with batch calls: the
+    context's caches (screening plane, exact-zero tiles, theta tables, tail
+    and candidate buffers, refinement state) are keyed by what they depend
+    on, so every result == the oracle."""
+    ctx = ea.Context(0)
+    specs = [
+        (dict(canvas_width=240, canvas_height=180, template_id="l_bracket", template_size=56,
+              true_pose=(118, 92, D(40)), clutter_segments=15, clutter_seed=3), 2, 3, 2),
+        (dict(canvas_width=150, canvas_height=200, template_id="cross", template_size=40,
+              true_pose=(70, 110, D(12)), clutter_segments=8, clutter_seed=4), 3, 5, 4),
+    ]
+    dets, imgs, wants = [], [], []
+    for spec, L, nb, st in specs:
+        img, tmpl = scene(ea, **spec)
+        W, H = spec["canvas_width"], spec["canvas_height"]
+        cfg = ea.SearchConfig(grid=ea.PoseGrid(0, W - 1, st, 0, H - 1, st, 0.0, D(356), D(4)),
+                              num_levels=L, score_params=ea.ScoreParams(nb), topk=4,
+                              min_score=0.3)
+        dets.append(ea.Detector(tmpl, cfg, ctx))
+        imgs.append(img)
+        wants.append(oracle.coarse_to_fine(oracle.build_pyramid(tmpl, L),
+                                           oracle.build_pyramid(img, L), cfg).key())
+    for order in ((0, 1, 0, 1), (1, 1, 0, 0)):
+        for i in order:
+            assert dets[i].detect(imgs[i]).key() == wants[i], i
+        for i in (1, 0):
+            assert [o.key() for o in dets[i].detect_batch([imgs[i]] * 3)] == [wants[i]] * 3
+    ctx.close()
+
+
 def test_flat_scene_no_detection(ea, oracle):
     flat = np.full((96, 96), 180.0)
     tmpl = oracle.render_template("rectangle", 32)
