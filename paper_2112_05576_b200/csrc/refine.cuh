@@ -38,7 +38,11 @@ struct RefineArgs {
     ea_outcome* outcome;  // device copy of the result
 };
 
-constexpr int kRefineThreads = 256;               // threads per pose (refine_entry_kernel)
+// threads per pose (refine_entry_kernel): 625 CTAs of a k = 5, radius 2
+// level fit one wave at 60 registers x 192 threads (5 CTAs per SM); 256
+// threads (4 per SM) left 33 CTAs for a second wave -- 21.1 -> 17.7 us per
+// level on cfg3 (128: 18.0, 96: 18.6, 64: 20.9)
+constexpr int kRefineThreads = 192;
 constexpr size_t kRefineSmemMax = 96 * 1024;      // vote rows in smem up to this size
 void launch_refine_level(ea_ctx* ctx, const RefineArgs& a);
 
